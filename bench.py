@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: FP64 matrix-free Q1 operator inside CG on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl native|reference]
+
+Default workload: BASELINE.json configs[3] -- isotropic elasticity on 384^3 hexes with cell-wise
+discontinuous lambda/mu, homogeneous Dirichlet box, CG (the configuration the headline metric
+"CG operator apply GDOF/s (FP64) and % of HBM roofline at 1/2/4/8 B200 vs CSR SpMV" is quoted
+on).  A step is one CG iteration = apply (+ fused p.Ap) + x/r update (+ fused r.r) + p update
+(+ the NCCL halo and the two allreduces when N > 1).  value = global DOF x steps / time.
+N > 1: the same global mesh is slab-decomposed in z (strong scaling), one rank per GPU.
+
+--impl reference: the CPU oracle (oracle/, plain quadrature apply + CG) timed on the host
+cores on a bounded sub-box of the same workload (this tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_2308_09839_b200 import inputs as I  # noqa: E402
+
+METRIC = "CG operator apply GDOF/s (FP64) and % of HBM roofline at 1/2/4/8 B200 vs CSR SpMV"
+UNIT = "GDOF/s"
+
+
+# ------------------------------------------------------------------------------------------
+# helpers
+# ------------------------------------------------------------------------------------------
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_apply_bytes(kind, nx, ny, nz):
+    """SURVEY §8(d) / DESIGN.md §6: x read once + y written once (8 B each per DOF), plus
+    lambda, mu once per cell for elasticity (16 B/cell).  Connectivity, coordinates and the
+    Dirichlet mask are implicit (0 B)."""
+    ndof = I.n_nodes(nx, ny, nz) * I.ncomp(kind)
+    b = 16 * ndof
+    if kind == "elastic":
+        b += 16 * nx * ny * nz
+    return b
+
+
+def cg_vector_bytes(ndof):
+    # update: read x,p,r,q write x,r (48 B/DOF); p-update: read r,p write p (24 B/DOF)
+    return 72 * ndof
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle legs (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------
+def oracle_sample_dims(kind):
+    # bounded sub-box of the same workload: ~3-5 s per oracle CG iteration on 16 cores
+    return {"elastic": (96, 96, 96), "vector": (48, 48, 48), "scalar": (160, 160, 160)}[kind]
+
+
+def oracle_cg_rate(kind, iters=2):
+    from oracle import oracle as O
+    nx, ny, nz = oracle_sample_dims(kind)
+    h = 1.0 / nx
+    g = I.rng(I.SEED_BASE + 77)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = I.interior_rhs(g, nx, ny, nz, I.ncomp(kind))
+    t0 = time.perf_counter()
+    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=0, lam=lam, mu=mu)
+    t1 = time.perf_counter()
+    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=iters, lam=lam, mu=mu)
+    t2 = time.perf_counter()
+    it_time = max((t2 - t1) - (t1 - t0), 1e-9) / iters
+    cores = O.max_threads()
+    return b.size / it_time / 1e9, cores, f"oracle CG on {kind} {nx}x{ny}x{nz} (same recipe), " \
+        f"{iters} iterations timed (init/true-residual applies subtracted), {b.size} DOF"
+
+
+def run_reference(args, cfg):
+    """Reference arm: the oracle as it stands, on host cores; rank 0 only."""
+    ws, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    kind = cfg["kind"]
+    nx, ny, nz = oracle_sample_dims(kind)
+    h = 1.0 / nx
+    g = I.rng(I.SEED_BASE + 77)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = I.interior_rhs(g, nx, ny, nz, I.ncomp(kind))
+    # each step = one oracle CG iteration on the bounded sub-box
+    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=0, lam=lam, mu=mu)  # warm the library
+    ta = time.perf_counter()
+    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=0, lam=lam, mu=mu)
+    t_fixed = time.perf_counter() - ta
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; warm-up steps are not re-run to bound the time
+    t0 = time.perf_counter()
+    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=args.steps, lam=lam, mu=mu)
+    t = max(time.perf_counter() - t0 - t_fixed, 1e-9)
+    value = b.size * args.steps / t / 1e9
+    cores = O.max_threads()
+    sample = (f"oracle CG on {kind} {nx}x{ny}x{nz} cells (sub-box of {cfg['name']}, same input "
+              f"recipe), {args.steps} iterations, init/true-residual applies subtracted")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "kind": kind, "cells": list(cfg["n"]),
+                   "sample_cells": [nx, ny, nz], "bc": "dirichlet_box"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# native arm
+# ------------------------------------------------------------------------------------------
+def run_native(args, cfg):
+    import torch
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2308_09839_b200 import fem
+    fem.load(build_if_missing=(rank == 0 and ws == 1))
+
+    kind = cfg["kind"]
+    nx, ny, nz = cfg["n"]
+    h = 1.0 / nx
+    c = I.ncomp(kind)
+    comm = None
+    if ws > 1:
+        uid = [fem.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = fem.Comm(ws, rank, uid[0])
+    mesh = fem.Mesh(nx, ny, nz, h, comm)
+    op = fem.Operator(mesh, kind, "dirichlet")
+    ndof_global = op.n_global
+    k0, k1 = mesh.plane_begin, mesh.plane_end
+    plane = (nx + 1) * (ny + 1)
+
+    # ---- inputs (seeded, synthetic, SURVEY §8(d) recipe) ----
+    g = I.rng(I.SEED_BASE + args.config)
+    if kind == "elastic":
+        lam, mu = I.materials(g, nx, ny, nz)
+        lb = max(k0 - 1, 0)
+        le = min(k1, nz)
+        sl = slice(lb * nx * ny, le * nx * ny)
+        op.set_material(torch.from_numpy(lam[sl]).cuda(), torch.from_numpy(mu[sl]).cuda(),
+                        layer_begin=lb, n_layers=le - lb)
+        del lam, mu
+    gb = I.rng(I.SEED_BASE + args.config + 1000)
+    b_full = I.interior_rhs(gb, nx, ny, nz, c)
+    b_loc = np.ascontiguousarray(b_full[k0 * plane * c:k1 * plane * c])
+    del b_full
+    b = torch.from_numpy(b_loc).cuda()
+    x = torch.zeros_like(b)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (W CG steps) ----
+    op.set_option("time_apply", 1)
+    op.cg_begin(b, x, tol=0.0, maxit=1 << 30)
+    op.cg_iterate(args.warmup)
+    torch.cuda.synchronize()
+    op.apply_time()  # discard warm-up events
+
+    # ---- timed region: exactly K CG steps ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = fem.launch_count()
+    wall0 = time.perf_counter()
+    e0.record(stream)
+    op.cg_iterate(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    launches = fem.launch_count() - l0
+    clocks = sampler.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    apply_ms_total, n_apply = op.apply_time()
+    apply_ms = max_over_ranks(apply_ms_total / max(n_apply, 1))
+    info = op.cg_end()
+    value = ndof_global * args.steps / (ms / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (the apply) ----
+    hbm_peak, peak_src = measured_peaks()
+    nloc_planes = k1 - k0
+    # algorithmic bytes of one rank's apply launch: owned planes (+ its cell layers)
+    alg_bytes = algorithmic_apply_bytes(kind, nx, ny, nz) * nloc_planes / (nz + 1)
+    achieved = alg_bytes / (apply_ms / 1e3) / 1e9
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}.json")
+    if os.path.exists(tr_path) and ws == 1:
+        with open(tr_path) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    share = apply_ms * args.steps / ms
+
+    extra = {}
+    # ---- operator-only throughput (Fig. 3/9 analogue) on the same stream ----
+    xx = torch.empty_like(b).uniform_(-1, 1)
+    yy = torch.empty_like(b)
+    for _ in range(3):
+        op.apply(xx, yy)
+    torch.cuda.synchronize()
+    R = 10
+    a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    a0.record(stream)
+    for _ in range(R):
+        op.apply(xx, yy)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    ams = max_over_ranks(a0.elapsed_time(a1) / R)
+    extra["apply_only_gdofs"] = ndof_global / (ams / 1e3) / 1e9
+    extra["apply_only_ms"] = ams
+    extra["apply_in_cg_ms"] = apply_ms
+    extra["apply_share_of_step"] = share
+    extra["cg_iteration_ms"] = ms / args.steps
+    extra["cg_bytes_per_dof_alg"] = algorithmic_apply_bytes(kind, nx, ny, nz) / ndof_global + 72
+    del xx, yy
+
+    # ---- e2e: the public call a user makes, with pinned HOST buffers ----
+    e2e = None
+    if not args.no_e2e:
+        bh = torch.from_numpy(b_loc).pin_memory()
+        xh = torch.zeros(b_loc.size, dtype=torch.float64).pin_memory()
+        M = args.e2e_iters
+        op.set_option("time_apply", 0)
+        op.cg_solve(bh.numpy(), xh.numpy(), tol=0.0, maxit=M)  # warm (graph capture)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = 2
+        for _ in range(reps):
+            xh.zero_()
+            op.cg_solve(bh.numpy(), xh.numpy(), tol=0.0, maxit=M)
+        torch.cuda.synchronize()
+        barrier()
+        et = max_over_ranks((time.perf_counter() - t0) / reps)
+        e2e = {"value": ndof_global * M / et / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(2 * b_loc.nbytes), "d2h_bytes_per_step": int(b_loc.nbytes),
+               "step": f"one fem_cg_solve call ({M} iterations) with pinned host b, x; per-rank bytes"}
+
+    # ---- CSR SpMV baseline, same box (N = 1) ----
+    if ws == 1 and not args.no_csr:
+        extra.update(csr_compare(fem, torch, kind, args))
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1) ----
+    cpu = None
+    if ws == 1 and rank == 0 and not args.no_cpu:
+        try:
+            v, cores, sample = oracle_cg_rate(kind)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg["name"], "kind": kind, "cells": [nx, ny, nz],
+                       "ndof": ndof_global, "bc": "dirichlet_box",
+                       "material": "E=10^U(0,2), nu=U(0.20,0.35) per cell" if kind == "elastic" else None,
+                       "parallelism": f"z-slab x{ws}" if ws > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (vectors %.2f GB each)" % (ndof_global * 8 / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "kernel": f"{kind} apply (CG mode, fused p.Ap)",
+                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                         "frac_of_8TBps_nominal": achieved / 8000.0},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "cpu_baseline": cpu,
+            "cg_info": {k: info[k] for k in ("iterations", "r0_norm", "r_norm", "true_r_norm")},
+            "wall_s_timed": wall,
+            "extra": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def csr_compare(fem, torch, kind, args):
+    """Matrix-free apply vs assembled CSR SpMV on the same box and operator (Table 1 analogue).
+    Elasticity at 384^3 needs 167 GB of CSR, so the comparison uses 256^3."""
+    n = args.csr_n if args.csr_n else (256 if kind == "elastic" else 256)
+    out = {}
+    try:
+        mesh = fem.Mesh(n, n, n, 1.0 / n)
+        op = fem.Operator(mesh, kind, "dirichlet")
+        if kind == "elastic":
+            g = I.rng(I.SEED_BASE + 55)
+            lam, mu = I.materials(g, n, n, n)
+            op.set_material(torch.from_numpy(lam).cuda(), torch.from_numpy(mu).cuda())
+            del lam, mu
+        t0 = time.perf_counter()
+        A = op.csr()
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
+        x = torch.empty(op.n_global, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+        y1 = torch.empty_like(x); y2 = torch.empty_like(x)
+        s = torch.cuda.current_stream()
+
+        def timeit(fn, R=10):
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(R):
+                fn()
+            b.record(s)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / R
+
+        t_csr = timeit(lambda: A.apply(x, y1))
+        t_mf = timeit(lambda: op.apply(x, y2))
+        rel = float((y1 - y2).abs().max() / y2.abs().max())
+        out = {"csr_cells": [n, n, n], "csr_nnz": A.nnz, "csr_bytes": A.bytes,
+               "csr_build_s": build_s, "csr_spmv_ms": t_csr,
+               "csr_gdofs": op.n_global / (t_csr / 1e3) / 1e9,
+               "csr_gbs": (A.bytes + 16 * op.n_global) / (t_csr / 1e3) / 1e9,
+               "mf_same_box_ms": t_mf, "mf_same_box_gdofs": op.n_global / (t_mf / 1e3) / 1e9,
+               "mf_over_csr": t_csr / t_mf, "mf_vs_csr_max_rel_diff": rel}
+        A.close()
+        del A
+        torch.cuda.empty_cache()
+    except Exception as ex:
+        out = {"csr_error": str(ex)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3, help="BASELINE.json configs index (0-3)")
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-csr", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--csr-n", type=int, default=0)
+    ap.add_argument("--e2e-iters", type=int, default=100)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = I.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_native(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * fem.h -- C ABI of the B200-native hot path of arXiv 2308.09839
+ * ("low-order matrix-free finite element operators in CG").
+ *
+ * Library: paper_2308_09839_b200/libfem.so (CUDA sm_100a, FP64).  No torch types cross this
+ * boundary: every argument is a plain integer, double, host pointer, device pointer or an
+ * opaque handle.  Citations "P:n" are lines of the paper text, "S:n" of SPEC.md.
+ *
+ * Problem (Eq. 1-3): Q1 trilinear hexahedra on the box [0,nx h]x[0,ny h]x[0,nz h];
+ *   kind FEM_SCALAR_LAPLACE  : A_ij = int grad phi_i . grad phi_j                 (Eq. 1 / 4)
+ *   kind FEM_VECTOR_LAPLACE  : 3 components, (e_k (x) grad phi_i):(e_l (x) grad phi_j) (Eq. 2 / 5)
+ *   kind FEM_ELASTICITY      : (e_k (x) grad phi_i) : sigma(e_l (x) grad phi_j),
+ *                              sigma = lambda_e tr(eps) I + 2 mu_e eps, cell-wise lambda_e, mu_e
+ *                                                                               (Eq. 3 / 6)
+ * integrated with 2x2x2 Gauss-Legendre quadrature (reading R1), applied
+ * matrix-free (three steps of P:188-196, Eq. 7-9, Alg. 1).
+ *
+ * Layouts (ABI level):
+ *   node n = i + (nx+1)(j + (ny+1) k), x fastest;  DOF = c n + comp, c = 1 or 3
+ *   ("3(i-1)+k").  Vectors are dense FP64, 8-byte aligned, length c * n_local_nodes,
+ *   covering the rank's OWNED node planes [plane_begin, plane_end) only.
+ *   Cells e = i + nx (j + ny k); lambda/mu are FP64 per cell.
+ * Boundary conditions (reading R6): FEM_BC_DIRICHLET_BOX applies
+ *   y = P A P x + (I - P) x, P zeroing every DOF of every node on the 6 box faces.
+ *
+ * Pointers: "device or host" arguments are classified with cudaPointerGetAttributes; host
+ * arguments are staged through library-owned device buffers inside the call (the e2e path).
+ * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every
+ * call is stream-ordered on it; calls returning host values (fem_dot, fem_cg_solve with
+ * info, fem_csr_create) synchronise that stream.
+ * Errors: every int-returning function returns a fem_status; it never throws, never aborts;
+ * on error a thread-local message is available from fem_last_error().
+ * Ownership: handles are created and destroyed by the caller through this API; the library
+ * owns everything behind a handle (workspace, ghost planes, material copies, CSR arrays).
+ */
+#ifndef PAPER_2308_09839_FEM_H
+#define PAPER_2308_09839_FEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FEM_OK = 0,
+  FEM_EINVAL = 1,       /* bad argument: dims < 1, h <= 0 or non-finite, NULL/misaligned pointer,
+                           aliasing x == y, material on a non-elastic op, unknown kind/bc      */
+  FEM_ENOMEM = 2,       /* device or host allocation failed                                    */
+  FEM_ECUDA = 3,        /* a CUDA runtime call failed (message has the CUDA error string)      */
+  FEM_ENCCL = 4,        /* an NCCL call failed                                                  */
+  FEM_EOVERFLOW = 5,    /* global node count >= 2^32 or DOF index overflow              */
+  FEM_EMATERIAL = 6,    /* some mu <= 0 or lambda + 2 mu / 3 < 0, or non-finite         */
+  FEM_EBREAKDOWN = 7,   /* CG: p^T A p <= 0 or non-finite while r^T r > 0               */
+  FEM_ESTATE = 8,       /* call out of order (e.g. elastic apply before fem_set_material)       */
+  FEM_EUNSUPPORTED = 9  /* valid request this build does not implement (message says what)      */
+} fem_status;
+
+typedef enum { FEM_SCALAR_LAPLACE = 0, FEM_VECTOR_LAPLACE = 1, FEM_ELASTICITY = 2 } fem_kind;
+typedef enum { FEM_BC_NONE = 0, FEM_BC_DIRICHLET_BOX = 1 } fem_bc;
+
+typedef struct fem_comm_s* fem_comm_t;
+typedef struct fem_mesh_s* fem_mesh_t;
+typedef struct fem_op_s* fem_op_t;
+typedef struct fem_csr_s* fem_csr_t;
+
+/* CG report (reduced).  status is a fem_status of the solve itself. */
+typedef struct {
+  int32_t iterations;      /* iterations performed                                             */
+  int32_t converged;       /* 1 if sqrt(r.r) <= tol * ||r0|| or r.r == 0 was reached            */
+  int32_t breakdown_iter;  /* iteration at which p.Ap <= 0 / non-finite was seen, else -1       */
+  int32_t status;          /* FEM_OK or FEM_EBREAKDOWN                                          */
+  double r0_norm;          /* ||b - A x0||_2 (global)                                           */
+  double r_norm;           /* recurrence residual norm sqrt(r.r) at exit                        */
+  double true_r_norm;      /* ||b - A x||_2 recomputed at exit (one extra apply)                */
+} fem_cg_info;
+
+/* ---- diagnostics --------------------------------------------------------------------- */
+const char* fem_last_error(void);           /* thread-local; "" if none                     */
+const char* fem_version(void);
+/* Number of CUDA kernels this process has launched through the library (graph replays count
+ * every kernel node).  Used by bench.py's "gpu_launches". */
+int64_t fem_launch_count(void);
+
+/* ---- communicator (slab decomposition over NCCL) ------------------------ */
+/* Rank 0 creates a 128-byte NCCL unique id; the caller broadcasts it (torch.distributed). */
+int fem_get_unique_id(void* id_out, int64_t id_bytes /* >= 128 */);
+/* nranks == 1: no NCCL is touched and id may be NULL.  The calling thread's current CUDA
+ * device is the rank's device. */
+int fem_comm_create(int32_t nranks, int32_t rank, const void* id, fem_comm_t* out);
+void fem_comm_destroy(fem_comm_t comm);
+
+/* ---- mesh ----------------------------------------------------------------- */
+/* nx, ny, nz >= 1 cells; h > 0 cell side.  comm NULL means one GPU.  Node planes (z) are split
+ * as evenly as possible over the ranks; rank r owns [plane_begin, plane_end). */
+int fem_mesh_create(int64_t nx, int64_t ny, int64_t nz, double h, fem_comm_t comm,
+                    fem_mesh_t* out);
+int fem_mesh_local(fem_mesh_t mesh, int64_t* plane_begin, int64_t* plane_end,
+                   int64_t* n_local_nodes);
+void fem_mesh_destroy(fem_mesh_t mesh);
+
+/* ---- operator -------------------------------------------------------------------------- */
+int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out);
+int fem_op_ndof(fem_op_t op, int64_t* n_local_dof, int64_t* n_global_dof);
+/* Cell-wise Lame parameters (P:9, "cell constant C").  lambda/mu (device or host) hold
+ * the cell layers [layer_begin, layer_begin + n_layers) of the global cell-lexicographic
+ * arrays; they must cover every layer the rank touches (its owned planes' adjacent cells).
+ * Values are validated (FEM_EMATERIAL) and copied; the caller may free them afterwards. */
+int fem_set_material(fem_op_t op, const double* lambda, const double* mu, int64_t layer_begin,
+                     int64_t n_layers);
+/* y = A_c x on the rank's owned DOFs.  x, y: device or host, length n_local_dof,
+ * x != y.  Collective when nranks > 1 (one node-plane halo per neighbour). */
+int fem_apply(fem_op_t op, const double* x, double* y, void* stream);
+/* Global sum_i a_i b_i over owned DOFs (Table 4 "ddot").  Deterministic for a
+ * fixed rank count.  Result written to *result (host).  Collective. */
+int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void* stream);
+/* Conjugate gradient (recurrences of Table 4) on A_c x = b.
+ * x holds x0 on entry and the iterate on exit (device or host).  tol > 0: stop when
+ * sqrt(r.r) <= tol * ||r0||; tol == 0: exactly maxit iterations unless r.r == 0.
+ * info may be NULL.  Returns FEM_EBREAKDOWN on breakdown (info filled).  Collective. */
+int fem_cg_solve(fem_op_t op, const double* b, double* x, double tol, int32_t maxit,
+                 fem_cg_info* info, void* stream);
+/* Split CG for benchmarking a fixed number of steps with inputs resident on the device:
+ * fem_cg_begin initialises r = b - A x, p = r (b, x device pointers that must stay valid),
+ * fem_cg_iterate runs `iters` iterations (CUDA-graph replay; stream-ordered, no host sync),
+ * fem_cg_end synchronises and fills info. */
+int fem_cg_begin(fem_op_t op, const double* b, double* x, double tol, int32_t maxit, void* stream);
+int fem_cg_iterate(fem_op_t op, int32_t iters, void* stream);
+int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
+/* Options: "use_graph" (default 1), "check_every" (default 16 iterations between host
+ * convergence polls in fem_cg_solve), "time_apply" (1: record CUDA events around every apply
+ * launched by fem_cg_iterate; read back with fem_apply_time). */
+int fem_set_option(fem_op_t op, const char* key, int64_t value);
+/* Total device time (ms) and count of the applies timed since the last call (time_apply). */
+int fem_apply_time(fem_op_t op, double* total_ms, int64_t* count);
+void fem_op_destroy(fem_op_t op);
+
+/* ---- assembled CSR baseline (Table 1) ------------------------------ */
+/* Builds A_c as CSR on the device from the same element matrices (int64 row offsets, int32
+ * columns, FP64 values: 12 B per non-zero).  Single rank only (FEM_EUNSUPPORTED else).
+ * Elasticity requires fem_set_material first. */
+int fem_csr_create(fem_op_t op, fem_csr_t* out);
+int fem_csr_info(fem_csr_t csr, int64_t* nrows, int64_t* nnz, int64_t* bytes);
+int fem_csr_apply(fem_csr_t csr, const double* x, double* y, void* stream);
+void fem_csr_destroy(fem_csr_t csr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAPER_2308_09839_FEM_H */

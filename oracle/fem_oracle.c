@@ -278,6 +278,64 @@ int orc_apply(int kind, int bc, int64_t nx, int64_t ny, int64_t nz, double h, co
   return ORC_OK;
 }
 
+/* y_n = (A_c x)_n for a list of nodes only (same three steps of P:188-196 restricted to the
+ * <= 8 cells around each requested node), for sampled parity at sizes where the full oracle
+ * apply is too slow.  out[c*t + comp] for t-th requested node. */
+int orc_apply_nodes(int kind, int bc, int64_t nx, int64_t ny, int64_t nz, double h,
+                    const double* lam, const double* mu, const double* x, const int64_t* nodes,
+                    int64_t nreq, double* out, int nthreads) {
+  if (nx < 1 || ny < 1 || nz < 1 || !(h > 0.0) || kind < 0 || kind > 2) return ORC_EINVAL;
+  const int c = (kind == ORC_SCALAR) ? 1 : 3;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+  int err = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < nreq; ++t) {
+    const int64_t n = nodes[t];
+    const int64_t ni = n % (nx + 1), nj = (n / (nx + 1)) % (ny + 1), nk = n / ((nx + 1) * (ny + 1));
+    double acc[3] = {0.0, 0.0, 0.0};
+    if (bc && orc_is_boundary_node(n, nx, ny, nz)) {
+      for (int comp = 0; comp < c; ++comp) out[c * t + comp] = x[c * n + comp];
+      continue;
+    }
+    for (int64_t k = nk - 1; k <= nk; ++k)
+      for (int64_t j = nj - 1; j <= nj; ++j)
+        for (int64_t i = ni - 1; i <= ni; ++i) {
+          if (i < 0 || j < 0 || k < 0 || i >= nx || j >= ny || k >= nz) continue;
+          double X[8][3], ue[24], Ae[24 * 24];
+          int arow = -1;
+          for (int a = 0; a < 8; ++a) {
+            int64_t ii = i + CORNER[a][0], jj = j + CORNER[a][1], kk = k + CORNER[a][2];
+            X[a][0] = (double)ii * h;
+            X[a][1] = (double)jj * h;
+            X[a][2] = (double)kk * h;
+            int64_t id = node_id(ii, jj, kk, nx, ny);
+            if (id == n) arow = a;
+            int masked = bc && orc_is_boundary_node(id, nx, ny, nz);
+            for (int comp = 0; comp < c; ++comp) ue[c * a + comp] = masked ? 0.0 : x[c * id + comp];
+          }
+          const int64_t e = i + nx * (j + ny * k);
+          if (orc_element_matrix(kind, X, kind == ORC_ELASTIC ? lam[e] : 0.0,
+                                 kind == ORC_ELASTIC ? mu[e] : 0.0, Ae) != ORC_OK) {
+#pragma omp atomic write
+            err = ORC_EGEOM;
+            continue;
+          }
+          const int nn = 8 * c;
+          for (int comp = 0; comp < c; ++comp) {
+            double s = 0.0;
+            for (int q = 0; q < nn; ++q) s += Ae[(c * arow + comp) * nn + q] * ue[q];
+            acc[comp] += s;
+          }
+        }
+    for (int comp = 0; comp < c; ++comp) out[c * t + comp] = acc[comp];
+  }
+  return err;
+}
+
 /* Dense assembly of A_c for tiny meshes: A[r*ndof + s] (same element matrices, scatter). */
 int orc_assemble_dense(int kind, int bc, int64_t nx, int64_t ny, int64_t nz, double h,
                        const double* lam, const double* mu, double* A) {

@@ -63,6 +63,9 @@ def lib():
         L.orc_cg.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, i64, ctypes.c_double, d, d, d, d,
                              ctypes.c_double, ctypes.c_int, ctypes.POINTER(CgInfoC), d, ctypes.c_int]
         L.orc_cg.restype = ctypes.c_int
+        L.orc_apply_nodes.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, i64, ctypes.c_double,
+                                      d, d, d, ctypes.POINTER(ctypes.c_int64), i64, d, ctypes.c_int]
+        L.orc_apply_nodes.restype = ctypes.c_int
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = ctypes.c_int
         _lib = L
@@ -151,6 +154,21 @@ def apply(kind, bc, nx, ny, nz, h, x, lam=None, mu=None, nthreads=0):
     if rc:
         raise ValueError(f"orc_apply failed: {rc}")
     return y
+
+
+def apply_nodes(kind, bc, nx, ny, nz, h, x, nodes, lam=None, mu=None, nthreads=0):
+    """(A_c x) at the given node ids only: array (len(nodes), c)."""
+    k = _kind(kind); c = 1 if k == SCALAR else 3
+    lam, mu = _mat(k, nx, ny, nz, lam, mu)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+    out = np.empty((nodes.size, c))
+    rc = lib().orc_apply_nodes(k, int(bc), nx, ny, nz, float(h), _p(lam), _p(mu), _p(x),
+                               nodes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nodes.size,
+                               _p(out), int(nthreads))
+    if rc:
+        raise ValueError(f"orc_apply_nodes failed: {rc}")
+    return out
 
 
 def assemble_dense(kind, bc, nx, ny, nz, h, lam=None, mu=None):

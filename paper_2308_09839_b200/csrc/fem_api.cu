@@ -1,0 +1,818 @@
+// fem_api.cu -- host side of libfem.so: the C ABI declared in include/fem.h.
+// Handles, validation, workspace, slab partition + NCCL halo/allreduce, the CG driver
+// (CUDA-graph captured iteration) and the CSR baseline.  Kernels live in kernels_*.cu.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fem.h"
+#include "fem_internal.cuh"
+
+namespace fem {
+cudaError_t upload_unit_matrices(const double* K, const double* Kl, const double* Km);
+static std::atomic<int64_t> g_launches{0};
+void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace fem
+
+using namespace fem;
+
+// ------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------
+static thread_local std::string t_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(FEM_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),     \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                    \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess)                                                                \
+      return fail(FEM_ENCCL, "%s failed: %s (%s:%d)", #expr, ncclGetErrorString(_r),      \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+#define FEM_TRY(expr)                \
+  do {                               \
+    int _s = (expr);                 \
+    if (_s != FEM_OK) return _s;     \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// handles
+// ------------------------------------------------------------------------------------------
+struct fem_comm_s {
+  int nranks = 1, rank = 0, device = 0;
+  ncclComm_t nccl = nullptr;
+};
+
+struct fem_mesh_s {
+  Grid g{};  // global sizes, owned planes [k0, k1)
+  fem_comm_s* comm = nullptr;
+  int nranks = 1, rank = 0, device = 0, sm_count = 148;
+};
+
+struct fem_op_s {
+  fem_mesh_s* mesh = nullptr;
+  int kind = 0, bc = 0, comps = 1;
+  int64_t n_local = 0, n_global = 0, plane_dofs = 0;
+  // material (local cell layers [mat_layer0, mat_layer0 + mat_layers))
+  double *lam = nullptr, *mu = nullptr;
+  int64_t mat_layer0 = 0, mat_layers = 0;
+  bool has_mat = false;
+  // workspace
+  double *r = nullptr, *p_ext = nullptr, *q = nullptr;
+  double *ghost_lo = nullptr, *ghost_hi = nullptr;
+  double *stage_a = nullptr, *stage_b = nullptr;
+  CgScalars* sc = nullptr;
+  CgScalars* sc_host = nullptr;
+  double* dot_dev = nullptr;
+  double* dot_host = nullptr;
+  unsigned long long* bad = nullptr;
+  Reduce red{};
+  // CG state
+  const double* cg_b = nullptr;
+  double* cg_x = nullptr;
+  bool cg_active = false;
+  cudaGraphExec_t graph1 = nullptr, graphN = nullptr;
+  int graphN_iters = 0;
+  const double* graph_b = nullptr;
+  double* graph_x = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  // options
+  int use_graph = 1, check_every = 16, time_apply = 0;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+};
+
+struct fem_csr_s {
+  int comps = 1, device = 0, sm_count = 148;
+  int64_t nrows = 0, nnz = 0;
+  int64_t* rowptr = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+};
+
+// ------------------------------------------------------------------------------------------
+// helpers
+// ------------------------------------------------------------------------------------------
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static int check_vec(const void* p, const char* name) {
+  if (!p) return fail(FEM_EINVAL, "%s is NULL", name);
+  if (((uintptr_t)p) & 7) return fail(FEM_EINVAL, "%s is not 8-byte aligned", name);
+  return FEM_OK;
+}
+
+static int set_device(int dev) {
+  int cur = -1;
+  CUDA_TRY(cudaGetDevice(&cur));
+  if (cur != dev) CUDA_TRY(cudaSetDevice(dev));
+  return FEM_OK;
+}
+
+template <class T>
+static int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FEM_ENOMEM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
+                cudaGetErrorString(e));
+  }
+  return FEM_OK;
+}
+
+// unit-cube element matrices by the library's own 2x2x2 Gauss quadrature (h = 1), corner
+// index a = dx + 2 dy + 4 dz.  Eq. 4 (scalar) and Eq. 6 split into its lambda and mu parts.
+static void unit_element_matrices(double K[64], double Kl[576], double Km[576]) {
+  const double gp[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
+  std::memset(K, 0, 64 * sizeof(double));
+  std::memset(Kl, 0, 576 * sizeof(double));
+  std::memset(Km, 0, 576 * sizeof(double));
+  for (int q = 0; q < 8; ++q) {
+    const double X[3] = {gp[q & 1], gp[(q >> 1) & 1], gp[(q >> 2) & 1]};
+    const double w = 1.0 / 8.0;
+    double G[8][3];
+    for (int a = 0; a < 8; ++a) {
+      const int o[3] = {a & 1, (a >> 1) & 1, (a >> 2) & 1};
+      for (int d = 0; d < 3; ++d) {
+        double v = 1.0;
+        for (int e = 0; e < 3; ++e) {
+          const double f = o[e] ? X[e] : 1.0 - X[e];
+          const double df = o[e] ? 1.0 : -1.0;
+          v *= (e == d) ? df : f;
+        }
+        G[a][d] = v;
+      }
+    }
+    for (int a = 0; a < 8; ++a)
+      for (int b = 0; b < 8; ++b) {
+        const double gg = G[a][0] * G[b][0] + G[a][1] * G[b][1] + G[a][2] * G[b][2];
+        K[a * 8 + b] += w * gg;
+        for (int k = 0; k < 3; ++k)
+          for (int l = 0; l < 3; ++l) {
+            const int ix = (3 * a + k) * 24 + 3 * b + l;
+            Kl[ix] += w * G[a][k] * G[b][l];
+            Km[ix] += w * ((k == l ? gg : 0.0) + G[a][l] * G[b][k]);
+          }
+      }
+  }
+}
+
+static std::vector<int> g_unit_devices;
+static std::mutex g_unit_mu;
+
+static int ensure_unit_matrices(int dev) {
+  std::lock_guard<std::mutex> lk(g_unit_mu);
+  if (std::find(g_unit_devices.begin(), g_unit_devices.end(), dev) != g_unit_devices.end())
+    return FEM_OK;
+  double K[64], Kl[576], Km[576];
+  unit_element_matrices(K, Kl, Km);
+  CUDA_TRY(upload_unit_matrices(K, Kl, Km));
+  g_unit_devices.push_back(dev);
+  return FEM_OK;
+}
+
+// one node-plane halo per neighbour (ncclSend/Recv pairs in one group)
+static int halo(fem_op_s* op, const double* owned, double* lo, double* hi, cudaStream_t s) {
+  fem_mesh_s* m = op->mesh;
+  if (m->nranks == 1) return FEM_OK;
+  const size_t cnt = (size_t)op->plane_dofs;
+  const int64_t np = m->g.k1 - m->g.k0;
+  ncclComm_t c = m->comm->nccl;
+  NCCL_TRY(ncclGroupStart());
+  if (m->rank > 0) {
+    NCCL_TRY(ncclSend(owned, cnt, ncclDouble, m->rank - 1, c, s));
+    NCCL_TRY(ncclRecv(lo, cnt, ncclDouble, m->rank - 1, c, s));
+  }
+  if (m->rank < m->nranks - 1) {
+    NCCL_TRY(ncclSend(owned + (np - 1) * op->plane_dofs, cnt, ncclDouble, m->rank + 1, c, s));
+    NCCL_TRY(ncclRecv(hi, cnt, ncclDouble, m->rank + 1, c, s));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return FEM_OK;
+}
+
+static int allreduce1(fem_op_s* op, double* dev_scalar, cudaStream_t s) {
+  fem_mesh_s* m = op->mesh;
+  if (m->nranks == 1) return FEM_OK;
+  NCCL_TRY(ncclAllReduce(dev_scalar, dev_scalar, 1, ncclDouble, ncclSum, m->comm->nccl, s));
+  return FEM_OK;
+}
+
+// apply kernel dispatch; x given as a plane source
+static int launch_apply(fem_op_s* op, PlaneSrc x, double* y, int mode, cudaStream_t s) {
+  fem_mesh_s* m = op->mesh;
+  cudaError_t e;
+  if (op->kind == FEM_ELASTICITY)
+    e = launch_elastic(op->bc, m->g, x, op->lam, op->mu, op->mat_layer0, y, mode, op->sc, op->red,
+                       s, m->sm_count);
+  else
+    e = launch_laplace(op->comps, op->bc, m->g, x, y, mode, op->sc, op->red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "apply launch failed: %s", cudaGetErrorString(e));
+  return FEM_OK;
+}
+
+// y = A_c x for a DEVICE owned vector x (halo via op ghost buffers)
+static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s) {
+  FEM_TRY(halo(op, x, op->ghost_lo, op->ghost_hi, s));
+  PlaneSrc src{x, op->mesh->rank > 0 ? op->ghost_lo : nullptr,
+               op->mesh->rank < op->mesh->nranks - 1 ? op->ghost_hi : nullptr};
+  return launch_apply(op, src, y, 0, s);
+}
+
+static int ensure_stage(fem_op_s* op) {
+  if (!op->stage_a) FEM_TRY(dalloc(&op->stage_a, op->n_local));
+  if (!op->stage_b) FEM_TRY(dalloc(&op->stage_b, op->n_local));
+  return FEM_OK;
+}
+
+static int dot_device(fem_op_s* op, const double* a, const double* b, cudaStream_t s,
+                      double* result) {
+  cudaError_t e = launch_dot(a, b, op->n_local, op->dot_dev, op->red, s, op->mesh->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "dot launch failed: %s", cudaGetErrorString(e));
+  FEM_TRY(allreduce1(op, op->dot_dev, s));
+  CUDA_TRY(cudaMemcpyAsync(op->dot_host, op->dot_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  *result = *op->dot_host;
+  return FEM_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// ABI
+// ------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* fem_last_error(void) { return t_err.c_str(); }
+const char* fem_version(void) { return "paper_2308_09839_b200 libfem 0.1 (sm_100a, fp64)"; }
+int64_t fem_launch_count(void) { return g_launches.load(); }
+
+int fem_get_unique_id(void* id_out, int64_t id_bytes) {
+  if (!id_out || id_bytes < (int64_t)sizeof(ncclUniqueId))
+    return fail(FEM_EINVAL, "id buffer must hold %zu bytes", sizeof(ncclUniqueId));
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof(id));
+  return FEM_OK;
+}
+
+int fem_comm_create(int32_t nranks, int32_t rank, const void* id, fem_comm_t* out) {
+  if (!out) return fail(FEM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(FEM_EINVAL, "bad nranks/rank %d/%d", nranks, rank);
+  auto* c = new (std::nothrow) fem_comm_s();
+  if (!c) return fail(FEM_ENOMEM, "host allocation failed");
+  c->nranks = nranks;
+  c->rank = rank;
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(FEM_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  }
+  if (nranks > 1) {
+    if (!id) {
+      delete c;
+      return fail(FEM_EINVAL, "id is NULL with nranks > 1");
+    }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return fail(FEM_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+  }
+  *out = c;
+  return FEM_OK;
+}
+
+void fem_comm_destroy(fem_comm_t c) {
+  if (!c) return;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+}
+
+int fem_mesh_create(int64_t nx, int64_t ny, int64_t nz, double h, fem_comm_t comm, fem_mesh_t* out) {
+  if (!out) return fail(FEM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (nx < 1 || ny < 1 || nz < 1) return fail(FEM_EINVAL, "dims must be >= 1 (got %lld %lld %lld)", (long long)nx, (long long)ny, (long long)nz);
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(FEM_EINVAL, "h must be finite and > 0");
+  // 32-bit global node index limit and int32 CSR column headroom
+  const double nn = (double)(nx + 1) * (double)(ny + 1) * (double)(nz + 1);
+  if (nn >= 4294967296.0) return fail(FEM_EOVERFLOW, "global node count %.0f >= 2^32", nn);
+  const int P = comm ? comm->nranks : 1;
+  const int R = comm ? comm->rank : 0;
+  if (nz + 1 < P) return fail(FEM_EINVAL, "fewer node planes (%lld) than ranks (%d)", (long long)(nz + 1), P);
+  auto* m = new (std::nothrow) fem_mesh_s();
+  if (!m) return fail(FEM_ENOMEM, "host allocation failed");
+  m->comm = comm;
+  m->nranks = P;
+  m->rank = R;
+  cudaGetDevice(&m->device);
+  cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, m->device);
+  const int64_t N = nz + 1, base = N / P, rem = N % P;
+  const int64_t k0 = R * base + std::min<int64_t>(R, rem);
+  const int64_t k1 = k0 + base + (R < rem ? 1 : 0);
+  m->g = Grid{nx, ny, nz, h, k0, k1, (nx + 1) * (ny + 1)};
+  *out = m;
+  return FEM_OK;
+}
+
+int fem_mesh_local(fem_mesh_t m, int64_t* pb, int64_t* pe, int64_t* nloc) {
+  if (!m) return fail(FEM_EINVAL, "mesh is NULL");
+  if (pb) *pb = m->g.k0;
+  if (pe) *pe = m->g.k1;
+  if (nloc) *nloc = (m->g.k1 - m->g.k0) * m->g.plane;
+  return FEM_OK;
+}
+
+void fem_mesh_destroy(fem_mesh_t m) { delete m; }
+
+static void op_free(fem_op_s* op) {
+  if (!op) return;
+  set_device(op->mesh->device);
+  if (op->graph1) cudaGraphExecDestroy(op->graph1);
+  if (op->graphN) cudaGraphExecDestroy(op->graphN);
+  for (auto e : op->ev) cudaEventDestroy(e);
+  cudaFree(op->lam); cudaFree(op->mu);
+  cudaFree(op->r); cudaFree(op->p_ext); cudaFree(op->q);
+  cudaFree(op->ghost_lo); cudaFree(op->ghost_hi);
+  cudaFree(op->stage_a); cudaFree(op->stage_b);
+  cudaFree(op->sc); cudaFree(op->dot_dev); cudaFree(op->bad);
+  cudaFree(op->red.partials); cudaFree(op->red.ticket);
+  cudaFreeHost(op->sc_host); cudaFreeHost(op->dot_host);
+  delete op;
+}
+
+int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
+  if (!out) return fail(FEM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!mesh) return fail(FEM_EINVAL, "mesh is NULL");
+  if (kind < 0 || kind > 2) return fail(FEM_EINVAL, "unknown kind %d", kind);
+  if (bc < 0 || bc > 1) return fail(FEM_EINVAL, "unknown bc %d", bc);
+  FEM_TRY(set_device(mesh->device));
+  auto* op = new (std::nothrow) fem_op_s();
+  if (!op) return fail(FEM_ENOMEM, "host allocation failed");
+  op->mesh = mesh;
+  op->kind = kind;
+  op->bc = bc;
+  op->comps = kind == FEM_SCALAR_LAPLACE ? 1 : 3;
+  const Grid& g = mesh->g;
+  op->plane_dofs = g.plane * op->comps;
+  op->n_local = (g.k1 - g.k0) * op->plane_dofs;
+  op->n_global = (g.nz + 1) * op->plane_dofs;
+  int st = FEM_OK;
+#define OP_TRY(x)                 \
+  do {                            \
+    st = (x);                     \
+    if (st != FEM_OK) {           \
+      op_free(op);                \
+      return st;                  \
+    }                             \
+  } while (0)
+  OP_TRY(dalloc(&op->r, op->n_local));
+  OP_TRY(dalloc(&op->p_ext, op->n_local + 2 * op->plane_dofs));
+  OP_TRY(dalloc(&op->q, op->n_local));
+  OP_TRY(dalloc(&op->ghost_lo, op->plane_dofs));
+  OP_TRY(dalloc(&op->ghost_hi, op->plane_dofs));
+  OP_TRY(dalloc(&op->sc, 1));
+  OP_TRY(dalloc(&op->dot_dev, 1));
+  OP_TRY(dalloc(&op->bad, 1));
+  OP_TRY(dalloc(&op->red.partials, kMaxCtas));
+  OP_TRY(dalloc(&op->red.ticket, 1));
+  op->red.capacity = kMaxCtas;
+  if (cudaMallocHost(&op->sc_host, sizeof(CgScalars)) != cudaSuccess ||
+      cudaMallocHost(&op->dot_host, sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    op_free(op);
+    return fail(FEM_ENOMEM, "pinned host allocation failed");
+  }
+  if (cudaMemset(op->red.ticket, 0, sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemset(op->sc, 0, sizeof(CgScalars)) != cudaSuccess ||
+      cudaMemset(op->p_ext, 0, sizeof(double) * (op->n_local + 2 * op->plane_dofs)) != cudaSuccess) {
+    op_free(op);
+    return fail(FEM_ECUDA, "cudaMemset failed");
+  }
+  OP_TRY(ensure_unit_matrices(mesh->device));
+#undef OP_TRY
+  *out = op;
+  return FEM_OK;
+}
+
+int fem_op_ndof(fem_op_t op, int64_t* nl, int64_t* ng) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  if (nl) *nl = op->n_local;
+  if (ng) *ng = op->n_global;
+  return FEM_OK;
+}
+
+int fem_set_material(fem_op_t op, const double* lam, const double* mu, int64_t layer_begin,
+                     int64_t n_layers) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  if (op->kind != FEM_ELASTICITY) return fail(FEM_EINVAL, "material given to a non-elastic operator");
+  FEM_TRY(check_vec(lam, "lambda"));
+  FEM_TRY(check_vec(mu, "mu"));
+  FEM_TRY(set_device(op->mesh->device));
+  const Grid& g = op->mesh->g;
+  const int64_t need0 = std::max<int64_t>(g.k0 - 1, 0);
+  const int64_t need1 = std::min<int64_t>(g.k1 - 1, g.nz - 1);  // inclusive
+  if (layer_begin < 0 || n_layers < 1 || layer_begin > need0 || layer_begin + n_layers - 1 < need1)
+    return fail(FEM_EINVAL, "material layers [%lld, %lld) do not cover the needed [%lld, %lld]",
+                (long long)layer_begin, (long long)(layer_begin + n_layers), (long long)need0, (long long)need1);
+  const int64_t nl = need1 - need0 + 1, nxy = g.nx * g.ny, cnt = nl * nxy;
+  if (op->mat_layers != nl) {
+    cudaFree(op->lam); cudaFree(op->mu);
+    op->lam = op->mu = nullptr;
+    FEM_TRY(dalloc(&op->lam, cnt));
+    FEM_TRY(dalloc(&op->mu, cnt));
+  }
+  const size_t off = (size_t)(need0 - layer_begin) * nxy;
+  const cudaMemcpyKind kl = is_device_ptr(lam) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const cudaMemcpyKind km = is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CUDA_TRY(cudaMemcpy(op->lam, lam + off, cnt * sizeof(double), kl));
+  CUDA_TRY(cudaMemcpy(op->mu, mu + off, cnt * sizeof(double), km));
+  op->mat_layer0 = need0;
+  op->mat_layers = nl;
+  CUDA_TRY(cudaMemset(op->bad, 0, sizeof(unsigned long long)));
+  CUDA_TRY(launch_check_material(op->lam, op->mu, cnt, op->bad, 0, op->mesh->sm_count));
+  unsigned long long bad = 0;
+  CUDA_TRY(cudaMemcpy(&bad, op->bad, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad) {
+    op->has_mat = false;
+    return fail(FEM_EMATERIAL, "%llu cells violate mu > 0, lambda + 2 mu / 3 >= 0 (S:249)", bad);
+  }
+  op->has_mat = true;
+  op->cg_active = false;
+  return FEM_OK;
+}
+
+int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(check_vec(x, "x"));
+  FEM_TRY(check_vec(y, "y"));
+  if ((const void*)x == (const void*)y) return fail(FEM_EINVAL, "x and y alias");
+  if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
+  FEM_TRY(set_device(op->mesh->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool xd = is_device_ptr(x), yd = is_device_ptr(y);
+  if (xd && yd) return apply_device(op, x, y, s);
+  FEM_TRY(ensure_stage(op));
+  const size_t bytes = op->n_local * sizeof(double);
+  const double* xs = x;
+  if (!xd) {
+    CUDA_TRY(cudaMemcpyAsync(op->stage_a, x, bytes, cudaMemcpyHostToDevice, s));
+    xs = op->stage_a;
+  }
+  double* ys = yd ? y : op->stage_b;
+  FEM_TRY(apply_device(op, xs, ys, s));
+  if (!yd) {
+    CUDA_TRY(cudaMemcpyAsync(y, ys, bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  return FEM_OK;
+}
+
+int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void* stream) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(check_vec(a, "a"));
+  FEM_TRY(check_vec(b, "b"));
+  if (!result) return fail(FEM_EINVAL, "result is NULL");
+  FEM_TRY(set_device(op->mesh->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool ad = is_device_ptr(a), bd = is_device_ptr(b);
+  const double *as = a, *bs = b;
+  if (!ad || !bd) {
+    FEM_TRY(ensure_stage(op));
+    const size_t bytes = op->n_local * sizeof(double);
+    if (!ad) { CUDA_TRY(cudaMemcpyAsync(op->stage_a, a, bytes, cudaMemcpyHostToDevice, s)); as = op->stage_a; }
+    if (!bd) { CUDA_TRY(cudaMemcpyAsync(op->stage_b, b, bytes, cudaMemcpyHostToDevice, s)); bs = op->stage_b; }
+  }
+  return dot_device(op, as, bs, s, result);
+}
+
+// ---- CG -----------------------------------------------------------------------------------
+static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
+  fem_mesh_s* m = op->mesh;
+  double* p = op->p_ext + op->plane_dofs;  // owned part
+  FEM_TRY(halo(op, p, op->p_ext, p + op->n_local, s));
+  PlaneSrc src{p, m->rank > 0 ? op->p_ext : nullptr, m->rank < m->nranks - 1 ? p + op->n_local : nullptr};
+  if (timed) {
+    if (op->ev_used + 2 > op->ev.size()) {
+      for (int t = 0; t < 64; ++t) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        op->ev.push_back(e);
+      }
+    }
+    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used], s));
+  }
+  FEM_TRY(launch_apply(op, src, op->q, 1, s));
+  if (timed) {
+    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used + 1], s));
+    op->ev_used += 2;
+  }
+  FEM_TRY(allreduce1(op, &op->sc->pq, s));
+  cudaError_t e = launch_cg_update(op->cg_x, op->r, p, op->q, op->n_local, op->sc, op->red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
+  FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
+  e = launch_cg_pupdate(op->r, p, op->n_local, op->sc, op->red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "pupdate launch: %s", cudaGetErrorString(e));
+  return FEM_OK;
+}
+
+static int capture(fem_op_s* op, int iters, cudaStream_t s, cudaGraphExec_t* out) {
+  // capture on a private stream (legacy stream 0 cannot be captured)
+  cudaStream_t cs;
+  CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  const int64_t before = g_launches.load();
+  int st = FEM_OK;
+  for (int t = 0; t < iters && st == FEM_OK; ++t) st = cg_iteration_body(op, cs, false);
+  g_launches.store(before);  // captured launches are counted at replay
+  cudaGraph_t graph;
+  cudaError_t e = cudaStreamEndCapture(cs, &graph);
+  if (st != FEM_OK) {
+    if (e == cudaSuccess) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+    return st;
+  }
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return fail(FEM_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(e));
+  }
+  e = cudaGraphInstantiate(out, graph, 0);
+  cudaGraphDestroy(graph);
+  cudaStreamDestroy(cs);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+  (void)s;
+  return FEM_OK;
+}
+
+static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, int maxit, cudaStream_t s) {
+  fem_mesh_s* m = op->mesh;
+  double* p = op->p_ext + op->plane_dofs;
+  FEM_TRY(apply_device(op, x, op->q, s));  // q = A x0
+  cudaError_t e = launch_cg_init(b, op->q, op->r, p, op->n_local, op->sc, op->red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "init launch: %s", cudaGetErrorString(e));
+  FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
+  e = launch_cg_finish_init(op->sc, tol, maxit, s);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "init launch: %s", cudaGetErrorString(e));
+  op->cg_b = b;
+  op->cg_x = x;
+  op->cg_active = true;
+  if (op->graph_x != x || op->graph_b != b) {
+    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
+    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
+    op->graph_x = x;
+    op->graph_b = b;
+  }
+  return FEM_OK;
+}
+
+static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
+  const int per_iter_launches = 3;
+  if (op->time_apply || !op->use_graph) {
+    for (int t = 0; t < iters; ++t) FEM_TRY(cg_iteration_body(op, s, op->time_apply != 0));
+    return FEM_OK;
+  }
+  const int N = 8;
+  if (!op->graph1) FEM_TRY(capture(op, 1, s, &op->graph1));
+  if (iters >= N && !op->graphN) FEM_TRY(capture(op, N, s, &op->graphN));
+  int left = iters;
+  while (left >= N) {
+    CUDA_TRY(cudaGraphLaunch(op->graphN, s));
+    add_launches(N * per_iter_launches);
+    left -= N;
+  }
+  while (left-- > 0) {
+    CUDA_TRY(cudaGraphLaunch(op->graph1, s));
+    add_launches(per_iter_launches);
+  }
+  return FEM_OK;
+}
+
+static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
+  CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const CgScalars h = *op->sc_host;
+  int status = (h.done == 2) ? FEM_EBREAKDOWN : FEM_OK;
+  if (info) {
+    info->iterations = h.it;
+    info->converged = (h.done == 1) || (h.rr == 0.0) || (h.rr <= h.stop_rr);
+    info->breakdown_iter = h.breakdown_iter;
+    info->status = status;
+    info->r0_norm = std::sqrt(h.rr0);
+    info->r_norm = std::sqrt(h.rr);
+    // true residual ||b - A x||
+    FEM_TRY(apply_device(op, op->cg_x, op->q, s));
+    cudaError_t e = launch_sub(op->cg_b, op->q, op->r, op->n_local, s, op->mesh->sm_count);
+    if (e != cudaSuccess) return fail(FEM_ECUDA, "sub launch: %s", cudaGetErrorString(e));
+    double tr = 0.0;
+    FEM_TRY(dot_device(op, op->r, op->r, s, &tr));
+    info->true_r_norm = std::sqrt(tr);
+    op->cg_active = false;  // r was overwritten
+  }
+  if (status == FEM_EBREAKDOWN) return fail(FEM_EBREAKDOWN, "CG breakdown at iteration %d (p.Ap <= 0 or non-finite)", h.breakdown_iter);
+  return FEM_OK;
+}
+
+int fem_cg_begin(fem_op_t op, const double* b, double* x, double tol, int32_t maxit, void* stream) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(check_vec(b, "b"));
+  FEM_TRY(check_vec(x, "x"));
+  if ((const void*)b == (const void*)x) return fail(FEM_EINVAL, "b and x alias");
+  if (!(tol >= 0.0) || !std::isfinite(tol)) return fail(FEM_EINVAL, "tol must be finite and >= 0");
+  if (maxit < 0) return fail(FEM_EINVAL, "maxit must be >= 0");
+  if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
+  if (!is_device_ptr(b) || !is_device_ptr(x)) return fail(FEM_EINVAL, "fem_cg_begin needs device pointers");
+  FEM_TRY(set_device(op->mesh->device));
+  return cg_begin_dev(op, b, x, tol, maxit, (cudaStream_t)stream);
+}
+
+int fem_cg_iterate(fem_op_t op, int32_t iters, void* stream) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  if (!op->cg_active) return fail(FEM_ESTATE, "fem_cg_begin not called");
+  if (iters < 0) return fail(FEM_EINVAL, "iters < 0");
+  FEM_TRY(set_device(op->mesh->device));
+  return cg_iterate_dev(op, iters, (cudaStream_t)stream);
+}
+
+int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  if (!op->cg_active) return fail(FEM_ESTATE, "fem_cg_begin not called");
+  FEM_TRY(set_device(op->mesh->device));
+  fem_cg_info tmp;
+  return cg_end_dev(op, info ? info : &tmp, (cudaStream_t)stream);
+}
+
+int fem_cg_solve(fem_op_t op, const double* b, double* x, double tol, int32_t maxit,
+                 fem_cg_info* info, void* stream) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(check_vec(b, "b"));
+  FEM_TRY(check_vec(x, "x"));
+  if ((const void*)b == (const void*)x) return fail(FEM_EINVAL, "b and x alias");
+  if (!(tol >= 0.0) || !std::isfinite(tol)) return fail(FEM_EINVAL, "tol must be finite and >= 0");
+  if (maxit < 0) return fail(FEM_EINVAL, "maxit must be >= 0");
+  if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
+  FEM_TRY(set_device(op->mesh->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool bd = is_device_ptr(b), xd = is_device_ptr(x);
+  const size_t bytes = op->n_local * sizeof(double);
+  const double* bs = b;
+  double* xs = x;
+  if (!bd || !xd) FEM_TRY(ensure_stage(op));
+  if (!bd) { CUDA_TRY(cudaMemcpyAsync(op->stage_b, b, bytes, cudaMemcpyHostToDevice, s)); bs = op->stage_b; }
+  if (!xd) { CUDA_TRY(cudaMemcpyAsync(op->stage_a, x, bytes, cudaMemcpyHostToDevice, s)); xs = op->stage_a; }
+  FEM_TRY(cg_begin_dev(op, bs, xs, tol, maxit, s));
+  int done_it = 0;
+  const int chunk = std::max(1, op->check_every);
+  while (done_it < maxit) {
+    const int n = std::min(chunk, maxit - done_it);
+    FEM_TRY(cg_iterate_dev(op, n, s));
+    done_it += n;
+    CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (op->sc_host->done) break;
+  }
+  fem_cg_info tmp;
+  int st = cg_end_dev(op, info ? info : &tmp, s);
+  if (!xd) {
+    CUDA_TRY(cudaMemcpyAsync(x, xs, bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  return st;
+}
+
+int fem_set_option(fem_op_t op, const char* key, int64_t value) {
+  if (!op || !key) return fail(FEM_EINVAL, "op/key is NULL");
+  if (!std::strcmp(key, "use_graph")) op->use_graph = value != 0;
+  else if (!std::strcmp(key, "check_every")) {
+    if (value < 1) return fail(FEM_EINVAL, "check_every must be >= 1");
+    op->check_every = (int)value;
+  } else if (!std::strcmp(key, "time_apply")) op->time_apply = value != 0;
+  else return fail(FEM_EINVAL, "unknown option '%s'", key);
+  return FEM_OK;
+}
+
+int fem_apply_time(fem_op_t op, double* total_ms, int64_t* count) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(set_device(op->mesh->device));
+  double tot = 0.0;
+  int64_t n = 0;
+  if (op->ev_used) CUDA_TRY(cudaEventSynchronize(op->ev[op->ev_used - 1]));
+  for (size_t t = 0; t + 1 < op->ev_used; t += 2) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, op->ev[t], op->ev[t + 1]));
+    tot += ms;
+    ++n;
+  }
+  op->ev_used = 0;
+  if (total_ms) *total_ms = tot;
+  if (count) *count = n;
+  return FEM_OK;
+}
+
+void fem_op_destroy(fem_op_t op) { op_free(op); }
+
+// ---- CSR ----------------------------------------------------------------------------------
+int fem_csr_create(fem_op_t op, fem_csr_t* out) {
+  if (!op || !out) return fail(FEM_EINVAL, "op/out is NULL");
+  *out = nullptr;
+  if (op->mesh->nranks != 1) return fail(FEM_EUNSUPPORTED, "CSR baseline is single-rank only");
+  if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
+  FEM_TRY(set_device(op->mesh->device));
+  const Grid& g = op->mesh->g;
+  const int64_t nrows = op->n_global;
+  if (nrows >= 2147483647LL) return fail(FEM_EOVERFLOW, "CSR column index exceeds int32");
+  auto* c = new (std::nothrow) fem_csr_s();
+  if (!c) return fail(FEM_ENOMEM, "host allocation failed");
+  c->comps = op->comps;
+  c->device = op->mesh->device;
+  c->sm_count = op->mesh->sm_count;
+  c->nrows = nrows;
+  int st = dalloc(&c->rowptr, nrows + 1);
+  if (st) { delete c; return st; }
+  cudaError_t e = launch_csr_rowcount(op->comps, op->bc, g, c->rowptr, 0);
+  if (e != cudaSuccess) { fem_csr_destroy(c); return fail(FEM_ECUDA, "csr rowcount: %s", cudaGetErrorString(e)); }
+  int64_t nnz = 0;
+  e = cudaMemcpy(&nnz, c->rowptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) { fem_csr_destroy(c); return fail(FEM_ECUDA, "csr nnz: %s", cudaGetErrorString(e)); }
+  c->nnz = nnz;
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  const double need = (double)nnz * 12.0;
+  if (need > (double)fr * 0.95) {
+    fem_csr_destroy(c);
+    return fail(FEM_ENOMEM, "CSR needs %.1f GB, %.1f GB free", need / 1e9, fr / 1e9);
+  }
+  if ((st = dalloc(&c->col, nnz)) || (st = dalloc(&c->val, nnz))) { fem_csr_destroy(c); return st; }
+  e = launch_csr_fill(op->kind, op->bc, g, op->lam, op->mu, c->rowptr, c->col, c->val, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { fem_csr_destroy(c); return fail(FEM_ECUDA, "csr fill: %s", cudaGetErrorString(e)); }
+  *out = c;
+  return FEM_OK;
+}
+
+int fem_csr_info(fem_csr_t c, int64_t* nrows, int64_t* nnz, int64_t* bytes) {
+  if (!c) return fail(FEM_EINVAL, "csr is NULL");
+  if (nrows) *nrows = c->nrows;
+  if (nnz) *nnz = c->nnz;
+  if (bytes) *bytes = c->nnz * 12 + (c->nrows + 1) * 8;
+  return FEM_OK;
+}
+
+int fem_csr_apply(fem_csr_t c, const double* x, double* y, void* stream) {
+  if (!c) return fail(FEM_EINVAL, "csr is NULL");
+  FEM_TRY(check_vec(x, "x"));
+  FEM_TRY(check_vec(y, "y"));
+  if ((const void*)x == (const void*)y) return fail(FEM_EINVAL, "x and y alias");
+  if (!is_device_ptr(x) || !is_device_ptr(y)) return fail(FEM_EINVAL, "fem_csr_apply needs device pointers");
+  FEM_TRY(set_device(c->device));
+  cudaError_t e = launch_csr_spmv(c->comps, c->nrows, c->rowptr, c->col, c->val, x, y,
+                                  (cudaStream_t)stream, c->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "spmv launch: %s", cudaGetErrorString(e));
+  return FEM_OK;
+}
+
+void fem_csr_destroy(fem_csr_t c) {
+  if (!c) return;
+  set_device(c->device);
+  cudaFree(c->rowptr);
+  cudaFree(c->col);
+  cudaFree(c->val);
+  delete c;
+}
+
+}  // extern "C"

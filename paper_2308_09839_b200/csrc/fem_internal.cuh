@@ -1,0 +1,145 @@
+// fem_internal.cuh -- shared device/host declarations of the CUDA path (libfem.so).
+// Not part of the ABI.  Independent of oracle/ (no shared code, tables or constants).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fem {
+
+// Geometry of the rank-local problem, in GLOBAL node-plane indices.
+struct Grid {
+  int64_t nx, ny, nz;    // cells per direction (global)
+  double h;              // cell side
+  int64_t k0, k1;        // owned node planes [k0, k1)
+  int64_t plane;         // nodes per plane = (nx+1)(ny+1)
+};
+
+// Source of a node-plane-indexed vector: owned planes at `main` (plane k at main + (k-k0)*plane*c),
+// optional ghost planes below/above (multi-GPU halo), others are outside the domain.
+struct PlaneSrc {
+  const double* main;
+  const double* lo;  // plane k0-1 (may be null: outside domain or not exchanged)
+  const double* hi;  // plane k1
+};
+
+// Device scalars of one CG solve (rank-global after the allreduce steps).
+struct CgScalars {
+  double rr;        // r.r of the current iterate
+  double pq;        // p.Ap (global after allreduce)
+  double rr_new;    // r.r after the update (global after allreduce)
+  double rr0;       // r0.r0
+  double stop_rr;   // tol^2 * rr0
+  double pad0;
+  int32_t done;     // 0 running, 1 converged, 2 breakdown, 3 maxit reached
+  int32_t it;       // iterations completed
+  int32_t maxit;
+  int32_t breakdown_iter;
+};
+
+// Last-block reduction workspace: per-CTA partials + ticket counter.
+struct Reduce {
+  double* partials;       // >= max CTAs of any reducing launch
+  unsigned int* ticket;   // zero-initialised, reset by the last block
+  int64_t capacity;
+};
+
+constexpr int kMaxCtas = 1 << 16;
+
+// ---- launchers (return cudaError_t of the launch) -----------------------------------------
+// mode: 0 plain apply (y = A_c x), 1 CG apply (also pq partial -> sc->pq; skips if sc->done)
+cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, double* y, int mode,
+                           CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
+cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double* lam, const double* mu,
+                           int64_t mat_layer0, double* y, int mode, CgScalars* sc, Reduce red,
+                           cudaStream_t s, int sm_count);
+// CG vector kernels (n = owned DOFs)
+cudaError_t launch_cg_init(const double* b, const double* ax, double* r, double* p, int64_t n,
+                           CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
+cudaError_t launch_cg_finish_init(CgScalars* sc, double tol, int maxit, cudaStream_t s);
+cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* q, int64_t n,
+                             CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
+cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* sc, Reduce red,
+                              cudaStream_t s, int sm_count);
+// deterministic dot -> *out (device)
+cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
+                       cudaStream_t s, int sm_count);
+// residual helper: out = b - ax (for true residual)
+cudaError_t launch_sub(const double* b, const double* ax, double* out, int64_t n, cudaStream_t s,
+                       int sm_count);
+// material validation: count of invalid cells -> *bad (device int64)
+cudaError_t launch_check_material(const double* lam, const double* mu, int64_t n,
+                                  unsigned long long* bad, cudaStream_t s, int sm_count);
+
+// CSR baseline
+cudaError_t launch_csr_rowcount(int comps, int bc, const Grid& g, int64_t* rowptr, cudaStream_t s);
+cudaError_t launch_csr_fill(int kind, int bc, const Grid& g, const double* lam, const double* mu,
+                            const int64_t* rowptr, int32_t* col, double* val, cudaStream_t s);
+cudaError_t launch_csr_spmv(int comps, int64_t nrows, const int64_t* rowptr, const int32_t* col,
+                            const double* val, const double* x, double* y, cudaStream_t s,
+                            int sm_count);
+
+void add_launches(int64_t n);
+
+}  // namespace fem
+
+// ---- small device helpers -------------------------------------------------------------------
+#ifdef __CUDACC__
+namespace fem {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed tree); result valid in thread 0. `sh` >= 32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int wid = tid >> 5;
+  const int nw = (blockDim.x * blockDim.y * blockDim.z + 31) >> 5;
+  // use linear lane from tid so 2-D blocks work
+  v = warp_sum(v);
+  __syncthreads();
+  if ((tid & 31) == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = (tid < nw) ? sh[tid] : 0.0;
+    r = warp_sum(r);
+  }
+  (void)lane;
+  return r;
+}
+
+// Last-block-done finalisation: every block writes its partial; the last block to arrive sums
+// the partials in block order (deterministic) and returns true in thread 0 with *total set.
+__device__ __forceinline__ bool last_block_reduce(double partial, Reduce red, double* sh,
+                                                  double* total) {
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nthr = blockDim.x * blockDim.y * blockDim.z;
+  const unsigned int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned int nblk = gridDim.x * gridDim.y * gridDim.z;
+  __shared__ unsigned int s_is_last;
+  if (tid == 0) {
+    red.partials[bid] = partial;
+    __threadfence();
+    unsigned int t = atomicAdd(red.ticket, 1u);
+    s_is_last = (t == nblk - 1);
+  }
+  __syncthreads();
+  if (!s_is_last) return false;
+  __threadfence();
+  double v = 0.0;
+  // fixed assignment of partials to threads, fixed tree -> bitwise deterministic
+  for (unsigned int b = tid; b < nblk; b += nthr) v += ((volatile double*)red.partials)[b];
+  double s = block_sum(v, sh);
+  if (tid == 0) {
+    *total = s;
+    *red.ticket = 0u;
+  }
+  return tid == 0;
+}
+
+}  // namespace fem
+#endif

@@ -1,0 +1,185 @@
+// kernels_cg.cu -- CG vector kernels (Table 4 rows) and the deterministic dot
+// ("the dot product ... implementation has dramatic impact").
+//
+// Per iteration, with p.Ap fused into the apply kernel's epilogue:
+//   apply   : q = A_c p,  pq = p.q            (kernels_laplace / kernels_elastic, mode 1)
+//   update  : alpha = rr/pq; x += alpha p; r -= alpha q; rr' = r.r     (48 B/DOF)
+//   pupdate : beta = rr'/rr; p = r + beta p; rr = rr'; convergence     (24 B/DOF)
+// Scalars live in device memory (CgScalars); kernels read them at start, so the iteration is
+// host-sync free and CUDA-graph capturable.  Every dot is a warp-shuffle + block tree + a
+// last-block-done pass summing the per-CTA partials in block order: bitwise reproducible for
+// a fixed launch configuration, no floating-point atomics.
+#include <algorithm>
+
+#include "fem_internal.cuh"
+
+namespace fem {
+
+constexpr int kVecThreads = 256;
+
+static inline unsigned vec_blocks(int64_t n, int sm_count) {
+  int64_t want = (n + kVecThreads * 4 - 1) / (kVecThreads * 4);
+  int64_t cap = (int64_t)sm_count * 8;
+  return (unsigned)std::max<int64_t>(1, std::min(want, cap));
+}
+
+__global__ void __launch_bounds__(kVecThreads) cg_init_kernel(const double* __restrict__ b,
+                                                              const double* __restrict__ ax,
+                                                              double* __restrict__ r,
+                                                              double* __restrict__ p, int64_t n,
+                                                              CgScalars* sc, Reduce red) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double ri = b[i] - ax[i];
+    r[i] = ri;
+    p[i] = ri;
+    acc = fma(ri, ri, acc);
+  }
+  double bs = block_sum(acc, sh);
+  double tot;
+  if (last_block_reduce(bs, red, sh, &tot)) sc->rr_new = tot;
+}
+
+__global__ void cg_finish_init_kernel(CgScalars* sc, double tol, int maxit) {
+  const double rr = sc->rr_new;
+  sc->rr = rr;
+  sc->rr0 = rr;
+  sc->stop_rr = tol * tol * rr;
+  sc->pq = 0.0;
+  sc->it = 0;
+  sc->maxit = maxit;
+  sc->breakdown_iter = -1;
+  sc->done = (rr == 0.0) ? 1 : (maxit <= 0 ? 3 : 0);
+}
+
+__global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restrict__ x,
+                                                                double* __restrict__ r,
+                                                                const double* __restrict__ p,
+                                                                const double* __restrict__ q,
+                                                                int64_t n, CgScalars* sc,
+                                                                Reduce red) {
+  __shared__ double sh[32];
+  if (sc->done) return;
+  const double pq = sc->pq;
+  if (!(pq > 0.0) || !isfinite(pq)) {  // breakdown: same decision in every block
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc->breakdown_iter = sc->it;
+      sc->done = 2;
+    }
+    return;
+  }
+  const double alpha = sc->rr / pq;
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    acc = fma(ri, ri, acc);
+  }
+  double bs = block_sum(acc, sh);
+  double tot;
+  if (last_block_reduce(bs, red, sh, &tot)) sc->rr_new = tot;
+}
+
+__global__ void __launch_bounds__(kVecThreads) cg_pupdate_kernel(const double* __restrict__ r,
+                                                                 double* __restrict__ p, int64_t n,
+                                                                 CgScalars* sc, Reduce red) {
+  __shared__ double sh[32];
+  if (sc->done) return;
+  const double rr_new = sc->rr_new;
+  const double beta = rr_new / sc->rr;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    p[i] = fma(beta, p[i], r[i]);
+  double tot;
+  if (last_block_reduce(0.0, red, sh, &tot)) {
+    // all blocks have read rr / rr_new: advance the recurrence
+    sc->rr = rr_new;
+    const int it = sc->it + 1;
+    sc->it = it;
+    if (rr_new == 0.0 || rr_new <= sc->stop_rr)
+      sc->done = 1;
+    else if (it >= sc->maxit)
+      sc->done = 3;
+  }
+}
+
+__global__ void __launch_bounds__(kVecThreads) dot_kernel(const double* __restrict__ a,
+                                                          const double* __restrict__ b, int64_t n,
+                                                          double* out, Reduce red) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    acc = fma(a[i], b[i], acc);
+  double bs = block_sum(acc, sh);
+  double tot;
+  if (last_block_reduce(bs, red, sh, &tot)) *out = tot;
+}
+
+__global__ void sub_kernel(const double* __restrict__ b, const double* __restrict__ ax,
+                           double* __restrict__ out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = b[i] - ax[i];
+}
+
+__global__ void check_material_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
+                                      int64_t n, unsigned long long* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long cnt = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double l = lam[i], m = mu[i];
+    // mu > 0 and lambda + 2 mu / 3 >= 0, finite
+    const bool ok = isfinite(l) && isfinite(m) && m > 0.0 && (l + 2.0 * m / 3.0) >= 0.0;
+    cnt += ok ? 0 : 1;
+  }
+  if (cnt) atomicAdd(bad, cnt);  // validation counter only (not on the apply path)
+}
+
+cudaError_t launch_cg_init(const double* b, const double* ax, double* r, double* p, int64_t n,
+                           CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  cg_init_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(b, ax, r, p, n, sc, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_finish_init(CgScalars* sc, double tol, int maxit, cudaStream_t s) {
+  cg_finish_init_kernel<<<1, 1, 0, s>>>(sc, tol, maxit);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* q, int64_t n,
+                             CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  cg_update_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* sc, Reduce red,
+                              cudaStream_t s, int sm_count) {
+  cg_pupdate_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(r, p, n, sc, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
+                       cudaStream_t s, int sm_count) {
+  dot_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(a, b, n, out, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_sub(const double* b, const double* ax, double* out, int64_t n, cudaStream_t s,
+                       int sm_count) {
+  sub_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(b, ax, out, n);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_check_material(const double* lam, const double* mu, int64_t n,
+                                  unsigned long long* bad, cudaStream_t s, int sm_count) {
+  check_material_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(lam, mu, n, bad);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace fem

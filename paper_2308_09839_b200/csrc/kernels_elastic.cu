@@ -1,0 +1,247 @@
+// kernels_elastic.cu -- isotropic linear elasticity apply y = A_c u with cell-wise lambda_e, mu_e
+// (Eq. 9 / Alg. 1), FP64.
+//
+// B200 form.  On the uniform box J = (h/2) I, so the 2x2x2-Gauss element
+// operator of Eq. 6 equals the exact integral and is diagonalised, up to a 3x3 / 2x2 coupling,
+// by the Hadamard ("modal") basis of the trilinear space: u(xi) = sum_m c_m xi^m over the eight
+// monomials m in {1, x, y, xy, z, xz, yz, xyz}.  Per cell:
+//   1. forward transform c' = H^T u^e: butterflies in x, y on each node face (the face of plane
+//      k+1 is computed once and carried to the next cell layer), then z;
+//   2. modal stress g = G(c'): the strain modes of grad u (Alg. 1 "gradient of input variable"),
+//      sigma = lambda tr eps I + 2 mu eps and the w_q detJ scaling fold into 9 scalar
+//      products per cell (lambda_e, mu_e premultiplied by h/16);
+//   3. inverse transform v^e = H g (Alg. 1 "P grad phi_i" steps) into the two faces of the cell.
+// Scatter without atomics: the bottom face of cell layer k is added to the top face of
+// layer k-1 (register carry), the four cells sharing a node in xy exchange corner values through
+// shared memory, and each node is written exactly once.  Summation order per node is fixed
+// (independent of the tiling and of the z-chunk / slab boundaries).
+#include "kernels_common.cuh"
+
+namespace fem {
+
+namespace {
+// per-component face transform of 4 node values (x fastest, then y):
+// returns (sum, y-diff, x-diff, xy) in the unnormalised Hadamard basis
+struct Face {
+  double s, y, x, xy;
+};
+__device__ __forceinline__ Face face_fwd(double u00, double u10, double u01, double u11) {
+  const double s0 = u00 + u10, d0 = u10 - u00, s1 = u01 + u11, d1 = u11 - u01;
+  return Face{s0 + s1, s1 - s0, d0 + d1, d1 - d0};
+}
+}  // namespace
+
+template <int TY, int S>
+__global__ void __launch_bounds__(32 * TY, 1)
+    elastic_kernel(Grid g, PlaneSrc x, const double* __restrict__ lam, const double* __restrict__ mu,
+                   int64_t mat_layer0, double* __restrict__ y, int bc, int mode, int64_t kchunk,
+                   CgScalars* sc, Reduce red) {
+  constexpr int TX = 32;
+  constexpr int NT = TX * TY;
+  constexpr int ROWS = TY + 1;     // node rows j0-1 .. j0+TY-1
+  constexpr int COLS = TX + 1;     // node cols i0-1 .. i0+TX-1
+  constexpr int PITCH = COLS * 3 + 1;
+  constexpr int SLOT = ROWS * PITCH;
+  extern __shared__ __align__(16) double smem[];
+  double* ring = smem;                      // S * SLOT
+  double* acc = smem + S * SLOT;            // [4][TY][TX][3]
+  __shared__ double red_sh[32];
+
+  if (mode == 1 && sc->done) return;
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = tx + TX * ty;
+  // output tile: nodes i0 .. i0+TX-2, j0 .. j0+TY-2; thread (tx,ty) owns cell (i0-1+tx, j0-1+ty)
+  const int64_t i0 = (int64_t)blockIdx.x * (TX - 1);
+  const int64_t j0 = (int64_t)blockIdx.y * (TY - 1);
+  const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
+  const int64_t ke = min(g.k1, kb + kchunk);
+  const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
+  const bool cell_xy = ci >= 0 && ci < g.nx && cj >= 0 && cj < g.ny;
+  const double hs = g.h * (1.0 / 16.0);
+  const int64_t nxy = g.nx * g.ny;
+
+  // planes kb-1 .. ke are needed (cell layers kb-1 .. ke-1)
+  const int64_t pfirst = kb - 1;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    stage_plane<ROWS, COLS, 3, PITCH, NT>(ring + s * SLOT, x, g, pfirst + s, i0 - 1, j0 - 1, bc, tid);
+    cp_async_commit();
+  }
+
+  Face fb[3];     // face transform of the bottom plane of the current cell layer
+  double cb[12];  // carried top-face contribution of the previous cell layer (4 modes x 3 comps)
+#pragma unroll
+  for (int t = 0; t < 12; ++t) cb[t] = 0.0;
+
+  // material of the first cell layer
+  auto load_mat = [&](int64_t k, double& L, double& M) {
+    if (cell_xy && k >= 0 && k < g.nz) {
+      const int64_t e = (k - mat_layer0) * nxy + cj * g.nx + ci;
+      L = __ldg(lam + e) * hs;
+      M = __ldg(mu + e) * hs;
+    } else {
+      L = 0.0; M = 0.0;
+    }
+  };
+  double Ln, Mn;
+  load_mat(pfirst, Ln, Mn);
+
+  double pq = 0.0;
+  for (int64_t p = pfirst; p <= ke; ++p) {
+    // iteration p: plane p is available; cell layer p-1 lies between planes p-1 and p
+    const int slot = (int)((p - pfirst) % S);
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    {
+      const int64_t pn = p + S - 1;
+      const int sn = (int)((pn - pfirst) % S);
+      if (pn <= ke) stage_plane<ROWS, COLS, 3, PITCH, NT>(ring + sn * SLOT, x, g, pn, i0 - 1, j0 - 1, bc, tid);
+      cp_async_commit();
+    }
+    const double* sp = ring + slot * SLOT;
+    Face ft[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double* r0 = sp + ty * PITCH;
+      const double* r1 = sp + (ty + 1) * PITCH;
+      ft[c] = face_fwd(r0[tx * 3 + c], r0[(tx + 1) * 3 + c], r1[tx * 3 + c], r1[(tx + 1) * 3 + c]);
+    }
+    if (p == pfirst) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) fb[c] = ft[c];
+      continue;
+    }
+    // ---- cell layer k = p-1 ----
+    const double L0 = Ln, M0 = Mn;
+    if (p < ke) load_mat(p, Ln, Mn);  // prefetch next layer
+    // modal coefficients (unnormalised): component u=0, v=1, w=2
+    // one = fb.s+ft.s (unused), x = ds, y = sd, xy = dd, z = ss_z, xz, yz, xyz
+    double ux = fb[0].x + ft[0].x, uy = fb[0].y + ft[0].y, uxy = fb[0].xy + ft[0].xy;
+    double uz = ft[0].s - fb[0].s, uxz = ft[0].x - fb[0].x, uyz = ft[0].y - fb[0].y, uxyz = ft[0].xy - fb[0].xy;
+    double vx = fb[1].x + ft[1].x, vy = fb[1].y + ft[1].y, vxy = fb[1].xy + ft[1].xy;
+    double vz = ft[1].s - fb[1].s, vxz = ft[1].x - fb[1].x, vyz = ft[1].y - fb[1].y, vxyz = ft[1].xy - fb[1].xy;
+    double wx = fb[2].x + ft[2].x, wy = fb[2].y + ft[2].y, wxy = fb[2].xy + ft[2].xy;
+    double wz = ft[2].s - fb[2].s, wxz = ft[2].x - fb[2].x, wyz = ft[2].y - fb[2].y, wxyz = ft[2].xy - fb[2].xy;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fb[c] = ft[c];
+
+    // modal stress (DESIGN.md §5.2 table): weights 1 (linear modes), 1/3 (bilinear), 1/9 (trilinear)
+    const double M2 = M0 + M0;
+    const double S0 = ux + vy + wz;
+    const double LS0 = L0 * S0;
+    const double gux = fma(M2, ux, LS0), gvy = fma(M2, vy, LS0), gwz = fma(M2, wz, LS0);
+    const double tuv = M0 * (uy + vx), tuw = M0 * (uz + wx), tvw = M0 * (vz + wy);
+    const double guy = tuv, gvx = tuv, guz = tuw, gwx = tuw, gvz = tvw, gwy = tvw;
+    const double L1 = L0 * (1.0 / 3.0), M1 = M0 * (1.0 / 3.0);
+    const double Sxi = vxy + wxz, Seta = uxy + wyz, Szeta = uxz + vyz;
+    const double LSxi = L1 * Sxi, LSeta = L1 * Seta, LSzeta = L1 * Szeta;
+    const double guxy = fma(M0, uxy, LSeta), gwyz = fma(M0, wyz, LSeta);
+    const double gvxy = fma(M0, vxy, LSxi), gwxz = fma(M0, wxz, LSxi);
+    const double guxz = fma(M0, uxz, LSzeta), gvyz = fma(M0, vyz, LSzeta);
+    const double T = uyz + vxz + wxy;
+    const double guyz = M1 * (T + uyz), gvxz = M1 * (T + vxz), gwxy = M1 * (T + wxy);
+    const double K3 = fma(4.0, M0, L0) * (1.0 / 9.0);
+    const double guxyz = K3 * uxyz, gvxyz = K3 * vxyz, gwxyz = K3 * wxyz;
+
+    // inverse z: face mode f at bottom = g_f - g_fz, top = g_f + g_fz (g_1 = 0)
+    // bottom face of this cell, plus the carried top face of layer k-1 -> face at plane p-1
+    double F[12];
+    {
+      const double gx[3] = {gux, gvx, gwx}, gy[3] = {guy, gvy, gwy}, gxy[3] = {guxy, gvxy, gwxy};
+      const double gz[3] = {guz, gvz, gwz}, gxz[3] = {guxz, gvxz, gwxz}, gyz[3] = {guyz, gvyz, gwyz};
+      const double gxyz[3] = {guxyz, gvxyz, gwxyz};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        F[4 * c + 0] = cb[4 * c + 0] - gz[c];
+        F[4 * c + 1] = cb[4 * c + 1] + (gx[c] - gxz[c]);
+        F[4 * c + 2] = cb[4 * c + 2] + (gy[c] - gyz[c]);
+        F[4 * c + 3] = cb[4 * c + 3] + (gxy[c] - gxyz[c]);
+        cb[4 * c + 0] = gz[c];
+        cb[4 * c + 1] = gx[c] + gxz[c];
+        cb[4 * c + 2] = gy[c] + gyz[c];
+        cb[4 * c + 3] = gxy[c] + gxyz[c];
+      }
+    }
+    const int64_t q = p - 1;  // node plane whose values are now complete in xy-corner form
+    if (q >= kb) {
+      // expand face modes to the 4 corner nodes of this cell column, exchange via smem
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double G1 = F[4 * c + 0], Gx = F[4 * c + 1], Gy = F[4 * c + 2], Gxy = F[4 * c + 3];
+        const double es = G1 - Gy, ed = Gx - Gxy, fs = G1 + Gy, fd = Gx + Gxy;
+        acc[((0 * TY + ty) * TX + tx) * 3 + c] = es - ed;  // corner (x0,y0)
+        acc[((1 * TY + ty) * TX + tx) * 3 + c] = es + ed;  // corner (x1,y0)
+        acc[((2 * TY + ty) * TX + tx) * 3 + c] = fs - fd;  // corner (x0,y1)
+        acc[((3 * TY + ty) * TX + tx) * 3 + c] = fs + fd;  // corner (x1,y1)
+      }
+      __syncthreads();
+      const int64_t ni = i0 - 1 + tx, nj = j0 - 1 + ty;
+      if (tx >= 1 && ty >= 1 && ni <= g.nx && nj <= g.ny) {
+        const bool bnode = bc && (q == 0 || q == g.nz || ni == 0 || ni == g.nx || nj == 0 || nj == g.ny);
+        const int64_t nid = (q - g.k0) * g.plane + nj * (g.nx + 1) + ni;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          // fixed order: cells (i-1,j-1), (i,j-1), (i-1,j), (i,j)
+          double v = acc[((3 * TY + ty - 1) * TX + tx - 1) * 3 + c];
+          v += acc[((2 * TY + ty - 1) * TX + tx) * 3 + c];
+          v += acc[((1 * TY + ty) * TX + tx - 1) * 3 + c];
+          v += acc[((0 * TY + ty) * TX + tx) * 3 + c];
+          double xv;
+          if (bnode) {
+            xv = x.main[nid * 3 + c];
+            v = xv;
+          } else if (mode == 1) {
+            xv = x.main[nid * 3 + c];
+          } else {
+            xv = 0.0;
+          }
+          y[nid * 3 + c] = v;
+          if (mode == 1) pq = fma(v, xv, pq);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (mode == 1) {
+    double bsum = block_sum(pq, red_sh);
+    double total;
+    if (last_block_reduce(bsum, red, red_sh, &total)) sc->pq = total;
+  }
+}
+
+template <int TY, int S>
+static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double* lam, const double* mu,
+                              int64_t mat_layer0, double* y, int bc, int mode, CgScalars* sc,
+                              Reduce red, cudaStream_t s, int sm_count) {
+  constexpr int TX = 32;
+  constexpr int PITCH = (TX + 1) * 3 + 1;
+  const size_t smem = ((size_t)S * (TY + 1) * PITCH + 4 * TY * TX * 3) * sizeof(double);
+  auto kern = elastic_kernel<TY, S>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t xt = (g.nx + 1 + (TX - 1) - 1) / (TX - 1);
+  const int64_t yt = (g.ny + 1 + (TY - 1) - 1) / (TY - 1);
+  const int64_t nplanes = g.k1 - g.k0;
+  int64_t zc = (4LL * sm_count + xt * yt - 1) / (xt * yt);
+  zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / 8));
+  int64_t kchunk = (nplanes + zc - 1) / zc;
+  zc = (nplanes + kchunk - 1) / kchunk;
+  if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY);
+  kern<<<grid, block, smem, s>>>(g, x, lam, mu, mat_layer0, y, bc, mode, kchunk, sc, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double* lam, const double* mu,
+                           int64_t mat_layer0, double* y, int mode, CgScalars* sc, Reduce red,
+                           cudaStream_t s, int sm_count) {
+  return launch_cfg<16, 3>(g, x, lam, mu, mat_layer0, y, bc, mode, sc, red, s, sm_count);
+}
+
+}  // namespace fem

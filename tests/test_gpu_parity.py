@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances:
+  * apply: ||y - y_ref||_inf / ||y_ref||_inf <= 1e-12 (north_star "max relative error 1e-12");
+  * CG: solutions compared once converged past 1e-13 relative residual, |x - x_ref|_inf <= 1e-10;
+  * dot: relative 1e-14 (different summation order, both fp64).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2308_09839_b200 import inputs as I
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2308_09839_b200 import fem
+    fem.load()
+    return fem
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def relerr(y, ref):
+    return float(np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-300))
+
+
+MESHES = [(1, 1, 1), (2, 2, 2), (5, 7, 9), (33, 17, 12), (40, 31, 20), (64, 3, 5), (3, 70, 4)]
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("dims", MESHES)
+def test_apply_parity(F, oracle, kind, bc, dims):
+    nx, ny, nz = dims
+    h = 1.0 / max(dims)
+    g = I.rng(I.SEED_BASE + 100 + nx + 7 * ny + 31 * nz)
+    c = I.ncomp(kind)
+    x = I.uniform_vector(g, nx, ny, nz, c)
+    lam, mu = I.materials(g, nx, ny, nz)
+    ref = oracle.apply(kind, bc, nx, ny, nz, h, x, lam=lam, mu=mu)
+    mesh = F.Mesh(nx, ny, nz, h)
+    op = F.Operator(mesh, kind, bc)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    y = op.apply(dev(x)).cpu().numpy()
+    assert relerr(y, ref) <= APPLY_TOL
+    if bc:
+        bm = np.repeat(I.boundary_mask(nx, ny, nz), c)
+        assert np.array_equal(y[bm], x[bm])
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+def test_apply_host_pointers(F, oracle, kind):
+    """Host buffers go through the library's staging (the e2e path) with identical results."""
+    nx, ny, nz, h = 9, 8, 7, 0.1
+    g = I.rng(I.SEED_BASE + 200)
+    c = I.ncomp(kind)
+    x = I.uniform_vector(g, nx, ny, nz, c)
+    lam, mu = I.materials(g, nx, ny, nz)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 1)
+    if kind == "elastic":
+        op.set_material(lam, mu)  # host material
+    yh = op.apply(x)  # numpy in, numpy out
+    yd = op.apply(dev(x)).cpu().numpy()
+    assert np.array_equal(yh, yd)
+    assert relerr(yh, oracle.apply(kind, 1, nx, ny, nz, h, x, lam=lam, mu=mu)) <= APPLY_TOL
+
+
+def test_apply_deterministic(F):
+    nx, ny, nz = 40, 33, 50
+    g = I.rng(I.SEED_BASE + 201)
+    x = dev(I.uniform_vector(g, nx, ny, nz, 3))
+    lam, mu = I.materials(g, nx, ny, nz)
+    op = F.Operator(F.Mesh(nx, ny, nz, 0.02), "elastic", 1)
+    op.set_material(dev(lam), dev(mu))
+    y1 = op.apply(x)
+    y2 = op.apply(x)
+    assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+def test_null_space_and_symmetry_gpu(F, kind):
+    """Properties that hold at any size, checked on the GPU alone (no oracle)."""
+    nx, ny, nz, h = 37, 29, 23, 0.05
+    g = I.rng(I.SEED_BASE + 202)
+    c = I.ncomp(kind)
+    lam, mu = I.materials(g, nx, ny, nz)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 0)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    n = I.n_nodes(nx, ny, nz)
+    if kind == "elastic":
+        k, j, i = np.meshgrid(np.arange(nz + 1), np.arange(ny + 1), np.arange(nx + 1), indexing="ij")
+        X = np.stack([i.ravel() * h, j.ravel() * h, k.ravel() * h], 1)
+        modes = [np.tile(np.eye(3)[d], n) for d in range(3)]
+        for W in ([[0, -1, 0], [1, 0, 0], [0, 0, 0]], [[0, 0, -1], [0, 0, 0], [1, 0, 0]]):
+            modes.append((X @ np.array(W, float).T).ravel())
+        scale = (lam + 2 * mu).max() * h * 16
+    else:
+        modes = [np.ones(n * c)]
+        scale = 16 * h
+    for m in modes:
+        y = op.apply(dev(m)).cpu().numpy()
+        assert np.abs(y).max() < 1e-12 * scale
+    a = dev(I.uniform_vector(g, nx, ny, nz, c)); b = dev(I.uniform_vector(g, nx, ny, nz, c))
+    ab = op.dot(b, op.apply(a)); ba = op.dot(a, op.apply(b))
+    assert abs(ab - ba) <= 1e-12 * abs(ab)
+
+
+def test_dot_parity(F, oracle):
+    for n_cells in [(1, 1, 1), (20, 20, 20), (63, 64, 65)]:
+        g = I.rng(I.SEED_BASE + 300)
+        a = I.uniform_vector(g, *n_cells, 1); b = I.uniform_vector(g, *n_cells, 1)
+        op = F.Operator(F.Mesh(*n_cells, 0.1), "scalar", 1)
+        d = op.dot(dev(a), dev(b))
+        ref = oracle.dot(a, b)
+        assert abs(d - ref) <= 1e-14 * np.abs(a * b).sum()
+        assert op.dot(a, b) == d  # host pointers, same kernel
+
+
+def test_cg_c1_parity(F, oracle):
+    """BASELINE configs[0]: scalar 8^3, Dirichlet, 50 CG iterations, FP64."""
+    nx = ny = nz = 8; h = 1 / 8
+    g = I.rng(I.SEED_BASE + 0)
+    b = I.interior_rhs(g, nx, ny, nz, 1)
+    ref = oracle.cg("scalar", 1, nx, ny, nz, h, b, tol=0.0, maxit=50)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), "scalar", 1)
+    x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+    info = op.cg_solve(dev(b), x, tol=0.0, maxit=50)
+    assert info["iterations"] == ref.iterations
+    assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10
+    assert abs(info["r0_norm"] - ref.r0_norm) <= 1e-13 * ref.r0_norm
+    assert info["true_r_norm"] <= 1e-12 * ref.r0_norm
+
+
+@pytest.mark.parametrize("dims,iters", [((8, 8, 8), 150), ((12, 10, 9), 250)])
+def test_cg_elastic_parity(F, oracle, dims, iters):
+    nx, ny, nz = dims
+    h = 1.0 / nx
+    g = I.rng(I.SEED_BASE + 3)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = I.interior_rhs(g, nx, ny, nz, 3)
+    ref = oracle.cg("elastic", 1, nx, ny, nz, h, b, tol=1e-14, maxit=iters, lam=lam, mu=mu)
+    assert ref.converged
+    op = F.Operator(F.Mesh(nx, ny, nz, h), "elastic", 1)
+    op.set_material(dev(lam), dev(mu))
+    x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+    info = op.cg_solve(dev(b), x, tol=1e-14, maxit=iters)
+    assert info["converged"]
+    assert abs(info["iterations"] - ref.iterations) <= 3
+    assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10 * max(1.0, np.abs(ref.x).max())
+
+
+def test_cg_vector_host_pointers(F, oracle):
+    nx, ny, nz, h = 10, 9, 8, 0.1
+    g = I.rng(I.SEED_BASE + 2)
+    b = I.interior_rhs(g, nx, ny, nz, 3)
+    ref = oracle.cg("vector", 1, nx, ny, nz, h, b, tol=1e-13, maxit=300)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), "vector", 1)
+    x = np.zeros_like(b)
+    info = op.cg_solve(b, x, tol=1e-13, maxit=300)
+    assert info["converged"] and abs(info["iterations"] - ref.iterations) <= 2
+    assert np.abs(x - ref.x).max() <= 1e-10
+
+
+def test_cg_breakdown_and_edge_cases(F):
+    # b = 0 -> rr = 0: converged at iteration 0, x stays 0
+    op = F.Operator(F.Mesh(4, 4, 4, 0.25), "scalar", 1)
+    b = torch.zeros(125, dtype=torch.float64, device="cuda")
+    x = torch.zeros_like(b)
+    info = op.cg_solve(b, x, tol=0.0, maxit=10)
+    assert info["iterations"] == 0 and info["converged"] and torch.count_nonzero(x) == 0
+    # single interior dof: exactly one iteration
+    op2 = F.Operator(F.Mesh(2, 2, 2, 0.5), "scalar", 1)
+    b2 = torch.zeros(27, dtype=torch.float64, device="cuda"); b2[13] = 0.7
+    x2 = torch.zeros_like(b2)
+    info = op2.cg_solve(b2, x2, tol=1e-14, maxit=10)
+    assert info["iterations"] == 1 and abs(x2[13].item() - 0.7 * 0.75) < 1e-15
+    # bc = none on a Laplace operator is singular: b = constant is in the null space's range
+    # complement -> p.Ap = 0 after r = 0? use b with a constant component to force breakdown
+    op3 = F.Operator(F.Mesh(3, 3, 3, 1 / 3), "scalar", 0)
+    b3 = torch.ones(64, dtype=torch.float64, device="cuda")
+    x3 = torch.zeros_like(b3)
+    info = op3.cg_solve(b3, x3, tol=0.0, maxit=5)
+    assert info["status"] == F.FEM_EBREAKDOWN and info["breakdown_iter"] == 0
+
+
+def test_material_validation(F):
+    op = F.Operator(F.Mesh(3, 3, 3, 0.1), "elastic", 1)
+    lam = np.ones(27); mu = np.ones(27); mu[5] = 0.0
+    with pytest.raises(F.FemError) as e:
+        op.set_material(lam, mu)
+    assert e.value.status == F.FEM_EMATERIAL
+    mu[5] = 1.0; lam[3] = -1.0  # lambda + 2mu/3 < 0
+    with pytest.raises(F.FemError):
+        op.set_material(lam, mu)
+    x = torch.zeros(64 * 3, dtype=torch.float64, device="cuda")
+    with pytest.raises(F.FemError) as e:
+        op.apply(x)
+    assert e.value.status == F.FEM_ESTATE
+    with pytest.raises(F.FemError):
+        F.Operator(F.Mesh(3, 3, 3, 0.1), "scalar", 1).set_material(lam, mu)
+
+
+def test_aliasing_and_alignment(F):
+    op = F.Operator(F.Mesh(3, 3, 3, 0.1), "scalar", 1)
+    x = torch.zeros(65, dtype=torch.float64, device="cuda")
+    with pytest.raises(F.FemError):
+        op.apply(x[:64], x[:64])
+
+
+@pytest.mark.parametrize("kind,dims", [("scalar", (40, 30, 20)), ("vector", (21, 22, 23)),
+                                       ("elastic", (20, 21, 22))])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_csr_parity(F, oracle, kind, dims, bc):
+    nx, ny, nz = dims
+    h = 0.07
+    g = I.rng(I.SEED_BASE + 400)
+    c = I.ncomp(kind)
+    x = I.uniform_vector(g, nx, ny, nz, c)
+    lam, mu = I.materials(g, nx, ny, nz)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, bc)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    A = op.csr()
+    y = A.apply(dev(x)).cpu().numpy()
+    ref = oracle.apply(kind, bc, nx, ny, nz, h, x, lam=lam, mu=mu)
+    assert relerr(y, ref) <= APPLY_TOL
+    # interior rows carry 27 (scalar) / 81 (vector, elasticity) entries (Table 1)
+    n_int = (nx - 1) * (ny - 1) * (nz - 1) if bc else None
+    if bc:
+        # interior nodes whose neighbours are all interior: (nx-3)(ny-3)(nz-3) rows of full stencil
+        full = (nx - 3) * (ny - 3) * (nz - 3)
+        assert A.nnz >= full * 27 * c * c
+        assert A.nnz <= n_int * 27 * c * c + (I.n_nodes(nx, ny, nz) - n_int) * c

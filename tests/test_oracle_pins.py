@@ -458,3 +458,18 @@ def test_cg_iterates_are_krylov_galerkin_solutions(oracle, kind):
         res = oracle.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=k, lam=lam, mu=mu)
         assert res.iterations == k
         assert np.abs(res.x - xk).max() < 1e-11 * np.abs(xk).max()
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_apply_nodes_equals_full_apply(oracle, kind, bc):
+    """The sampled-node oracle is the same definition restricted to the cells around a node."""
+    nx, ny, nz, h = 6, 5, 4, 0.3
+    g = np.random.default_rng(30)
+    c = I.ncomp(kind)
+    lam, mu = I.materials(g, nx, ny, nz)
+    x = I.uniform_vector(g, nx, ny, nz, c)
+    y = oracle.apply(kind, bc, nx, ny, nz, h, x, lam=lam, mu=mu).reshape(-1, c)
+    nodes = np.arange(I.n_nodes(nx, ny, nz))
+    ys = oracle.apply_nodes(kind, bc, nx, ny, nz, h, x, nodes, lam=lam, mu=mu)
+    assert np.abs(ys - y).max() <= 1e-13 * np.abs(y).max()
