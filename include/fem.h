@@ -86,8 +86,14 @@ int64_t fem_launch_count(void);
 /* Rank 0 creates a 128-byte NCCL unique id; the caller broadcasts it (torch.distributed). */
 int fem_get_unique_id(void* id_out, int64_t id_bytes /* >= 128 */);
 /* nranks == 1: no NCCL is touched and id may be NULL.  The calling thread's current CUDA
- * device is the rank's device. */
+ * device is the rank's device.  nranks > 1 with id == NULL creates a VIRTUAL communicator:
+ * it only defines the slab partition (for single-process tests with fem_apply_ghost); calls that
+ * need an exchange (fem_apply, fem_dot, fem_cg_*) then return FEM_EUNSUPPORTED. */
 int fem_comm_create(int32_t nranks, int32_t rank, const void* id, fem_comm_t* out);
+/* Slab partition (pure host function, no CUDA): the nz+1 node planes split as evenly as
+ * possible, rank r owns [plane_begin, plane_end); the first (nz+1) % nranks ranks get one more. */
+int fem_partition(int64_t nz, int32_t nranks, int32_t rank, int64_t* plane_begin,
+                  int64_t* plane_end);
 void fem_comm_destroy(fem_comm_t comm);
 
 /* ---- mesh ----------------------------------------------------------------- */
@@ -111,6 +117,11 @@ int fem_set_material(fem_op_t op, const double* lambda, const double* mu, int64_
 /* y = A_c x on the rank's owned DOFs.  x, y: device or host, length n_local_dof,
  * x != y.  Collective when nranks > 1 (one node-plane halo per neighbour). */
 int fem_apply(fem_op_t op, const double* x, double* y, void* stream);
+/* y = A_c x with caller-supplied ghost node planes and no communication: ghost_lo is node
+ * plane plane_begin-1, ghost_hi is plane plane_end (device pointers, plane_dofs = c (nx+1)(ny+1)
+ * values each; NULL where the plane is outside the box).  x, y device, owned planes. */
+int fem_apply_ghost(fem_op_t op, const double* x, const double* ghost_lo, const double* ghost_hi,
+                    double* y, void* stream);
 /* Global sum_i a_i b_i over owned DOFs (Table 4 "ddot").  Deterministic for a
  * fixed rank count.  Result written to *result (host).  Collective. */
 int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void* stream);

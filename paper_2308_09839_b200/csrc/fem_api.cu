@@ -205,6 +205,13 @@ static int ensure_unit_matrices(int dev) {
   return FEM_OK;
 }
 
+static int need_comm(fem_op_s* op) {
+  fem_mesh_s* m = op->mesh;
+  if (m->nranks > 1 && (!m->comm || !m->comm->nccl))
+    return fail(FEM_EUNSUPPORTED, "virtual communicator: use fem_apply_ghost (no exchange available)");
+  return FEM_OK;
+}
+
 // one node-plane halo per neighbour (ncclSend/Recv pairs in one group)
 static int halo(fem_op_s* op, const double* owned, double* lo, double* hi, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
@@ -301,11 +308,7 @@ int fem_comm_create(int32_t nranks, int32_t rank, const void* id, fem_comm_t* ou
     delete c;
     return fail(FEM_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
   }
-  if (nranks > 1) {
-    if (!id) {
-      delete c;
-      return fail(FEM_EINVAL, "id is NULL with nranks > 1");
-    }
+  if (nranks > 1 && id) {
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, uid, rank);
@@ -322,6 +325,16 @@ void fem_comm_destroy(fem_comm_t c) {
   if (!c) return;
   if (c->nccl) ncclCommDestroy(c->nccl);
   delete c;
+}
+
+int fem_partition(int64_t nz, int32_t nranks, int32_t rank, int64_t* pb, int64_t* pe) {
+  if (nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || !pb || !pe)
+    return fail(FEM_EINVAL, "bad partition arguments");
+  if (nz + 1 < nranks) return fail(FEM_EINVAL, "fewer node planes (%lld) than ranks (%d)", (long long)(nz + 1), nranks);
+  const int64_t N = nz + 1, base = N / nranks, rem = N % nranks;
+  *pb = rank * base + std::min<int64_t>(rank, rem);
+  *pe = *pb + base + (rank < rem ? 1 : 0);
+  return FEM_OK;
 }
 
 int fem_mesh_create(int64_t nx, int64_t ny, int64_t nz, double h, fem_comm_t comm, fem_mesh_t* out) {
@@ -342,9 +355,8 @@ int fem_mesh_create(int64_t nx, int64_t ny, int64_t nz, double h, fem_comm_t com
   m->rank = R;
   cudaGetDevice(&m->device);
   cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, m->device);
-  const int64_t N = nz + 1, base = N / P, rem = N % P;
-  const int64_t k0 = R * base + std::min<int64_t>(R, rem);
-  const int64_t k1 = k0 + base + (R < rem ? 1 : 0);
+  int64_t k0 = 0, k1 = 0;
+  fem_partition(nz, P, R, &k0, &k1);
   m->g = Grid{nx, ny, nz, h, k0, k1, (nx + 1) * (ny + 1)};
   *out = m;
   return FEM_OK;
@@ -478,8 +490,26 @@ int fem_set_material(fem_op_t op, const double* lam, const double* mu, int64_t l
   return FEM_OK;
 }
 
+int fem_apply_ghost(fem_op_t op, const double* x, const double* glo, const double* ghi, double* y,
+                    void* stream) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(check_vec(x, "x"));
+  FEM_TRY(check_vec(y, "y"));
+  if ((const void*)x == (const void*)y) return fail(FEM_EINVAL, "x and y alias");
+  if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
+  const Grid& g = op->mesh->g;
+  if ((g.k0 > 0 && !glo) || (g.k1 <= g.nz && !ghi))
+    return fail(FEM_EINVAL, "a ghost plane inside the box is NULL");
+  if (!is_device_ptr(x) || !is_device_ptr(y) || (glo && !is_device_ptr(glo)) || (ghi && !is_device_ptr(ghi)))
+    return fail(FEM_EINVAL, "fem_apply_ghost needs device pointers");
+  FEM_TRY(set_device(op->mesh->device));
+  PlaneSrc src{x, g.k0 > 0 ? glo : nullptr, g.k1 <= g.nz ? ghi : nullptr};
+  return launch_apply(op, src, y, 0, (cudaStream_t)stream);
+}
+
 int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
   if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(need_comm(op));
   FEM_TRY(check_vec(x, "x"));
   FEM_TRY(check_vec(y, "y"));
   if ((const void*)x == (const void*)y) return fail(FEM_EINVAL, "x and y alias");
@@ -506,6 +536,7 @@ int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
 
 int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void* stream) {
   if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(need_comm(op));
   FEM_TRY(check_vec(a, "a"));
   FEM_TRY(check_vec(b, "b"));
   if (!result) return fail(FEM_EINVAL, "result is NULL");
@@ -650,6 +681,7 @@ static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
 
 int fem_cg_begin(fem_op_t op, const double* b, double* x, double tol, int32_t maxit, void* stream) {
   if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(need_comm(op));
   FEM_TRY(check_vec(b, "b"));
   FEM_TRY(check_vec(x, "x"));
   if ((const void*)b == (const void*)x) return fail(FEM_EINVAL, "b and x alias");
@@ -680,6 +712,7 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream) {
 int fem_cg_solve(fem_op_t op, const double* b, double* x, double tol, int32_t maxit,
                  fem_cg_info* info, void* stream) {
   if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(need_comm(op));
   FEM_TRY(check_vec(b, "b"));
   FEM_TRY(check_vec(x, "x"));
   if ((const void*)b == (const void*)x) return fail(FEM_EINVAL, "b and x alias");

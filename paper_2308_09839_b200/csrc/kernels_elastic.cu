@@ -15,6 +15,8 @@
 // layer k-1 (register carry), the four cells sharing a node in xy exchange corner values through
 // shared memory, and each node is written exactly once.  Summation order per node is fixed
 // (independent of the tiling and of the z-chunk / slab boundaries).
+#include <algorithm>
+
 #include "kernels_common.cuh"
 
 namespace fem {
@@ -38,20 +40,25 @@ __global__ void __launch_bounds__(32 * TY, 1)
                    CgScalars* sc, Reduce red) {
   constexpr int TX = 32;
   constexpr int NT = TX * TY;
-  constexpr int ROWS = TY + 1;     // node rows j0-1 .. j0+TY-1
-  constexpr int COLS = TX + 1;     // node cols i0-1 .. i0+TX-1
-  constexpr int PITCH = COLS * 3 + 1;
-  constexpr int SLOT = ROWS * PITCH;
-  extern __shared__ __align__(16) double smem[];
-  double* ring = smem;                      // S * SLOT
-  double* acc = smem + S * SLOT;            // [4][TY][TX][3]
+  constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
+  constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
+  using Ring = PlaneRing<ROWS, COLS, 3, S>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
+  Ring ring;
+  ring.buf = reinterpret_cast<double*>(smem_raw);
+  double* acc = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // [4][TY][TX][3]
+  ring.full = reinterpret_cast<uint64_t*>(acc + 4 * TY * TX * 3);
+  ring.lead = reinterpret_cast<int*>(ring.full + S);
+  ring.valid = ring.lead + (S + 1) * ROWS;
 
   if (mode == 1 && sc->done) return;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
+  const int warp = tid >> 5, lane = tid & 31;
   // output tile: nodes i0 .. i0+TX-2, j0 .. j0+TY-2; thread (tx,ty) owns cell (i0-1+tx, j0-1+ty)
+  // and node (i0-1+tx, j0-1+ty) (written when tx, ty >= 1)
   const int64_t i0 = (int64_t)blockIdx.x * (TX - 1);
   const int64_t j0 = (int64_t)blockIdx.y * (TY - 1);
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
@@ -60,24 +67,28 @@ __global__ void __launch_bounds__(32 * TY, 1)
   const bool cell_xy = ci >= 0 && ci < g.nx && cj >= 0 && cj < g.ny;
   const double hs = g.h * (1.0 / 16.0);
   const int64_t nxy = g.nx * g.ny;
+  const int64_t cell_off = cell_xy ? cj * g.nx + ci : 0;
+  const bool owner = tx >= 1 && ty >= 1 && ci <= g.nx && cj <= g.ny;
+  const bool bnode_xy = bc && (ci == 0 || ci == g.nx || cj == 0 || cj == g.ny);
+  const int64_t node_off = owner ? (cj * (g.nx + 1) + ci) * 3 : 0;
 
-  // planes kb-1 .. ke are needed (cell layers kb-1 .. ke-1)
-  const int64_t pfirst = kb - 1;
-#pragma unroll
-  for (int s = 0; s < S - 1; ++s) {
-    stage_plane<ROWS, COLS, 3, PITCH, NT>(ring + s * SLOT, x, g, pfirst + s, i0 - 1, j0 - 1, bc, tid);
-    cp_async_commit();
+  ring.init(tid, NT);
+  const int64_t pfirst = kb - 1;  // planes kb-1 .. ke (cell layers kb-1 .. ke-1)
+  if (warp == 0) {
+#pragma unroll 1
+    for (int s = 0; s < S - 1; ++s)
+      if (pfirst + s <= ke) ring.issue(s, x, g, pfirst + s, i0 - 1, j0 - 1, bc, lane);
   }
 
   Face fb[3];     // face transform of the bottom plane of the current cell layer
   double cb[12];  // carried top-face contribution of the previous cell layer (4 modes x 3 comps)
+  double xc[3];   // this thread's node value at the bottom plane (for p.Ap)
 #pragma unroll
   for (int t = 0; t < 12; ++t) cb[t] = 0.0;
 
-  // material of the first cell layer
   auto load_mat = [&](int64_t k, double& L, double& M) {
     if (cell_xy && k >= 0 && k < g.nz) {
-      const int64_t e = (k - mat_layer0) * nxy + cj * g.nx + ci;
+      const int64_t e = (k - mat_layer0) * nxy + cell_off;
       L = __ldg(lam + e) * hs;
       M = __ldg(mu + e) * hs;
     } else {
@@ -88,45 +99,46 @@ __global__ void __launch_bounds__(32 * TY, 1)
   load_mat(pfirst, Ln, Mn);
 
   double pq = 0.0;
+#pragma unroll 1
   for (int64_t p = pfirst; p <= ke; ++p) {
     // iteration p: plane p is available; cell layer p-1 lies between planes p-1 and p
-    const int slot = (int)((p - pfirst) % S);
-    cp_async_wait<S - 2>();
+    const int t = (int)(p - pfirst);
+    const int slot = t % S;
+    ring.wait(slot, (uint32_t)((t / S) & 1));
     __syncthreads();
-    {
-      const int64_t pn = p + S - 1;
-      const int sn = (int)((pn - pfirst) % S);
-      if (pn <= ke) stage_plane<ROWS, COLS, 3, PITCH, NT>(ring + sn * SLOT, x, g, pn, i0 - 1, j0 - 1, bc, tid);
-      cp_async_commit();
-    }
-    const double* sp = ring + slot * SLOT;
+    if (warp == 0 && p + S - 1 <= ke) ring.issue((t + S - 1) % S, x, g, p + S - 1, i0 - 1, j0 - 1, bc, lane);
     Face ft[3];
+    double xn[3];
+    {
+      const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
+      const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double* r0 = sp + ty * PITCH;
-      const double* r1 = sp + (ty + 1) * PITCH;
-      ft[c] = face_fwd(r0[tx * 3 + c], r0[(tx + 1) * 3 + c], r1[tx * 3 + c], r1[(tx + 1) * 3 + c]);
+      for (int c = 0; c < 3; ++c) {
+        xn[c] = r0[c];
+        ft[c] = face_fwd(r0[c], r0[3 + c], r1[c], r1[3 + c]);
+      }
     }
     if (p == pfirst) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) fb[c] = ft[c];
+      for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xc[c] = xn[c]; }
       continue;
     }
     // ---- cell layer k = p-1 ----
     const double L0 = Ln, M0 = Mn;
     if (p < ke) load_mat(p, Ln, Mn);  // prefetch next layer
     // modal coefficients (unnormalised): component u=0, v=1, w=2
-    // one = fb.s+ft.s (unused), x = ds, y = sd, xy = dd, z = ss_z, xz, yz, xyz
-    double ux = fb[0].x + ft[0].x, uy = fb[0].y + ft[0].y, uxy = fb[0].xy + ft[0].xy;
-    double uz = ft[0].s - fb[0].s, uxz = ft[0].x - fb[0].x, uyz = ft[0].y - fb[0].y, uxyz = ft[0].xy - fb[0].xy;
-    double vx = fb[1].x + ft[1].x, vy = fb[1].y + ft[1].y, vxy = fb[1].xy + ft[1].xy;
-    double vz = ft[1].s - fb[1].s, vxz = ft[1].x - fb[1].x, vyz = ft[1].y - fb[1].y, vxyz = ft[1].xy - fb[1].xy;
-    double wx = fb[2].x + ft[2].x, wy = fb[2].y + ft[2].y, wxy = fb[2].xy + ft[2].xy;
-    double wz = ft[2].s - fb[2].s, wxz = ft[2].x - fb[2].x, wyz = ft[2].y - fb[2].y, wxyz = ft[2].xy - fb[2].xy;
+    // x = ds, y = sd, xy = dd summed over z; z, xz, yz, xyz = differences in z
+    const double ux = fb[0].x + ft[0].x, uy = fb[0].y + ft[0].y, uxy = fb[0].xy + ft[0].xy;
+    const double uz = ft[0].s - fb[0].s, uxz = ft[0].x - fb[0].x, uyz = ft[0].y - fb[0].y, uxyz = ft[0].xy - fb[0].xy;
+    const double vx = fb[1].x + ft[1].x, vy = fb[1].y + ft[1].y, vxy = fb[1].xy + ft[1].xy;
+    const double vz = ft[1].s - fb[1].s, vxz = ft[1].x - fb[1].x, vyz = ft[1].y - fb[1].y, vxyz = ft[1].xy - fb[1].xy;
+    const double wx = fb[2].x + ft[2].x, wy = fb[2].y + ft[2].y, wxy = fb[2].xy + ft[2].xy;
+    const double wz = ft[2].s - fb[2].s, wxz = ft[2].x - fb[2].x, wyz = ft[2].y - fb[2].y, wxyz = ft[2].xy - fb[2].xy;
+    double xq[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) fb[c] = ft[c];
+    for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xq[c] = xc[c]; xc[c] = xn[c]; }
 
-    // modal stress (DESIGN.md §5.2 table): weights 1 (linear modes), 1/3 (bilinear), 1/9 (trilinear)
+    // modal stress: weights 1 (linear modes), 1/3 (bilinear), 1/9 (trilinear)
     const double M2 = M0 + M0;
     const double S0 = ux + vy + wz;
     const double LS0 = L0 * S0;
@@ -144,8 +156,8 @@ __global__ void __launch_bounds__(32 * TY, 1)
     const double K3 = fma(4.0, M0, L0) * (1.0 / 9.0);
     const double guxyz = K3 * uxyz, gvxyz = K3 * vxyz, gwxyz = K3 * wxyz;
 
-    // inverse z: face mode f at bottom = g_f - g_fz, top = g_f + g_fz (g_1 = 0)
-    // bottom face of this cell, plus the carried top face of layer k-1 -> face at plane p-1
+    // inverse z: face mode f at bottom = g_f - g_fz, top = g_f + g_fz (g_1 = 0);
+    // bottom face of this cell + carried top face of layer k-1 -> complete face at plane p-1
     double F[12];
     {
       const double gx[3] = {gux, gvx, gwx}, gy[3] = {guy, gvy, gwy}, gxy[3] = {guxy, gvxy, gwxy};
@@ -163,7 +175,7 @@ __global__ void __launch_bounds__(32 * TY, 1)
         cb[4 * c + 3] = gxy[c] + gxyz[c];
       }
     }
-    const int64_t q = p - 1;  // node plane whose values are now complete in xy-corner form
+    const int64_t q = p - 1;  // node plane whose xy-corner contributions are now complete
     if (q >= kb) {
       // expand face modes to the 4 corner nodes of this cell column, exchange via smem
 #pragma unroll
@@ -176,10 +188,9 @@ __global__ void __launch_bounds__(32 * TY, 1)
         acc[((3 * TY + ty) * TX + tx) * 3 + c] = fs + fd;  // corner (x1,y1)
       }
       __syncthreads();
-      const int64_t ni = i0 - 1 + tx, nj = j0 - 1 + ty;
-      if (tx >= 1 && ty >= 1 && ni <= g.nx && nj <= g.ny) {
-        const bool bnode = bc && (q == 0 || q == g.nz || ni == 0 || ni == g.nx || nj == 0 || nj == g.ny);
-        const int64_t nid = (q - g.k0) * g.plane + nj * (g.nx + 1) + ni;
+      if (owner) {
+        const bool bnode = bnode_xy || (bc && (q == 0 || q == g.nz));
+        const int64_t nid = (q - g.k0) * g.plane * 3 + node_off;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           // fixed order: cells (i-1,j-1), (i,j-1), (i-1,j), (i,j)
@@ -187,22 +198,17 @@ __global__ void __launch_bounds__(32 * TY, 1)
           v += acc[((2 * TY + ty - 1) * TX + tx) * 3 + c];
           v += acc[((1 * TY + ty) * TX + tx - 1) * 3 + c];
           v += acc[((0 * TY + ty) * TX + tx) * 3 + c];
-          double xv;
+          double xv = xq[c];
           if (bnode) {
-            xv = x.main[nid * 3 + c];
+            xv = x.main[nid + c];
             v = xv;
-          } else if (mode == 1) {
-            xv = x.main[nid * 3 + c];
-          } else {
-            xv = 0.0;
           }
-          y[nid * 3 + c] = v;
+          y[nid + c] = v;
           if (mode == 1) pq = fma(v, xv, pq);
         }
       }
     }
   }
-  cp_async_wait<0>();
   if (mode == 1) {
     double bsum = block_sum(pq, red_sh);
     double total;
@@ -215,8 +221,9 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double* lam, cons
                               int64_t mat_layer0, double* y, int bc, int mode, CgScalars* sc,
                               Reduce red, cudaStream_t s, int sm_count) {
   constexpr int TX = 32;
-  constexpr int PITCH = (TX + 1) * 3 + 1;
-  const size_t smem = ((size_t)S * (TY + 1) * PITCH + 4 * TY * TX * 3) * sizeof(double);
+  using Ring = PlaneRing<TY + 1, TX + 1, 3, S>;
+  const size_t smem = Ring::BYTES + 4 * TY * TX * 3 * sizeof(double) + S * sizeof(uint64_t) +
+                      ((S + 1) * (TY + 1) + S) * sizeof(int);
   auto kern = elastic_kernel<TY, S>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -241,7 +248,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double* lam, cons
 cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double* lam, const double* mu,
                            int64_t mat_layer0, double* y, int mode, CgScalars* sc, Reduce red,
                            cudaStream_t s, int sm_count) {
-  return launch_cfg<16, 3>(g, x, lam, mu, mat_layer0, y, bc, mode, sc, red, s, sm_count);
+  return launch_cfg<16, 4>(g, x, lam, mu, mat_layer0, y, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem

@@ -8,45 +8,66 @@
 //   a = Mx x, b = Kx x           (per node row, from smem)
 //   c1 = My a, c2 = My b + Ky a  (per node, from the thread's rows)
 //   y(k) = (h/36) [Mz c2 + Kz c1] over the register window c(k-1), c(k), c(k+1).
-// The CTA marches along z over node planes staged in a cp.async ring (x read from HBM once;
-// the one-node xy halo comes from L2).  Vector Laplace (Eq. 8) is the same per component.
+// The CTA marches along z over node planes staged by bulk copies (PlaneRing); x is read from
+// HBM once, the one-node xy halo from L2.  Vector Laplace (Eq. 8) is the same per component.
+#include <algorithm>
+
 #include "kernels_common.cuh"
 
 namespace fem {
 
 template <int C, int TX, int TY, int R, int S>
-__global__ void __launch_bounds__(TX* TY) laplace_kernel(Grid g, PlaneSrc x, double* __restrict__ y,
-                                                         int bc, int mode, int64_t kchunk,
-                                                         CgScalars* sc, Reduce red) {
+__global__ void __launch_bounds__(TX* TY, 2) laplace_kernel(Grid g, PlaneSrc x, double* __restrict__ y,
+                                                            int bc, int mode, int64_t kchunk,
+                                                            CgScalars* sc, Reduce red) {
   constexpr int NT = TX * TY;
   constexpr int ROWS = TY * R + 2;
   constexpr int COLS = TX + 2;
-  constexpr int PITCH = COLS * C + (C == 1 ? 0 : 1);
-  constexpr int SLOT = ROWS * PITCH;
-  extern __shared__ __align__(16) double smem[];
+  using Ring = PlaneRing<ROWS, COLS, C, S>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
+  Ring ring;
+  ring.buf = reinterpret_cast<double*>(smem_raw);
+  ring.full = reinterpret_cast<uint64_t*>(smem_raw + Ring::BYTES);
+  ring.lead = reinterpret_cast<int*>(ring.full + S);
+  ring.valid = ring.lead + (S + 1) * ROWS;
 
   if (mode == 1 && sc->done) return;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
+  const int warp = tid >> 5, lane = tid & 31;
   const int64_t i0 = (int64_t)blockIdx.x * TX;
   const int64_t j0 = (int64_t)blockIdx.y * (TY * R);
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t i = i0 + tx;
-  const double h36 = g.h / 36.0;
+  const double h36 = g.h * (1.0 / 36.0);
+  const int64_t rowlen = g.nx + 1;
 
   // per-node 1-D multiplicities m = (#1-D elements touching the node) in x, y
   const double mx = (double)((i > 0) + (i < g.nx));
   double my[R];
+  bool active[R], bnode_xy[R];
+  int64_t off_xy[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t j = j0 + ty * R + r;
     my[r] = (double)((j > 0) + (j < g.ny));
+    active[r] = (i <= g.nx) && (j <= g.ny);
+    bnode_xy[r] = bc && (i == 0 || i == g.nx || j == 0 || j == g.ny);
+    off_xy[r] = (j * rowlen + i) * C;
   }
 
-  // window of c1, c2 and the (masked) centre value for planes p-2, p-1, p
+  ring.init(tid, NT);
+  const int64_t pfirst = kb - 1;
+  if (warp == 0) {
+#pragma unroll 1
+    for (int s = 0; s < S - 1; ++s)
+      if (pfirst + s <= ke) ring.issue(s, x, g, pfirst + s, i0 - 1, j0 - 1, bc, lane);
+  }
+
+  // windows: c1, c2 and the centre value for planes p-2, p-1, p
   double c1w[3][R][C], c2w[3][R][C], xcw[2][R][C];
 #pragma unroll
   for (int w = 0; w < 3; ++w)
@@ -61,28 +82,15 @@ __global__ void __launch_bounds__(TX* TY) laplace_kernel(Grid g, PlaneSrc x, dou
 #pragma unroll
       for (int c = 0; c < C; ++c) xcw[w][r][c] = 0.0;
 
-  // prologue: planes kb-1 .. kb+S-3
-  const int64_t pfirst = kb - 1;
-#pragma unroll
-  for (int s = 0; s < S - 1; ++s) {
-    stage_plane<ROWS, COLS, C, PITCH, NT>(smem + s * SLOT, x, g, pfirst + s, i0 - 1, j0 - 1, bc, tid);
-    cp_async_commit();
-  }
-
   double pq = 0.0;
+#pragma unroll 1
   for (int64_t p = pfirst; p <= ke; ++p) {
-    const int slot = (int)((p - pfirst) % S);
-    cp_async_wait<S - 2>();
-    __syncthreads();
-    // refill the slot of plane p-1 (free: all threads are past iteration p-1)
-    {
-      const int64_t pn = p + S - 1;
-      const int sn = (int)((pn - pfirst) % S);
-      if (pn <= ke) stage_plane<ROWS, COLS, C, PITCH, NT>(smem + sn * SLOT, x, g, pn, i0 - 1, j0 - 1, bc, tid);
-      cp_async_commit();
-    }
-    const double* sp = smem + slot * SLOT;
-    // shift windows
+    const int t = (int)(p - pfirst);
+    const int slot = t % S;
+    ring.wait(slot, (uint32_t)((t / S) & 1));
+    __syncthreads();  // all threads are past iteration p-1: its slot may be refilled
+    if (warp == 0 && p + S - 1 <= ke) ring.issue((t + S - 1) % S, x, g, p + S - 1, i0 - 1, j0 - 1, bc, lane);
+
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -95,12 +103,12 @@ __global__ void __launch_bounds__(TX* TY) laplace_kernel(Grid g, PlaneSrc x, dou
     double a[R + 2][C], b[R + 2][C];
 #pragma unroll
     for (int rr = 0; rr < R + 2; ++rr) {
-      const double* row = sp + (ty * R + rr) * PITCH;
+      const double* row = ring.row_ptr(slot, ty * R + rr) + tx * C;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const double xm = row[tx * C + c];
-        const double x0 = row[(tx + 1) * C + c];
-        const double xp = row[(tx + 2) * C + c];
+        const double xm = row[c];
+        const double x0 = row[C + c];
+        const double xp = row[2 * C + c];
         const double sn = xm + xp;
         a[rr][c] = fma(2.0 * mx, x0, sn);
         b[rr][c] = fma(mx, x0, -sn);
@@ -121,32 +129,28 @@ __global__ void __launch_bounds__(TX* TY) laplace_kernel(Grid g, PlaneSrc x, dou
     const int64_t q = p - 1;
     if (q >= kb) {
       const double mz = (double)((q > 0) + (q < g.nz));
-      const bool qface = (q == 0 || q == g.nz);
-      const int64_t qoff = (q - g.k0) * g.plane;
+      const bool qface = bc && (q == 0 || q == g.nz);
+      double* yq = y + (q - g.k0) * g.plane * C;
+      const double* xq = x.main + (q - g.k0) * g.plane * C;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int64_t j = j0 + ty * R + r;
-        if (i > g.nx || j > g.ny) continue;
-        const bool bnode = bc && (qface || i == 0 || i == g.nx || j == 0 || j == g.ny);
-        const int64_t nid = qoff + j * (g.nx + 1) + i;
+        if (!active[r]) continue;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          double v;
-          double xv = xcw[0][r][c];
-          if (bnode) {
-            xv = x.main[nid * C + c];
+          double v, xv = xcw[0][r][c];
+          if (qface || bnode_xy[r]) {
+            xv = xq[off_xy[r] + c];
             v = xv;
           } else {
             const double nb = (c2w[0][r][c] - c1w[0][r][c]) + (c2w[2][r][c] - c1w[2][r][c]);
             v = h36 * fma(2.0 * mz, c2w[1][r][c], fma(mz, c1w[1][r][c], nb));
           }
-          y[nid * C + c] = v;
+          yq[off_xy[r] + c] = v;
           if (mode == 1) pq = fma(v, xv, pq);
         }
       }
     }
   }
-  cp_async_wait<0>();
   if (mode == 1) {
     double bsum = block_sum(pq, red_sh);
     double total;
@@ -157,9 +161,8 @@ __global__ void __launch_bounds__(TX* TY) laplace_kernel(Grid g, PlaneSrc x, dou
 template <int C, int TX, int TY, int R, int S>
 static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, double* y, int bc, int mode, CgScalars* sc,
                               Reduce red, cudaStream_t s, int sm_count) {
-  constexpr int ROWS = TY * R + 2;
-  constexpr int PITCH = (TX + 2) * C + (C == 1 ? 0 : 1);
-  const size_t smem = (size_t)S * ROWS * PITCH * sizeof(double);
+  using Ring = PlaneRing<TY * R + 2, TX + 2, C, S>;
+  const size_t smem = Ring::BYTES + S * sizeof(uint64_t) + ((S + 1) * (TY * R + 2) + S) * sizeof(int);
   auto kern = laplace_kernel<C, TX, TY, R, S>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -170,10 +173,9 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, double* y, int bc, int 
   const int64_t xt = (g.nx + 1 + TX - 1) / TX;
   const int64_t yt = (g.ny + 1 + TY * R - 1) / (TY * R);
   const int64_t nplanes = g.k1 - g.k0;
-  // z-chunks: enough CTAs for ~8 per SM, chunks of >= 8 planes
+  // z-chunks: about 4 resident waves of CTAs (2 per SM), chunks of >= 16 planes
   int64_t zc = (8LL * sm_count + xt * yt - 1) / (xt * yt);
-  zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / 8));
-  if (zc < 1) zc = 1;
+  zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / 16));
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
@@ -185,8 +187,8 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, double* y, int bc, int 
 
 cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, double* y, int mode,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
-  if (comps == 1) return launch_cfg<1, 32, 8, 2, 4>(g, x, y, bc, mode, sc, red, s, sm_count);
-  return launch_cfg<3, 32, 8, 1, 4>(g, x, y, bc, mode, sc, red, s, sm_count);
+  if (comps == 1) return launch_cfg<1, 32, 8, 2, 8>(g, x, y, bc, mode, sc, red, s, sm_count);
+  return launch_cfg<3, 32, 8, 1, 6>(g, x, y, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem

@@ -43,7 +43,7 @@ class CgInfo(ctypes.Structure):
 # every symbol include/fem.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fem_last_error", "fem_version", "fem_launch_count", "fem_get_unique_id", "fem_comm_create",
-    "fem_comm_destroy", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy", "fem_op_create",
+    "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy", "fem_op_create",
     "fem_op_ndof", "fem_set_material", "fem_apply", "fem_dot", "fem_cg_solve", "fem_cg_begin",
     "fem_cg_iterate", "fem_cg_end", "fem_set_option", "fem_apply_time", "fem_op_destroy",
     "fem_csr_create", "fem_csr_info", "fem_csr_apply", "fem_csr_destroy",
@@ -74,6 +74,8 @@ def load(build_if_missing: bool = True):
         "fem_get_unique_id": ([vp, i64], ctypes.c_int),
         "fem_comm_create": ([i32, i32, vp, P(vp)], ctypes.c_int),
         "fem_comm_destroy": ([vp], None),
+        "fem_partition": ([i64, i32, i32, P(i64), P(i64)], ctypes.c_int),
+        "fem_apply_ghost": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "fem_mesh_create": ([i64, i64, i64, dbl, vp, P(vp)], ctypes.c_int),
         "fem_mesh_local": ([vp, P(i64), P(i64), P(i64)], ctypes.c_int),
         "fem_mesh_destroy": ([vp], None),
@@ -135,6 +137,13 @@ def _stream(stream):
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+def partition(nz: int, nranks: int, rank: int):
+    """Slab partition of the nz+1 node planes (pure host call, no GPU needed)."""
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().fem_partition(nz, nranks, rank, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
 
 
 def launch_count() -> int:
@@ -217,6 +226,15 @@ class Operator:
                 import torch
                 y = torch.empty_like(x)
         _check(load().fem_apply(self.h, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def apply_ghost(self, x, ghost_lo, ghost_hi, y=None, stream=None):
+        """y = A_c x with caller-provided ghost planes (single-process slab tests)."""
+        if y is None:
+            import torch
+            y = torch.empty_like(x)
+        _check(load().fem_apply_ghost(self.h, _ptr(x), _ptr(ghost_lo), _ptr(ghost_hi), _ptr(y),
+                                      _stream(stream)))
         return y
 
     def dot(self, a, b, stream=None) -> float:
