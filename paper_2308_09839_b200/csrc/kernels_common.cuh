@@ -39,6 +39,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -74,29 +80,63 @@ __device__ __forceinline__ void fence_mbar_init() {
 
 // Ring of S plane slots + one zero slot.  Slot layout: ROWS rows of PITCH doubles (PITCH even,
 // >= COLS*C + 4); a row's data starts at element lead[slot][row] in {2, 3} (+ col*C + comp).
+// full[s]: completes when plane data landed (ROWS+1 arrivals + tx bytes);
+// empty[s]: completes when the NCW consumer warps released the slot.
 template <int ROWS, int COLS, int C, int S>
 struct PlaneRing {
   static constexpr int PITCH = ((COLS * C + 4) + 1) & ~1;
   static constexpr int SLOT = ROWS * PITCH;
   static constexpr size_t BYTES = (size_t)(S + 1) * SLOT * sizeof(double);  // + zero slot
+  static constexpr size_t META = 2 * S * sizeof(uint64_t) + ((S + 1) * ROWS + S) * sizeof(int);
   static_assert(ROWS <= 32, "one producer lane per row");
+  static_assert((S & (S - 1)) == 0, "S must be a power of two");
 
   double* buf;      // (S+1) * SLOT doubles, 16-B aligned; slot S is the zero slot
   uint64_t* full;   // S mbarriers
+  uint64_t* empty;  // S mbarriers
   int* lead;        // (S+1) * ROWS
   int* valid;       // S: plane holds operator data
 
+  __device__ __forceinline__ void carve(unsigned char* ring_base, unsigned char* meta_base) {
+    buf = reinterpret_cast<double*>(ring_base);
+    full = reinterpret_cast<uint64_t*>(meta_base);
+    empty = full + S;
+    lead = reinterpret_cast<int*>(empty + S);
+    valid = lead + (S + 1) * ROWS;
+  }
+
   // all threads: zero the ring, init barriers; ends with __syncthreads
-  __device__ __forceinline__ void init(int tid, int nthreads) {
+  __device__ __forceinline__ void init(int tid, int nthreads, int n_consumer_warps) {
     double2* b2 = reinterpret_cast<double2*>(buf);
     for (int t = tid; t < (S + 1) * SLOT / 2; t += nthreads) b2[t] = make_double2(0.0, 0.0);
     for (int t = tid; t < (S + 1) * ROWS; t += nthreads) lead[t] = 2;
     if (tid == 0) {
-      for (int s = 0; s < S; ++s) mbar_init(&full[s], ROWS + 1);
+      for (int s = 0; s < S; ++s) {
+        mbar_init(&full[s], ROWS + 1);
+        mbar_init(&empty[s], n_consumer_warps);
+      }
       fence_mbar_init();
     }
     fence_proxy_async();
     __syncthreads();
+  }
+
+  // producer warp: stream planes pfirst .. plast through the ring
+  __device__ __forceinline__ void produce(const PlaneSrc& x, const Grid& g, int64_t pfirst, int64_t plast,
+                                          int64_t ilo, int64_t jlo, int bc, int lane) {
+#pragma unroll 1
+    for (int64_t p = pfirst; p <= plast; ++p) {
+      const int t = (int)(p - pfirst);
+      const int s = t & (S - 1);
+      if (t >= S) mbar_wait(&empty[s], (uint32_t)(((t / S) - 1) & 1));
+      issue(s, x, g, p, ilo, jlo, bc, lane);
+    }
+  }
+
+  // consumer warp: release slot s after its last read
+  __device__ __forceinline__ void release(int s, int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 
   // warp 0 only (all 32 lanes): copy node plane k into slot s.

@@ -34,177 +34,175 @@ __device__ __forceinline__ Face face_fwd(double u00, double u10, double u01, dou
 }  // namespace
 
 template <int TY, int S>
-__global__ void __launch_bounds__(32 * TY, 1)
+__global__ void __launch_bounds__(32 * (TY + 1), 1)
     elastic_kernel(Grid g, PlaneSrc x, const double* __restrict__ lam, const double* __restrict__ mu,
                    int64_t mat_layer0, double* __restrict__ y, int bc, int mode, int64_t kchunk,
                    CgScalars* sc, Reduce red) {
+  // TY consumer warps (lane = cell column, warp = cell row) + 1 producer warp
   constexpr int TX = 32;
-  constexpr int NT = TX * TY;
+  constexpr int NT = TX * (TY + 1);
+  constexpr int NC = TX * TY;   // consumer threads
   constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
   constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
+  constexpr int ACC = 4 * TY * TX * 3;
   using Ring = PlaneRing<ROWS, COLS, 3, S>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
-  ring.buf = reinterpret_cast<double*>(smem_raw);
-  double* acc = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // [4][TY][TX][3]
-  ring.full = reinterpret_cast<uint64_t*>(acc + 4 * TY * TX * 3);
-  ring.lead = reinterpret_cast<int*>(ring.full + S);
-  ring.valid = ring.lead + (S + 1) * ROWS;
+  double* acc0 = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // 2 x [4][TY][TX][3]
+  ring.carve(smem_raw, reinterpret_cast<unsigned char*>(acc0 + 2 * ACC));
 
   if (mode == 1 && sc->done) return;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
-  const int warp = tid >> 5, lane = tid & 31;
   // output tile: nodes i0 .. i0+TX-2, j0 .. j0+TY-2; thread (tx,ty) owns cell (i0-1+tx, j0-1+ty)
   // and node (i0-1+tx, j0-1+ty) (written when tx, ty >= 1)
   const int64_t i0 = (int64_t)blockIdx.x * (TX - 1);
   const int64_t j0 = (int64_t)blockIdx.y * (TY - 1);
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(g.k1, kb + kchunk);
-  const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
-  const bool cell_xy = ci >= 0 && ci < g.nx && cj >= 0 && cj < g.ny;
-  const double hs = g.h * (1.0 / 16.0);
-  const int64_t nxy = g.nx * g.ny;
-  const int64_t cell_off = cell_xy ? cj * g.nx + ci : 0;
-  const bool owner = tx >= 1 && ty >= 1 && ci <= g.nx && cj <= g.ny;
-  const bool bnode_xy = bc && (ci == 0 || ci == g.nx || cj == 0 || cj == g.ny);
-  const int64_t node_off = owner ? (cj * (g.nx + 1) + ci) * 3 : 0;
-
-  ring.init(tid, NT);
   const int64_t pfirst = kb - 1;  // planes kb-1 .. ke (cell layers kb-1 .. ke-1)
-  if (warp == 0) {
-#pragma unroll 1
-    for (int s = 0; s < S - 1; ++s)
-      if (pfirst + s <= ke) ring.issue(s, x, g, pfirst + s, i0 - 1, j0 - 1, bc, lane);
-  }
-
-  Face fb[3];     // face transform of the bottom plane of the current cell layer
-  double cb[12];  // carried top-face contribution of the previous cell layer (4 modes x 3 comps)
-  double xc[3];   // this thread's node value at the bottom plane (for p.Ap)
-#pragma unroll
-  for (int t = 0; t < 12; ++t) cb[t] = 0.0;
-
-  auto load_mat = [&](int64_t k, double& L, double& M) {
-    if (cell_xy && k >= 0 && k < g.nz) {
-      const int64_t e = (k - mat_layer0) * nxy + cell_off;
-      L = __ldg(lam + e) * hs;
-      M = __ldg(mu + e) * hs;
-    } else {
-      L = 0.0; M = 0.0;
-    }
-  };
-  double Ln, Mn;
-  load_mat(pfirst, Ln, Mn);
+  ring.init(tid, NT, TY);
 
   double pq = 0.0;
+  if (ty == TY) {
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx);
+  } else {
+    const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
+    const bool cell_xy = ci >= 0 && ci < g.nx && cj >= 0 && cj < g.ny;
+    const double hs = g.h * (1.0 / 16.0);
+    const int64_t nxy = g.nx * g.ny;
+    const double* lam_c = lam + (cell_xy ? cj * g.nx + ci : 0) - mat_layer0 * nxy;
+    const double* mu_c = mu + (cell_xy ? cj * g.nx + ci : 0) - mat_layer0 * nxy;
+    const bool owner = tx >= 1 && ty >= 1 && ci <= g.nx && cj <= g.ny;
+    const bool bnode_xy = bc && (ci == 0 || ci == g.nx || cj == 0 || cj == g.ny);
+    const int64_t node_off = owner ? (cj * (g.nx + 1) + ci) * 3 : 0;
+
+    Face fb[3];     // face transform of the bottom plane of the current cell layer
+    double cb[12];  // carried top-face contribution of the previous cell layer (4 modes x 3 comps)
+    double xc[3];   // this thread's node value at the bottom plane (for p.Ap)
+#pragma unroll
+    for (int t = 0; t < 12; ++t) cb[t] = 0.0;
+
+    auto load_mat = [&](int64_t k, double& L, double& M) {
+      if (cell_xy && k >= 0 && k < g.nz) {
+        L = __ldg(lam_c + k * nxy) * hs;
+        M = __ldg(mu_c + k * nxy) * hs;
+      } else {
+        L = 0.0; M = 0.0;
+      }
+    };
+    double Ln, Mn;
+    load_mat(pfirst, Ln, Mn);
+
 #pragma unroll 1
-  for (int64_t p = pfirst; p <= ke; ++p) {
-    // iteration p: plane p is available; cell layer p-1 lies between planes p-1 and p
-    const int t = (int)(p - pfirst);
-    const int slot = t % S;
-    ring.wait(slot, (uint32_t)((t / S) & 1));
-    __syncthreads();
-    if (warp == 0 && p + S - 1 <= ke) ring.issue((t + S - 1) % S, x, g, p + S - 1, i0 - 1, j0 - 1, bc, lane);
-    Face ft[3];
-    double xn[3];
-    {
-      const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
-      const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        xn[c] = r0[c];
-        ft[c] = face_fwd(r0[c], r0[3 + c], r1[c], r1[3 + c]);
-      }
-    }
-    if (p == pfirst) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xc[c] = xn[c]; }
-      continue;
-    }
-    // ---- cell layer k = p-1 ----
-    const double L0 = Ln, M0 = Mn;
-    if (p < ke) load_mat(p, Ln, Mn);  // prefetch next layer
-    // modal coefficients (unnormalised): component u=0, v=1, w=2
-    // x = ds, y = sd, xy = dd summed over z; z, xz, yz, xyz = differences in z
-    const double ux = fb[0].x + ft[0].x, uy = fb[0].y + ft[0].y, uxy = fb[0].xy + ft[0].xy;
-    const double uz = ft[0].s - fb[0].s, uxz = ft[0].x - fb[0].x, uyz = ft[0].y - fb[0].y, uxyz = ft[0].xy - fb[0].xy;
-    const double vx = fb[1].x + ft[1].x, vy = fb[1].y + ft[1].y, vxy = fb[1].xy + ft[1].xy;
-    const double vz = ft[1].s - fb[1].s, vxz = ft[1].x - fb[1].x, vyz = ft[1].y - fb[1].y, vxyz = ft[1].xy - fb[1].xy;
-    const double wx = fb[2].x + ft[2].x, wy = fb[2].y + ft[2].y, wxy = fb[2].xy + ft[2].xy;
-    const double wz = ft[2].s - fb[2].s, wxz = ft[2].x - fb[2].x, wyz = ft[2].y - fb[2].y, wxyz = ft[2].xy - fb[2].xy;
-    double xq[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xq[c] = xc[c]; xc[c] = xn[c]; }
-
-    // modal stress: weights 1 (linear modes), 1/3 (bilinear), 1/9 (trilinear)
-    const double M2 = M0 + M0;
-    const double S0 = ux + vy + wz;
-    const double LS0 = L0 * S0;
-    const double gux = fma(M2, ux, LS0), gvy = fma(M2, vy, LS0), gwz = fma(M2, wz, LS0);
-    const double tuv = M0 * (uy + vx), tuw = M0 * (uz + wx), tvw = M0 * (vz + wy);
-    const double guy = tuv, gvx = tuv, guz = tuw, gwx = tuw, gvz = tvw, gwy = tvw;
-    const double L1 = L0 * (1.0 / 3.0), M1 = M0 * (1.0 / 3.0);
-    const double Sxi = vxy + wxz, Seta = uxy + wyz, Szeta = uxz + vyz;
-    const double LSxi = L1 * Sxi, LSeta = L1 * Seta, LSzeta = L1 * Szeta;
-    const double guxy = fma(M0, uxy, LSeta), gwyz = fma(M0, wyz, LSeta);
-    const double gvxy = fma(M0, vxy, LSxi), gwxz = fma(M0, wxz, LSxi);
-    const double guxz = fma(M0, uxz, LSzeta), gvyz = fma(M0, vyz, LSzeta);
-    const double T = uyz + vxz + wxy;
-    const double guyz = M1 * (T + uyz), gvxz = M1 * (T + vxz), gwxy = M1 * (T + wxy);
-    const double K3 = fma(4.0, M0, L0) * (1.0 / 9.0);
-    const double guxyz = K3 * uxyz, gvxyz = K3 * vxyz, gwxyz = K3 * wxyz;
-
-    // inverse z: face mode f at bottom = g_f - g_fz, top = g_f + g_fz (g_1 = 0);
-    // bottom face of this cell + carried top face of layer k-1 -> complete face at plane p-1
-    double F[12];
-    {
-      const double gx[3] = {gux, gvx, gwx}, gy[3] = {guy, gvy, gwy}, gxy[3] = {guxy, gvxy, gwxy};
-      const double gz[3] = {guz, gvz, gwz}, gxz[3] = {guxz, gvxz, gwxz}, gyz[3] = {guyz, gvyz, gwyz};
-      const double gxyz[3] = {guxyz, gvxyz, gwxyz};
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        F[4 * c + 0] = cb[4 * c + 0] - gz[c];
-        F[4 * c + 1] = cb[4 * c + 1] + (gx[c] - gxz[c]);
-        F[4 * c + 2] = cb[4 * c + 2] + (gy[c] - gyz[c]);
-        F[4 * c + 3] = cb[4 * c + 3] + (gxy[c] - gxyz[c]);
-        cb[4 * c + 0] = gz[c];
-        cb[4 * c + 1] = gx[c] + gxz[c];
-        cb[4 * c + 2] = gy[c] + gyz[c];
-        cb[4 * c + 3] = gxy[c] + gxyz[c];
-      }
-    }
-    const int64_t q = p - 1;  // node plane whose xy-corner contributions are now complete
-    if (q >= kb) {
-      // expand face modes to the 4 corner nodes of this cell column, exchange via smem
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double G1 = F[4 * c + 0], Gx = F[4 * c + 1], Gy = F[4 * c + 2], Gxy = F[4 * c + 3];
-        const double es = G1 - Gy, ed = Gx - Gxy, fs = G1 + Gy, fd = Gx + Gxy;
-        acc[((0 * TY + ty) * TX + tx) * 3 + c] = es - ed;  // corner (x0,y0)
-        acc[((1 * TY + ty) * TX + tx) * 3 + c] = es + ed;  // corner (x1,y0)
-        acc[((2 * TY + ty) * TX + tx) * 3 + c] = fs - fd;  // corner (x0,y1)
-        acc[((3 * TY + ty) * TX + tx) * 3 + c] = fs + fd;  // corner (x1,y1)
-      }
-      __syncthreads();
-      if (owner) {
-        const bool bnode = bnode_xy || (bc && (q == 0 || q == g.nz));
-        const int64_t nid = (q - g.k0) * g.plane * 3 + node_off;
+    for (int64_t p = pfirst; p <= ke; ++p) {
+      // iteration p: plane p is available; cell layer p-1 lies between planes p-1 and p
+      const int t = (int)(p - pfirst);
+      const int slot = t & (S - 1);
+      ring.wait(slot, (uint32_t)((t / S) & 1));
+      Face ft[3];
+      double xn[3];
+      {
+        const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
+        const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          // fixed order: cells (i-1,j-1), (i,j-1), (i-1,j), (i,j)
-          double v = acc[((3 * TY + ty - 1) * TX + tx - 1) * 3 + c];
-          v += acc[((2 * TY + ty - 1) * TX + tx) * 3 + c];
-          v += acc[((1 * TY + ty) * TX + tx - 1) * 3 + c];
-          v += acc[((0 * TY + ty) * TX + tx) * 3 + c];
-          double xv = xq[c];
-          if (bnode) {
-            xv = x.main[nid + c];
-            v = xv;
+          xn[c] = r0[c];
+          ft[c] = face_fwd(r0[c], r0[3 + c], r1[c], r1[3 + c]);
+        }
+      }
+      ring.release(slot, tx);
+      if (p == pfirst) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xc[c] = xn[c]; }
+        continue;
+      }
+      // ---- cell layer k = p-1 ----
+      const double L0 = Ln, M0 = Mn;
+      if (p < ke) load_mat(p, Ln, Mn);  // prefetch next layer
+      // modal coefficients (unnormalised): component u=0, v=1, w=2
+      // x = ds, y = sd, xy = dd summed over z; z, xz, yz, xyz = differences in z
+      const double ux = fb[0].x + ft[0].x, uy = fb[0].y + ft[0].y, uxy = fb[0].xy + ft[0].xy;
+      const double uz = ft[0].s - fb[0].s, uxz = ft[0].x - fb[0].x, uyz = ft[0].y - fb[0].y, uxyz = ft[0].xy - fb[0].xy;
+      const double vx = fb[1].x + ft[1].x, vy = fb[1].y + ft[1].y, vxy = fb[1].xy + ft[1].xy;
+      const double vz = ft[1].s - fb[1].s, vxz = ft[1].x - fb[1].x, vyz = ft[1].y - fb[1].y, vxyz = ft[1].xy - fb[1].xy;
+      const double wx = fb[2].x + ft[2].x, wy = fb[2].y + ft[2].y, wxy = fb[2].xy + ft[2].xy;
+      const double wz = ft[2].s - fb[2].s, wxz = ft[2].x - fb[2].x, wyz = ft[2].y - fb[2].y, wxyz = ft[2].xy - fb[2].xy;
+      double xq[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xq[c] = xc[c]; xc[c] = xn[c]; }
+
+      // modal stress: weights 1 (linear modes), 1/3 (bilinear), 1/9 (trilinear)
+      const double M2 = M0 + M0;
+      const double S0 = ux + vy + wz;
+      const double LS0 = L0 * S0;
+      const double gux = fma(M2, ux, LS0), gvy = fma(M2, vy, LS0), gwz = fma(M2, wz, LS0);
+      const double tuv = M0 * (uy + vx), tuw = M0 * (uz + wx), tvw = M0 * (vz + wy);
+      const double guy = tuv, gvx = tuv, guz = tuw, gwx = tuw, gvz = tvw, gwy = tvw;
+      const double L1 = L0 * (1.0 / 3.0), M1 = M0 * (1.0 / 3.0);
+      const double Sxi = vxy + wxz, Seta = uxy + wyz, Szeta = uxz + vyz;
+      const double LSxi = L1 * Sxi, LSeta = L1 * Seta, LSzeta = L1 * Szeta;
+      const double guxy = fma(M0, uxy, LSeta), gwyz = fma(M0, wyz, LSeta);
+      const double gvxy = fma(M0, vxy, LSxi), gwxz = fma(M0, wxz, LSxi);
+      const double guxz = fma(M0, uxz, LSzeta), gvyz = fma(M0, vyz, LSzeta);
+      const double T = uyz + vxz + wxy;
+      const double guyz = M1 * (T + uyz), gvxz = M1 * (T + vxz), gwxy = M1 * (T + wxy);
+      const double K3 = fma(4.0, M0, L0) * (1.0 / 9.0);
+      const double guxyz = K3 * uxyz, gvxyz = K3 * vxyz, gwxyz = K3 * wxyz;
+
+      // inverse z: face mode f at bottom = g_f - g_fz, top = g_f + g_fz (g_1 = 0);
+      // bottom face of this cell + carried top face of layer k-1 -> complete face at plane p-1
+      double F[12];
+      {
+        const double gx[3] = {gux, gvx, gwx}, gy[3] = {guy, gvy, gwy}, gxy[3] = {guxy, gvxy, gwxy};
+        const double gz[3] = {guz, gvz, gwz}, gxz[3] = {guxz, gvxz, gwxz}, gyz[3] = {guyz, gvyz, gwyz};
+        const double gxyz[3] = {guxyz, gvxyz, gwxyz};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          F[4 * c + 0] = cb[4 * c + 0] - gz[c];
+          F[4 * c + 1] = cb[4 * c + 1] + (gx[c] - gxz[c]);
+          F[4 * c + 2] = cb[4 * c + 2] + (gy[c] - gyz[c]);
+          F[4 * c + 3] = cb[4 * c + 3] + (gxy[c] - gxyz[c]);
+          cb[4 * c + 0] = gz[c];
+          cb[4 * c + 1] = gx[c] + gxz[c];
+          cb[4 * c + 2] = gy[c] + gyz[c];
+          cb[4 * c + 3] = gxy[c] + gxyz[c];
+        }
+      }
+      const int64_t q = p - 1;  // node plane whose xy-corner contributions are now complete
+      if (q >= kb) {
+        double* acc = acc0 + (q & 1) * ACC;  // double-buffered: one consumer barrier per plane
+        // expand face modes to the 4 corner nodes of this cell column, exchange via smem
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double G1 = F[4 * c + 0], Gx = F[4 * c + 1], Gy = F[4 * c + 2], Gxy = F[4 * c + 3];
+          const double es = G1 - Gy, ed = Gx - Gxy, fs = G1 + Gy, fd = Gx + Gxy;
+          acc[((0 * TY + ty) * TX + tx) * 3 + c] = es - ed;  // corner (x0,y0)
+          acc[((1 * TY + ty) * TX + tx) * 3 + c] = es + ed;  // corner (x1,y0)
+          acc[((2 * TY + ty) * TX + tx) * 3 + c] = fs - fd;  // corner (x0,y1)
+          acc[((3 * TY + ty) * TX + tx) * 3 + c] = fs + fd;  // corner (x1,y1)
+        }
+        named_bar_sync(1, NC);
+        if (owner) {
+          const bool bnode = bnode_xy || (bc && (q == 0 || q == g.nz));
+          const int64_t nid = (q - g.k0) * g.plane * 3 + node_off;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            // fixed order: cells (i-1,j-1), (i,j-1), (i-1,j), (i,j)
+            double v = acc[((3 * TY + ty - 1) * TX + tx - 1) * 3 + c];
+            v += acc[((2 * TY + ty - 1) * TX + tx) * 3 + c];
+            v += acc[((1 * TY + ty) * TX + tx - 1) * 3 + c];
+            v += acc[((0 * TY + ty) * TX + tx) * 3 + c];
+            double xv = xq[c];
+            if (bnode) {
+              xv = x.main[nid + c];
+              v = xv;
+            }
+            y[nid + c] = v;
+            if (mode == 1) pq = fma(v, xv, pq);
           }
-          y[nid + c] = v;
-          if (mode == 1) pq = fma(v, xv, pq);
         }
       }
     }
@@ -222,8 +220,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double* lam, cons
                               Reduce red, cudaStream_t s, int sm_count) {
   constexpr int TX = 32;
   using Ring = PlaneRing<TY + 1, TX + 1, 3, S>;
-  const size_t smem = Ring::BYTES + 4 * TY * TX * 3 * sizeof(double) + S * sizeof(uint64_t) +
-                      ((S + 1) * (TY + 1) + S) * sizeof(int);
+  const size_t smem = Ring::BYTES + 2 * 4 * TY * TX * 3 * sizeof(double) + Ring::META;
   auto kern = elastic_kernel<TY, S>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -239,7 +236,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double* lam, cons
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY);
+  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
   kern<<<grid, block, smem, s>>>(g, x, lam, mu, mat_layer0, y, bc, mode, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
@@ -248,7 +245,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double* lam, cons
 cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double* lam, const double* mu,
                            int64_t mat_layer0, double* y, int mode, CgScalars* sc, Reduce red,
                            cudaStream_t s, int sm_count) {
-  return launch_cfg<16, 4>(g, x, lam, mu, mat_layer0, y, bc, mode, sc, red, s, sm_count);
+  return launch_cfg<15, 4>(g, x, lam, mu, mat_layer0, y, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem

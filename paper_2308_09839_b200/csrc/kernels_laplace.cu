@@ -17,136 +17,128 @@
 namespace fem {
 
 template <int C, int TX, int TY, int R, int S>
-__global__ void __launch_bounds__(TX* TY, 2) laplace_kernel(Grid g, PlaneSrc x, double* __restrict__ y,
-                                                            int bc, int mode, int64_t kchunk,
-                                                            CgScalars* sc, Reduce red) {
-  constexpr int NT = TX * TY;
+__global__ void __launch_bounds__(TX*(TY + 1), 2) laplace_kernel(Grid g, PlaneSrc x, double* __restrict__ y,
+                                                                 int bc, int mode, int64_t kchunk,
+                                                                 CgScalars* sc, Reduce red) {
+  // TY consumer warps (one node column per lane, R node rows each) + 1 producer warp
+  constexpr int NT = TX * (TY + 1);
   constexpr int ROWS = TY * R + 2;
   constexpr int COLS = TX + 2;
   using Ring = PlaneRing<ROWS, COLS, C, S>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
-  ring.buf = reinterpret_cast<double*>(smem_raw);
-  ring.full = reinterpret_cast<uint64_t*>(smem_raw + Ring::BYTES);
-  ring.lead = reinterpret_cast<int*>(ring.full + S);
-  ring.valid = ring.lead + (S + 1) * ROWS;
+  ring.carve(smem_raw, smem_raw + Ring::BYTES);
 
   if (mode == 1 && sc->done) return;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
-  const int warp = tid >> 5, lane = tid & 31;
   const int64_t i0 = (int64_t)blockIdx.x * TX;
   const int64_t j0 = (int64_t)blockIdx.y * (TY * R);
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(g.k1, kb + kchunk);
-  const int64_t i = i0 + tx;
-  const double h36 = g.h * (1.0 / 36.0);
-  const int64_t rowlen = g.nx + 1;
-
-  // per-node 1-D multiplicities m = (#1-D elements touching the node) in x, y
-  const double mx = (double)((i > 0) + (i < g.nx));
-  double my[R];
-  bool active[R], bnode_xy[R];
-  int64_t off_xy[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int64_t j = j0 + ty * R + r;
-    my[r] = (double)((j > 0) + (j < g.ny));
-    active[r] = (i <= g.nx) && (j <= g.ny);
-    bnode_xy[r] = bc && (i == 0 || i == g.nx || j == 0 || j == g.ny);
-    off_xy[r] = (j * rowlen + i) * C;
-  }
-
-  ring.init(tid, NT);
   const int64_t pfirst = kb - 1;
-  if (warp == 0) {
-#pragma unroll 1
-    for (int s = 0; s < S - 1; ++s)
-      if (pfirst + s <= ke) ring.issue(s, x, g, pfirst + s, i0 - 1, j0 - 1, bc, lane);
-  }
-
-  // windows: c1, c2 and the centre value for planes p-2, p-1, p
-  double c1w[3][R][C], c2w[3][R][C], xcw[2][R][C];
-#pragma unroll
-  for (int w = 0; w < 3; ++w)
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < C; ++c) { c1w[w][r][c] = 0.0; c2w[w][r][c] = 0.0; }
-#pragma unroll
-  for (int w = 0; w < 2; ++w)
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < C; ++c) xcw[w][r][c] = 0.0;
+  ring.init(tid, NT, TY);
 
   double pq = 0.0;
-#pragma unroll 1
-  for (int64_t p = pfirst; p <= ke; ++p) {
-    const int t = (int)(p - pfirst);
-    const int slot = t % S;
-    ring.wait(slot, (uint32_t)((t / S) & 1));
-    __syncthreads();  // all threads are past iteration p-1: its slot may be refilled
-    if (warp == 0 && p + S - 1 <= ke) ring.issue((t + S - 1) % S, x, g, p + S - 1, i0 - 1, j0 - 1, bc, lane);
-
+  if (ty == TY) {
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx);
+  } else {
+    const int64_t i = i0 + tx;
+    const double h36 = g.h * (1.0 / 36.0);
+    const int64_t rowlen = g.nx + 1;
+    // per-node 1-D multiplicities m = (#1-D elements touching the node) in x, y
+    const double mx = (double)((i > 0) + (i < g.nx));
+    double my[R];
+    bool active[R], bnode_xy[R];
+    int64_t off_xy[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        c1w[0][r][c] = c1w[1][r][c]; c2w[0][r][c] = c2w[1][r][c];
-        c1w[1][r][c] = c1w[2][r][c]; c2w[1][r][c] = c2w[2][r][c];
-        xcw[0][r][c] = xcw[1][r][c];
-      }
-    // x-direction filters for the R+2 rows this thread needs
-    double a[R + 2][C], b[R + 2][C];
-#pragma unroll
-    for (int rr = 0; rr < R + 2; ++rr) {
-      const double* row = ring.row_ptr(slot, ty * R + rr) + tx * C;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const double xm = row[c];
-        const double x0 = row[C + c];
-        const double xp = row[2 * C + c];
-        const double sn = xm + xp;
-        a[rr][c] = fma(2.0 * mx, x0, sn);
-        b[rr][c] = fma(mx, x0, -sn);
-        if (rr >= 1 && rr <= R) xcw[1][rr - 1][c] = x0;
-      }
+    for (int r = 0; r < R; ++r) {
+      const int64_t j = j0 + ty * R + r;
+      my[r] = (double)((j > 0) + (j < g.ny));
+      active[r] = (i <= g.nx) && (j <= g.ny);
+      bnode_xy[r] = bc && (i == 0 || i == g.nx || j == 0 || j == g.ny);
+      off_xy[r] = (j * rowlen + i) * C;
     }
-    // y-direction
+    // windows: c1, c2 and the centre value for planes p-2, p-1, p
+    double c1w[3][R][C], c2w[3][R][C], xcw[2][R][C];
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+    for (int w = 0; w < 3; ++w)
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const double an = a[r][c] + a[r + 2][c];
-        const double bn = b[r][c] + b[r + 2][c];
-        c1w[2][r][c] = fma(2.0 * my[r], a[r + 1][c], an);
-        c2w[2][r][c] = fma(2.0 * my[r], b[r + 1][c], bn) + fma(my[r], a[r + 1][c], -an);
-      }
-    // z-direction: output plane q = p-1
-    const int64_t q = p - 1;
-    if (q >= kb) {
-      const double mz = (double)((q > 0) + (q < g.nz));
-      const bool qface = bc && (q == 0 || q == g.nz);
-      double* yq = y + (q - g.k0) * g.plane * C;
-      const double* xq = x.main + (q - g.k0) * g.plane * C;
+      for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!active[r]) continue;
+        for (int c = 0; c < C; ++c) { c1w[w][r][c] = 0.0; c2w[w][r][c] = 0.0; }
+#pragma unroll
+    for (int w = 0; w < 2; ++w)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) xcw[w][r][c] = 0.0;
+
+#pragma unroll 1
+    for (int64_t p = pfirst; p <= ke; ++p) {
+      const int t = (int)(p - pfirst);
+      const int slot = t & (S - 1);
+      ring.wait(slot, (uint32_t)((t / S) & 1));
+#pragma unroll
+      for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          double v, xv = xcw[0][r][c];
-          if (qface || bnode_xy[r]) {
-            xv = xq[off_xy[r] + c];
-            v = xv;
-          } else {
-            const double nb = (c2w[0][r][c] - c1w[0][r][c]) + (c2w[2][r][c] - c1w[2][r][c]);
-            v = h36 * fma(2.0 * mz, c2w[1][r][c], fma(mz, c1w[1][r][c], nb));
+          c1w[0][r][c] = c1w[1][r][c]; c2w[0][r][c] = c2w[1][r][c];
+          c1w[1][r][c] = c1w[2][r][c]; c2w[1][r][c] = c2w[2][r][c];
+          xcw[0][r][c] = xcw[1][r][c];
+        }
+      // x-direction filters for the R+2 rows this thread needs
+      double a[R + 2][C], b[R + 2][C];
+#pragma unroll
+      for (int rr = 0; rr < R + 2; ++rr) {
+        const double* row = ring.row_ptr(slot, ty * R + rr) + tx * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double xm = row[c];
+          const double x0 = row[C + c];
+          const double xp = row[2 * C + c];
+          const double sn = xm + xp;
+          a[rr][c] = fma(2.0 * mx, x0, sn);
+          b[rr][c] = fma(mx, x0, -sn);
+          if (rr >= 1 && rr <= R) xcw[1][rr - 1][c] = x0;
+        }
+      }
+      ring.release(slot, tx);
+      // y-direction
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double an = a[r][c] + a[r + 2][c];
+          const double bn = b[r][c] + b[r + 2][c];
+          c1w[2][r][c] = fma(2.0 * my[r], a[r + 1][c], an);
+          c2w[2][r][c] = fma(2.0 * my[r], b[r + 1][c], bn) + fma(my[r], a[r + 1][c], -an);
+        }
+      // z-direction: output plane q = p-1
+      const int64_t q = p - 1;
+      if (q >= kb) {
+        const double mz = (double)((q > 0) + (q < g.nz));
+        const bool qface = bc && (q == 0 || q == g.nz);
+        double* yq = y + (q - g.k0) * g.plane * C;
+        const double* xq = x.main + (q - g.k0) * g.plane * C;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!active[r]) continue;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            double v, xv = xcw[0][r][c];
+            if (qface || bnode_xy[r]) {
+              xv = xq[off_xy[r] + c];
+              v = xv;
+            } else {
+              const double nb = (c2w[0][r][c] - c1w[0][r][c]) + (c2w[2][r][c] - c1w[2][r][c]);
+              v = h36 * fma(2.0 * mz, c2w[1][r][c], fma(mz, c1w[1][r][c], nb));
+            }
+            yq[off_xy[r] + c] = v;
+            if (mode == 1) pq = fma(v, xv, pq);
           }
-          yq[off_xy[r] + c] = v;
-          if (mode == 1) pq = fma(v, xv, pq);
         }
       }
     }
@@ -162,7 +154,7 @@ template <int C, int TX, int TY, int R, int S>
 static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, double* y, int bc, int mode, CgScalars* sc,
                               Reduce red, cudaStream_t s, int sm_count) {
   using Ring = PlaneRing<TY * R + 2, TX + 2, C, S>;
-  const size_t smem = Ring::BYTES + S * sizeof(uint64_t) + ((S + 1) * (TY * R + 2) + S) * sizeof(int);
+  const size_t smem = Ring::BYTES + Ring::META;
   auto kern = laplace_kernel<C, TX, TY, R, S>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -179,7 +171,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, double* y, int bc, int 
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY);
+  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
   kern<<<grid, block, smem, s>>>(g, x, y, bc, mode, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
@@ -188,7 +180,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, double* y, int bc, int 
 cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, double* y, int mode,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   if (comps == 1) return launch_cfg<1, 32, 8, 2, 8>(g, x, y, bc, mode, sc, red, s, sm_count);
-  return launch_cfg<3, 32, 8, 1, 6>(g, x, y, bc, mode, sc, red, s, sm_count);
+  return launch_cfg<3, 32, 8, 1, 8>(g, x, y, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem
