@@ -80,8 +80,8 @@ struct fem_op_s {
   fem_mesh_s* mesh = nullptr;
   int kind = 0, bc = 0, comps = 1;
   int64_t n_local = 0, n_global = 0, plane_dofs = 0;
-  // material (local cell layers [mat_layer0, mat_layer0 + mat_layers))
-  double *lam = nullptr, *mu = nullptr;
+  // material (local cell layers [mat_layer0, mat_layer0 + mat_layers)), (lambda, mu) interleaved
+  double2* lm = nullptr;
   int64_t mat_layer0 = 0, mat_layers = 0;
   bool has_mat = false;
   // workspace
@@ -244,8 +244,8 @@ static int launch_apply(fem_op_s* op, PlaneSrc x, double* y, int mode, cudaStrea
   fem_mesh_s* m = op->mesh;
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
-    e = launch_elastic(op->bc, m->g, x, op->lam, op->mu, op->mat_layer0, y, mode, op->sc, op->red,
-                       s, m->sm_count);
+    e = launch_elastic(op->bc, m->g, x, op->lm, op->mat_layer0, y, mode, op->sc, op->red, s,
+                       m->sm_count);
   else
     e = launch_laplace(op->comps, op->bc, m->g, x, y, mode, op->sc, op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "apply launch failed: %s", cudaGetErrorString(e));
@@ -378,7 +378,7 @@ static void op_free(fem_op_s* op) {
   if (op->graph1) cudaGraphExecDestroy(op->graph1);
   if (op->graphN) cudaGraphExecDestroy(op->graphN);
   for (auto e : op->ev) cudaEventDestroy(e);
-  cudaFree(op->lam); cudaFree(op->mu);
+  cudaFree(op->lm);
   cudaFree(op->r); cudaFree(op->p_ext); cudaFree(op->q);
   cudaFree(op->ghost_lo); cudaFree(op->ghost_hi);
   cudaFree(op->stage_a); cudaFree(op->stage_b);
@@ -464,21 +464,22 @@ int fem_set_material(fem_op_t op, const double* lam, const double* mu, int64_t l
     return fail(FEM_EINVAL, "material layers [%lld, %lld) do not cover the needed [%lld, %lld]",
                 (long long)layer_begin, (long long)(layer_begin + n_layers), (long long)need0, (long long)need1);
   const int64_t nl = need1 - need0 + 1, nxy = g.nx * g.ny, cnt = nl * nxy;
-  if (op->mat_layers != nl) {
-    cudaFree(op->lam); cudaFree(op->mu);
-    op->lam = op->mu = nullptr;
-    FEM_TRY(dalloc(&op->lam, cnt));
-    FEM_TRY(dalloc(&op->mu, cnt));
+  if (op->mat_layers != nl || !op->lm) {
+    cudaFree(op->lm);
+    op->lm = nullptr;
+    op->mat_layers = 0;
+    FEM_TRY(dalloc(&op->lm, cnt));
   }
   const size_t off = (size_t)(need0 - layer_begin) * nxy;
   const cudaMemcpyKind kl = is_device_ptr(lam) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   const cudaMemcpyKind km = is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  CUDA_TRY(cudaMemcpy(op->lam, lam + off, cnt * sizeof(double), kl));
-  CUDA_TRY(cudaMemcpy(op->mu, mu + off, cnt * sizeof(double), km));
+  // interleave (lambda, mu) per cell: one 16-B record ("cell constant C", 2 x 8 B)
+  CUDA_TRY(cudaMemcpy2D(op->lm, 16, lam + off, 8, 8, cnt, kl));
+  CUDA_TRY(cudaMemcpy2D(reinterpret_cast<double*>(op->lm) + 1, 16, mu + off, 8, 8, cnt, km));
   op->mat_layer0 = need0;
   op->mat_layers = nl;
   CUDA_TRY(cudaMemset(op->bad, 0, sizeof(unsigned long long)));
-  CUDA_TRY(launch_check_material(op->lam, op->mu, cnt, op->bad, 0, op->mesh->sm_count));
+  CUDA_TRY(launch_check_material(op->lm, cnt, op->bad, 0, op->mesh->sm_count));
   unsigned long long bad = 0;
   CUDA_TRY(cudaMemcpy(&bad, op->bad, sizeof(bad), cudaMemcpyDeviceToHost));
   if (bad) {
@@ -811,7 +812,7 @@ int fem_csr_create(fem_op_t op, fem_csr_t* out) {
     return fail(FEM_ENOMEM, "CSR needs %.1f GB, %.1f GB free", need / 1e9, fr / 1e9);
   }
   if ((st = dalloc(&c->col, nnz)) || (st = dalloc(&c->val, nnz))) { fem_csr_destroy(c); return st; }
-  e = launch_csr_fill(op->kind, op->bc, g, op->lam, op->mu, c->rowptr, c->col, c->val, 0);
+  e = launch_csr_fill(op->kind, op->bc, g, op->lm, c->rowptr, c->col, c->val, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { fem_csr_destroy(c); return fail(FEM_ECUDA, "csr fill: %s", cudaGetErrorString(e)); }
   *out = c;

@@ -49,9 +49,10 @@ constexpr int kMaxCtas = 1 << 16;
 // mode: 0 plain apply (y = A_c x), 1 CG apply (also pq partial -> sc->pq; skips if sc->done)
 cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, double* y, int mode,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
-cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double* lam, const double* mu,
-                           int64_t mat_layer0, double* y, int mode, CgScalars* sc, Reduce red,
-                           cudaStream_t s, int sm_count);
+// lm: interleaved (lambda, mu) per cell, cell layers [mat_layer0, ...)
+cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double2* lm, int64_t mat_layer0,
+                           double* y, int mode, CgScalars* sc, Reduce red, cudaStream_t s,
+                           int sm_count);
 // CG vector kernels (n = owned DOFs)
 cudaError_t launch_cg_init(const double* b, const double* ax, double* r, double* p, int64_t n,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
@@ -67,12 +68,12 @@ cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out,
 cudaError_t launch_sub(const double* b, const double* ax, double* out, int64_t n, cudaStream_t s,
                        int sm_count);
 // material validation: count of invalid cells -> *bad (device int64)
-cudaError_t launch_check_material(const double* lam, const double* mu, int64_t n,
-                                  unsigned long long* bad, cudaStream_t s, int sm_count);
+cudaError_t launch_check_material(const double2* lm, int64_t n, unsigned long long* bad,
+                                  cudaStream_t s, int sm_count);
 
 // CSR baseline
 cudaError_t launch_csr_rowcount(int comps, int bc, const Grid& g, int64_t* rowptr, cudaStream_t s);
-cudaError_t launch_csr_fill(int kind, int bc, const Grid& g, const double* lam, const double* mu,
+cudaError_t launch_csr_fill(int kind, int bc, const Grid& g, const double2* lm,
                             const int64_t* rowptr, int32_t* col, double* val, cudaStream_t s);
 cudaError_t launch_csr_spmv(int comps, int64_t nrows, const int64_t* rowptr, const int32_t* col,
                             const double* val, const double* x, double* y, cudaStream_t s,

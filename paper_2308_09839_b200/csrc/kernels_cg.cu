@@ -127,12 +127,12 @@ __global__ void sub_kernel(const double* __restrict__ b, const double* __restric
     out[i] = b[i] - ax[i];
 }
 
-__global__ void check_material_kernel(const double* __restrict__ lam, const double* __restrict__ mu,
-                                      int64_t n, unsigned long long* bad) {
+__global__ void check_material_kernel(const double2* __restrict__ lm, int64_t n,
+                                      unsigned long long* bad) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned long long cnt = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const double l = lam[i], m = mu[i];
+    const double l = lm[i].x, m = lm[i].y;
     // mu > 0 and lambda + 2 mu / 3 >= 0, finite
     const bool ok = isfinite(l) && isfinite(m) && m > 0.0 && (l + 2.0 * m / 3.0) >= 0.0;
     cnt += ok ? 0 : 1;
@@ -175,9 +175,9 @@ cudaError_t launch_sub(const double* b, const double* ax, double* out, int64_t n
   add_launches(1);
   return cudaGetLastError();
 }
-cudaError_t launch_check_material(const double* lam, const double* mu, int64_t n,
-                                  unsigned long long* bad, cudaStream_t s, int sm_count) {
-  check_material_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(lam, mu, n, bad);
+cudaError_t launch_check_material(const double2* lm, int64_t n, unsigned long long* bad,
+                                  cudaStream_t s, int sm_count) {
+  check_material_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(lm, n, bad);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -51,8 +51,8 @@ __global__ void csr_rowcount_kernel(int comps, int bc, Grid g, int64_t* __restri
   }
 }
 
-__global__ void csr_fill_kernel(int kind, int bc, Grid g, const double* __restrict__ lam,
-                                const double* __restrict__ mu, const int64_t* __restrict__ rowptr,
+__global__ void csr_fill_kernel(int kind, int bc, Grid g, const double2* __restrict__ lm,
+                                const int64_t* __restrict__ rowptr,
                                 int32_t* __restrict__ col, double* __restrict__ val) {
   const int comps = kind == 0 ? 1 : 3;
   const int64_t nrows = g.plane * (g.nz + 1) * comps;
@@ -86,7 +86,7 @@ __global__ void csr_fill_kernel(int kind, int bc, Grid g, const double* __restri
                 const int rb = (int)((a - ci) + 2 * (b - cj) + 4 * (d - ck));
                 if (kind == 2) {
                   const int64_t e = ci + g.nx * (cj + g.ny * ck);
-                  const double le = lam[e] * g.h, me = mu[e] * g.h;
+                  const double le = lm[e].x * g.h, me = lm[e].y * g.h;
                   for (int l = 0; l < 3; ++l) {
                     const int ix = (3 * ra + kk) * 24 + 3 * rb + l;
                     v[l] += le * c_Kl[ix] + me * c_Km[ix];
@@ -154,12 +154,12 @@ cudaError_t launch_csr_rowcount(int comps, int bc, const Grid& g, int64_t* rowpt
   return e;
 }
 
-cudaError_t launch_csr_fill(int kind, int bc, const Grid& g, const double* lam, const double* mu,
+cudaError_t launch_csr_fill(int kind, int bc, const Grid& g, const double2* lm,
                             const int64_t* rowptr, int32_t* col, double* val, cudaStream_t s) {
   const int comps = kind == 0 ? 1 : 3;
   const int64_t nrows = g.plane * (g.nz + 1) * comps;
   csr_fill_kernel<<<(unsigned)std::min<int64_t>((nrows + 255) / 256, 65535 * 8), 256, 0, s>>>(
-      kind, bc, g, lam, mu, rowptr, col, val);
+      kind, bc, g, lm, rowptr, col, val);
   add_launches(1);
   return cudaGetLastError();
 }

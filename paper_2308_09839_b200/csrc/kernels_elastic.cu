@@ -35,9 +35,8 @@ __device__ __forceinline__ Face face_fwd(double u00, double u10, double u01, dou
 
 template <int TY, int S>
 __global__ void __launch_bounds__(32 * (TY + 1), 1)
-    elastic_kernel(Grid g, PlaneSrc x, const double* __restrict__ lam, const double* __restrict__ mu,
-                   int64_t mat_layer0, double* __restrict__ y, int bc, int mode, int64_t kchunk,
-                   CgScalars* sc, Reduce red) {
+    elastic_kernel(Grid g, PlaneSrc x, const double2* __restrict__ lm, int64_t mat_layer0,
+                   double* __restrict__ y, int bc, int mode, int64_t kchunk, CgScalars* sc, Reduce red) {
   // TY consumer warps (lane = cell column, warp = cell row) + 1 producer warp
   constexpr int TX = 32;
   constexpr int NT = TX * (TY + 1);
@@ -45,7 +44,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
   constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
   constexpr int ACC = 4 * TY * TX * 3;
-  using Ring = PlaneRing<ROWS, COLS, 3, S>;
+  using Ring = PlaneRing<ROWS, COLS, 3, S, TY, TX>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
@@ -67,14 +66,10 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
 
   double pq = 0.0;
   if (ty == TY) {
-    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx);
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, MatSrc{lm, mat_layer0});
   } else {
     const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
-    const bool cell_xy = ci >= 0 && ci < g.nx && cj >= 0 && cj < g.ny;
     const double hs = g.h * (1.0 / 16.0);
-    const int64_t nxy = g.nx * g.ny;
-    const double* lam_c = lam + (cell_xy ? cj * g.nx + ci : 0) - mat_layer0 * nxy;
-    const double* mu_c = mu + (cell_xy ? cj * g.nx + ci : 0) - mat_layer0 * nxy;
     const bool owner = tx >= 1 && ty >= 1 && ci <= g.nx && cj <= g.ny;
     const bool bnode_xy = bc && (ci == 0 || ci == g.nx || cj == 0 || cj == g.ny);
     const int64_t node_off = owner ? (cj * (g.nx + 1) + ci) * 3 : 0;
@@ -85,16 +80,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
 #pragma unroll
     for (int t = 0; t < 12; ++t) cb[t] = 0.0;
 
-    auto load_mat = [&](int64_t k, double& L, double& M) {
-      if (cell_xy && k >= 0 && k < g.nz) {
-        L = __ldg(lam_c + k * nxy) * hs;
-        M = __ldg(mu_c + k * nxy) * hs;
-      } else {
-        L = 0.0; M = 0.0;
-      }
-    };
-    double Ln, Mn;
-    load_mat(pfirst, Ln, Mn);
+    double Ln = 0.0, Mn = 0.0;  // material of the cell layer below the current plane (x h/16)
 
 #pragma unroll 1
     for (int64_t p = pfirst; p <= ke; ++p) {
@@ -104,6 +90,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       ring.wait(slot, (uint32_t)((t / S) & 1));
       Face ft[3];
       double xn[3];
+      const double2 lmn = ring.mat(slot, ty, tx);  // material layer p (used at iteration p+1)
       {
         const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
         const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
@@ -117,11 +104,12 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       if (p == pfirst) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xc[c] = xn[c]; }
+        Ln = lmn.x * hs; Mn = lmn.y * hs;
         continue;
       }
       // ---- cell layer k = p-1 ----
       const double L0 = Ln, M0 = Mn;
-      if (p < ke) load_mat(p, Ln, Mn);  // prefetch next layer
+      Ln = lmn.x * hs; Mn = lmn.y * hs;
       // modal coefficients (unnormalised): component u=0, v=1, w=2
       // x = ds, y = sd, xy = dd summed over z; z, xz, yz, xyz = differences in z
       const double ux = fb[0].x + ft[0].x, uy = fb[0].y + ft[0].y, uxy = fb[0].xy + ft[0].xy;
@@ -215,11 +203,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
 }
 
 template <int TY, int S>
-static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double* lam, const double* mu,
-                              int64_t mat_layer0, double* y, int bc, int mode, CgScalars* sc,
-                              Reduce red, cudaStream_t s, int sm_count) {
+static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double2* lm, int64_t mat_layer0,
+                              double* y, int bc, int mode, CgScalars* sc, Reduce red, cudaStream_t s,
+                              int sm_count) {
   constexpr int TX = 32;
-  using Ring = PlaneRing<TY + 1, TX + 1, 3, S>;
+  using Ring = PlaneRing<TY + 1, TX + 1, 3, S, TY, TX>;
   const size_t smem = Ring::BYTES + 2 * 4 * TY * TX * 3 * sizeof(double) + Ring::META;
   auto kern = elastic_kernel<TY, S>;
   static bool attr_set = false;
@@ -237,15 +225,15 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double* lam, cons
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
-  kern<<<grid, block, smem, s>>>(g, x, lam, mu, mat_layer0, y, bc, mode, kchunk, sc, red);
+  kern<<<grid, block, smem, s>>>(g, x, lm, mat_layer0, y, bc, mode, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double* lam, const double* mu,
-                           int64_t mat_layer0, double* y, int mode, CgScalars* sc, Reduce red,
-                           cudaStream_t s, int sm_count) {
-  return launch_cfg<15, 4>(g, x, lam, mu, mat_layer0, y, bc, mode, sc, red, s, sm_count);
+cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double2* lm, int64_t mat_layer0,
+                           double* y, int mode, CgScalars* sc, Reduce red, cudaStream_t s,
+                           int sm_count) {
+  return launch_cfg<15, 4>(g, x, lm, mat_layer0, y, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2) laplace_kernel(Grid g, PlaneSr
 
   double pq = 0.0;
   if (ty == TY) {
-    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx);
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, MatSrc{nullptr, 0});
   } else {
     const int64_t i = i0 + tx;
     const double h36 = g.h * (1.0 / 36.0);
