@@ -445,10 +445,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--csr-n", type=int, default=0)
     ap.add_argument("--e2e-iters", type=int, default=100)
+    ap.add_argument("--n", type=int, default=0, help="override cells per direction (debug)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = I.CONFIGS[args.config]
+    cfg = dict(I.CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = (args.n, args.n, args.n)
+        cfg["name"] += f"_n{args.n}"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

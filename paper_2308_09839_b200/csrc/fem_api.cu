@@ -1,6 +1,8 @@
 // fem_api.cu -- host side of libfem.so: the C ABI declared in include/fem.h.
 // Handles, validation, workspace, slab partition + NCCL halo/allreduce, the CG driver
 // (CUDA-graph captured iteration) and the CSR baseline.  Kernels live in kernels_*.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -79,15 +81,21 @@ struct fem_mesh_s {
 struct fem_op_s {
   fem_mesh_s* mesh = nullptr;
   int kind = 0, bc = 0, comps = 1;
-  int64_t n_local = 0, n_global = 0, plane_dofs = 0;
+  int64_t n_local = 0, n_global = 0, plane_dofs = 0, nloc_planes = 0;
   // material (local cell layers [mat_layer0, mat_layer0 + mat_layers)), (lambda, mu) interleaved
   double2* lm = nullptr;
   int64_t mat_layer0 = 0, mat_layers = 0;
   bool has_mat = false;
-  // workspace
-  double *r = nullptr, *p_ext = nullptr, *q = nullptr;
+  // dense-layout workspace (fem_apply on caller vectors, host staging)
   double *ghost_lo = nullptr, *ghost_hi = nullptr;
   double *stage_a = nullptr, *stage_b = nullptr;
+  // CG vectors in the library padded layout: node (i,j) comp c of local plane kk
+  // (kk = 0 is the ghost plane k0-1) at v[pl_lead + kk*pl_pp + j*pl_rp + i*C + c]
+  int64_t pl_lead = 0, pl_rp = 0, pl_pp = 0, pl_n = 0;
+  double *x_pl = nullptr, *r_pl = nullptr, *p_pl = nullptr, *q_pl = nullptr;
+  CUtensorMap tm_x{}, tm_p{}, tm_mat{};
+  bool tm_ok = false;
+  int64_t tm_i0 = 0, tm_j0 = 0, tm_k0 = 0;
   CgScalars* sc = nullptr;
   CgScalars* sc_host = nullptr;
   double* dot_dev = nullptr;
@@ -99,10 +107,6 @@ struct fem_op_s {
   double* cg_x = nullptr;
   bool cg_active = false;
   cudaGraphExec_t graph1 = nullptr, graphN = nullptr;
-  int graphN_iters = 0;
-  const double* graph_b = nullptr;
-  double* graph_x = nullptr;
-  cudaStream_t graph_stream = nullptr;
   // options
   int use_graph = 1, check_every = 16, time_apply = 0;
   std::vector<cudaEvent_t> ev;
@@ -212,11 +216,12 @@ static int need_comm(fem_op_s* op) {
   return FEM_OK;
 }
 
-// one node-plane halo per neighbour (ncclSend/Recv pairs in one group)
-static int halo(fem_op_s* op, const double* owned, double* lo, double* hi, cudaStream_t s) {
+// one node-plane halo per neighbour (ncclSend/Recv pairs in one group); planes `pitch` apart
+static int halo_pitch(fem_op_s* op, const double* owned, double* lo, double* hi, int64_t pitch,
+                      cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
   if (m->nranks == 1) return FEM_OK;
-  const size_t cnt = (size_t)op->plane_dofs;
+  const size_t cnt = (size_t)pitch;
   const int64_t np = m->g.k1 - m->g.k0;
   ncclComm_t c = m->comm->nccl;
   NCCL_TRY(ncclGroupStart());
@@ -225,11 +230,14 @@ static int halo(fem_op_s* op, const double* owned, double* lo, double* hi, cudaS
     NCCL_TRY(ncclRecv(lo, cnt, ncclDouble, m->rank - 1, c, s));
   }
   if (m->rank < m->nranks - 1) {
-    NCCL_TRY(ncclSend(owned + (np - 1) * op->plane_dofs, cnt, ncclDouble, m->rank + 1, c, s));
+    NCCL_TRY(ncclSend(owned + (np - 1) * pitch, cnt, ncclDouble, m->rank + 1, c, s));
     NCCL_TRY(ncclRecv(hi, cnt, ncclDouble, m->rank + 1, c, s));
   }
   NCCL_TRY(ncclGroupEnd());
   return FEM_OK;
+}
+static int halo(fem_op_s* op, const double* owned, double* lo, double* hi, cudaStream_t s) {
+  return halo_pitch(op, owned, lo, hi, op->plane_dofs, s);
 }
 
 static int allreduce1(fem_op_s* op, double* dev_scalar, cudaStream_t s) {
@@ -239,25 +247,129 @@ static int allreduce1(fem_op_s* op, double* dev_scalar, cudaStream_t s) {
   return FEM_OK;
 }
 
-// apply kernel dispatch; x given as a plane source
-static int launch_apply(fem_op_s* op, PlaneSrc x, double* y, int mode, cudaStream_t s) {
+// ---- TMA tensor maps (driver entry point; no link against libcuda) --------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encode() {
+  if (g_encode) return FEM_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return fail(FEM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return FEM_OK;
+}
+
+// 3-D FP64 tiled map: dims (d0 contiguous, d1 rows of stride s1 bytes, d2 planes of stride s2),
+// box (b0, b1, 1); out-of-range elements of a box are zero-filled by the copy engine.
+static int make_map3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint64_t s1, uint64_t s2, uint32_t b0, uint32_t b1) {
+  FEM_TRY(get_encode());
+  if (((uintptr_t)base & 15) || (s1 & 15) || (s2 & 15) || ((b0 * 8) & 15))
+    return fail(FEM_EINVAL, "tensor map alignment violated");
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {s1, s2};
+  const cuuint32_t box[3] = {b0, b1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FEM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return FEM_OK;
+}
+
+// u-plane maps of the padded CG vectors: only the nodes the operator may read (the interior
+// with the Dirichlet box) lie inside the tensor, so the TMA zero fill is the mask P.
+static int make_pl_maps(fem_op_s* op) {
+  const Grid& g = op->mesh->g;
+  const int C = op->comps;
+  const int64_t lo = op->bc ? 1 : 0;
+  const int64_t i1 = op->bc ? g.nx - 1 : g.nx, j1 = op->bc ? g.ny - 1 : g.ny;
+  const int64_t k0 = std::max<int64_t>(lo, g.k0 - 1), k1 = std::min<int64_t>(op->bc ? g.nz - 1 : g.nz, g.k1);
+  op->tm_ok = false;
+  if (i1 < lo || j1 < lo || k1 < k0) return FEM_OK;  // degenerate: the bulk-row path is used
+  unsigned bw, bh;
+  u_box(op->kind, &bw, &bh);
+  op->tm_i0 = lo;
+  op->tm_j0 = lo;
+  op->tm_k0 = k0;
+  const int64_t off = op->pl_lead + (k0 - (g.k0 - 1)) * op->pl_pp + lo * op->pl_rp + lo * C;
+  for (int v = 0; v < 2; ++v) {
+    const double* base = (v == 0 ? op->x_pl : op->p_pl) + off;
+    FEM_TRY(make_map3d(v == 0 ? &op->tm_x : &op->tm_p, base, (uint64_t)((i1 - lo + 1) * C),
+                       (uint64_t)(j1 - lo + 1), (uint64_t)(k1 - k0 + 1), op->pl_rp * 8, op->pl_pp * 8,
+                       bw, bh));
+  }
+  op->tm_ok = true;
+  return FEM_OK;
+}
+
+static int make_mat_map(fem_op_s* op) {
+  const Grid& g = op->mesh->g;
+  unsigned bw, bh;
+  mat_box(&bw, &bh);
+  return make_map3d(&op->tm_mat, op->lm, (uint64_t)(2 * g.nx), (uint64_t)g.ny, (uint64_t)op->mat_layers,
+                    (uint64_t)g.nx * 16, (uint64_t)g.nx * g.ny * 16, bw, bh);
+}
+
+// apply kernel dispatch
+static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* umap, int mode,
+                        cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
+  ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
-    e = launch_elastic(op->bc, m->g, x, op->lm, op->mat_layer0, y, mode, op->sc, op->red, s,
-                       m->sm_count);
+    e = launch_elastic(op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
   else
-    e = launch_laplace(op->comps, op->bc, m->g, x, y, mode, op->sc, op->red, s, m->sm_count);
+    e = launch_laplace(op->comps, op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "apply launch failed: %s", cudaGetErrorString(e));
   return FEM_OK;
 }
 
-// y = A_c x for a DEVICE owned vector x (halo via op ghost buffers)
+static PlaneSrc dense_src(fem_op_s* op, const double* x, const double* lo, const double* hi) {
+  const Grid& g = op->mesh->g;
+  return PlaneSrc{x, lo, hi, (g.nx + 1) * op->comps, g.plane * op->comps};
+}
+static OutVec dense_out(fem_op_s* op, double* y) {
+  const Grid& g = op->mesh->g;
+  return OutVec{y, (g.nx + 1) * op->comps, g.plane * op->comps};
+}
+static double* pl_owned(fem_op_s* op, double* v) { return v + op->pl_lead + op->pl_pp; }
+static PlaneSrc pl_src(fem_op_s* op, double* v) {
+  fem_mesh_s* m = op->mesh;
+  return PlaneSrc{pl_owned(op, v), m->rank > 0 ? v + op->pl_lead : nullptr,
+                  m->rank < m->nranks - 1 ? v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp : nullptr,
+                  op->pl_rp, op->pl_pp};
+}
+static OutVec pl_out(fem_op_s* op, double* v) { return OutVec{pl_owned(op, v), op->pl_rp, op->pl_pp}; }
+static int64_t pl_count(fem_op_s* op) { return op->nloc_planes * op->pl_pp; }  // owned range
+
+// y = A_c x for a DEVICE dense owned vector x (halo via op ghost buffers)
 static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s) {
   FEM_TRY(halo(op, x, op->ghost_lo, op->ghost_hi, s));
-  PlaneSrc src{x, op->mesh->rank > 0 ? op->ghost_lo : nullptr,
-               op->mesh->rank < op->mesh->nranks - 1 ? op->ghost_hi : nullptr};
-  return launch_apply(op, src, y, 0, s);
+  PlaneSrc src = dense_src(op, x, op->mesh->rank > 0 ? op->ghost_lo : nullptr,
+                           op->mesh->rank < op->mesh->nranks - 1 ? op->ghost_hi : nullptr);
+  return launch_apply(op, src, dense_out(op, y), nullptr, 0, s);
+}
+
+// q_pl = A_c v for a padded CG vector v (x_pl or p_pl): halo into its ghost planes, TMA path
+static int apply_pl(fem_op_s* op, double* v, const CUtensorMap* map, int mode, cudaStream_t s) {
+  fem_mesh_s* m = op->mesh;
+  if (m->nranks > 1) {
+    double* own = pl_owned(op, v);
+    FEM_TRY(halo_pitch(op, own, v + op->pl_lead, v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp,
+                       op->pl_pp, s));
+  }
+  return launch_apply(op, pl_src(op, v), pl_out(op, op->q_pl), op->tm_ok ? map : nullptr, mode, s);
+}
+
+static int pack(fem_op_s* op, const double* dense, double* v, int to_padded, cudaStream_t s) {
+  const Grid& g = op->mesh->g;
+  cudaError_t e = launch_pack(dense, pl_owned(op, v), op->pl_rp, op->pl_pp, op->nloc_planes, g.nx + 1,
+                              g.ny + 1, op->comps, to_padded, s, op->mesh->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "pack launch: %s", cudaGetErrorString(e));
+  return FEM_OK;
 }
 
 static int ensure_stage(fem_op_s* op) {
@@ -267,8 +379,8 @@ static int ensure_stage(fem_op_s* op) {
 }
 
 static int dot_device(fem_op_s* op, const double* a, const double* b, cudaStream_t s,
-                      double* result) {
-  cudaError_t e = launch_dot(a, b, op->n_local, op->dot_dev, op->red, s, op->mesh->sm_count);
+                      double* result, int64_t n = -1) {
+  cudaError_t e = launch_dot(a, b, n < 0 ? op->n_local : n, op->dot_dev, op->red, s, op->mesh->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "dot launch failed: %s", cudaGetErrorString(e));
   FEM_TRY(allreduce1(op, op->dot_dev, s));
   CUDA_TRY(cudaMemcpyAsync(op->dot_host, op->dot_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -379,7 +491,7 @@ static void op_free(fem_op_s* op) {
   if (op->graphN) cudaGraphExecDestroy(op->graphN);
   for (auto e : op->ev) cudaEventDestroy(e);
   cudaFree(op->lm);
-  cudaFree(op->r); cudaFree(op->p_ext); cudaFree(op->q);
+  cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl);
   cudaFree(op->ghost_lo); cudaFree(op->ghost_hi);
   cudaFree(op->stage_a); cudaFree(op->stage_b);
   cudaFree(op->sc); cudaFree(op->dot_dev); cudaFree(op->bad);
@@ -403,8 +515,14 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   op->comps = kind == FEM_SCALAR_LAPLACE ? 1 : 3;
   const Grid& g = mesh->g;
   op->plane_dofs = g.plane * op->comps;
-  op->n_local = (g.k1 - g.k0) * op->plane_dofs;
+  op->nloc_planes = g.k1 - g.k0;
+  op->n_local = op->nloc_planes * op->plane_dofs;
   op->n_global = (g.nz + 1) * op->plane_dofs;
+  // padded layout: even row pitch, lead so that the tensor origin node is 16-B aligned
+  op->pl_rp = ((g.nx + 1) * op->comps + 1) & ~1LL;
+  op->pl_pp = op->pl_rp * (g.ny + 1);
+  op->pl_lead = bc ? (op->comps & 1) : 0;
+  op->pl_n = (op->pl_lead + (op->nloc_planes + 2) * op->pl_pp + 1) & ~1LL;
   int st = FEM_OK;
 #define OP_TRY(x)                 \
   do {                            \
@@ -414,9 +532,10 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
       return st;                  \
     }                             \
   } while (0)
-  OP_TRY(dalloc(&op->r, op->n_local));
-  OP_TRY(dalloc(&op->p_ext, op->n_local + 2 * op->plane_dofs));
-  OP_TRY(dalloc(&op->q, op->n_local));
+  OP_TRY(dalloc(&op->x_pl, op->pl_n));
+  OP_TRY(dalloc(&op->r_pl, op->pl_n));
+  OP_TRY(dalloc(&op->p_pl, op->pl_n));
+  OP_TRY(dalloc(&op->q_pl, op->pl_n));
   OP_TRY(dalloc(&op->ghost_lo, op->plane_dofs));
   OP_TRY(dalloc(&op->ghost_hi, op->plane_dofs));
   OP_TRY(dalloc(&op->sc, 1));
@@ -433,11 +552,15 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   }
   if (cudaMemset(op->red.ticket, 0, sizeof(unsigned int)) != cudaSuccess ||
       cudaMemset(op->sc, 0, sizeof(CgScalars)) != cudaSuccess ||
-      cudaMemset(op->p_ext, 0, sizeof(double) * (op->n_local + 2 * op->plane_dofs)) != cudaSuccess) {
+      cudaMemset(op->x_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
+      cudaMemset(op->r_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
+      cudaMemset(op->p_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
+      cudaMemset(op->q_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess) {
     op_free(op);
     return fail(FEM_ECUDA, "cudaMemset failed");
   }
   OP_TRY(ensure_unit_matrices(mesh->device));
+  OP_TRY(make_pl_maps(op));
 #undef OP_TRY
   *out = op;
   return FEM_OK;
@@ -486,6 +609,7 @@ int fem_set_material(fem_op_t op, const double* lam, const double* mu, int64_t l
     op->has_mat = false;
     return fail(FEM_EMATERIAL, "%llu cells violate mu > 0, lambda + 2 mu / 3 >= 0 (S:249)", bad);
   }
+  FEM_TRY(make_mat_map(op));
   op->has_mat = true;
   op->cg_active = false;
   return FEM_OK;
@@ -504,8 +628,8 @@ int fem_apply_ghost(fem_op_t op, const double* x, const double* glo, const doubl
   if (!is_device_ptr(x) || !is_device_ptr(y) || (glo && !is_device_ptr(glo)) || (ghi && !is_device_ptr(ghi)))
     return fail(FEM_EINVAL, "fem_apply_ghost needs device pointers");
   FEM_TRY(set_device(op->mesh->device));
-  PlaneSrc src{x, g.k0 > 0 ? glo : nullptr, g.k1 <= g.nz ? ghi : nullptr};
-  return launch_apply(op, src, y, 0, (cudaStream_t)stream);
+  PlaneSrc src = dense_src(op, x, g.k0 > 0 ? glo : nullptr, g.k1 <= g.nz ? ghi : nullptr);
+  return launch_apply(op, src, dense_out(op, y), nullptr, 0, (cudaStream_t)stream);
 }
 
 int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
@@ -557,9 +681,7 @@ int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void*
 // ---- CG -----------------------------------------------------------------------------------
 static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
-  double* p = op->p_ext + op->plane_dofs;  // owned part
-  FEM_TRY(halo(op, p, op->p_ext, p + op->n_local, s));
-  PlaneSrc src{p, m->rank > 0 ? op->p_ext : nullptr, m->rank < m->nranks - 1 ? p + op->n_local : nullptr};
+  const int64_t n = pl_count(op);
   if (timed) {
     if (op->ev_used + 2 > op->ev.size()) {
       for (int t = 0; t < 64; ++t) {
@@ -570,16 +692,17 @@ static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
     }
     CUDA_TRY(cudaEventRecord(op->ev[op->ev_used], s));
   }
-  FEM_TRY(launch_apply(op, src, op->q, 1, s));
+  FEM_TRY(apply_pl(op, op->p_pl, &op->tm_p, 1, s));  // q = A p, pq (halo inside when P > 1)
   if (timed) {
     CUDA_TRY(cudaEventRecord(op->ev[op->ev_used + 1], s));
     op->ev_used += 2;
   }
   FEM_TRY(allreduce1(op, &op->sc->pq, s));
-  cudaError_t e = launch_cg_update(op->cg_x, op->r, p, op->q, op->n_local, op->sc, op->red, s, m->sm_count);
+  cudaError_t e = launch_cg_update(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, op->p_pl),
+                                   pl_owned(op, op->q_pl), n, op->sc, op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
   FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
-  e = launch_cg_pupdate(op->r, p, op->n_local, op->sc, op->red, s, m->sm_count);
+  e = launch_cg_pupdate(pl_owned(op, op->r_pl), pl_owned(op, op->p_pl), n, op->sc, op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "pupdate launch: %s", cudaGetErrorString(e));
   return FEM_OK;
 }
@@ -612,11 +735,14 @@ static int capture(fem_op_s* op, int iters, cudaStream_t s, cudaGraphExec_t* out
   return FEM_OK;
 }
 
+// CG on the padded copies: x_pl = x0; r = b - A x0; p = r (the caller's x is written at the end)
 static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, int maxit, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
-  double* p = op->p_ext + op->plane_dofs;
-  FEM_TRY(apply_device(op, x, op->q, s));  // q = A x0
-  cudaError_t e = launch_cg_init(b, op->q, op->r, p, op->n_local, op->sc, op->red, s, m->sm_count);
+  FEM_TRY(pack(op, x, op->x_pl, 1, s));
+  FEM_TRY(apply_pl(op, op->x_pl, &op->tm_x, 0, s));  // q = A x0
+  FEM_TRY(pack(op, b, op->r_pl, 1, s));              // r = b
+  cudaError_t e = launch_cg_init(pl_owned(op, op->r_pl), pl_owned(op, op->q_pl), pl_owned(op, op->r_pl),
+                                 pl_owned(op, op->p_pl), pl_count(op), op->sc, op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "init launch: %s", cudaGetErrorString(e));
   FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
   e = launch_cg_finish_init(op->sc, tol, maxit, s);
@@ -624,12 +750,6 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
   op->cg_b = b;
   op->cg_x = x;
   op->cg_active = true;
-  if (op->graph_x != x || op->graph_b != b) {
-    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
-    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
-    op->graph_x = x;
-    op->graph_b = b;
-  }
   return FEM_OK;
 }
 
@@ -656,6 +776,7 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
 }
 
 static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
+  FEM_TRY(pack(op, op->cg_x, op->x_pl, 0, s));  // x = x_pl (caller layout)
   CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   const CgScalars h = *op->sc_host;
@@ -668,11 +789,13 @@ static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
     info->r0_norm = std::sqrt(h.rr0);
     info->r_norm = std::sqrt(h.rr);
     // true residual ||b - A x||
-    FEM_TRY(apply_device(op, op->cg_x, op->q, s));
-    cudaError_t e = launch_sub(op->cg_b, op->q, op->r, op->n_local, s, op->mesh->sm_count);
+    FEM_TRY(apply_pl(op, op->x_pl, &op->tm_x, 0, s));
+    FEM_TRY(pack(op, op->cg_b, op->r_pl, 1, s));
+    double* r = pl_owned(op, op->r_pl);
+    cudaError_t e = launch_sub(r, pl_owned(op, op->q_pl), r, pl_count(op), s, op->mesh->sm_count);
     if (e != cudaSuccess) return fail(FEM_ECUDA, "sub launch: %s", cudaGetErrorString(e));
     double tr = 0.0;
-    FEM_TRY(dot_device(op, op->r, op->r, s, &tr));
+    FEM_TRY(dot_device(op, r, r, s, &tr, pl_count(op)));
     info->true_r_norm = std::sqrt(tr);
     op->cg_active = false;  // r was overwritten
   }

@@ -1,6 +1,7 @@
 // fem_internal.cuh -- shared device/host declarations of the CUDA path (libfem.so).
 // Not part of the ABI.  Independent of oracle/ (no shared code, tables or constants).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -14,12 +15,30 @@ struct Grid {
   int64_t plane;         // nodes per plane = (nx+1)(ny+1)
 };
 
-// Source of a node-plane-indexed vector: owned planes at `main` (plane k at main + (k-k0)*plane*c),
-// optional ghost planes below/above (multi-GPU halo), others are outside the domain.
+// Source of a node-plane-indexed vector: node (i, j) comp c of owned plane k at
+//   main[(k - k0) * ppitch + j * rpitch + i * C + c]
+// (dense ABI layout: rpitch = (nx+1) C, ppitch = (nx+1)(ny+1) C; the library's padded layout has
+// even pitches), optional ghost planes below/above (multi-GPU halo) with the same
+// row pitch; other planes are outside the domain.
 struct PlaneSrc {
   const double* main;
   const double* lo;  // plane k0-1 (may be null: outside domain or not exchanged)
   const double* hi;  // plane k1
+  int64_t rpitch, ppitch;
+};
+
+// Output vector: node (i, j) comp c of owned plane k at y[(k - k0) * ppitch + j * rpitch + i*C + c].
+struct OutVec {
+  double* y;
+  int64_t rpitch, ppitch;
+};
+
+// TMA tensor maps of one apply launch (u plane: padded layout; material: interleaved lambda/mu)
+struct ApplyMaps {
+  const CUtensorMap* u;    // nullptr: use the bulk-row path
+  int64_t t_i0, t_j0, t_k0;  // global node of the u tensor origin
+  const CUtensorMap* mat;  // elasticity only
+  int64_t mat_layer0;
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).
@@ -45,14 +64,27 @@ struct Reduce {
 
 constexpr int kMaxCtas = 1 << 16;
 
+// Tile shapes of the apply kernels (kernel templates and host tensor-map boxes must agree).
+constexpr int kLapTX = 32, kLapTY = 8, kLapR1 = 2, kLapR3 = 1;  // Laplace: C=1 / C=3 rows per thread
+constexpr int kElTY = 15;                                         // elasticity consumer warps
+// u-plane TMA box (doubles x rows) per kind: width = (((cols * C) + 1) & ~1) + 2
+inline void u_box(int kind, unsigned* w, unsigned* h) {
+  if (kind == 0) { *w = ((((kLapTX + 2) * 1) + 1) & ~1) + 2; *h = kLapTY * kLapR1 + 2; }
+  else if (kind == 1) { *w = ((((kLapTX + 2) * 3) + 1) & ~1) + 2; *h = kLapTY * kLapR3 + 2; }
+  else { *w = ((((32 + 1) * 3) + 1) & ~1) + 2; *h = kElTY + 1; }
+}
+inline void mat_box(unsigned* w, unsigned* h) { *w = 2 * 32; *h = kElTY; }
+
 // ---- launchers (return cudaError_t of the launch) -----------------------------------------
 // mode: 0 plain apply (y = A_c x), 1 CG apply (also pq partial -> sc->pq; skips if sc->done)
-cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, double* y, int mode,
+cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps,
+                           int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
+cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int mode,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
-// lm: interleaved (lambda, mu) per cell, cell layers [mat_layer0, ...)
-cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double2* lm, int64_t mat_layer0,
-                           double* y, int mode, CgScalars* sc, Reduce red, cudaStream_t s,
-                           int sm_count);
+// dense ABI <-> padded layout (owned planes): n_planes planes of (nx+1)(ny+1) nodes x C
+cudaError_t launch_pack(const double* dense, double* padded, int64_t rpitch, int64_t ppitch,
+                        int64_t n_planes, int64_t nxn, int64_t nyn, int comps, int to_padded,
+                        cudaStream_t s, int sm_count);
 // CG vector kernels (n = owned DOFs)
 cudaError_t launch_cg_init(const double* b, const double* ax, double* r, double* p, int64_t n,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);

@@ -183,3 +183,35 @@ cudaError_t launch_check_material(const double2* lm, int64_t n, unsigned long lo
 }
 
 }  // namespace fem
+
+namespace fem {
+// dense ABI layout <-> library padded layout for n_planes planes:
+// dense (i,j,k,c) at ((k*nyn + j)*nxn + i)*C + c; padded at k*ppitch + j*rpitch + i*C + c.
+__global__ void pack_kernel(const double* __restrict__ dense, double* __restrict__ padded,
+                            int64_t rpitch, int64_t ppitch, int64_t n_planes, int64_t nxn,
+                            int64_t nyn, int comps, int to_padded) {
+  const int64_t rowlen = nxn * comps;
+  const int64_t nrows = n_planes * nyn;
+  // one warp-strided pass per row
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrows; r += warps) {
+    const int64_t k = r / nyn, j = r - k * nyn;
+    const double* d = dense + r * rowlen;
+    double* pd = padded + k * ppitch + j * rpitch;
+    if (to_padded)
+      for (int64_t e = lane; e < rowlen; e += 32) pd[e] = d[e];
+    else
+      for (int64_t e = lane; e < rowlen; e += 32) const_cast<double*>(d)[e] = pd[e];
+  }
+}
+
+cudaError_t launch_pack(const double* dense, double* padded, int64_t rpitch, int64_t ppitch,
+                        int64_t n_planes, int64_t nxn, int64_t nyn, int comps, int to_padded,
+                        cudaStream_t s, int sm_count) {
+  pack_kernel<<<(unsigned)sm_count * 8, 256, 0, s>>>(dense, padded, rpitch, ppitch, n_planes, nxn,
+                                                      nyn, comps, to_padded);
+  add_launches(1);
+  return cudaGetLastError();
+}
+}  // namespace fem

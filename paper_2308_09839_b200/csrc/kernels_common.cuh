@@ -1,33 +1,39 @@
 // kernels_common.cuh -- node-plane staging shared by the apply kernels (sm_100a).
 //
-// A CTA marches along z over node planes.  A dedicated producer warp streams plane k's halo tile
-// (ROWS rows x COLS node columns x C components) into a ring slot of shared memory: lane r issues
-// ONE bulk copy (cp.async.bulk, the TMA copy engine; SASS UBLKCP) for the 16-B aligned middle of
-// row r and at most two 8-B cp.async for its ragged ends, all completing on the slot's `full`
-// mbarrier; consumer warps release a slot through its `empty` mbarrier (no CTA-wide barrier).
-// The caller's vectors keep the dense ABI layout whose rows are only 8-B aligned (257 or 385
-// nodes per row), which is why tiled TMA tensor maps (16-B strides) are not used.  Per-row copy
-// descriptors are computed once per CTA; per plane the producer only adds the plane base.
+// A CTA marches along z over node planes.  A dedicated producer warp streams each plane's halo
+// tile (ROWS rows x COLS node columns x C components) into a ring slot of shared memory; consumer
+// warps wait on the slot's `full` mbarrier and release it through its `empty` mbarrier (no
+// CTA-wide barrier on the data path).  Two staging policies for the u plane:
 //
-// Masking: only DOFs that the operator may read are copied -- domain nodes, and with the
-// Dirichlet box only interior nodes.  Every other position of the ring is zero: zeroed
-// once at kernel start, and the two positions adjacent to a row's valid range are re-zeroed per
-// copy (the 8-B alignment shift `lead` of a row can differ between planes).  Planes with no
-// operator data (outside the box, or a Dirichlet face plane) are served from a permanent zero
-// slot.  The consumer therefore reads without any per-element mask.
+//  * TM = true  (library-internal "padded layout", used inside CG): ONE TMA tensor copy per plane
+//    (cp.async.bulk.tensor.3d, SASS UTMALDG) of a ROWS x BOXW box.  The tensor map describes only
+//    the nodes the operator may read (the interior with the Dirichlet box), so TMA's
+//    out-of-bounds zero fill IS the mask P of y = P A P x + (I-P) x and the domain-edge padding.
+//  * TM = false (caller vectors in the dense ABI layout, rows only 8-B aligned e.g. 257/385
+//    nodes, which tensor maps cannot describe): lane r issues one bulk copy (cp.async.bulk, SASS
+//    UBLKCP) for the 16-B aligned middle of row r and <= 2 8-B cp.async for its ragged ends.  Only
+//    readable nodes are copied; every other ring position is zero (zeroed at start, the two
+//    positions next to a row's valid range re-zeroed per copy because the 8-B shift `lead` can
+//    change between planes; planes without operator data are served from a zero slot).
 //
-// Optional second stream (elasticity): the cell-material layer k (lambda, mu interleaved as
-// double2, always 16-B aligned) is copied with the same slot, one bulk copy per cell row.
+// Measured on this pool (tools/microbench/bulk_copy.cu, profiles/r01_microbench_bulk_copy.txt):
+// the copy engine accepts ~65 bulk copies / us / SM, so copies must be >= 1 KB to reach HBM
+// bandwidth -- the reason for the tensor path (one copy per plane) inside CG.
+//
+// Optional material stream (elasticity): the cell layer k of interleaved (lambda, mu) is fetched
+// with the same slot by one TMA tensor copy (cells outside the box read as zero -> no
+// contribution).
 #pragma once
+#include <cuda.h>
+
 #include "fem_internal.cuh"
 
 namespace fem {
 
 // Pointer to node plane k of a plane-indexed vector (nullptr: outside the domain / not held).
-__device__ __forceinline__ const double* plane_ptr(const PlaneSrc& x, const Grid& g, int64_t k,
-                                                   int comps) {
+__device__ __forceinline__ const double* plane_ptr(const PlaneSrc& x, const Grid& g, int64_t k) {
   if (k < 0 || k > g.nz) return nullptr;
-  if (k >= g.k0 && k < g.k1) return x.main + (k - g.k0) * g.plane * comps;
+  if (k >= g.k0 && k < g.k1) return x.main + (k - g.k0) * x.ppitch;
   if (k == g.k0 - 1) return x.lo;
   if (k == g.k1) return x.hi;
   return nullptr;
@@ -70,6 +76,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -83,32 +100,47 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
 
-// Optional material stream (elasticity): interleaved (lambda, mu) per cell, cell layers.
-struct MatSrc {
-  const double2* lm;  // cell (i,j,k) at lm[(k - layer0) * nx * ny + j * nx + i]; nullptr: none
-  int64_t layer0;
+// Tensor-map coordinates of a tile: box origin = node (ilo, jlo) of plane k, relative to the
+// tensor origin (node (t_i0, t_j0) of plane t_k0).  Out-of-range coordinates zero-fill.
+struct TmaOrigin {
+  int64_t t_i0, t_j0, t_k0;
 };
 
-// Ring of S plane slots + one zero slot.  Slot layout: ROWS rows of PITCH doubles (PITCH even,
-// >= COLS*C + 4); a row's data starts at element lead[slot][row] in {2, 3} (+ col*C + comp).
-// With MROWS > 0 each slot also holds MROWS x MCOLS double2 of material.
-// full[s]: completes when plane data landed (ROWS+1 arrivals + tx bytes);
-// empty[s]: completes when the consumer warps released the slot.
-template <int ROWS, int COLS, int C, int S, int MROWS = 0, int MCOLS = 0>
+// Ring of S plane slots.  Slot: u region ROWS x PITCH doubles (+ material MROWS x MPITCH).
+//   TM:  PITCH = BOXW (box width, doubles); data at row r, element col*C + comp.
+//   !TM: PITCH even >= COLS*C + 4, row data start at lead[slot][row] in {2,3}; slot S = zeros.
+template <bool TM, int ROWS, int COLS, int C, int S, int MROWS = 0, int MCOLS = 0>
 struct PlaneRing {
-  static constexpr int PITCH = ((COLS * C + 4) + 1) & ~1;
-  static constexpr int SLOT = ROWS * PITCH + 2 * MROWS * MCOLS;  // doubles
-  static constexpr size_t BYTES = (size_t)(S + 1) * SLOT * sizeof(double);  // + zero slot
+  // box width: COLS*C rounded to even, +2 so the box can start one element early (the box x
+  // origin must be 16-B aligned: odd element offsets are shifted, see tshift)
+  static constexpr int BOXW = (((COLS * C) + 1) & ~1) + 2;
+  static constexpr int PITCH = TM ? BOXW : (((COLS * C + 4) + 1) & ~1);
+  static constexpr int UDBL = ((ROWS * PITCH) + 15) & ~15;          // 128-B multiple
+  static constexpr int MPITCH = 2 * MCOLS;                           // doubles per material row
+  static constexpr int MDBL = ((MROWS * MPITCH) + 15) & ~15;
+  static constexpr int SLOT = UDBL + MDBL;                           // doubles, 128-B multiple
+  static constexpr int NSLOT = TM ? S : S + 1;
+  static constexpr size_t BYTES = (size_t)NSLOT * SLOT * sizeof(double);
   static constexpr size_t META = 2 * S * sizeof(uint64_t) + ((S + 1) * ROWS + 2 * S) * sizeof(int);
-  static_assert(ROWS <= 32 && MROWS <= 32, "one producer lane per row");
+  static constexpr uint32_t UBOX_BYTES = ROWS * BOXW * 8;
+  static constexpr uint32_t MBOX_BYTES = MROWS * MPITCH * 8;
+  static_assert(ROWS <= 32, "one producer lane per row");
   static_assert((S & (S - 1)) == 0, "S must be a power of two");
+  static_assert(ROWS <= 256 && BOXW <= 256 && MPITCH <= 256, "TMA box dims <= 256");
 
-  double* buf;      // (S+1) * SLOT doubles, 16-B aligned; slot S is the zero slot
+  double* buf;      // NSLOT * SLOT doubles, 128-B aligned
   uint64_t* full;   // S mbarriers
   uint64_t* empty;  // S mbarriers
-  int* lead;        // (S+1) * ROWS
-  int* valid;       // S: plane holds operator data
-  int* mvalid;      // S: material layer present
+  int* lead;        // (S+1) * ROWS     (!TM)
+  int* valid;       // S               (!TM)
+  int tshift = 0;   // TM: 1 if the tile's first element sits at an odd offset of the tensor
+
+  // TM: the box must start at an even element (16 B); returns the (even) x coordinate
+  __device__ __forceinline__ int set_tshift(int64_t ilo, const TmaOrigin& uorg) {
+    const int64_t ux = (ilo - uorg.t_i0) * C;
+    tshift = (int)(ux & 1);
+    return (int)(ux - tshift);
+  }
 
   __device__ __forceinline__ void carve(unsigned char* ring_base, unsigned char* meta_base) {
     buf = reinterpret_cast<double*>(ring_base);
@@ -116,17 +148,18 @@ struct PlaneRing {
     empty = full + S;
     lead = reinterpret_cast<int*>(empty + S);
     valid = lead + (S + 1) * ROWS;
-    mvalid = valid + S;
   }
 
-  // all threads: zero the ring, init barriers; ends with __syncthreads
+  // all threads: zero the ring (row path), init barriers; ends with __syncthreads
   __device__ __forceinline__ void init(int tid, int nthreads, int n_consumer_warps) {
-    double2* b2 = reinterpret_cast<double2*>(buf);
-    for (int t = tid; t < (S + 1) * SLOT / 2; t += nthreads) b2[t] = make_double2(0.0, 0.0);
-    for (int t = tid; t < (S + 1) * ROWS; t += nthreads) lead[t] = 2;
+    if (!TM) {
+      double2* b2 = reinterpret_cast<double2*>(buf);
+      for (int t = tid; t < NSLOT * SLOT / 2; t += nthreads) b2[t] = make_double2(0.0, 0.0);
+      for (int t = tid; t < (S + 1) * ROWS; t += nthreads) lead[t] = 2;
+    }
     if (tid == 0) {
       for (int s = 0; s < S; ++s) {
-        mbar_init(&full[s], ROWS + 1);
+        mbar_init(&full[s], TM ? 1 : ROWS + 1);
         mbar_init(&empty[s], n_consumer_warps);
       }
       fence_mbar_init();
@@ -137,53 +170,63 @@ struct PlaneRing {
 
   // producer warp: stream planes pfirst .. plast (and material layers) through the ring.
   //   ilo, jlo: global node index of tile column 0 / row 0 (may be -1); material tile cells
-  //   start at (ilo, jlo) too.
+  //   start at cell (ilo, jlo).  umap / uorg used when TM; mmap: material tensor (or nullptr).
   __device__ __forceinline__ void produce(const PlaneSrc& x, const Grid& g, int64_t pfirst, int64_t plast,
-                                          int64_t ilo, int64_t jlo, int bc, int lane, MatSrc mat) {
-    // ---- per-lane row descriptors (plane independent) ----
+                                          int64_t ilo, int64_t jlo, int bc, int lane,
+                                          const CUtensorMap* umap, TmaOrigin uorg,
+                                          const CUtensorMap* mmap, int64_t mlayer0) {
+    if (lane == 0) {
+      if (TM) tma_prefetch_desc(umap);
+      if (MROWS > 0) tma_prefetch_desc(mmap);
+    }
+    // ---- row-path per-lane descriptors (plane independent) ----
     const int64_t imin = bc ? 1 : 0, imax = bc ? g.nx - 1 : g.nx;
     const int64_t jmin = bc ? 1 : 0, jmax = bc ? g.ny - 1 : g.ny;
     const int64_t j = jlo + lane;
     const int64_t ca = max(ilo, imin), cb = min(ilo + COLS - 1, imax);
-    const bool rvalid = lane < ROWS && j >= jmin && j <= jmax && cb >= ca;
-    const int64_t offV = (j * (g.nx + 1) + ilo) * C;  // element offset of virtual column 0
-    const int64_t offA0 = (j * (g.nx + 1) + ca) * C;
-    const int64_t offA1 = (j * (g.nx + 1) + cb + 1) * C;
-    // bytes of this row's bulk copy for an even / odd plane base element index
-    uint32_t rb[2];
+    const bool rvalid = !TM && lane < ROWS && j >= jmin && j <= jmax && cb >= ca;
+    const int64_t offV = j * x.rpitch + ilo * C;  // element offset of virtual column 0
+    const int64_t offA0 = j * x.rpitch + ca * C;
+    const int64_t offA1 = j * x.rpitch + (cb + 1) * C;
+    uint32_t tot0 = 0, tot1 = 0;
+    if (!TM) {
+      uint32_t rb[2];
 #pragma unroll
-    for (int par = 0; par < 2; ++par) {
-      const uint64_t a0 = (uint64_t)(offA0 + par) * 8, a1 = (uint64_t)(offA1 + par) * 8;
-      const uint64_t b0 = (a0 + 15) & ~15ull, b1 = a1 & ~15ull;
-      rb[par] = (rvalid && b1 > b0) ? (uint32_t)(b1 - b0) : 0u;
+      for (int par = 0; par < 2; ++par) {
+        const uint64_t a0 = (uint64_t)(offA0 + par) * 8, a1 = (uint64_t)(offA1 + par) * 8;
+        const uint64_t b0 = (a0 + 15) & ~15ull, b1 = a1 & ~15ull;
+        rb[par] = (rvalid && b1 > b0) ? (uint32_t)(b1 - b0) : 0u;
+      }
+      tot0 = rb[0];
+      tot1 = rb[1];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        tot0 += __shfl_xor_sync(0xffffffffu, tot0, o);
+        tot1 += __shfl_xor_sync(0xffffffffu, tot1, o);
+      }
     }
-    uint32_t tot0 = rb[0], tot1 = rb[1];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      tot0 += __shfl_xor_sync(0xffffffffu, tot0, o);
-      tot1 += __shfl_xor_sync(0xffffffffu, tot1, o);
-    }
-    // material rows (cells): lane r = cell row jlo + r, cells [max(ilo,0), min(ilo+MCOLS-1, nx-1)]
-    const int64_t mi0 = max(ilo, (int64_t)0), mi1 = min(ilo + MCOLS - 1, g.nx - 1);
-    const bool mrow = MROWS > 0 && mat.lm != nullptr && lane < MROWS && j >= 0 && j < g.ny && mi1 >= mi0;
-    const uint32_t mbytes = mrow ? (uint32_t)((mi1 - mi0 + 1) * 16) : 0u;
-    uint32_t mtot = mbytes;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mtot += __shfl_xor_sync(0xffffffffu, mtot, o);
-    const int64_t moff = j * g.nx + mi0;
-    const int mdst = (int)(mi0 - ilo);
+    const int ux = TM ? set_tshift(ilo, uorg) : 0, uy = (int)(jlo - uorg.t_j0);
+    const int mx = (int)(2 * ilo), my = (int)jlo;
 
 #pragma unroll 1
     for (int64_t p = pfirst; p <= plast; ++p) {
       const int t = (int)(p - pfirst);
       const int s = t & (S - 1);
       if (t >= S) mbar_wait(&empty[s], (uint32_t)(((t / S) - 1) & 1));
+      double* slot = buf + (size_t)s * SLOT;
+      if (TM) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[s], UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
+          tma_load_3d(slot, umap, ux, uy, (int)(p - uorg.t_k0), &full[s]);
+          if (MROWS > 0) tma_load_3d(slot + UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
+        }
+        continue;
+      }
       fence_proxy_async();
-      const double* base = plane_ptr(x, g, p, C);
+      const double* base = plane_ptr(x, g, p);
       const bool pvalid = base != nullptr && !(bc && (p == 0 || p == g.nz));
-      const bool mlayer = MROWS > 0 && mat.lm != nullptr && p >= 0 && p < g.nz;
       const int par = (int)(((uintptr_t)base >> 3) & 1);
-      double* row = buf + (size_t)s * SLOT + lane * PITCH;
+      double* row = slot + lane * PITCH;
       const bool go = pvalid && rvalid;
       uintptr_t A0 = 0, A1 = 0, B0 = 0, B1 = 0, V0 = 0;
       int ld = 2;
@@ -201,8 +244,8 @@ struct PlaneRing {
       }
       if (lane == 0) {
         valid[s] = pvalid ? 1 : 0;
-        mvalid[s] = mlayer ? 1 : 0;
-        mbar_arrive_expect_tx(&full[s], (pvalid ? (par ? tot1 : tot0) : 0u) + (mlayer ? mtot : 0u));
+        mbar_arrive_expect_tx(&full[s], (pvalid ? (par ? tot1 : tot0) : 0u) + (MROWS > 0 ? MBOX_BYTES : 0u));
+        if (MROWS > 0) tma_load_3d(slot + UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
       }
       __syncwarp();
       if (go) {
@@ -210,10 +253,6 @@ struct PlaneRing {
         if (B1 > B0) bulk_g2s(dst(B0), (const void*)B0, (uint32_t)(B1 - B0), &full[s]);
         if ((A0 & 15) && A0 < A1) cp_async8(dst(A0), (const void*)A0);
         if ((A1 & 15) && B1 >= A0) cp_async8(dst(B1), (const void*)B1);
-      }
-      if (MROWS > 0 && mlayer && mrow) {
-        double2* md = reinterpret_cast<double2*>(buf + (size_t)s * SLOT + ROWS * PITCH) + lane * MCOLS + mdst;
-        bulk_g2s(md, mat.lm + (p - mat.layer0) * g.nx * g.ny + moff, mbytes, &full[s]);
       }
       if (lane < ROWS) cp_async_arrive_noinc(&full[s]);
     }
@@ -228,15 +267,15 @@ struct PlaneRing {
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // base of row r of slot s for reading (zero slot if the plane has no operator data)
+  // base of row r of slot s for reading the u plane
   __device__ __forceinline__ const double* row_ptr(int s, int r) const {
+    if (TM) return buf + (size_t)s * SLOT + r * PITCH + tshift;
     const int ss = valid[s] ? s : S;
     return buf + (size_t)ss * SLOT + r * PITCH + lead[ss * ROWS + r];
   }
-  // material (lambda, mu) of tile cell (col, row) in slot s; zeros outside the box
+  // material (lambda, mu) of tile cell (col, row) in slot s (zeros outside the box)
   __device__ __forceinline__ double2 mat(int s, int row, int col) const {
-    const int ss = mvalid[s] ? s : S;
-    return reinterpret_cast<const double2*>(buf + (size_t)ss * SLOT + ROWS * PITCH)[row * MCOLS + col];
+    return reinterpret_cast<const double2*>(buf + (size_t)s * SLOT + UDBL)[row * MCOLS + col];
   }
 };
 

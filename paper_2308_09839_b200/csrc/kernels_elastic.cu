@@ -16,6 +16,7 @@
 // shared memory, and each node is written exactly once.  Summation order per node is fixed
 // (independent of the tiling and of the z-chunk / slab boundaries).
 #include <algorithm>
+#include <cstring>
 
 #include "kernels_common.cuh"
 
@@ -33,10 +34,11 @@ __device__ __forceinline__ Face face_fwd(double u00, double u10, double u01, dou
 }
 }  // namespace
 
-template <int TY, int S>
+template <bool TM, int TY, int S>
 __global__ void __launch_bounds__(32 * (TY + 1), 1)
-    elastic_kernel(Grid g, PlaneSrc x, const double2* __restrict__ lm, int64_t mat_layer0,
-                   double* __restrict__ y, int bc, int mode, int64_t kchunk, CgScalars* sc, Reduce red) {
+    elastic_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
+                   TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
+                   int bc, int mode, int64_t kchunk, CgScalars* sc, Reduce red) {
   // TY consumer warps (lane = cell column, warp = cell row) + 1 producer warp
   constexpr int TX = 32;
   constexpr int NT = TX * (TY + 1);
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
   constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
   constexpr int ACC = 4 * TY * TX * 3;
-  using Ring = PlaneRing<ROWS, COLS, 3, S, TY, TX>;
+  using Ring = PlaneRing<TM, ROWS, COLS, 3, S, TY, TX>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
@@ -63,16 +65,18 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;  // planes kb-1 .. ke (cell layers kb-1 .. ke-1)
   ring.init(tid, NT, TY);
+  if (TM) ring.set_tshift(i0 - 1, uorg);
 
   double pq = 0.0;
   if (ty == TY) {
-    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, MatSrc{lm, mat_layer0});
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, &mmap, mat_layer0);
   } else {
     const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
     const double hs = g.h * (1.0 / 16.0);
     const bool owner = tx >= 1 && ty >= 1 && ci <= g.nx && cj <= g.ny;
     const bool bnode_xy = bc && (ci == 0 || ci == g.nx || cj == 0 || cj == g.ny);
-    const int64_t node_off = owner ? (cj * (g.nx + 1) + ci) * 3 : 0;
+    const int64_t off_y = owner ? cj * yo.rpitch + ci * 3 : 0;
+    const int64_t off_x = owner ? cj * x.rpitch + ci * 3 : 0;
 
     Face fb[3];     // face transform of the bottom plane of the current cell layer
     double cb[12];  // carried top-face contribution of the previous cell layer (4 modes x 3 comps)
@@ -175,7 +179,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
         named_bar_sync(1, NC);
         if (owner) {
           const bool bnode = bnode_xy || (bc && (q == 0 || q == g.nz));
-          const int64_t nid = (q - g.k0) * g.plane * 3 + node_off;
+          double* yq = yo.y + (q - g.k0) * yo.ppitch + off_y;
+          const double* xq = x.main + (q - g.k0) * x.ppitch + off_x;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             // fixed order: cells (i-1,j-1), (i,j-1), (i-1,j), (i,j)
@@ -185,10 +190,10 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
             v += acc[((0 * TY + ty) * TX + tx) * 3 + c];
             double xv = xq[c];
             if (bnode) {
-              xv = x.main[nid + c];
+              xv = xq[c];
               v = xv;
             }
-            y[nid + c] = v;
+            yq[c] = v;
             if (mode == 1) pq = fma(v, xv, pq);
           }
         }
@@ -202,14 +207,13 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   }
 }
 
-template <int TY, int S>
-static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double2* lm, int64_t mat_layer0,
-                              double* y, int bc, int mode, CgScalars* sc, Reduce red, cudaStream_t s,
-                              int sm_count) {
+template <bool TM, int TY, int S>
+static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int bc, int mode,
+                              CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   constexpr int TX = 32;
-  using Ring = PlaneRing<TY + 1, TX + 1, 3, S, TY, TX>;
+  using Ring = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX>;
   const size_t smem = Ring::BYTES + 2 * 4 * TY * TX * 3 * sizeof(double) + Ring::META;
-  auto kern = elastic_kernel<TY, S>;
+  auto kern = elastic_kernel<TM, TY, S>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -225,15 +229,18 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, const double2* lm, int6
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
-  kern<<<grid, block, smem, s>>>(g, x, lm, mat_layer0, y, bc, mode, kchunk, sc, red);
+  CUtensorMap um;
+  if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
+  TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, bc, mode, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, const double2* lm, int64_t mat_layer0,
-                           double* y, int mode, CgScalars* sc, Reduce red, cudaStream_t s,
-                           int sm_count) {
-  return launch_cfg<15, 4>(g, x, lm, mat_layer0, y, bc, mode, sc, red, s, sm_count);
+cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int mode,
+                           CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  if (maps.u) return launch_cfg<true, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  return launch_cfg<false, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem

@@ -8,23 +8,25 @@
 //   a = Mx x, b = Kx x           (per node row, from smem)
 //   c1 = My a, c2 = My b + Ky a  (per node, from the thread's rows)
 //   y(k) = (h/36) [Mz c2 + Kz c1] over the register window c(k-1), c(k), c(k+1).
-// The CTA marches along z over node planes staged by bulk copies (PlaneRing); x is read from
-// HBM once, the one-node xy halo from L2.  Vector Laplace (Eq. 8) is the same per component.
+// The CTA marches along z over node planes staged by the producer warp (PlaneRing: one TMA
+// tensor copy per plane inside CG, bulk row copies for caller vectors); x is read from HBM once,
+// the one-node xy halo from L2.  Vector Laplace (Eq. 8) is the same per component.
 #include <algorithm>
+#include <cstring>
 
 #include "kernels_common.cuh"
 
 namespace fem {
 
-template <int C, int TX, int TY, int R, int S>
-__global__ void __launch_bounds__(TX*(TY + 1), 2) laplace_kernel(Grid g, PlaneSrc x, double* __restrict__ y,
-                                                                 int bc, int mode, int64_t kchunk,
-                                                                 CgScalars* sc, Reduce red) {
+template <bool TM, int C, int TX, int TY, int R, int S>
+__global__ void __launch_bounds__(TX*(TY + 1), 2)
+    laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
+                   TmaOrigin uorg, int bc, int mode, int64_t kchunk, CgScalars* sc, Reduce red) {
   // TY consumer warps (one node column per lane, R node rows each) + 1 producer warp
   constexpr int NT = TX * (TY + 1);
   constexpr int ROWS = TY * R + 2;
   constexpr int COLS = TX + 2;
-  using Ring = PlaneRing<ROWS, COLS, C, S>;
+  using Ring = PlaneRing<TM, ROWS, COLS, C, S>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
@@ -40,26 +42,27 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2) laplace_kernel(Grid g, PlaneSr
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;
   ring.init(tid, NT, TY);
+  if (TM) ring.set_tshift(i0 - 1, uorg);
 
   double pq = 0.0;
   if (ty == TY) {
-    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, MatSrc{nullptr, 0});
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, nullptr, 0);
   } else {
     const int64_t i = i0 + tx;
     const double h36 = g.h * (1.0 / 36.0);
-    const int64_t rowlen = g.nx + 1;
     // per-node 1-D multiplicities m = (#1-D elements touching the node) in x, y
     const double mx = (double)((i > 0) + (i < g.nx));
     double my[R];
     bool active[R], bnode_xy[R];
-    int64_t off_xy[R];
+    int64_t off_y[R], off_x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int64_t j = j0 + ty * R + r;
       my[r] = (double)((j > 0) + (j < g.ny));
       active[r] = (i <= g.nx) && (j <= g.ny);
       bnode_xy[r] = bc && (i == 0 || i == g.nx || j == 0 || j == g.ny);
-      off_xy[r] = (j * rowlen + i) * C;
+      off_y[r] = j * yo.rpitch + i * C;
+      off_x[r] = j * x.rpitch + i * C;
     }
     // windows: c1, c2 and the centre value for planes p-2, p-1, p
     double c1w[3][R][C], c2w[3][R][C], xcw[2][R][C];
@@ -121,8 +124,8 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2) laplace_kernel(Grid g, PlaneSr
       if (q >= kb) {
         const double mz = (double)((q > 0) + (q < g.nz));
         const bool qface = bc && (q == 0 || q == g.nz);
-        double* yq = y + (q - g.k0) * g.plane * C;
-        const double* xq = x.main + (q - g.k0) * g.plane * C;
+        double* yq = yo.y + (q - g.k0) * yo.ppitch;
+        const double* xq = x.main + (q - g.k0) * x.ppitch;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!active[r]) continue;
@@ -130,13 +133,13 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2) laplace_kernel(Grid g, PlaneSr
           for (int c = 0; c < C; ++c) {
             double v, xv = xcw[0][r][c];
             if (qface || bnode_xy[r]) {
-              xv = xq[off_xy[r] + c];
+              xv = xq[off_x[r] + c];
               v = xv;
             } else {
               const double nb = (c2w[0][r][c] - c1w[0][r][c]) + (c2w[2][r][c] - c1w[2][r][c]);
               v = h36 * fma(2.0 * mz, c2w[1][r][c], fma(mz, c1w[1][r][c], nb));
             }
-            yq[off_xy[r] + c] = v;
+            yq[off_y[r] + c] = v;
             if (mode == 1) pq = fma(v, xv, pq);
           }
         }
@@ -150,12 +153,12 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2) laplace_kernel(Grid g, PlaneSr
   }
 }
 
-template <int C, int TX, int TY, int R, int S>
-static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, double* y, int bc, int mode, CgScalars* sc,
-                              Reduce red, cudaStream_t s, int sm_count) {
-  using Ring = PlaneRing<TY * R + 2, TX + 2, C, S>;
+template <bool TM, int C, int TX, int TY, int R, int S>
+static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int bc, int mode,
+                              CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  using Ring = PlaneRing<TM, TY * R + 2, TX + 2, C, S>;
   const size_t smem = Ring::BYTES + Ring::META;
-  auto kern = laplace_kernel<C, TX, TY, R, S>;
+  auto kern = laplace_kernel<TM, C, TX, TY, R, S>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -172,15 +175,22 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, double* y, int bc, int 
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
-  kern<<<grid, block, smem, s>>>(g, x, y, bc, mode, kchunk, sc, red);
+  CUtensorMap um;
+  if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
+  TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, bc, mode, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, double* y, int mode,
-                           CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
-  if (comps == 1) return launch_cfg<1, 32, 8, 2, 8>(g, x, y, bc, mode, sc, red, s, sm_count);
-  return launch_cfg<3, 32, 8, 1, 8>(g, x, y, bc, mode, sc, red, s, sm_count);
+cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps,
+                           int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  if (maps.u) {
+    if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  }
+  if (comps == 1) return launch_cfg<false, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  return launch_cfg<false, 3, kLapTX, kLapTY, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem
