@@ -45,13 +45,15 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   constexpr int NC = TX * TY;   // consumer threads
   constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
   constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
-  constexpr int ACC = 4 * TY * TX * 3;
+  constexpr int TPART = 2 * TY * TX * 3;  // y hand-off buffers (double-buffered)
   using Ring = PlaneRing<TM, ROWS, COLS, 3, S, TY, TX>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
-  double* acc0 = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // 2 x [4][TY][TX][3]
-  ring.carve(smem_raw, reinterpret_cast<unsigned char*>(acc0 + 2 * ACC));
+  double* tpart = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // [2][TY][TX][3]
+  uint64_t* tfull = reinterpret_cast<uint64_t*>(tpart + TPART);        // [2][TY]
+  uint64_t* tempty = tfull + 2 * TY;                                    // [2][TY]
+  ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + 2 * TY));
 
   if (mode == 1 && sc->done) return;
 
@@ -64,7 +66,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;  // planes kb-1 .. ke (cell layers kb-1 .. ke-1)
-  ring.init(tid, NT, TY);
+  if (tid < 2 * TY) {
+    mbar_init(&tfull[tid], 1);
+    mbar_init(&tempty[tid], 1);
+  }
+  ring.init(tid, NT, TY);  // (fences + __syncthreads cover the hand-off barriers too)
   if (TM) ring.set_tshift(i0 - 1, uorg);
 
   double pq = 0.0;
@@ -81,6 +87,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
     Face fb[3];     // face transform of the bottom plane of the current cell layer
     double cb[12];  // carried top-face contribution of the previous cell layer (4 modes x 3 comps)
     double xc[3];   // this thread's node value at the bottom plane (for p.Ap)
+    int64_t nq = 0;  // planes output so far (exchange buffer use counter)
 #pragma unroll
     for (int t = 0; t < 12; ++t) cb[t] = 0.0;
 
@@ -122,9 +129,9 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       const double vz = ft[1].s - fb[1].s, vxz = ft[1].x - fb[1].x, vyz = ft[1].y - fb[1].y, vxyz = ft[1].xy - fb[1].xy;
       const double wx = fb[2].x + ft[2].x, wy = fb[2].y + ft[2].y, wxy = fb[2].xy + ft[2].xy;
       const double wz = ft[2].s - fb[2].s, wxz = ft[2].x - fb[2].x, wyz = ft[2].y - fb[2].y, wxyz = ft[2].xy - fb[2].xy;
-      double xq[3];
+      double xsave[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xq[c] = xc[c]; xc[c] = xn[c]; }
+      for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xsave[c] = xc[c]; xc[c] = xn[c]; }
 
       // modal stress: weights 1 (linear modes), 1/3 (bilinear), 1/9 (trilinear)
       const double M2 = M0 + M0;
@@ -165,36 +172,53 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       }
       const int64_t q = p - 1;  // node plane whose xy-corner contributions are now complete
       if (q >= kb) {
-        double* acc = acc0 + (q & 1) * ACC;  // double-buffered: one consumer barrier per plane
-        // expand face modes to the 4 corner nodes of this cell column, exchange via smem
+        // expand face modes to the 4 corner nodes of this cell column; combine x-neighbours in
+        // registers (warp shuffle), y-neighbours through a point-to-point smem hand-off from the
+        // warp below (no CTA-wide barrier).  Fixed order per node:
+        //   ((i-1,j-1) + (i,j-1)) + ((i-1,j) + (i,j))   independent of tiles and slabs.
+        const int b = (int)(nq & 1);
+        const uint32_t n = (uint32_t)(nq >> 1);
+        ++nq;
+        double B[3], T[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double G1 = F[4 * c + 0], Gx = F[4 * c + 1], Gy = F[4 * c + 2], Gxy = F[4 * c + 3];
           const double es = G1 - Gy, ed = Gx - Gxy, fs = G1 + Gy, fd = Gx + Gxy;
-          acc[((0 * TY + ty) * TX + tx) * 3 + c] = es - ed;  // corner (x0,y0)
-          acc[((1 * TY + ty) * TX + tx) * 3 + c] = es + ed;  // corner (x1,y0)
-          acc[((2 * TY + ty) * TX + tx) * 3 + c] = fs - fd;  // corner (x0,y1)
-          acc[((3 * TY + ty) * TX + tx) * 3 + c] = fs + fd;  // corner (x1,y1)
+          const double c00 = es - ed, c10 = es + ed, c01 = fs - fd, c11 = fs + fd;
+          const double c10l = __shfl_up_sync(0xffffffffu, c10, 1);  // from cell i-1
+          const double c11l = __shfl_up_sync(0xffffffffu, c11, 1);
+          B[c] = c10l + c00;  // node row cj,   cells (i-1,j), (i,j)
+          T[c] = c11l + c01;  // node row cj+1, cells (i-1,j), (i,j)
         }
-        named_bar_sync(1, NC);
-        if (owner) {
-          const bool bnode = bnode_xy || (bc && (q == 0 || q == g.nz));
-          double* yq = yo.y + (q - g.k0) * yo.ppitch + off_y;
-          const double* xq = x.main + (q - g.k0) * x.ppitch + off_x;
+        if (ty < TY - 1) {  // hand T to the warp above
+          if (n >= 1) mbar_wait(&tempty[b * TY + ty], (n - 1) & 1);
+          double* dst = tpart + ((b * TY + ty) * TX + tx) * 3;
+          dst[0] = T[0]; dst[1] = T[1]; dst[2] = T[2];
+          __syncwarp();
+          if (tx == 0) mbar_arrive(&tfull[b * TY + ty]);
+        }
+        if (ty >= 1) {
+          mbar_wait(&tfull[b * TY + ty - 1], n & 1);
+          const double* src = tpart + ((b * TY + ty - 1) * TX + tx) * 3;
+          double v[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            // fixed order: cells (i-1,j-1), (i,j-1), (i-1,j), (i,j)
-            double v = acc[((3 * TY + ty - 1) * TX + tx - 1) * 3 + c];
-            v += acc[((2 * TY + ty - 1) * TX + tx) * 3 + c];
-            v += acc[((1 * TY + ty) * TX + tx - 1) * 3 + c];
-            v += acc[((0 * TY + ty) * TX + tx) * 3 + c];
-            double xv = xq[c];
-            if (bnode) {
-              xv = xq[c];
-              v = xv;
+          for (int c = 0; c < 3; ++c) v[c] = src[c] + B[c];
+          __syncwarp();
+          if (tx == 0) mbar_arrive(&tempty[b * TY + ty - 1]);
+          if (owner) {
+            const bool bnode = bnode_xy || (bc && (q == 0 || q == g.nz));
+            double* yq = yo.y + (q - g.k0) * yo.ppitch + off_y;
+            const double* xq = x.main + (q - g.k0) * x.ppitch + off_x;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              double vv = v[c], xv = xsave[c];
+              if (bnode) {
+                xv = xq[c];
+                vv = xv;
+              }
+              yq[c] = vv;
+              if (mode == 1) pq = fma(vv, xv, pq);
             }
-            yq[c] = v;
-            if (mode == 1) pq = fma(v, xv, pq);
           }
         }
       }
@@ -212,7 +236,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
                               CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   constexpr int TX = 32;
   using Ring = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX>;
-  const size_t smem = Ring::BYTES + 2 * 4 * TY * TX * 3 * sizeof(double) + Ring::META;
+  const size_t smem = Ring::BYTES + 2 * TY * TX * 3 * sizeof(double) + 4 * TY * sizeof(uint64_t) + Ring::META;
   auto kern = elastic_kernel<TM, TY, S>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -239,8 +263,8 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
 
 cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int mode,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
-  if (maps.u) return launch_cfg<true, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
-  return launch_cfg<false, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  if (maps.u) return launch_cfg<true, kElTY, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  return launch_cfg<false, kElTY, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem
