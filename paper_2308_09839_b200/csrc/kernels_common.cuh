@@ -56,6 +56,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void mbar_wait_a(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -134,6 +150,7 @@ struct PlaneRing {
   int* lead;        // (S+1) * ROWS     (!TM)
   int* valid;       // S               (!TM)
   int tshift = 0;   // TM: 1 if the tile's first element sits at an odd offset of the tensor
+  uint32_t full_a = 0, empty_a = 0;  // shared-window addresses of full[0], empty[0]
 
   // TM: the box must start at an even element (16 B); returns the (even) x coordinate
   __device__ __forceinline__ int set_tshift(int64_t ilo, const TmaOrigin& uorg) {
@@ -146,6 +163,8 @@ struct PlaneRing {
     buf = reinterpret_cast<double*>(ring_base);
     full = reinterpret_cast<uint64_t*>(meta_base);
     empty = full + S;
+    full_a = smem_u32(full);
+    empty_a = smem_u32(empty);
     lead = reinterpret_cast<int*>(empty + S);
     valid = lead + (S + 1) * ROWS;
   }
@@ -212,7 +231,7 @@ struct PlaneRing {
     for (int64_t p = pfirst; p <= plast; ++p) {
       const int t = (int)(p - pfirst);
       const int s = t & (S - 1);
-      if (t >= S) mbar_wait(&empty[s], (uint32_t)(((t / S) - 1) & 1));
+      if (t >= S) mbar_wait_a(empty_a + 8u * s, (uint32_t)(((t / S) - 1) & 1));
       double* slot = buf + (size_t)s * SLOT;
       if (TM) {
         if (lane == 0) {
@@ -259,12 +278,12 @@ struct PlaneRing {
   }
 
   // consumers: wait until slot s holds its plane (phase parity ph)
-  __device__ __forceinline__ void wait(int s, uint32_t ph) { mbar_wait(&full[s], ph); }
+  __device__ __forceinline__ void wait(int s, uint32_t ph) { mbar_wait_a(full_a + 8u * s, ph); }
 
   // consumer warp: release slot s after its last read
   __device__ __forceinline__ void release(int s, int lane) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive_a(empty_a + 8u * s);
   }
 
   // base of row r of slot s for reading the u plane

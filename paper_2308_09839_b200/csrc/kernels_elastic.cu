@@ -34,11 +34,12 @@ __device__ __forceinline__ Face face_fwd(double u00, double u10, double u01, dou
 }
 }  // namespace
 
-template <bool TM, int TY, int S>
+template <bool TM, int MODE, int TY, int S>
 __global__ void __launch_bounds__(32 * (TY + 1), 1)
     elastic_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
-                   int bc, int mode, int64_t kchunk, CgScalars* sc, Reduce red) {
+                   int bc, int64_t kchunk, CgScalars* sc, Reduce red) {
+  constexpr int mode = MODE;
   // TY consumer warps (lane = cell column, warp = cell row) + 1 producer warp
   constexpr int TX = 32;
   constexpr int NT = TX * (TY + 1);
@@ -54,6 +55,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   uint64_t* tfull = reinterpret_cast<uint64_t*>(tpart + TPART);        // [2][TY]
   uint64_t* tempty = tfull + 2 * TY;                                    // [2][TY]
   ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + 2 * TY));
+  const uint32_t tfull_a = smem_u32(tfull), tempty_a = smem_u32(tempty);
 
   if (mode == 1 && sc->done) return;
 
@@ -191,20 +193,20 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
           T[c] = c11l + c01;  // node row cj+1, cells (i-1,j), (i,j)
         }
         if (ty < TY - 1) {  // hand T to the warp above
-          if (n >= 1) mbar_wait(&tempty[b * TY + ty], (n - 1) & 1);
+          if (n >= 1) mbar_wait_a(tempty_a + 8u * (b * TY + ty), (n - 1) & 1);
           double* dst = tpart + ((b * TY + ty) * TX + tx) * 3;
           dst[0] = T[0]; dst[1] = T[1]; dst[2] = T[2];
           __syncwarp();
-          if (tx == 0) mbar_arrive(&tfull[b * TY + ty]);
+          if (tx == 0) mbar_arrive_a(tfull_a + 8u * (b * TY + ty));
         }
         if (ty >= 1) {
-          mbar_wait(&tfull[b * TY + ty - 1], n & 1);
+          mbar_wait_a(tfull_a + 8u * (b * TY + ty - 1), n & 1);
           const double* src = tpart + ((b * TY + ty - 1) * TX + tx) * 3;
           double v[3];
 #pragma unroll
           for (int c = 0; c < 3; ++c) v[c] = src[c] + B[c];
           __syncwarp();
-          if (tx == 0) mbar_arrive(&tempty[b * TY + ty - 1]);
+          if (tx == 0) mbar_arrive_a(tempty_a + 8u * (b * TY + ty - 1));
           if (owner) {
             const bool bnode = bnode_xy || (bc && (q == 0 || q == g.nz));
             double* yq = yo.y + (q - g.k0) * yo.ppitch + off_y;
@@ -237,12 +239,12 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   constexpr int TX = 32;
   using Ring = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX>;
   const size_t smem = Ring::BYTES + 2 * TY * TX * 3 * sizeof(double) + 4 * TY * sizeof(uint64_t) + Ring::META;
-  auto kern = elastic_kernel<TM, TY, S>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  auto kern = mode ? elastic_kernel<TM, 1, TY, S> : elastic_kernel<TM, 0, TY, S>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[mode]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[mode] = true;
   }
   const int64_t xt = (g.nx + 1 + (TX - 1) - 1) / (TX - 1);
   const int64_t yt = (g.ny + 1 + (TY - 1) - 1) / (TY - 1);
@@ -256,7 +258,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   CUtensorMap um;
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
-  kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, bc, mode, kchunk, sc, red);
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, bc, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -18,10 +18,11 @@
 
 namespace fem {
 
-template <bool TM, int C, int TX, int TY, int R, int S>
+template <bool TM, int MODE, int C, int TX, int TY, int R, int S>
 __global__ void __launch_bounds__(TX*(TY + 1), 2)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
-                   TmaOrigin uorg, int bc, int mode, int64_t kchunk, CgScalars* sc, Reduce red) {
+                   TmaOrigin uorg, int bc, int64_t kchunk, CgScalars* sc, Reduce red) {
+  constexpr int mode = MODE;
   // TY consumer warps (one node column per lane, R node rows each) + 1 producer warp
   constexpr int NT = TX * (TY + 1);
   constexpr int ROWS = TY * R + 2;
@@ -158,12 +159,12 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
                               CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   using Ring = PlaneRing<TM, TY * R + 2, TX + 2, C, S>;
   const size_t smem = Ring::BYTES + Ring::META;
-  auto kern = laplace_kernel<TM, C, TX, TY, R, S>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  auto kern = mode ? laplace_kernel<TM, 1, C, TX, TY, R, S> : laplace_kernel<TM, 0, C, TX, TY, R, S>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[mode]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[mode] = true;
   }
   const int64_t xt = (g.nx + 1 + TX - 1) / TX;
   const int64_t yt = (g.ny + 1 + TY * R - 1) / (TY * R);
@@ -178,7 +179,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   CUtensorMap um;
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
-  kern<<<grid, block, smem, s>>>(g, x, y, um, org, bc, mode, kchunk, sc, red);
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, bc, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }
