@@ -83,46 +83,49 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
     const double hs = g.h * (1.0 / 16.0);
     const bool owner = tx >= 1 && ty >= 1 && ci <= g.nx && cj <= g.ny;
     const bool bnode_xy = bc && (ci == 0 || ci == g.nx || cj == 0 || cj == g.ny);
-    const int64_t off_y = owner ? cj * yo.rpitch + ci * 3 : 0;
-    const int64_t off_x = owner ? cj * x.rpitch + ci * 3 : 0;
+    // output / boundary-read pointers, advanced by one plane per output plane
+    double* yp = yo.y + (kb - g.k0) * yo.ppitch + (owner ? cj * yo.rpitch + ci * 3 : 0);
+    const double* xpb = x.main + (kb - g.k0) * x.ppitch + (owner ? cj * x.rpitch + ci * 3 : 0);
+    const int nplane = (int)(ke - pfirst + 1);  // planes kb-1 .. ke
+    const int qface0 = bc ? (int)(0 - kb) : -1000000;     // output index of node plane 0
+    const int qface1 = bc ? (int)(g.nz - kb) : -1000000;  // ... of node plane nz
+    // hand-off buffers / barriers (b = output parity)
+    double* const tw0 = tpart + (ty * TX + tx) * 3;                 // + b * TY*TX*3
+    const double* const tr0 = tpart + ((ty - 1) * TX + tx) * 3;
+    const uint32_t tfw0 = tfull_a + 8u * ty, tew0 = tempty_a + 8u * ty;  // + b * 8*TY
+    const uint32_t tfr0 = tfull_a + 8u * (ty - 1), ter0 = tempty_a + 8u * (ty - 1);
 
     Face fb[3];     // face transform of the bottom plane of the current cell layer
     double cb[12];  // carried top-face contribution of the previous cell layer (4 modes x 3 comps)
     double xc[3];   // this thread's node value at the bottom plane (for p.Ap)
-    int64_t nq = 0;  // planes output so far (exchange buffer use counter)
 #pragma unroll
     for (int t = 0; t < 12; ++t) cb[t] = 0.0;
+    double Ln, Mn;  // material of the cell layer above the bottom plane (x h/16)
 
-    double Ln = 0.0, Mn = 0.0;  // material of the cell layer below the current plane (x h/16)
-
-#pragma unroll 1
-    for (int64_t p = pfirst; p <= ke; ++p) {
-      // iteration p: plane p is available; cell layer p-1 lies between planes p-1 and p
-      const int t = (int)(p - pfirst);
+    auto load_plane = [&](int t, Face* ft, double* xn, double& L, double& M) {
       const int slot = t & (S - 1);
       ring.wait(slot, (uint32_t)((t / S) & 1));
-      Face ft[3];
-      double xn[3];
-      const double2 lmn = ring.mat(slot, ty, tx);  // material layer p (used at iteration p+1)
-      {
-        const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
-        const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
+      const double2 lmn = ring.mat(slot, ty, tx);  // material layer of this plane
+      const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
+      const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          xn[c] = r0[c];
-          ft[c] = face_fwd(r0[c], r0[3 + c], r1[c], r1[3 + c]);
-        }
+      for (int c = 0; c < 3; ++c) {
+        xn[c] = r0[c];
+        ft[c] = face_fwd(r0[c], r0[3 + c], r1[c], r1[3 + c]);
       }
       ring.release(slot, tx);
-      if (p == pfirst) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) { fb[c] = ft[c]; xc[c] = xn[c]; }
-        Ln = lmn.x * hs; Mn = lmn.y * hs;
-        continue;
-      }
-      // ---- cell layer k = p-1 ----
+      L = lmn.x * hs;
+      M = lmn.y * hs;
+    };
+    load_plane(0, fb, xc, Ln, Mn);
+
+#pragma unroll 1
+    for (int t = 1; t < nplane; ++t) {
+      // plane kb-1+t is available; cell layer kb-2+t lies below it
+      Face ft[3];
+      double xn[3];
       const double L0 = Ln, M0 = Mn;
-      Ln = lmn.x * hs; Mn = lmn.y * hs;
+      load_plane(t, ft, xn, Ln, Mn);
       // modal coefficients (unnormalised): component u=0, v=1, w=2
       // x = ds, y = sd, xy = dd summed over z; z, xz, yz, xyz = differences in z
       const double ux = fb[0].x + ft[0].x, uy = fb[0].y + ft[0].y, uxy = fb[0].xy + ft[0].xy;
@@ -172,16 +175,13 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
           cb[4 * c + 3] = gxy[c] + gxyz[c];
         }
       }
-      const int64_t q = p - 1;  // node plane whose xy-corner contributions are now complete
-      if (q >= kb) {
-        // expand face modes to the 4 corner nodes of this cell column; combine x-neighbours in
-        // registers (warp shuffle), y-neighbours through a point-to-point smem hand-off from the
-        // warp below (no CTA-wide barrier).  Fixed order per node:
-        //   ((i-1,j-1) + (i,j-1)) + ((i-1,j) + (i,j))   independent of tiles and slabs.
-        const int b = (int)(nq & 1);
-        const uint32_t n = (uint32_t)(nq >> 1);
-        ++nq;
-        double B[3], T[3];
+      if (t >= 2) {  // node plane q = kb + t - 2 is complete in xy-corner form
+        const int qo = t - 2;
+        const int b = qo & 1;
+        const uint32_t n = (uint32_t)(qo >> 1);
+        // corners; x-neighbours by warp shuffle, y-neighbours by a point-to-point hand-off
+        // from the warp below.  Fixed order per node: ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j)).
+        double B[3], Tt[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double G1 = F[4 * c + 0], Gx = F[4 * c + 1], Gy = F[4 * c + 2], Gxy = F[4 * c + 3];
@@ -189,39 +189,39 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
           const double c00 = es - ed, c10 = es + ed, c01 = fs - fd, c11 = fs + fd;
           const double c10l = __shfl_up_sync(0xffffffffu, c10, 1);  // from cell i-1
           const double c11l = __shfl_up_sync(0xffffffffu, c11, 1);
-          B[c] = c10l + c00;  // node row cj,   cells (i-1,j), (i,j)
-          T[c] = c11l + c01;  // node row cj+1, cells (i-1,j), (i,j)
+          B[c] = c10l + c00;   // node row cj,   cells (i-1,j), (i,j)
+          Tt[c] = c11l + c01;  // node row cj+1, cells (i-1,j), (i,j)
         }
-        if (ty < TY - 1) {  // hand T to the warp above
-          if (n >= 1) mbar_wait_a(tempty_a + 8u * (b * TY + ty), (n - 1) & 1);
-          double* dst = tpart + ((b * TY + ty) * TX + tx) * 3;
-          dst[0] = T[0]; dst[1] = T[1]; dst[2] = T[2];
+        if (ty < TY - 1) {  // hand Tt to the warp above
+          if (n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
+          double* dst = tw0 + b * (TY * TX * 3);
+          dst[0] = Tt[0]; dst[1] = Tt[1]; dst[2] = Tt[2];
           __syncwarp();
-          if (tx == 0) mbar_arrive_a(tfull_a + 8u * (b * TY + ty));
+          if (tx == 0) mbar_arrive_a(tfw0 + 8u * TY * b);
         }
         if (ty >= 1) {
-          mbar_wait_a(tfull_a + 8u * (b * TY + ty - 1), n & 1);
-          const double* src = tpart + ((b * TY + ty - 1) * TX + tx) * 3;
+          mbar_wait_a(tfr0 + 8u * TY * b, n & 1);
+          const double* src = tr0 + b * (TY * TX * 3);
           double v[3];
 #pragma unroll
           for (int c = 0; c < 3; ++c) v[c] = src[c] + B[c];
           __syncwarp();
-          if (tx == 0) mbar_arrive_a(tempty_a + 8u * (b * TY + ty - 1));
+          if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
           if (owner) {
-            const bool bnode = bnode_xy || (bc && (q == 0 || q == g.nz));
-            double* yq = yo.y + (q - g.k0) * yo.ppitch + off_y;
-            const double* xq = x.main + (q - g.k0) * x.ppitch + off_x;
+            const bool bnode = bnode_xy || qo == qface0 || qo == qface1;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               double vv = v[c], xv = xsave[c];
               if (bnode) {
-                xv = xq[c];
+                xv = xpb[c];
                 vv = xv;
               }
-              yq[c] = vv;
+              yp[c] = vv;
               if (mode == 1) pq = fma(vv, xv, pq);
             }
           }
+          yp += yo.ppitch;
+          xpb += x.ppitch;
         }
       }
     }
