@@ -46,15 +46,15 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   constexpr int NC = TX * TY;   // consumer threads
   constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
   constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
-  constexpr int TPART = 2 * TY * TX * 3;  // y hand-off buffers (double-buffered)
+  constexpr int TPART = 4 * TY * TX * 3;  // y hand-off buffers (ring of 4)
   using Ring = PlaneRing<TM, ROWS, COLS, 3, S, TY, TX>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
-  double* tpart = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // [2][TY][TX][3]
-  uint64_t* tfull = reinterpret_cast<uint64_t*>(tpart + TPART);        // [2][TY]
-  uint64_t* tempty = tfull + 2 * TY;                                    // [2][TY]
-  ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + 2 * TY));
+  double* tpart = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // [4][TY][TX][3]
+  uint64_t* tfull = reinterpret_cast<uint64_t*>(tpart + TPART);        // [4][TY]
+  uint64_t* tempty = tfull + 4 * TY;                                    // [4][TY]
+  ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + 4 * TY));
   const uint32_t tfull_a = smem_u32(tfull), tempty_a = smem_u32(tempty);
 
   if (mode == 1 && sc->done) return;
@@ -62,13 +62,14 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
   // output tile: nodes i0 .. i0+TX-2, j0 .. j0+TY-2; thread (tx,ty) owns cell (i0-1+tx, j0-1+ty)
-  // and node (i0-1+tx, j0-1+ty) (written when tx, ty >= 1)
+  // and outputs node (i0-1+tx, j0+ty) (when tx >= 1, ty <= TY-2) from its top corners + the
+  // bottom corners handed down by the warp above
   const int64_t i0 = (int64_t)blockIdx.x * (TX - 1);
   const int64_t j0 = (int64_t)blockIdx.y * (TY - 1);
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;  // planes kb-1 .. ke (cell layers kb-1 .. ke-1)
-  if (tid < 2 * TY) {
+  if (tid < 4 * TY) {
     mbar_init(&tfull[tid], 1);
     mbar_init(&tempty[tid], 1);
   }
@@ -81,19 +82,20 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   } else {
     const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
     const double hs = g.h * (1.0 / 16.0);
-    const bool owner = tx >= 1 && ty >= 1 && ci <= g.nx && cj <= g.ny;
-    const bool bnode_xy = bc && (ci == 0 || ci == g.nx || cj == 0 || cj == g.ny);
+    const int64_t nj = cj + 1;  // node row this thread outputs (top corners of its cell)
+    const bool owner = tx >= 1 && ty <= TY - 2 && ci <= g.nx && nj <= g.ny;
+    const bool bnode_xy = bc && (ci == 0 || ci == g.nx || nj == 0 || nj == g.ny);
     // output / boundary-read pointers, advanced by one plane per output plane
-    double* yp = yo.y + (kb - g.k0) * yo.ppitch + (owner ? cj * yo.rpitch + ci * 3 : 0);
-    const double* xpb = x.main + (kb - g.k0) * x.ppitch + (owner ? cj * x.rpitch + ci * 3 : 0);
+    double* yp = yo.y + (kb - g.k0) * yo.ppitch + (owner ? nj * yo.rpitch + ci * 3 : 0);
+    const double* xpb = x.main + (kb - g.k0) * x.ppitch + (owner ? nj * x.rpitch + ci * 3 : 0);
     const int nplane = (int)(ke - pfirst + 1);  // planes kb-1 .. ke
     const int qface0 = bc ? (int)(0 - kb) : -1000000;     // output index of node plane 0
     const int qface1 = bc ? (int)(g.nz - kb) : -1000000;  // ... of node plane nz
     // hand-off buffers / barriers (b = output parity)
     double* const tw0 = tpart + (ty * TX + tx) * 3;                 // + b * TY*TX*3
-    const double* const tr0 = tpart + ((ty - 1) * TX + tx) * 3;
+    const double* const tr0 = tpart + ((ty + 1) * TX + tx) * 3;
     const uint32_t tfw0 = tfull_a + 8u * ty, tew0 = tempty_a + 8u * ty;  // + b * 8*TY
-    const uint32_t tfr0 = tfull_a + 8u * (ty - 1), ter0 = tempty_a + 8u * (ty - 1);
+    const uint32_t tfr0 = tfull_a + 8u * (ty + 1), ter0 = tempty_a + 8u * (ty + 1);
 
     Face fb[3];     // face transform of the bottom plane of the current cell layer
     double cb[12];  // carried top-face contribution of the previous cell layer (4 modes x 3 comps)
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        xn[c] = r0[c];
+        xn[c] = r1[c];  // node (ci, cj+1): the node this thread outputs
         ft[c] = face_fwd(r0[c], r0[3 + c], r1[c], r1[3 + c]);
       }
       ring.release(slot, tx);
@@ -177,8 +179,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       }
       if (t >= 2) {  // node plane q = kb + t - 2 is complete in xy-corner form
         const int qo = t - 2;
-        const int b = qo & 1;
-        const uint32_t n = (uint32_t)(qo >> 1);
+        const int b = qo & 3;
+        const uint32_t n = (uint32_t)(qo >> 2);
         // corners; x-neighbours by warp shuffle, y-neighbours by a point-to-point hand-off
         // from the warp below.  Fixed order per node: ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j)).
         double B[3], Tt[3];
@@ -192,19 +194,21 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
           B[c] = c10l + c00;   // node row cj,   cells (i-1,j), (i,j)
           Tt[c] = c11l + c01;  // node row cj+1, cells (i-1,j), (i,j)
         }
-        if (ty < TY - 1) {  // hand Tt to the warp above
+        // the warp above (higher id: scheduled first, so usually ahead) hands its B down;
+        // this warp outputs node row cj+1 = Tt (own, lower cells) + B (cells above).
+        if (ty >= 1) {
           if (n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
           double* dst = tw0 + b * (TY * TX * 3);
-          dst[0] = Tt[0]; dst[1] = Tt[1]; dst[2] = Tt[2];
+          dst[0] = B[0]; dst[1] = B[1]; dst[2] = B[2];
           __syncwarp();
           if (tx == 0) mbar_arrive_a(tfw0 + 8u * TY * b);
         }
-        if (ty >= 1) {
+        if (ty < TY - 1) {
           mbar_wait_a(tfr0 + 8u * TY * b, n & 1);
           const double* src = tr0 + b * (TY * TX * 3);
           double v[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) v[c] = src[c] + B[c];
+          for (int c = 0; c < 3; ++c) v[c] = Tt[c] + src[c];
           __syncwarp();
           if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
           if (owner) {
@@ -238,7 +242,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
                               CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   constexpr int TX = 32;
   using Ring = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX>;
-  const size_t smem = Ring::BYTES + 2 * TY * TX * 3 * sizeof(double) + 4 * TY * sizeof(uint64_t) + Ring::META;
+  const size_t smem = Ring::BYTES + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t) + Ring::META;
   auto kern = mode ? elastic_kernel<TM, 1, TY, S> : elastic_kernel<TM, 0, TY, S>;
   static bool attr_set[2] = {false, false};
   if (!attr_set[mode]) {
@@ -266,7 +270,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
 cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int mode,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   if (maps.u) return launch_cfg<true, kElTY, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
-  return launch_cfg<false, kElTY, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  return launch_cfg<false, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
 }
 
 }  // namespace fem
