@@ -92,8 +92,9 @@ struct fem_op_s {
   // CG vectors in the library padded layout: node (i,j) comp c of local plane kk
   // (kk = 0 is the ghost plane k0-1) at v[pl_lead + kk*pl_pp + j*pl_rp + i*C + c]
   int64_t pl_lead = 0, pl_rp = 0, pl_pp = 0, pl_n = 0;
-  double *x_pl = nullptr, *r_pl = nullptr, *p_pl = nullptr, *q_pl = nullptr;
-  CUtensorMap tm_x{}, tm_p{}, tm_mat{};
+  double *x_pl = nullptr, *r_pl = nullptr, *p_pl = nullptr, *q_pl = nullptr, *p2_pl = nullptr;
+  CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{};
+  int cg_parity = 0;  // fused CG: iteration parity (p_pl / p2_pl ping-pong)
   bool tm_ok = false;
   int64_t tm_i0 = 0, tm_j0 = 0, tm_k0 = 0;
   CgScalars* sc = nullptr;
@@ -106,7 +107,7 @@ struct fem_op_s {
   const double* cg_b = nullptr;
   double* cg_x = nullptr;
   bool cg_active = false;
-  cudaGraphExec_t graph1 = nullptr, graphN = nullptr;
+  cudaGraphExec_t graph1 = nullptr, graphN = nullptr, graph1b = nullptr;
   // options
   int use_graph = 1, check_every = 16, time_apply = 0;
   std::vector<cudaEvent_t> ev;
@@ -295,11 +296,11 @@ static int make_pl_maps(fem_op_s* op) {
   op->tm_j0 = lo;
   op->tm_k0 = k0;
   const int64_t off = op->pl_lead + (k0 - (g.k0 - 1)) * op->pl_pp + lo * op->pl_rp + lo * C;
-  for (int v = 0; v < 2; ++v) {
-    const double* base = (v == 0 ? op->x_pl : op->p_pl) + off;
-    FEM_TRY(make_map3d(v == 0 ? &op->tm_x : &op->tm_p, base, (uint64_t)((i1 - lo + 1) * C),
-                       (uint64_t)(j1 - lo + 1), (uint64_t)(k1 - k0 + 1), op->pl_rp * 8, op->pl_pp * 8,
-                       bw, bh));
+  double* vecs[4] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl};
+  CUtensorMap* maps[4] = {&op->tm_x, &op->tm_p, &op->tm_r, &op->tm_p2};
+  for (int v = 0; v < 4; ++v) {
+    FEM_TRY(make_map3d(maps[v], vecs[v] + off, (uint64_t)((i1 - lo + 1) * C), (uint64_t)(j1 - lo + 1),
+                       (uint64_t)(k1 - k0 + 1), op->pl_rp * 8, op->pl_pp * 8, bw, bh));
   }
   op->tm_ok = true;
   return FEM_OK;
@@ -317,7 +318,7 @@ static int make_mat_map(fem_op_s* op) {
 static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* umap, int mode,
                         cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
-  ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0};
+  ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
@@ -491,7 +492,8 @@ static void op_free(fem_op_s* op) {
   if (op->graphN) cudaGraphExecDestroy(op->graphN);
   for (auto e : op->ev) cudaEventDestroy(e);
   cudaFree(op->lm);
-  cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl);
+  cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
+  if (op->graph1b) cudaGraphExecDestroy(op->graph1b);
   cudaFree(op->ghost_lo); cudaFree(op->ghost_hi);
   cudaFree(op->stage_a); cudaFree(op->stage_b);
   cudaFree(op->sc); cudaFree(op->dot_dev); cudaFree(op->bad);
@@ -536,6 +538,7 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   OP_TRY(dalloc(&op->r_pl, op->pl_n));
   OP_TRY(dalloc(&op->p_pl, op->pl_n));
   OP_TRY(dalloc(&op->q_pl, op->pl_n));
+  OP_TRY(dalloc(&op->p2_pl, op->pl_n));
   OP_TRY(dalloc(&op->ghost_lo, op->plane_dofs));
   OP_TRY(dalloc(&op->ghost_hi, op->plane_dofs));
   OP_TRY(dalloc(&op->sc, 1));
@@ -555,7 +558,8 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
       cudaMemset(op->x_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
       cudaMemset(op->r_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
       cudaMemset(op->p_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
-      cudaMemset(op->q_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess) {
+      cudaMemset(op->q_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
+      cudaMemset(op->p2_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess) {
     op_free(op);
     return fail(FEM_ECUDA, "cudaMemset failed");
   }
@@ -707,14 +711,61 @@ static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
   return FEM_OK;
 }
 
-static int capture(fem_op_s* op, int iters, cudaStream_t s, cudaGraphExec_t* out) {
+// fused CG iteration (TMA path): p = r + beta p_old formed inside the apply (NEXT #1 of the
+// survey, 88 -> 80 B/DOF for Laplace); parity selects the p ping-pong buffers.
+static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
+  fem_mesh_s* m = op->mesh;
+  double* pold = parity ? op->p2_pl : op->p_pl;
+  double* pnew = parity ? op->p_pl : op->p2_pl;
+  if (m->nranks > 1) {
+    for (double* v : {op->r_pl, pold})
+      FEM_TRY(halo_pitch(op, pl_owned(op, v), v + op->pl_lead,
+                         v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp, op->pl_pp, s));
+  }
+  if (timed) {
+    if (op->ev_used + 2 > op->ev.size()) {
+      for (int t = 0; t < 64; ++t) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        op->ev.push_back(e);
+      }
+    }
+    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used], s));
+  }
+  ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
+                 parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew)};
+  cudaError_t e;
+  if (op->kind == FEM_ELASTICITY)
+    e = launch_elastic(op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc, op->red, s,
+                       m->sm_count);
+  else
+    e = launch_laplace(op->comps, op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc,
+                       op->red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "fused apply launch: %s", cudaGetErrorString(e));
+  if (timed) {
+    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used + 1], s));
+    op->ev_used += 2;
+  }
+  FEM_TRY(allreduce1(op, &op->sc->pq, s));
+  e = launch_cg_update_fused(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, pnew),
+                             pl_owned(op, op->q_pl), pl_count(op), op->sc, op->red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
+  FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
+  return FEM_OK;
+}
+
+static int iteration(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
+  return op->tm_ok ? cg_fused_body(op, parity, s, timed) : cg_iteration_body(op, s, timed);
+}
+
+static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGraphExec_t* out) {
   // capture on a private stream (legacy stream 0 cannot be captured)
   cudaStream_t cs;
   CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   const int64_t before = g_launches.load();
   int st = FEM_OK;
-  for (int t = 0; t < iters && st == FEM_OK; ++t) st = cg_iteration_body(op, cs, false);
+  for (int t = 0; t < iters && st == FEM_OK; ++t) st = iteration(op, (parity + t) & 1, cs, false);
   g_launches.store(before);  // captured launches are counted at replay
   cudaGraph_t graph;
   cudaError_t e = cudaStreamEndCapture(cs, &graph);
@@ -747,6 +798,7 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
   FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
   e = launch_cg_finish_init(op->sc, tol, maxit, s);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "init launch: %s", cudaGetErrorString(e));
+  op->cg_parity = 0;
   op->cg_b = b;
   op->cg_x = x;
   op->cg_active = true;
@@ -754,23 +806,30 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
 }
 
 static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
-  const int per_iter_launches = 3;
+  const int per_iter_launches = op->tm_ok ? 2 : 3;
   if (op->time_apply || !op->use_graph) {
-    for (int t = 0; t < iters; ++t) FEM_TRY(cg_iteration_body(op, s, op->time_apply != 0));
+    for (int t = 0; t < iters; ++t) {
+      FEM_TRY(iteration(op, op->cg_parity, s, op->time_apply != 0));
+      op->cg_parity ^= 1;
+    }
     return FEM_OK;
   }
-  const int N = 8;
-  if (!op->graph1) FEM_TRY(capture(op, 1, s, &op->graph1));
-  if (iters >= N && !op->graphN) FEM_TRY(capture(op, N, s, &op->graphN));
+  const int N = 8;  // even: a graph of N iterations starts and ends on parity 0
+  if (!op->graph1) FEM_TRY(capture(op, 1, 0, s, &op->graph1));
+  if (!op->graph1b) FEM_TRY(capture(op, 1, 1, s, &op->graph1b));
+  if (iters >= N && !op->graphN) FEM_TRY(capture(op, N, 0, s, &op->graphN));
   int left = iters;
-  while (left >= N) {
-    CUDA_TRY(cudaGraphLaunch(op->graphN, s));
-    add_launches(N * per_iter_launches);
-    left -= N;
-  }
-  while (left-- > 0) {
-    CUDA_TRY(cudaGraphLaunch(op->graph1, s));
-    add_launches(per_iter_launches);
+  while (left > 0) {
+    if (op->cg_parity == 0 && left >= N) {
+      CUDA_TRY(cudaGraphLaunch(op->graphN, s));
+      add_launches(N * per_iter_launches);
+      left -= N;
+    } else {
+      CUDA_TRY(cudaGraphLaunch(op->cg_parity ? op->graph1b : op->graph1, s));
+      add_launches(per_iter_launches);
+      op->cg_parity ^= 1;
+      --left;
+    }
   }
   return FEM_OK;
 }

@@ -34,11 +34,16 @@ struct OutVec {
 };
 
 // TMA tensor maps of one apply launch (u plane: padded layout; material: interleaved lambda/mu)
+// mode 2 (fused CG): the operator input is p = r + beta p_old formed in the kernel; u is r,
+// u2 is p_old, p is written to pnew (owned nodes, padded layout of x).
 struct ApplyMaps {
   const CUtensorMap* u;    // nullptr: use the bulk-row path
   int64_t t_i0, t_j0, t_k0;  // global node of the u tensor origin
   const CUtensorMap* mat;  // elasticity only
   int64_t mat_layer0;
+  const CUtensorMap* u2;   // mode 2: p_old
+  const double* pold;      // mode 2: p_old owned plane k0 (same layout as x)
+  double* pnew;            // mode 2: p output owned plane k0 (same layout as x)
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).
@@ -53,6 +58,8 @@ struct CgScalars {
   int32_t it;       // iterations completed
   int32_t maxit;
   int32_t breakdown_iter;
+  int32_t first;    // fused CG: 1 before the first apply (beta = 0, p = r)
+  int32_t pad1;
 };
 
 // Last-block reduction workspace: per-CTA partials + ticket counter.
@@ -76,7 +83,8 @@ inline void u_box(int kind, unsigned* w, unsigned* h) {
 inline void mat_box(unsigned* w, unsigned* h) { *w = 2 * 32; *h = kElTY; }
 
 // ---- launchers (return cudaError_t of the launch) -----------------------------------------
-// mode: 0 plain apply (y = A_c x), 1 CG apply (also pq partial -> sc->pq; skips if sc->done)
+// mode: 0 plain apply (y = A_c x), 1 CG apply (also pq partial -> sc->pq; skips if sc->done),
+//       2 fused CG apply (p = r + beta p_old in the kernel, writes p and q, pq)
 cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps,
                            int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
 cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int mode,
@@ -93,6 +101,9 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
                              CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
 cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* sc, Reduce red,
                               cudaStream_t s, int sm_count);
+// fused CG: x += alpha p; r -= alpha q; rr_new = r.r; iteration bookkeeping (p update is in the apply)
+cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
+                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
 // deterministic dot -> *out (device)
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
                        cudaStream_t s, int sm_count);

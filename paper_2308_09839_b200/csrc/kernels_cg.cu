@@ -51,6 +51,7 @@ __global__ void cg_finish_init_kernel(CgScalars* sc, double tol, int maxit) {
   sc->it = 0;
   sc->maxit = maxit;
   sc->breakdown_iter = -1;
+  sc->first = 1;
   sc->done = (rr == 0.0) ? 1 : (maxit <= 0 ? 3 : 0);
 }
 
@@ -82,6 +83,47 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
   double bs = block_sum(acc, sh);
   double tot;
   if (last_block_reduce(bs, red, sh, &tot)) sc->rr_new = tot;
+}
+
+// fused CG (mode-2 apply has formed p = r + beta p_old and q = A p):
+//   alpha = rr / pq; x += alpha p; r -= alpha q; rr_new = r.r; it++; convergence -> done.
+// The next mode-2 apply reads beta = rr_new / rr and rolls rr = rr_new in its last block.
+__global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __restrict__ x,
+                                                                      double* __restrict__ r,
+                                                                      const double* __restrict__ p,
+                                                                      const double* __restrict__ q,
+                                                                      int64_t n, CgScalars* sc,
+                                                                      Reduce red) {
+  __shared__ double sh[32];
+  if (sc->done) return;
+  const double pq = sc->pq;
+  if (!(pq > 0.0) || !isfinite(pq)) {  // breakdown: same decision in every block
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc->breakdown_iter = sc->it;
+      sc->done = 2;
+    }
+    return;
+  }
+  const double alpha = sc->rr / pq;
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    acc = fma(ri, ri, acc);
+  }
+  double bs = block_sum(acc, sh);
+  double tot;
+  if (last_block_reduce(bs, red, sh, &tot)) {
+    sc->rr_new = tot;
+    const int it = sc->it + 1;
+    sc->it = it;
+    if (tot == 0.0 || tot <= sc->stop_rr)
+      sc->done = 1;
+    else if (it >= sc->maxit)
+      sc->done = 3;
+  }
 }
 
 __global__ void __launch_bounds__(kVecThreads) cg_pupdate_kernel(const double* __restrict__ r,
@@ -154,6 +196,12 @@ cudaError_t launch_cg_finish_init(CgScalars* sc, double tol, int maxit, cudaStre
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* q, int64_t n,
                              CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   cg_update_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
+                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  cg_update_fused_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -125,7 +125,7 @@ struct TmaOrigin {
 // Ring of S plane slots.  Slot: u region ROWS x PITCH doubles (+ material MROWS x MPITCH).
 //   TM:  PITCH = BOXW (box width, doubles); data at row r, element col*C + comp.
 //   !TM: PITCH even >= COLS*C + 4, row data start at lead[slot][row] in {2,3}; slot S = zeros.
-template <bool TM, int ROWS, int COLS, int C, int S, int MROWS = 0, int MCOLS = 0>
+template <bool TM, int ROWS, int COLS, int C, int S, int MROWS = 0, int MCOLS = 0, int NU = 1>
 struct PlaneRing {
   // box width: COLS*C rounded to even, +2 so the box can start one element early (the box x
   // origin must be 16-B aligned: odd element offsets are shifted, see tshift)
@@ -134,7 +134,8 @@ struct PlaneRing {
   static constexpr int UDBL = ((ROWS * PITCH) + 15) & ~15;          // 128-B multiple
   static constexpr int MPITCH = 2 * MCOLS;                           // doubles per material row
   static constexpr int MDBL = ((MROWS * MPITCH) + 15) & ~15;
-  static constexpr int SLOT = UDBL + MDBL;                           // doubles, 128-B multiple
+  static constexpr int SLOT = NU * UDBL + MDBL;                      // doubles, 128-B multiple
+  static_assert(NU == 1 || TM, "two u boxes only on the tensor path");
   static constexpr int NSLOT = TM ? S : S + 1;
   static constexpr size_t BYTES = (size_t)NSLOT * SLOT * sizeof(double);
   static constexpr size_t META = 2 * S * sizeof(uint64_t) + ((S + 1) * ROWS + 2 * S) * sizeof(int);
@@ -193,9 +194,11 @@ struct PlaneRing {
   __device__ __forceinline__ void produce(const PlaneSrc& x, const Grid& g, int64_t pfirst, int64_t plast,
                                           int64_t ilo, int64_t jlo, int bc, int lane,
                                           const CUtensorMap* umap, TmaOrigin uorg,
-                                          const CUtensorMap* mmap, int64_t mlayer0) {
+                                          const CUtensorMap* mmap, int64_t mlayer0,
+                                          const CUtensorMap* umap2 = nullptr) {
     if (lane == 0) {
       if (TM) tma_prefetch_desc(umap);
+      if (NU == 2) tma_prefetch_desc(umap2);
       if (MROWS > 0) tma_prefetch_desc(mmap);
     }
     // ---- row-path per-lane descriptors (plane independent) ----
@@ -235,9 +238,10 @@ struct PlaneRing {
       double* slot = buf + (size_t)s * SLOT;
       if (TM) {
         if (lane == 0) {
-          mbar_arrive_expect_tx(&full[s], UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
+          mbar_arrive_expect_tx(&full[s], NU * UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
           tma_load_3d(slot, umap, ux, uy, (int)(p - uorg.t_k0), &full[s]);
-          if (MROWS > 0) tma_load_3d(slot + UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
+          if (NU == 2) tma_load_3d(slot + UDBL, umap2, ux, uy, (int)(p - uorg.t_k0), &full[s]);
+          if (MROWS > 0) tma_load_3d(slot + NU * UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
         }
         continue;
       }
@@ -288,13 +292,13 @@ struct PlaneRing {
 
   // base of row r of slot s for reading the u plane
   __device__ __forceinline__ const double* row_ptr(int s, int r) const {
-    if (TM) return buf + (size_t)s * SLOT + r * PITCH + tshift;
+    if (TM) return buf + (size_t)s * SLOT + r * PITCH + tshift;  // (second box: + UDBL)
     const int ss = valid[s] ? s : S;
     return buf + (size_t)ss * SLOT + r * PITCH + lead[ss * ROWS + r];
   }
   // material (lambda, mu) of tile cell (col, row) in slot s (zeros outside the box)
   __device__ __forceinline__ double2 mat(int s, int row, int col) const {
-    return reinterpret_cast<const double2*>(buf + (size_t)s * SLOT + UDBL)[row * MCOLS + col];
+    return reinterpret_cast<const double2*>(buf + (size_t)s * SLOT + NU * UDBL)[row * MCOLS + col];
   }
 };
 

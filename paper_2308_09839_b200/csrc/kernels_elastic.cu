@@ -38,8 +38,10 @@ template <bool TM, int MODE, int TY, int S>
 __global__ void __launch_bounds__(32 * (TY + 1), 1)
     elastic_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
+                   const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
                    int bc, int64_t kchunk, CgScalars* sc, Reduce red) {
   constexpr int mode = MODE;
+  constexpr int NU = (MODE == 2) ? 2 : 1;
   // TY consumer warps (lane = cell column, warp = cell row) + 1 producer warp
   constexpr int TX = 32;
   constexpr int NT = TX * (TY + 1);
@@ -47,7 +49,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
   constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
   constexpr int TPART = 4 * TY * TX * 3;  // y hand-off buffers (ring of 4)
-  using Ring = PlaneRing<TM, ROWS, COLS, 3, S, TY, TX>;
+  using Ring = PlaneRing<TM, ROWS, COLS, 3, S, TY, TX, NU>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
@@ -57,7 +59,9 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + 4 * TY));
   const uint32_t tfull_a = smem_u32(tfull), tempty_a = smem_u32(tempty);
 
-  if (mode == 1 && sc->done) return;
+  if (mode >= 1 && sc->done) return;
+  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
+  const double beta = (mode == 2) ? (sc->first ? 0.0 : sc->rr_new / sc->rr) : 0.0;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
@@ -78,7 +82,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
 
   double pq = 0.0;
   if (ty == TY) {
-    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, &mmap, mat_layer0);
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, &mmap, mat_layer0, &umap2);
   } else {
     const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
     const double hs = g.h * (1.0 / 16.0);
@@ -87,7 +91,10 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
     const bool bnode_xy = bc && (ci == 0 || ci == g.nx || nj == 0 || nj == g.ny);
     // output / boundary-read pointers, advanced by one plane per output plane
     double* yp = yo.y + (kb - g.k0) * yo.ppitch + (owner ? nj * yo.rpitch + ci * 3 : 0);
-    const double* xpb = x.main + (kb - g.k0) * x.ppitch + (owner ? nj * x.rpitch + ci * 3 : 0);
+    const int64_t xoff0 = (kb - g.k0) * x.ppitch + (owner ? nj * x.rpitch + ci * 3 : 0);
+    const double* xpb = x.main + xoff0;
+    const double* ppb = (mode == 2) ? pold + xoff0 : nullptr;  // p_old (mode 2, boundary nodes)
+    double* pnb = (mode == 2) ? pnew + xoff0 : nullptr;        // p written here (mode 2)
     const int nplane = (int)(ke - pfirst + 1);  // planes kb-1 .. ke
     const int qface0 = bc ? (int)(0 - kb) : -1000000;     // output index of node plane 0
     const int qface1 = bc ? (int)(g.nz - kb) : -1000000;  // ... of node plane nz
@@ -112,8 +119,17 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        xn[c] = r1[c];  // node (ci, cj+1): the node this thread outputs
-        ft[c] = face_fwd(r0[c], r0[3 + c], r1[c], r1[3 + c]);
+        double a00 = r0[c], a10 = r0[3 + c], a01 = r1[c], a11 = r1[3 + c];
+        if (mode == 2) {  // p = r + beta p_old (second box)
+          const double* q0 = r0 + Ring::UDBL;
+          const double* q1 = r1 + Ring::UDBL;
+          a00 = fma(beta, q0[c], a00);
+          a10 = fma(beta, q0[3 + c], a10);
+          a01 = fma(beta, q1[c], a01);
+          a11 = fma(beta, q1[3 + c], a11);
+        }
+        xn[c] = a01;  // node (ci, cj+1): the node this thread outputs
+        ft[c] = face_fwd(a00, a10, a01, a11);
       }
       ring.release(slot, tx);
       L = lmn.x * hs;
@@ -218,22 +234,31 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
               double vv = v[c], xv = xsave[c];
               if (bnode) {
                 xv = xpb[c];
+                if (mode == 2) xv = fma(beta, ppb[c], xv);
                 vv = xv;
               }
               yp[c] = vv;
-              if (mode == 1) pq = fma(vv, xv, pq);
+              if (mode == 2) pnb[c] = xv;
+              if (mode >= 1) pq = fma(vv, xv, pq);
             }
           }
+          if (mode == 2) { ppb += x.ppitch; pnb += x.ppitch; }
           yp += yo.ppitch;
           xpb += x.ppitch;
         }
       }
     }
   }
-  if (mode == 1) {
+  if (mode >= 1) {
     double bsum = block_sum(pq, red_sh);
     double total;
-    if (last_block_reduce(bsum, red, red_sh, &total)) sc->pq = total;
+    if (last_block_reduce(bsum, red, red_sh, &total)) {
+      sc->pq = total;
+      if (mode == 2) {  // every block has read rr / rr_new / first: roll the recurrence
+        sc->rr = sc->rr_new;
+        sc->first = 0;
+      }
+    }
   }
 }
 
@@ -241,10 +266,13 @@ template <bool TM, int TY, int S>
 static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int bc, int mode,
                               CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   constexpr int TX = 32;
-  using Ring = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX>;
-  const size_t smem = Ring::BYTES + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t) + Ring::META;
-  auto kern = mode ? elastic_kernel<TM, 1, TY, S> : elastic_kernel<TM, 0, TY, S>;
-  static bool attr_set[2] = {false, false};
+  using Ring1 = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX, 1>;
+  using Ring2 = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX, (TM ? 2 : 1)>;
+  const size_t ring_bytes = mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META;
+  const size_t smem = ring_bytes + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t);
+  auto kern = mode == 2 ? elastic_kernel<TM, (TM ? 2 : 1), TY, S>
+                        : (mode ? elastic_kernel<TM, 1, TY, S> : elastic_kernel<TM, 0, TY, S>);
+  static bool attr_set[3] = {false, false, false};
   if (!attr_set[mode]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -259,17 +287,23 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
-  CUtensorMap um;
+  CUtensorMap um, um2;
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
+  if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
-  kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, bc, kchunk, sc, red);
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
+                                 bc, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int mode,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
-  if (maps.u) return launch_cfg<true, kElTY, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
+  if (maps.u) {
+    if (mode == 2) return launch_cfg<true, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    return launch_cfg<true, kElTY, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  }
   return launch_cfg<false, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
 }
 

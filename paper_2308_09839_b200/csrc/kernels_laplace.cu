@@ -21,19 +21,23 @@ namespace fem {
 template <bool TM, int MODE, int C, int TX, int TY, int R, int S>
 __global__ void __launch_bounds__(TX*(TY + 1), 2)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
-                   TmaOrigin uorg, int bc, int64_t kchunk, CgScalars* sc, Reduce red) {
+                   TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
+                   double* pnew, int bc, int64_t kchunk, CgScalars* sc, Reduce red) {
   constexpr int mode = MODE;
+  constexpr int NU = (MODE == 2) ? 2 : 1;
   // TY consumer warps (one node column per lane, R node rows each) + 1 producer warp
   constexpr int NT = TX * (TY + 1);
   constexpr int ROWS = TY * R + 2;
   constexpr int COLS = TX + 2;
-  using Ring = PlaneRing<TM, ROWS, COLS, C, S>;
+  using Ring = PlaneRing<TM, ROWS, COLS, C, S, 0, 0, NU>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
   ring.carve(smem_raw, smem_raw + Ring::BYTES);
 
-  if (mode == 1 && sc->done) return;
+  if (mode >= 1 && sc->done) return;
+  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
+  const double beta = (mode == 2) ? (sc->first ? 0.0 : sc->rr_new / sc->rr) : 0.0;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
@@ -47,7 +51,7 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
 
   double pq = 0.0;
   if (ty == TY) {
-    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, nullptr, 0);
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, nullptr, 0, &umap2);
   } else {
     const int64_t i = i0 + tx;
     const double h36 = g.h * (1.0 / 36.0);
@@ -98,11 +102,15 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
 #pragma unroll
       for (int rr = 0; rr < R + 2; ++rr) {
         const double* row = ring.row_ptr(slot, ty * R + rr) + tx * C;
+        const double* row2 = row + Ring::UDBL;  // mode 2: p_old box
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          const double xm = row[c];
-          const double x0 = row[C + c];
-          const double xp = row[2 * C + c];
+          double xm = row[c], x0 = row[C + c], xp = row[2 * C + c];
+          if (mode == 2) {
+            xm = fma(beta, row2[c], xm);
+            x0 = fma(beta, row2[C + c], x0);
+            xp = fma(beta, row2[2 * C + c], xp);
+          }
           const double sn = xm + xp;
           a[rr][c] = fma(2.0 * mx, x0, sn);
           b[rr][c] = fma(mx, x0, -sn);
@@ -127,6 +135,8 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
         const bool qface = bc && (q == 0 || q == g.nz);
         double* yq = yo.y + (q - g.k0) * yo.ppitch;
         const double* xq = x.main + (q - g.k0) * x.ppitch;
+        const double* pq_old = (mode == 2) ? pold + (q - g.k0) * x.ppitch : nullptr;
+        double* pq_new = (mode == 2) ? pnew + (q - g.k0) * x.ppitch : nullptr;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!active[r]) continue;
@@ -135,32 +145,42 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
             double v, xv = xcw[0][r][c];
             if (qface || bnode_xy[r]) {
               xv = xq[off_x[r] + c];
+              if (mode == 2) xv = fma(beta, pq_old[off_x[r] + c], xv);
               v = xv;
             } else {
               const double nb = (c2w[0][r][c] - c1w[0][r][c]) + (c2w[2][r][c] - c1w[2][r][c]);
               v = h36 * fma(2.0 * mz, c2w[1][r][c], fma(mz, c1w[1][r][c], nb));
             }
             yq[off_y[r] + c] = v;
-            if (mode == 1) pq = fma(v, xv, pq);
+            if (mode == 2) pq_new[off_x[r] + c] = xv;
+            if (mode >= 1) pq = fma(v, xv, pq);
           }
         }
       }
     }
   }
-  if (mode == 1) {
+  if (mode >= 1) {
     double bsum = block_sum(pq, red_sh);
     double total;
-    if (last_block_reduce(bsum, red, red_sh, &total)) sc->pq = total;
+    if (last_block_reduce(bsum, red, red_sh, &total)) {
+      sc->pq = total;
+      if (mode == 2) {  // every block has read rr / rr_new / first: roll the recurrence
+        sc->rr = sc->rr_new;
+        sc->first = 0;
+      }
+    }
   }
 }
 
 template <bool TM, int C, int TX, int TY, int R, int S>
 static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int bc, int mode,
                               CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
-  using Ring = PlaneRing<TM, TY * R + 2, TX + 2, C, S>;
-  const size_t smem = Ring::BYTES + Ring::META;
-  auto kern = mode ? laplace_kernel<TM, 1, C, TX, TY, R, S> : laplace_kernel<TM, 0, C, TX, TY, R, S>;
-  static bool attr_set[2] = {false, false};
+  using Ring1 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, 1>;
+  using Ring2 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, (TM ? 2 : 1)>;
+  const size_t smem = (mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META);
+  auto kern = mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S>
+                        : (mode ? laplace_kernel<TM, 1, C, TX, TY, R, S> : laplace_kernel<TM, 0, C, TX, TY, R, S>);
+  static bool attr_set[3] = {false, false, false};
   if (!attr_set[mode]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -176,18 +196,21 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
-  CUtensorMap um;
+  CUtensorMap um, um2;
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
+  if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
-  kern<<<grid, block, smem, s>>>(g, x, y, um, org, bc, kchunk, sc, red);
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, um2, maps.pold, maps.pnew, bc, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps,
                            int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
   if (maps.u) {
     if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    if (mode == 2) return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
   }
   if (comps == 1) return launch_cfg<false, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
