@@ -58,9 +58,19 @@ def algorithmic_apply_bytes(kind, nx, ny, nz):
     return b
 
 
-def cg_vector_bytes(ndof):
-    # update: read x,p,r,q write x,r (48 B/DOF); p-update: read r,p write p (24 B/DOF)
-    return 72 * ndof
+def cg_apply_bytes(kind, nx, ny, nz, fused):
+    """Algorithmic bytes of the apply launched inside one CG iteration.  Fused:
+    read r and p_old, write p and q (32 B/DOF) + lambda, mu (16 B/cell); unfused: 16 B/DOF."""
+    ndof = I.n_nodes(nx, ny, nz) * I.ncomp(kind)
+    b = (32 if fused else 16) * ndof
+    if kind == "elastic":
+        b += 16 * nx * ny * nz
+    return b
+
+
+def cg_vector_bytes(ndof, fused):
+    # update: read x,p,r,q write x,r (48 B/DOF); unfused p-update: read r,p write p (24 B/DOF)
+    return (48 if fused else 72) * ndof
 
 
 class ClockSampler:
@@ -284,8 +294,9 @@ def run_native(args, cfg):
     # ---- roofline of the dominant kernel (the apply) ----
     hbm_peak, peak_src = measured_peaks()
     nloc_planes = k1 - k0
+    fused = bool(op.get_option("fused_cg"))
     # algorithmic bytes of one rank's apply launch: owned planes (+ its cell layers)
-    alg_bytes = algorithmic_apply_bytes(kind, nx, ny, nz) * nloc_planes / (nz + 1)
+    alg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) * nloc_planes / (nz + 1)
     achieved = alg_bytes / (apply_ms / 1e3) / 1e9
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}.json")
@@ -315,7 +326,10 @@ def run_native(args, cfg):
     extra["apply_in_cg_ms"] = apply_ms
     extra["apply_share_of_step"] = share
     extra["cg_iteration_ms"] = ms / args.steps
-    extra["cg_bytes_per_dof_alg"] = algorithmic_apply_bytes(kind, nx, ny, nz) / ndof_global + 72
+    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused)
+    extra["cg_bytes_per_dof_alg"] = cg_bytes / ndof_global
+    extra["cg_iteration_gbs"] = cg_bytes / (ms / args.steps / 1e3) / 1e9
+    extra["fused_cg"] = fused
     del xx, yy
 
     # ---- e2e: the public call a user makes, with pinned HOST buffers ----
@@ -367,7 +381,8 @@ def run_native(args, cfg):
                        "l2": "inputs larger than L2 (vectors %.2f GB each)" % (ndof_global * 8 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": f"{kind} apply (CG mode, fused p.Ap)",
+                         "kernel": (f"{kind} fused CG apply (p = r + beta p_old, q = A p, p.q)" if fused
+                                    else f"{kind} apply (CG mode, fused p.Ap)"),
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                          "frac_of_8TBps_nominal": achieved / 8000.0},
             "clocks": clocks,

@@ -142,6 +142,10 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * convergence polls in fem_cg_solve), "time_apply" (1: record CUDA events around every apply
  * launched by fem_cg_iterate; read back with fem_apply_time). */
 int fem_set_option(fem_op_t op, const char* key, int64_t value);
+/* Read-only properties: "fused_cg" (1: CG iterations use the fused apply -- p = r + beta p_old
+ * formed inside the TMA apply kernel -- and 2 kernels per iteration; 0: apply + update +
+ * p-update), "tma" (1: CG applies stage planes with TMA tensor maps), plus the options above. */
+int fem_get_option(fem_op_t op, const char* key, int64_t* value);
 /* Total device time (ms) and count of the applies timed since the last call (time_apply). */
 int fem_apply_time(fem_op_t op, double* total_ms, int64_t* count);
 void fem_op_destroy(fem_op_t op);

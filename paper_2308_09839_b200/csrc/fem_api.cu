@@ -942,6 +942,16 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
   return FEM_OK;
 }
 
+int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
+  if (!op || !key || !value) return fail(FEM_EINVAL, "op/key/value is NULL");
+  if (!std::strcmp(key, "fused_cg") || !std::strcmp(key, "tma")) *value = op->tm_ok ? 1 : 0;
+  else if (!std::strcmp(key, "use_graph")) *value = op->use_graph;
+  else if (!std::strcmp(key, "check_every")) *value = op->check_every;
+  else if (!std::strcmp(key, "time_apply")) *value = op->time_apply;
+  else return fail(FEM_EINVAL, "unknown option '%s'", key);
+  return FEM_OK;
+}
+
 int fem_apply_time(fem_op_t op, double* total_ms, int64_t* count) {
   if (!op) return fail(FEM_EINVAL, "op is NULL");
   FEM_TRY(set_device(op->mesh->device));

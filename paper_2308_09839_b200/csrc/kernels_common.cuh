@@ -56,17 +56,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
+// Wait for phase `parity` of an mbarrier.  The suspend-time hint lets the hardware park the warp
+// until the phase completes instead of spinning on issue slots (warps that run ahead of the
+// slowest consumer otherwise burn the issue bandwidth the slow warps need).
 __device__ __forceinline__ void mbar_wait_a(uint32_t addr, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@P1 bra DONE;\n"
       "bra LAB_WAIT;\n"
       "DONE:\n"
       "}\n" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(1000000)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_a(uint32_t addr) {

@@ -45,7 +45,7 @@ EXPORTS = [
     "fem_last_error", "fem_version", "fem_launch_count", "fem_get_unique_id", "fem_comm_create",
     "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy", "fem_op_create",
     "fem_op_ndof", "fem_set_material", "fem_apply", "fem_dot", "fem_cg_solve", "fem_cg_begin",
-    "fem_cg_iterate", "fem_cg_end", "fem_set_option", "fem_apply_time", "fem_op_destroy",
+    "fem_cg_iterate", "fem_cg_end", "fem_set_option", "fem_get_option", "fem_apply_time", "fem_op_destroy",
     "fem_csr_create", "fem_csr_info", "fem_csr_apply", "fem_csr_destroy",
 ]
 
@@ -89,6 +89,7 @@ def load(build_if_missing: bool = True):
         "fem_cg_iterate": ([vp, i32, vp], ctypes.c_int),
         "fem_cg_end": ([vp, P(CgInfo), vp], ctypes.c_int),
         "fem_set_option": ([vp, ctypes.c_char_p, i64], ctypes.c_int),
+        "fem_get_option": ([vp, ctypes.c_char_p, P(i64)], ctypes.c_int),
         "fem_apply_time": ([vp, P(dbl), P(i64)], ctypes.c_int),
         "fem_op_destroy": ([vp], None),
         "fem_csr_create": ([vp, P(vp)], ctypes.c_int),
@@ -270,6 +271,11 @@ class Operator:
 
     def set_option(self, key: str, value: int):
         _check(load().fem_set_option(self.h, key.encode(), int(value)))
+
+    def get_option(self, key: str) -> int:
+        v = ctypes.c_int64()
+        _check(load().fem_get_option(self.h, key.encode(), ctypes.byref(v)))
+        return v.value
 
     def apply_time(self):
         ms, n = ctypes.c_double(), ctypes.c_int64()
