@@ -26,6 +26,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "fem_internal.cuh"
 
 namespace fem {
@@ -119,6 +121,36 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
 
+// Persistent schedule: work item w = (tile x, tile y, z-chunk), CTAs take w = blockIdx.x,
+// blockIdx.x + gridDim.x, ... (consecutive items -> neighbouring tiles run together, L2 halo reuse).
+struct WorkGrid {
+  int xt, yt, zc;      // tiles in x, y; z-chunks
+  int64_t kchunk;      // node planes per z-chunk
+  __device__ __forceinline__ int items() const { return xt * yt * zc; }
+};
+
+// Host: choose the z-chunking so that the items (xt*yt*zc) spread evenly over `slots` resident
+// CTAs (minimise the idle fraction of the last round), with chunks of >= min_chunk planes.
+inline WorkGrid make_workgrid(int xt, int yt, int64_t nplanes, int64_t slots, int64_t min_chunk) {
+  WorkGrid best{xt, yt, 1, nplanes};
+  double best_eff = -1.0;
+  const int64_t tiles = (int64_t)xt * yt;
+  const int64_t zmax = std::max<int64_t>(1, nplanes / min_chunk);
+  for (int64_t zc = 1; zc <= zmax; ++zc) {
+    const int64_t kchunk = (nplanes + zc - 1) / zc;
+    const int64_t z = (nplanes + kchunk - 1) / kchunk;
+    const int64_t items = tiles * z;
+    const int64_t rounds = (items + slots - 1) / slots;
+    // useful work / (rounds * slots * chunk length incl. the 2-plane halo)
+    const double eff = (double)nplanes * tiles / ((double)rounds * slots * (kchunk + 2));
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = WorkGrid{xt, yt, (int)z, kchunk};
+    }
+  }
+  return best;
+}
+
 // Tensor-map coordinates of a tile: box origin = node (ilo, jlo) of plane k, relative to the
 // tensor origin (node (t_i0, t_j0) of plane t_k0).  Out-of-range coordinates zero-fill.
 struct TmaOrigin {
@@ -194,11 +226,12 @@ struct PlaneRing {
   // producer warp: stream planes pfirst .. plast (and material layers) through the ring.
   //   ilo, jlo: global node index of tile column 0 / row 0 (may be -1); material tile cells
   //   start at cell (ilo, jlo).  umap / uorg used when TM; mmap: material tensor (or nullptr).
+  //   tbase: ring position of plane pfirst (persistent CTAs continue the ring across work items)
   __device__ __forceinline__ void produce(const PlaneSrc& x, const Grid& g, int64_t pfirst, int64_t plast,
                                           int64_t ilo, int64_t jlo, int bc, int lane,
                                           const CUtensorMap* umap, TmaOrigin uorg,
                                           const CUtensorMap* mmap, int64_t mlayer0,
-                                          const CUtensorMap* umap2 = nullptr) {
+                                          const CUtensorMap* umap2 = nullptr, int tbase = 0) {
     if (lane == 0) {
       if (TM) tma_prefetch_desc(umap);
       if (NU == 2) tma_prefetch_desc(umap2);
@@ -235,7 +268,7 @@ struct PlaneRing {
 
 #pragma unroll 1
     for (int64_t p = pfirst; p <= plast; ++p) {
-      const int t = (int)(p - pfirst);
+      const int t = tbase + (int)(p - pfirst);
       const int s = t & (S - 1);
       if (t >= S) mbar_wait_a(empty_a + 8u * s, (uint32_t)(((t / S) - 1) & 1));
       double* slot = buf + (size_t)s * SLOT;
