@@ -96,6 +96,7 @@ struct fem_op_s {
   CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{};
   int cg_parity = 0;  // fused CG: iteration parity (p_pl / p2_pl ping-pong)
   bool tm_ok = false;
+  bool tm_interior = false;  // u tensor spans the interior only (Laplace + Dirichlet)
   int64_t tm_i0 = 0, tm_j0 = 0, tm_k0 = 0;
   CgScalars* sc = nullptr;
   CgScalars* sc_host = nullptr;
@@ -285,11 +286,16 @@ static int make_map3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1
 static int make_pl_maps(fem_op_s* op) {
   const Grid& g = op->mesh->g;
   const int C = op->comps;
-  const int64_t lo = op->bc ? 1 : 0;
-  const int64_t i1 = op->bc ? g.nx - 1 : g.nx, j1 = op->bc ? g.ny - 1 : g.ny;
-  const int64_t k0 = std::max<int64_t>(lo, g.k0 - 1), k1 = std::min<int64_t>(op->bc ? g.nz - 1 : g.nz, g.k1);
+  // Elasticity: the tensor spans the whole box (boundary nodes included: the Dirichlet mask P is
+  // applied in registers and the unmasked boundary values feed the identity rows without a
+  // global load).  Laplace with the Dirichlet box: the tensor spans only the interior, so the
+  // copy engine's zero fill is the mask (boundary rows read x from global memory).
+  const bool interior = op->tm_interior;
+  const int64_t lo = interior ? 1 : 0;
+  const int64_t i1 = interior ? g.nx - 1 : g.nx, j1 = interior ? g.ny - 1 : g.ny;
+  const int64_t k0 = std::max<int64_t>(lo, g.k0 - 1), k1 = std::min<int64_t>(interior ? g.nz - 1 : g.nz, g.k1);
   op->tm_ok = false;
-  if (i1 < lo || j1 < lo || k1 < k0) return FEM_OK;  // degenerate: the bulk-row path is used
+  if (i1 < lo || j1 < lo || k1 < k0) return FEM_OK;  // degenerate: bulk-row path, unfused CG
   unsigned bw, bh;
   u_box(op->kind, &bw, &bh);
   op->tm_i0 = lo;
@@ -318,7 +324,8 @@ static int make_mat_map(fem_op_s* op) {
 static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* umap, int mode,
                         cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
-  ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr};
+  ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr,
+                 op->tm_interior ? 1 : 0};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
@@ -523,7 +530,8 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   // padded layout: even row pitch, lead so that the tensor origin node is 16-B aligned
   op->pl_rp = ((g.nx + 1) * op->comps + 1) & ~1LL;
   op->pl_pp = op->pl_rp * (g.ny + 1);
-  op->pl_lead = bc ? (op->comps & 1) : 0;
+  op->tm_interior = bc && kind != FEM_ELASTICITY;
+  op->pl_lead = op->tm_interior ? (op->comps & 1) : 0;  // tensor-origin node 16-B aligned
   op->pl_n = (op->pl_lead + (op->nloc_planes + 2) * op->pl_pp + 1) & ~1LL;
   int st = FEM_OK;
 #define OP_TRY(x)                 \
@@ -733,7 +741,8 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
     CUDA_TRY(cudaEventRecord(op->ev[op->ev_used], s));
   }
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
-                 parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew)};
+                 parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
+                 op->tm_interior ? 1 : 0};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc, op->red, s,

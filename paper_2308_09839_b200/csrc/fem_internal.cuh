@@ -44,6 +44,7 @@ struct ApplyMaps {
   const CUtensorMap* u2;   // mode 2: p_old
   const double* pold;      // mode 2: p_old owned plane k0 (same layout as x)
   double* pnew;            // mode 2: p output owned plane k0 (same layout as x)
+  int interior;            // 1: u tensor spans only the Dirichlet interior (zero fill = mask)
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).

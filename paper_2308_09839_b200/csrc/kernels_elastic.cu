@@ -87,6 +87,9 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
     const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
     const double hs = g.h * (1.0 / 16.0);
     const int64_t nj = cj + 1;  // node row this thread outputs (top corners of its cell)
+    // Dirichlet mask flags of the cell's node columns ci, ci+1 and rows cj, cj+1 (TMA path)
+    const bool mc0 = bc && (ci == 0 || ci == g.nx), mc1 = bc && (ci + 1 == 0 || ci + 1 == g.nx);
+    const bool mr0 = bc && (cj == 0 || cj == g.ny), mr1 = bc && (cj + 1 == 0 || cj + 1 == g.ny);
     const bool owner = tx >= 1 && ty <= TY - 2 && ci <= g.nx && nj <= g.ny;
     const bool bnode_xy = bc && (ci == 0 || ci == g.nx || nj == 0 || nj == g.ny);
     // output / boundary-read pointers, advanced by one plane per output plane
@@ -117,6 +120,12 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       const double2 lmn = ring.mat(slot, ty, tx);  // material layer of this plane
       const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
       const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
+      // TMA path: the box holds every node of the box domain; the Dirichlet mask P is
+      // applied here (boundary nodes read as 0 for the operator, unmasked for the identity rows)
+      const int64_t pl = pfirst + t;
+      const bool pface = TM && bc && (pl == 0 || pl == g.nz);
+      const bool m00 = pface || mc0 || mr0, m10 = pface || mc1 || mr0;
+      const bool m01 = pface || mc0 || mr1, m11 = pface || mc1 || mr1;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         double a00 = r0[c], a10 = r0[3 + c], a01 = r1[c], a11 = r1[3 + c];
@@ -128,7 +137,13 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
           a01 = fma(beta, q1[c], a01);
           a11 = fma(beta, q1[3 + c], a11);
         }
-        xn[c] = a01;  // node (ci, cj+1): the node this thread outputs
+        xn[c] = a01;  // node (ci, cj+1): the node this thread outputs (unmasked)
+        if (TM && bc && (m00 || m10 || m01 || m11)) {
+          a00 = m00 ? 0.0 : a00;
+          a10 = m10 ? 0.0 : a10;
+          a01 = m01 ? 0.0 : a01;
+          a11 = m11 ? 0.0 : a11;
+        }
         ft[c] = face_fwd(a00, a10, a01, a11);
       }
       ring.release(slot, tx);
@@ -233,8 +248,10 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
             for (int c = 0; c < 3; ++c) {
               double vv = v[c], xv = xsave[c];
               if (bnode) {
-                xv = xpb[c];
-                if (mode == 2) xv = fma(beta, ppb[c], xv);
+                if (!TM) {  // row path: boundary values are not staged
+                  xv = xpb[c];
+                  if (mode == 2) xv = fma(beta, ppb[c], xv);
+                }
                 vv = xv;
               }
               yp[c] = vv;

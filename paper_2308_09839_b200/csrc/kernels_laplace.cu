@@ -22,7 +22,8 @@ template <bool TM, int MODE, int C, int TX, int TY, int R, int S>
 __global__ void __launch_bounds__(TX*(TY + 1), 2)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
-                   double* pnew, int bc, int64_t kchunk, CgScalars* sc, Reduce red) {
+                   double* pnew, int bc, int tmint, int64_t kchunk, CgScalars* sc, Reduce red) {
+  (void)tmint;  // Laplace uses interior-only tensors with the Dirichlet box (zero fill = mask)
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   // TY consumer warps (one node column per lane, R node rows each) + 1 producer warp
@@ -200,7 +201,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
   if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
-  kern<<<grid, block, smem, s>>>(g, x, y, um, org, um2, maps.pold, maps.pnew, bc, kchunk, sc, red);
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, um2, maps.pold, maps.pnew, bc, maps.interior, kchunk, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }
