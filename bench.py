@@ -190,9 +190,9 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+        "higher_is_better": True, "scaling": "weak" if "planes_per_rank" in cfg else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "kind": kind, "cells": list(cfg["n"]),
+        "config": {"workload": cfg["name"], "kind": kind, "cells": list(I.config_cells(cfg, ws)),
                    "sample_cells": [nx, ny, nz], "bc": "dirichlet_box"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": sample},
@@ -217,9 +217,10 @@ def run_native(args, cfg):
     fem.load(build_if_missing=(rank == 0 and ws == 1))
 
     kind = cfg["kind"]
-    nx, ny, nz = cfg["n"]
+    nx, ny, nz = I.config_cells(cfg, ws)
     h = 1.0 / nx
     c = I.ncomp(kind)
+    scaling = "weak" if "planes_per_rank" in cfg else "strong"
     comm = None
     if ws > 1:
         uid = [fem.unique_id() if rank == 0 else None]
@@ -372,7 +373,7 @@ def run_native(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg["name"], "kind": kind, "cells": [nx, ny, nz],
                        "ndof": ndof_global, "bc": "dirichlet_box",
@@ -453,7 +454,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=3, help="BASELINE.json configs index (0-3)")
+    ap.add_argument("--config", type=int, default=3,
+                    help="0-3: BASELINE.json configs[0..3]; 4/5: configs[4] weak scaling (scalar / elasticity)")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-csr", action="store_true")

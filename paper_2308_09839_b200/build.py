@@ -64,6 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                      "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
     if verbose:
         common += ["-Xptxas", "-v"]
+    common += os.environ.get("FEM_NVCC_FLAGS", "").split()  # experiments only (e.g. -DFEM_EL_TY=12)
     objs = []
 
     def compile_one(src):

@@ -74,7 +74,10 @@ constexpr int kMaxCtas = 1 << 16;
 
 // Tile shapes of the apply kernels (kernel templates and host tensor-map boxes must agree).
 constexpr int kLapTX = 32, kLapTY = 8, kLapR1 = 2, kLapR3 = 1;  // Laplace: C=1 / C=3 rows per thread
-constexpr int kElTY = 15;                                         // elasticity consumer warps
+#ifndef FEM_EL_TY
+#define FEM_EL_TY 15
+#endif
+constexpr int kElTY = FEM_EL_TY;                                      // elasticity consumer warps
 // u-plane TMA box (doubles x rows) per kind: width = (((cols * C) + 1) & ~1) + 2
 inline void u_box(int kind, unsigned* w, unsigned* h) {
   if (kind == 0) { *w = ((((kLapTX + 2) * 1) + 1) & ~1) + 2; *h = kLapTY * kLapR1 + 2; }

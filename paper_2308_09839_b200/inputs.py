@@ -24,7 +24,21 @@ CONFIGS = {
     1: dict(name="C2_scalar_256", kind="scalar", n=(256, 256, 256), bc=1, cg_iters=100),
     2: dict(name="C3_vector_256", kind="vector", n=(256, 256, 256), bc=1, cg_iters=100),
     3: dict(name="C4_elastic_384", kind="elastic", n=(384, 384, 384), bc=1, cg_iters=100),
+    # BASELINE configs[4], weak scaling: fixed node planes per GPU,
+    # nz = planes_per_rank * P - 1 cells -> ~1.25e8 DOF per GPU, ~1e9 DOF at P = 8
+    4: dict(name="C5a_scalar_weak", kind="scalar", n=(999, 999, None), planes_per_rank=125, bc=1,
+            cg_iters=100),
+    5: dict(name="C5b_elastic_weak", kind="elastic", n=(665, 665, None), planes_per_rank=94, bc=1,
+            cg_iters=100),
 }
+
+
+def config_cells(cfg: dict, nranks: int = 1):
+    """Cells per direction of a config at P ranks (weak configs grow in z with P)."""
+    nx, ny, nz = cfg["n"]
+    if nz is None:
+        nz = cfg["planes_per_rank"] * nranks - 1
+    return nx, ny, nz
 
 
 def rng(seed: int) -> np.random.Generator:

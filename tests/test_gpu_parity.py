@@ -35,7 +35,9 @@ def relerr(y, ref):
     return float(np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-300))
 
 
-MESHES = [(1, 1, 1), (2, 2, 2), (5, 7, 9), (33, 17, 12), (40, 31, 20), (64, 3, 5), (3, 70, 4)]
+# (64, 3, 5), (32, 32, 6): nx+1 (ny+1) = 1 mod the Laplace tile, so the last boundary column (row)
+# is written by the previous tile's producer warp (kernels_laplace.cu `ext`)
+MESHES = [(1, 1, 1), (2, 2, 2), (5, 7, 9), (33, 17, 12), (40, 31, 20), (64, 3, 5), (3, 70, 4), (32, 32, 6)]
 
 
 @pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
@@ -127,6 +129,25 @@ def test_dot_parity(F, oracle):
         ref = oracle.dot(a, b)
         assert abs(d - ref) <= 1e-14 * np.abs(a * b).sum()
         assert op.dot(a, b) == d  # host pointers, same kernel
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector"])
+def test_cg_laplace_edge_tiles(F, oracle, kind):
+    """Fused (TMA) CG on a mesh whose last boundary column and row are beyond the last tile, with
+    a right-hand side that is nonzero on the Dirichlet rows too (identity rows carry p, q, p.q)."""
+    nx, ny, nz = 32, 32, 6
+    h = 1.0 / 32
+    g = I.rng(I.SEED_BASE + 400)
+    c = I.ncomp(kind)
+    b = I.uniform_vector(g, nx, ny, nz, c)
+    ref = oracle.cg(kind, 1, nx, ny, nz, h, b, tol=1e-13, maxit=400)
+    assert ref.converged
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 1)
+    assert op.get_option("fused_cg") == 1
+    x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+    info = op.cg_solve(dev(b), x, tol=1e-13, maxit=400)
+    assert info["converged"] and abs(info["iterations"] - ref.iterations) <= 2
+    assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10 * max(1.0, np.abs(ref.x).max())
 
 
 def test_cg_c1_parity(F, oracle):
