@@ -397,19 +397,17 @@ typedef struct {
   double r0_norm, r_norm, true_r_norm;
 } orc_cg_info;
 
-/* ---------------------------------------------------------------------------------------
- * CG (P:185 Krylov method; recurrences of Table 4; stopping per reading R12):
+/* Apply callback of the CG core: y = A_c x for one of the two mesh descriptions below. */
+typedef int (*orc_apply_fn)(const void* ctx, const double* x, double* y);
+
+/* CG core (P:185 Krylov method; recurrences of Table 4; stopping per reading R12):
  *   r = b - A x0; p = r; rr = r.r; rho0 = sqrt(rr)
  *   for k < maxit: stop if sqrt(rr) <= tol*rho0 or rr == 0
  *     q = A p; pq = p.q; (pq <= 0 or non-finite -> breakdown)
  *     alpha = rr/pq; x += alpha p; r -= alpha q; rr' = r.r; beta = rr'/rr; p = r + beta p
- * res_hist (optional, length maxit+1) receives sqrt(rr) per iteration.
- * ------------------------------------------------------------------------------------- */
-int orc_cg(int kind, int bc, int64_t nx, int64_t ny, int64_t nz, double h, const double* lam,
-           const double* mu, const double* b, double* x, double tol, int maxit, orc_cg_info* info,
-           double* res_hist, int nthreads) {
-  const int c = (kind == ORC_SCALAR) ? 1 : 3;
-  const int64_t n = (nx + 1) * (ny + 1) * (nz + 1) * c;
+ * res_hist (optional, length maxit+1) receives sqrt(rr) per iteration. */
+static int cg_core(orc_apply_fn apply, const void* ctx, int64_t n, const double* b, double* x,
+                   double tol, int maxit, orc_cg_info* info, double* res_hist) {
   double* r = (double*)malloc(sizeof(double) * n);
   double* p = (double*)malloc(sizeof(double) * n);
   double* q = (double*)malloc(sizeof(double) * n);
@@ -417,7 +415,7 @@ int orc_cg(int kind, int bc, int64_t nx, int64_t ny, int64_t nz, double h, const
     free(r); free(p); free(q);
     return ORC_ENOMEM;
   }
-  int rc = orc_apply(kind, bc, nx, ny, nz, h, lam, mu, x, q, nthreads);
+  int rc = apply(ctx, x, q);
   if (rc) goto done;
   for (int64_t i = 0; i < n; ++i) {
     r[i] = b[i] - q[i];
@@ -436,7 +434,7 @@ int orc_cg(int kind, int bc, int64_t nx, int64_t ny, int64_t nz, double h, const
       info->converged = 1;
       break;
     }
-    rc = orc_apply(kind, bc, nx, ny, nz, h, lam, mu, p, q, nthreads);
+    rc = apply(ctx, p, q);
     if (rc) goto done;
     double pq = orc_dot(n, p, q);
     if (!(pq > 0.0) || !isfinite(pq)) {
@@ -460,7 +458,7 @@ int orc_cg(int kind, int bc, int64_t nx, int64_t ny, int64_t nz, double h, const
   info->iterations = it;
   info->r_norm = sqrt(rr);
   /* true residual ||b - A x|| */
-  if (orc_apply(kind, bc, nx, ny, nz, h, lam, mu, x, q, nthreads) == ORC_OK) {
+  if (apply(ctx, x, q) == ORC_OK) {
     for (int64_t i = 0; i < n; ++i) q[i] = b[i] - q[i];
     info->true_r_norm = sqrt(orc_dot(n, q, q));
   }
@@ -469,6 +467,127 @@ done:
   free(p);
   free(q);
   return rc;
+}
+
+typedef struct {
+  int kind, bc;
+  int64_t nx, ny, nz;
+  double h;
+  const double *lam, *mu;
+  int nthreads;
+} box_ctx;
+
+static int box_apply(const void* c, const double* x, double* y) {
+  const box_ctx* b = (const box_ctx*)c;
+  return orc_apply(b->kind, b->bc, b->nx, b->ny, b->nz, b->h, b->lam, b->mu, x, y, b->nthreads);
+}
+
+/* CG on the box mesh (orc_apply). */
+int orc_cg(int kind, int bc, int64_t nx, int64_t ny, int64_t nz, double h, const double* lam,
+           const double* mu, const double* b, double* x, double tol, int maxit, orc_cg_info* info,
+           double* res_hist, int nthreads) {
+  const int c = (kind == ORC_SCALAR) ? 1 : 3;
+  const int64_t n = (nx + 1) * (ny + 1) * (nz + 1) * c;
+  box_ctx ctx = {kind, bc, nx, ny, nz, h, lam, mu, nthreads};
+  return cg_core(box_apply, &ctx, n, b, x, tol, maxit, info, res_hist);
+}
+
+/* ---------------------------------------------------------------------------------------
+ * General hexahedral mesh: Algorithm 1 as written, i.e. an explicit node map
+ * ("node map", Table 2) and nodal coordinates ("read nodal position", Table 2), the
+ * Jacobian recomputed at every quadrature point from the gathered coordinates.
+ *   coords[3 n + d]   node n, coordinate d
+ *   cells[8 e + a]    global node of local node a of cell e, VTK order (reading R2)
+ *   dirichlet[n]      != 0: node n constrained (all components); NULL: no constraint
+ *   lam, mu           per cell e (elasticity)
+ * y = P A P x + (I - P) x with P zeroing the constrained DOFs.  Cells are visited
+ * in index order; element products are formed in parallel, the scatter is sequential
+ * in cell order (deterministic).
+ * ------------------------------------------------------------------------------------- */
+int orc_apply_hex(int kind, int64_t n_nodes, int64_t n_cells, const double* coords,
+                  const int32_t* cells, const uint8_t* dirichlet, const double* lam,
+                  const double* mu, const double* x, double* y, int nthreads) {
+  if (n_nodes < 1 || n_cells < 1 || kind < 0 || kind > 2 || !coords || !cells) return ORC_EINVAL;
+  if (kind == ORC_ELASTIC && (!lam || !mu)) return ORC_EINVAL;
+  for (int64_t e = 0; e < 8 * n_cells; ++e)
+    if (cells[e] < 0 || cells[e] >= n_nodes) return ORC_EINVAL;
+  const int c = (kind == ORC_SCALAR) ? 1 : 3;
+  const int n = 8 * c;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+  memset(y, 0, sizeof(double) * n_nodes * c);
+  const int64_t CH = 4096; /* cells per chunk: products in parallel, scatter in order */
+  double* ve = (double*)malloc(sizeof(double) * CH * n);
+  if (!ve) return ORC_ENOMEM;
+  int err = ORC_OK;
+  for (int64_t e0 = 0; e0 < n_cells && !err; e0 += CH) {
+    const int64_t e1 = (e0 + CH < n_cells) ? e0 + CH : n_cells;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = e0; e < e1; ++e) {
+      /* step 1: gather x^e and u^e (Alg. 1 line 1) */
+      double X[8][3], ue[24], Ae[24 * 24];
+      for (int a = 0; a < 8; ++a) {
+        const int64_t id = cells[8 * e + a];
+        for (int d = 0; d < 3; ++d) X[a][d] = coords[3 * id + d];
+        const int masked = dirichlet && dirichlet[id];
+        for (int comp = 0; comp < c; ++comp) ue[c * a + comp] = masked ? 0.0 : x[c * id + comp];
+      }
+      /* step 2: v^e = A^e u^e with A^e by quadrature at the gathered geometry */
+      if (orc_element_matrix(kind, X, kind == ORC_ELASTIC ? lam[e] : 0.0,
+                             kind == ORC_ELASTIC ? mu[e] : 0.0, Ae) != ORC_OK) {
+#pragma omp atomic write
+        err = ORC_EGEOM;
+        continue;
+      }
+      for (int r = 0; r < n; ++r) {
+        double s = 0.0;
+        for (int q = 0; q < n; ++q) s += Ae[r * n + q] * ue[q];
+        ve[(e - e0) * n + r] = s;
+      }
+    }
+    /* step 3: assemble into v, in cell order */
+    for (int64_t e = e0; e < e1 && !err; ++e)
+      for (int a = 0; a < 8; ++a) {
+        const int64_t id = cells[8 * e + a];
+        for (int comp = 0; comp < c; ++comp) y[c * id + comp] += ve[(e - e0) * n + c * a + comp];
+      }
+  }
+  free(ve);
+  if (err) return err;
+  if (dirichlet)
+    for (int64_t nn = 0; nn < n_nodes; ++nn)
+      if (dirichlet[nn])
+        for (int comp = 0; comp < c; ++comp) y[c * nn + comp] = x[c * nn + comp];
+  return ORC_OK;
+}
+
+typedef struct {
+  int kind;
+  int64_t n_nodes, n_cells;
+  const double* coords;
+  const int32_t* cells;
+  const uint8_t* dirichlet;
+  const double *lam, *mu;
+  int nthreads;
+} hex_ctx;
+
+static int hex_apply(const void* c, const double* x, double* y) {
+  const hex_ctx* m = (const hex_ctx*)c;
+  return orc_apply_hex(m->kind, m->n_nodes, m->n_cells, m->coords, m->cells, m->dirichlet, m->lam,
+                       m->mu, x, y, m->nthreads);
+}
+
+/* CG on a general hexahedral mesh (orc_apply_hex), same recurrences. */
+int orc_cg_hex(int kind, int64_t n_nodes, int64_t n_cells, const double* coords,
+               const int32_t* cells, const uint8_t* dirichlet, const double* lam, const double* mu,
+               const double* b, double* x, double tol, int maxit, orc_cg_info* info,
+               double* res_hist, int nthreads) {
+  const int c = (kind == ORC_SCALAR) ? 1 : 3;
+  hex_ctx ctx = {kind, n_nodes, n_cells, coords, cells, dirichlet, lam, mu, nthreads};
+  return cg_core(hex_apply, &ctx, n_nodes * c, b, x, tol, maxit, info, res_hist);
 }
 
 int orc_max_threads(void) {

@@ -66,6 +66,12 @@ def lib():
         L.orc_apply_nodes.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, i64, ctypes.c_double,
                                       d, d, d, ctypes.POINTER(ctypes.c_int64), i64, d, ctypes.c_int]
         L.orc_apply_nodes.restype = ctypes.c_int
+        u8p = ctypes.POINTER(ctypes.c_uint8); i32p = ctypes.POINTER(ctypes.c_int32)
+        L.orc_apply_hex.argtypes = [ctypes.c_int, i64, i64, d, i32p, u8p, d, d, d, d, ctypes.c_int]
+        L.orc_apply_hex.restype = ctypes.c_int
+        L.orc_cg_hex.argtypes = [ctypes.c_int, i64, i64, d, i32p, u8p, d, d, d, d, ctypes.c_double,
+                                 ctypes.c_int, ctypes.POINTER(CgInfoC), d, ctypes.c_int]
+        L.orc_cg_hex.restype = ctypes.c_int
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = ctypes.c_int
         _lib = L
@@ -198,6 +204,57 @@ def cg(kind, bc, nx, ny, nz, h, b, x0=None, tol=0.0, maxit=50, lam=None, mu=None
                       float(tol), int(maxit), ctypes.byref(info), _p(hist), int(nthreads))
     if rc not in (0, 3):
         raise ValueError(f"orc_cg failed: {rc}")
+    return CgResult(x=x, iterations=info.iterations, converged=bool(info.converged),
+                    breakdown_iter=info.breakdown_iter, status=info.status, r0_norm=info.r0_norm,
+                    r_norm=info.r_norm, true_r_norm=info.true_r_norm,
+                    res_hist=hist[: info.iterations + 1])
+
+
+def _hex_args(kind, coords, cells, dirichlet, lam, mu):
+    k = _kind(kind)
+    coords = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 3)
+    cells = np.ascontiguousarray(cells, dtype=np.int32).reshape(-1, 8)
+    dp = None
+    if dirichlet is not None:
+        dirichlet = np.ascontiguousarray(dirichlet, dtype=np.uint8).reshape(-1)
+        dp = dirichlet.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+    if k == ELASTIC:
+        ne = cells.shape[0]
+        lam = np.ascontiguousarray(np.broadcast_to(np.asarray(lam, dtype=np.float64), (ne,)))
+        mu = np.ascontiguousarray(np.broadcast_to(np.asarray(mu, dtype=np.float64), (ne,)))
+    else:
+        lam = mu = None
+    keep = (coords, cells, dirichlet, lam, mu)
+    return k, keep, dp
+
+
+def apply_hex(kind, coords, cells, x, dirichlet=None, lam=None, mu=None, nthreads=0):
+    """y = A_c x on a general hexahedral mesh (Alg. 1 as written): coords (n, 3), cells (ne, 8)
+    int32 in VTK corner order, dirichlet (n,) flags or None."""
+    k, (co, ce, di, la, m), dp = _hex_args(kind, coords, cells, dirichlet, lam, mu)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    rc = lib().orc_apply_hex(k, co.shape[0], ce.shape[0], _p(co),
+                             ce.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), dp, _p(la), _p(m),
+                             _p(x), _p(y), int(nthreads))
+    if rc:
+        raise ValueError(f"orc_apply_hex failed: {rc}")
+    return y
+
+
+def cg_hex(kind, coords, cells, b, dirichlet=None, x0=None, tol=0.0, maxit=50, lam=None, mu=None,
+           nthreads=0):
+    k, (co, ce, di, la, m), dp = _hex_args(kind, coords, cells, dirichlet, lam, mu)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    info = CgInfoC()
+    hist = np.full(maxit + 1, np.nan)
+    rc = lib().orc_cg_hex(k, co.shape[0], ce.shape[0], _p(co),
+                          ce.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), dp, _p(la), _p(m),
+                          _p(b), _p(x), float(tol), int(maxit), ctypes.byref(info), _p(hist),
+                          int(nthreads))
+    if rc not in (0, 3):
+        raise ValueError(f"orc_cg_hex failed: {rc}")
     return CgResult(x=x, iterations=info.iterations, converged=bool(info.converged),
                     breakdown_iter=info.breakdown_iter, status=info.status, r0_norm=info.r0_norm,
                     r_norm=info.r_norm, true_r_norm=info.true_r_norm,

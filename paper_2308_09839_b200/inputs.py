@@ -88,3 +88,44 @@ def lognormal_materials(g: np.random.Generator, nx, ny, nz, lo=-1.0, hi=1.0):
     """Independent lambda, mu = 10**U(lo, hi) (parity-test variant)."""
     ne = nx * ny * nz
     return 10.0 ** g.uniform(lo, hi, size=ne), 10.0 ** g.uniform(lo, hi, size=ne)
+
+
+# ------------------------------------------------------------------------------------------
+# General hexahedral meshes (Alg. 1 as written: explicit node map + nodal coordinates)
+# ------------------------------------------------------------------------------------------
+VTK_CORNERS = ((0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1))
+
+
+def hex_box_mesh(nx, ny, nz, h=None, g=None, jitter=0.0, permute=False):
+    """Box of nx*ny*nz hexahedra as an explicit (unstructured) mesh.
+
+    Returns coords (n, 3) float64, cells (ne, 8) int32 in VTK corner order and
+    dirichlet (n,) uint8 marking the nodes on the 6 box faces.
+      jitter  : interior nodes moved by U(-jitter, jitter) * h per coordinate (non-affine
+                cells; |jitter| < 0.25 keeps every det J > 0), boundary nodes stay on the box;
+      permute : random node labels and random cell order (a genuinely unstructured numbering).
+    Index bookkeeping and random numbers only (no arithmetic of the method).
+    """
+    h = 1.0 / nx if h is None else h
+    k, j, i = np.meshgrid(np.arange(nz + 1), np.arange(ny + 1), np.arange(nx + 1), indexing="ij")
+    coords = np.stack([i.ravel() * h, j.ravel() * h, k.ravel() * h], 1).astype(np.float64)
+    bnd = boundary_mask(nx, ny, nz)
+    if jitter:
+        g = rng(SEED_BASE + 900) if g is None else g
+        d = g.uniform(-jitter, jitter, size=coords.shape) * h
+        d[bnd] = 0.0
+        coords = coords + d
+    ck, cj, ci = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    ci, cj, ck = ci.ravel(), cj.ravel(), ck.ravel()
+    cells = np.stack([(ci + a) + (nx + 1) * ((cj + b) + (ny + 1) * (ck + c)) for a, b, c in VTK_CORNERS],
+                     1).astype(np.int64)
+    dirichlet = bnd.astype(np.uint8)
+    if permute:
+        g = rng(SEED_BASE + 901) if g is None else g
+        perm = g.permutation(coords.shape[0])  # new label of old node n: perm[n]
+        inv = np.empty_like(perm); inv[perm] = np.arange(perm.size)
+        coords = coords[inv]
+        dirichlet = dirichlet[inv]
+        cells = perm[cells]
+        cells = cells[g.permutation(cells.shape[0])]
+    return coords, cells.astype(np.int32), dirichlet
