@@ -105,6 +105,28 @@ int fem_mesh_local(fem_mesh_t mesh, int64_t* plane_begin, int64_t* plane_end,
                    int64_t* n_local_nodes);
 void fem_mesh_destroy(fem_mesh_t mesh);
 
+/* ---- general (deformed) hexahedral mesh: Algorithm 1 as written ------------- */
+/* An explicit mesh of trilinear hexahedra, the input of Alg. 1 ("global support point
+ * coordinates", node map; Table 2):
+ *   coords[3 n + d]  FP64 coordinate d of node n (device or host, 8-byte aligned);
+ *   cells[8 e + a]   int32 global node of local node a of cell e, VTK corner order:
+ *                    (0,0,0) (1,0,0) (1,1,0) (0,1,0) (0,0,1) (1,0,1) (1,1,1) (0,1,1);
+ *   dirichlet[n]     uint8, != 0 marks a constrained node (all components; device or host), or
+ *                    NULL.  Operators created with FEM_BC_DIRICHLET_BOX on this mesh apply
+ *                    y = P A P x + (I - P) x for these nodes.
+ * The arrays are copied (the caller may free them).  The Jacobian, its determinant and inverse
+ * are recomputed at each 2x2x2 Gauss point of every apply (Alg. 1 lines 4-5).  Errors:
+ * FEM_EINVAL for n_nodes / n_cells < 1, a node index outside [0, n_nodes), or det J <= 0 at any
+ * Gauss point; FEM_EOVERFLOW for n_nodes >= 2^31.  Single GPU.  Vectors on this
+ * mesh are dense, DOF = c n + comp over all n_nodes nodes; fem_set_material takes n_cells values
+ * with layer_begin = 0, n_layers = 1; fem_apply, fem_dot and fem_cg_* work as on the box (CG
+ * unfused: apply + update + p-update); fem_apply_ghost and fem_csr_create return
+ * FEM_EUNSUPPORTED.  The scatter adds element contributions with FP64 atomics, so results are
+ * exact up to the (run-dependent) summation order of the <= 8 contributions per node. */
+int fem_mesh_create_hex(int64_t n_nodes, int64_t n_cells, const double* coords, const int32_t* cells,
+                        const uint8_t* dirichlet, fem_mesh_t* out);
+int fem_mesh_info_hex(fem_mesh_t mesh, int64_t* n_nodes, int64_t* n_cells, int64_t* n_constrained);
+
 /* ---- operator -------------------------------------------------------------------------- */
 int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out);
 int fem_op_ndof(fem_op_t op, int64_t* n_local_dof, int64_t* n_global_dof);

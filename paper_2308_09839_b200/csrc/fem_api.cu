@@ -76,6 +76,13 @@ struct fem_mesh_s {
   Grid g{};  // global sizes, owned planes [k0, k1)
   fem_comm_s* comm = nullptr;
   int nranks = 1, rank = 0, device = 0, sm_count = 148;
+  // general hexahedral mesh (fem_mesh_create_hex; Alg. 1 as written): explicit node map and
+  // coordinates, single GPU.  hx_cells: 2 int4 per cell (corner-bit order, bit 31 = Dirichlet)
+  bool hex = false;
+  int64_t hx_nodes = 0, hx_ncells = 0, hx_nb = 0;
+  double4* hx_xyz = nullptr;
+  int4* hx_cells = nullptr;
+  int32_t* hx_bnodes = nullptr;  // constrained nodes (identity rows)
 };
 
 struct fem_op_s {
@@ -92,6 +99,7 @@ struct fem_op_s {
   // CG vectors in the library padded layout: node (i,j) comp c of local plane kk
   // (kk = 0 is the ghost plane k0-1) at v[pl_lead + kk*pl_pp + j*pl_rp + i*C + c]
   int64_t pl_lead = 0, pl_rp = 0, pl_pp = 0, pl_n = 0;
+  int64_t pl_off = 0;  // offset of the owned range (pl_lead + pl_pp; 0 on general hex meshes)
   double *x_pl = nullptr, *r_pl = nullptr, *p_pl = nullptr, *q_pl = nullptr, *p2_pl = nullptr;
   CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{};
   int cg_parity = 0;  // fused CG: iteration parity (p_pl / p2_pl ping-pong)
@@ -343,7 +351,7 @@ static OutVec dense_out(fem_op_s* op, double* y) {
   const Grid& g = op->mesh->g;
   return OutVec{y, (g.nx + 1) * op->comps, g.plane * op->comps};
 }
-static double* pl_owned(fem_op_s* op, double* v) { return v + op->pl_lead + op->pl_pp; }
+static double* pl_owned(fem_op_s* op, double* v) { return v + op->pl_off; }
 static PlaneSrc pl_src(fem_op_s* op, double* v) {
   fem_mesh_s* m = op->mesh;
   return PlaneSrc{pl_owned(op, v), m->rank > 0 ? v + op->pl_lead : nullptr,
@@ -353,8 +361,23 @@ static PlaneSrc pl_src(fem_op_s* op, double* v) {
 static OutVec pl_out(fem_op_s* op, double* v) { return OutVec{pl_owned(op, v), op->pl_rp, op->pl_pp}; }
 static int64_t pl_count(fem_op_s* op) { return op->nloc_planes * op->pl_pp; }  // owned range
 
+// general hex mesh: y = A_c x (zero y, element kernel with red.add scatter, identity rows)
+static int apply_hex(fem_op_s* op, const double* x, double* y, int mode, cudaStream_t s) {
+  fem_mesh_s* m = op->mesh;
+  CUDA_TRY(cudaMemsetAsync(y, 0, op->n_local * sizeof(double), s));
+  cudaError_t e = launch_hex_apply(op->kind, op->bc, m->hx_cells, m->hx_xyz, op->lm, x, y, m->hx_ncells, mode, op->sc,
+                                   op->red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "hex apply launch: %s", cudaGetErrorString(e));
+  if (op->bc && m->hx_nb) {
+    e = launch_hex_dirichlet(m->hx_bnodes, m->hx_nb, op->comps, x, y, mode, op->sc, op->red, s, m->sm_count);
+    if (e != cudaSuccess) return fail(FEM_ECUDA, "hex identity-row launch: %s", cudaGetErrorString(e));
+  }
+  return FEM_OK;
+}
+
 // y = A_c x for a DEVICE dense owned vector x (halo via op ghost buffers)
 static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s) {
+  if (op->mesh->hex) return apply_hex(op, x, y, 0, s);
   FEM_TRY(halo(op, x, op->ghost_lo, op->ghost_hi, s));
   PlaneSrc src = dense_src(op, x, op->mesh->rank > 0 ? op->ghost_lo : nullptr,
                            op->mesh->rank < op->mesh->nranks - 1 ? op->ghost_hi : nullptr);
@@ -364,6 +387,7 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
 // q_pl = A_c v for a padded CG vector v (x_pl or p_pl): halo into its ghost planes, TMA path
 static int apply_pl(fem_op_s* op, double* v, const CUtensorMap* map, int mode, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
+  if (m->hex) return apply_hex(op, pl_owned(op, v), pl_owned(op, op->q_pl), mode, s);
   if (m->nranks > 1) {
     double* own = pl_owned(op, v);
     FEM_TRY(halo_pitch(op, own, v + op->pl_lead, v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp,
@@ -373,6 +397,14 @@ static int apply_pl(fem_op_s* op, double* v, const CUtensorMap* map, int mode, c
 }
 
 static int pack(fem_op_s* op, const double* dense, double* v, int to_padded, cudaStream_t s) {
+  if (op->mesh->hex) {  // CG vectors are dense on general meshes
+    if (to_padded)
+      CUDA_TRY(cudaMemcpyAsync(pl_owned(op, v), dense, op->n_local * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    else
+      CUDA_TRY(cudaMemcpyAsync(const_cast<double*>(dense), pl_owned(op, v), op->n_local * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));
+    return FEM_OK;
+  }
   const Grid& g = op->mesh->g;
   cudaError_t e = launch_pack(dense, pl_owned(op, v), op->pl_rp, op->pl_pp, op->nloc_planes, g.nx + 1,
                               g.ny + 1, op->comps, to_padded, s, op->mesh->sm_count);
@@ -484,13 +516,107 @@ int fem_mesh_create(int64_t nx, int64_t ny, int64_t nz, double h, fem_comm_t com
 
 int fem_mesh_local(fem_mesh_t m, int64_t* pb, int64_t* pe, int64_t* nloc) {
   if (!m) return fail(FEM_EINVAL, "mesh is NULL");
+  if (m->hex) {  // one "plane": all nodes
+    if (pb) *pb = 0;
+    if (pe) *pe = 1;
+    if (nloc) *nloc = m->hx_nodes;
+    return FEM_OK;
+  }
   if (pb) *pb = m->g.k0;
   if (pe) *pe = m->g.k1;
   if (nloc) *nloc = (m->g.k1 - m->g.k0) * m->g.plane;
   return FEM_OK;
 }
 
-void fem_mesh_destroy(fem_mesh_t m) { delete m; }
+int fem_mesh_create_hex(int64_t n_nodes, int64_t n_cells, const double* coords, const int32_t* cells,
+                        const uint8_t* dirichlet, fem_mesh_t* out) {
+  if (!out) return fail(FEM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_nodes < 1 || n_cells < 1) return fail(FEM_EINVAL, "n_nodes and n_cells must be >= 1");
+  if (n_nodes > 2147483647LL) return fail(FEM_EOVERFLOW, "node count %lld exceeds 2^31 - 1", (long long)n_nodes);
+  if (!coords || !cells) return fail(FEM_EINVAL, "coords / cells is NULL");
+  if ((reinterpret_cast<uintptr_t>(coords) & 7) || (reinterpret_cast<uintptr_t>(cells) & 3))
+    return fail(FEM_EINVAL, "coords must be 8-byte and cells 4-byte aligned");
+  auto* m = new (std::nothrow) fem_mesh_s();
+  if (!m) return fail(FEM_ENOMEM, "host allocation failed");
+  cudaGetDevice(&m->device);
+  cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, m->device);
+  m->hex = true;
+  m->hx_nodes = n_nodes;
+  m->hx_ncells = n_cells;
+  m->g = Grid{0, 0, 0, 0.0, 0, 1, n_nodes};
+  int32_t* d_vtk = nullptr;
+  uint8_t* d_dir = nullptr;
+  unsigned long long* d_bad = nullptr;
+  auto cleanup = [&]() { cudaFree(d_vtk); cudaFree(d_dir); cudaFree(d_bad); };
+  auto bail = [&](int st) { cleanup(); fem_mesh_destroy(m); return st; };
+  // coordinates -> double4 records (cudaMemcpy2D: 24-B source rows, 32-B destination rows)
+  if (dalloc(&m->hx_xyz, n_nodes) != FEM_OK) return bail(FEM_ENOMEM);
+  const cudaMemcpyKind kc = is_device_ptr(coords) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (cudaMemset(m->hx_xyz, 0, n_nodes * sizeof(double4)) != cudaSuccess ||
+      cudaMemcpy2D(m->hx_xyz, sizeof(double4), coords, 3 * sizeof(double), 3 * sizeof(double), n_nodes, kc) !=
+          cudaSuccess)
+    return bail(fail(FEM_ECUDA, "coordinate copy failed"));
+  // node map (+ Dirichlet flags) -> internal cell records, validated on the device
+  if (dalloc(&d_vtk, n_cells * 8) != FEM_OK || dalloc(&d_bad, 2) != FEM_OK ||
+      dalloc(&m->hx_cells, n_cells * 2) != FEM_OK)
+    return bail(FEM_ENOMEM);
+  if (cudaMemcpy(d_vtk, cells, n_cells * 8 * sizeof(int32_t),
+                 is_device_ptr(cells) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(d_bad, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(FEM_ECUDA, "node map copy failed"));
+  std::vector<uint8_t> hdir;
+  if (dirichlet) {
+    if (dalloc(&d_dir, n_nodes) != FEM_OK) return bail(FEM_ENOMEM);
+    hdir.resize(n_nodes);
+    const cudaMemcpyKind kd = is_device_ptr(dirichlet) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
+    if (cudaMemcpy(hdir.data(), dirichlet, n_nodes, kd) != cudaSuccess ||
+        cudaMemcpy(d_dir, hdir.data(), n_nodes, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(FEM_ECUDA, "Dirichlet flag copy failed"));
+  }
+  if (launch_hex_pack_cells(d_vtk, d_dir, n_cells, n_nodes, reinterpret_cast<int*>(m->hx_cells), d_bad, 0,
+                            m->sm_count) != cudaSuccess ||
+      launch_hex_check(m->hx_cells, m->hx_xyz, n_cells, n_nodes, d_bad, 0, m->sm_count) != cudaSuccess)
+    return bail(fail(FEM_ECUDA, "mesh validation launch failed"));
+  unsigned long long bad[2] = {0, 0};
+  if (cudaMemcpy(bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return bail(fail(FEM_ECUDA, "mesh validation failed: %s", cudaGetErrorString(cudaGetLastError())));
+  if (bad[0]) return bail(fail(FEM_EINVAL, "%llu node-map entries outside [0, n_nodes)", bad[0]));
+  if (bad[1]) return bail(fail(FEM_EINVAL, "%llu cells have det J <= 0 at a Gauss point (S:265, S:333)", bad[1]));
+  // constrained node list (identity rows)
+  std::vector<int32_t> bn;
+  for (int64_t n = 0; n < (int64_t)hdir.size(); ++n)
+    if (hdir[n]) bn.push_back((int32_t)n);
+  m->hx_nb = (int64_t)bn.size();
+  if (m->hx_nb) {
+    if (dalloc(&m->hx_bnodes, m->hx_nb) != FEM_OK) return bail(FEM_ENOMEM);
+    if (cudaMemcpy(m->hx_bnodes, bn.data(), bn.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(FEM_ECUDA, "constrained-node copy failed"));
+  }
+  cleanup();
+  *out = m;
+  return FEM_OK;
+}
+
+int fem_mesh_info_hex(fem_mesh_t m, int64_t* n_nodes, int64_t* n_cells, int64_t* n_constrained) {
+  if (!m) return fail(FEM_EINVAL, "mesh is NULL");
+  if (!m->hex) return fail(FEM_EINVAL, "not a general hexahedral mesh");
+  if (n_nodes) *n_nodes = m->hx_nodes;
+  if (n_cells) *n_cells = m->hx_ncells;
+  if (n_constrained) *n_constrained = m->hx_nb;
+  return FEM_OK;
+}
+
+void fem_mesh_destroy(fem_mesh_t m) {
+  if (!m) return;
+  if (m->hex) {
+    set_device(m->device);
+    cudaFree(m->hx_xyz);
+    cudaFree(m->hx_cells);
+    cudaFree(m->hx_bnodes);
+  }
+  delete m;
+}
 
 static void op_free(fem_op_s* op) {
   if (!op) return;
@@ -509,6 +635,48 @@ static void op_free(fem_op_s* op) {
   delete op;
 }
 
+static int op_common_alloc(fem_op_s* op) {
+  FEM_TRY(dalloc(&op->sc, 1));
+  FEM_TRY(dalloc(&op->dot_dev, 1));
+  FEM_TRY(dalloc(&op->bad, 1));
+  FEM_TRY(dalloc(&op->red.partials, kMaxCtas));
+  FEM_TRY(dalloc(&op->red.ticket, 1));
+  op->red.capacity = kMaxCtas;
+  if (cudaMallocHost(&op->sc_host, sizeof(CgScalars)) != cudaSuccess ||
+      cudaMallocHost(&op->dot_host, sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FEM_ENOMEM, "pinned host allocation failed");
+  }
+  if (cudaMemset(op->red.ticket, 0, sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemset(op->sc, 0, sizeof(CgScalars)) != cudaSuccess)
+    return fail(FEM_ECUDA, "cudaMemset failed");
+  return FEM_OK;
+}
+
+// operator on a general hexahedral mesh: dense CG vectors (no padded layout, no tensor maps);
+// CG runs the unfused iteration (apply + update + p-update)
+static int op_create_hex(fem_op_s* op, fem_op_t* out) {
+  const fem_mesh_s* m = op->mesh;
+  op->plane_dofs = m->hx_nodes * op->comps;
+  op->nloc_planes = 1;
+  op->n_local = op->n_global = op->plane_dofs;
+  op->pl_lead = 0;
+  op->pl_rp = op->pl_pp = op->n_local;
+  op->pl_off = 0;
+  op->pl_n = op->n_local;
+  op->tm_ok = false;
+  int st = FEM_OK;
+  for (double** v : {&op->x_pl, &op->r_pl, &op->p_pl, &op->q_pl})
+    if (st == FEM_OK) st = dalloc(v, op->pl_n);
+  if (st == FEM_OK) st = op_common_alloc(op);
+  if (st != FEM_OK) {
+    op_free(op);
+    return st;
+  }
+  *out = op;
+  return FEM_OK;
+}
+
 int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   if (!out) return fail(FEM_EINVAL, "out is NULL");
   *out = nullptr;
@@ -522,6 +690,7 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   op->kind = kind;
   op->bc = bc;
   op->comps = kind == FEM_SCALAR_LAPLACE ? 1 : 3;
+  if (mesh->hex) return op_create_hex(op, out);
   const Grid& g = mesh->g;
   op->plane_dofs = g.plane * op->comps;
   op->nloc_planes = g.k1 - g.k0;
@@ -533,6 +702,7 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   op->tm_interior = bc && kind != FEM_ELASTICITY;
   op->pl_lead = op->tm_interior ? (op->comps & 1) : 0;  // tensor-origin node 16-B aligned
   op->pl_n = (op->pl_lead + (op->nloc_planes + 2) * op->pl_pp + 1) & ~1LL;
+  op->pl_off = op->pl_lead + op->pl_pp;
   int st = FEM_OK;
 #define OP_TRY(x)                 \
   do {                            \
@@ -585,6 +755,29 @@ int fem_op_ndof(fem_op_t op, int64_t* nl, int64_t* ng) {
   return FEM_OK;
 }
 
+static int set_material_hex(fem_op_s* op, const double* lam, const double* mu, int64_t layer_begin,
+                            int64_t n_layers) {
+  if (layer_begin != 0 || n_layers != 1)
+    return fail(FEM_EINVAL, "general hex mesh: pass layer_begin 0, n_layers 1 (arrays of n_cells values)");
+  const int64_t cnt = op->mesh->hx_ncells;
+  if (!op->lm) FEM_TRY(dalloc(&op->lm, cnt));
+  const cudaMemcpyKind kl = is_device_ptr(lam) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const cudaMemcpyKind km = is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CUDA_TRY(cudaMemcpy2D(op->lm, 16, lam, 8, 8, cnt, kl));
+  CUDA_TRY(cudaMemcpy2D(reinterpret_cast<double*>(op->lm) + 1, 16, mu, 8, 8, cnt, km));
+  CUDA_TRY(cudaMemset(op->bad, 0, sizeof(unsigned long long)));
+  CUDA_TRY(launch_check_material(op->lm, cnt, op->bad, 0, op->mesh->sm_count));
+  unsigned long long bad = 0;
+  CUDA_TRY(cudaMemcpy(&bad, op->bad, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad) {
+    op->has_mat = false;
+    return fail(FEM_EMATERIAL, "%llu cells violate mu > 0, lambda + 2 mu / 3 >= 0 (S:249)", bad);
+  }
+  op->has_mat = true;
+  op->cg_active = false;
+  return FEM_OK;
+}
+
 int fem_set_material(fem_op_t op, const double* lam, const double* mu, int64_t layer_begin,
                      int64_t n_layers) {
   if (!op) return fail(FEM_EINVAL, "op is NULL");
@@ -592,6 +785,7 @@ int fem_set_material(fem_op_t op, const double* lam, const double* mu, int64_t l
   FEM_TRY(check_vec(lam, "lambda"));
   FEM_TRY(check_vec(mu, "mu"));
   FEM_TRY(set_device(op->mesh->device));
+  if (op->mesh->hex) return set_material_hex(op, lam, mu, layer_begin, n_layers);
   const Grid& g = op->mesh->g;
   const int64_t need0 = std::max<int64_t>(g.k0 - 1, 0);
   const int64_t need1 = std::min<int64_t>(g.k1 - 1, g.nz - 1);  // inclusive
@@ -634,6 +828,7 @@ int fem_apply_ghost(fem_op_t op, const double* x, const double* glo, const doubl
   FEM_TRY(check_vec(y, "y"));
   if ((const void*)x == (const void*)y) return fail(FEM_EINVAL, "x and y alias");
   if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
+  if (op->mesh->hex) return fail(FEM_EUNSUPPORTED, "fem_apply_ghost: general hex meshes are single-GPU");
   const Grid& g = op->mesh->g;
   if ((g.k0 > 0 && !glo) || (g.k1 <= g.nz && !ghi))
     return fail(FEM_EINVAL, "a ghost plane inside the box is NULL");
@@ -815,7 +1010,8 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
 }
 
 static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
-  const int per_iter_launches = op->tm_ok ? 2 : 3;
+  const int per_iter_launches =
+      op->tm_ok ? 2 : (op->mesh->hex ? 3 + ((op->bc && op->mesh->hx_nb) ? 1 : 0) : 3);
   if (op->time_apply || !op->use_graph) {
     for (int t = 0; t < iters; ++t) {
       FEM_TRY(iteration(op, op->cg_parity, s, op->time_apply != 0));
@@ -986,6 +1182,7 @@ int fem_csr_create(fem_op_t op, fem_csr_t* out) {
   if (!op || !out) return fail(FEM_EINVAL, "op/out is NULL");
   *out = nullptr;
   if (op->mesh->nranks != 1) return fail(FEM_EUNSUPPORTED, "CSR baseline is single-rank only");
+  if (op->mesh->hex) return fail(FEM_EUNSUPPORTED, "CSR baseline is built for the box mesh only");
   if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
   FEM_TRY(set_device(op->mesh->device));
   const Grid& g = op->mesh->g;

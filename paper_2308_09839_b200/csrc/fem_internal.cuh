@@ -108,6 +108,22 @@ cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* 
 // fused CG: x += alpha p; r -= alpha q; rr_new = r.r; iteration bookkeeping (p update is in the apply)
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
                                    CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
+// general hexahedral meshes (kernels_hex.cu): cells = 2 int4 per cell (node ids in corner-bit
+// order, bit 31 = Dirichlet node), xyz = node coordinates (w unused), lm = (lambda, mu) per cell.
+// mode 0: y += A (P x) at unconstrained nodes (y zeroed by the caller); mode 1: + sc->pq = the
+// sum of the element energies (P x)^T A (P x).
+cudaError_t launch_hex_apply(int kind, int bc, const int4* cells, const double4* xyz, const double2* lm,
+                             const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
+                             Reduce red, cudaStream_t s, int sm_count);
+// y = x on the constrained nodes; mode 1: sc->pq += sum x_b^2
+cudaError_t launch_hex_dirichlet(const int32_t* nodes, int64_t nb, int comps, const double* x, double* y,
+                                 int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
+// bad[0] += cells with an out-of-range node, bad[1] += cells with det J <= 0 at a Gauss point
+cudaError_t launch_hex_check(const int4* cells, const double4* xyz, int64_t ncells, int64_t nnodes,
+                             unsigned long long* bad, cudaStream_t s, int sm_count);
+// VTK-ordered int32 node map (+ optional uint8 Dirichlet flags) -> internal cell records
+cudaError_t launch_hex_pack_cells(const int32_t* vtk, const uint8_t* dir, int64_t ncells, int64_t nnodes,
+                                  int* out, unsigned long long* bad, cudaStream_t s, int sm_count);
 // deterministic dot -> *out (device)
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
                        cudaStream_t s, int sm_count);

@@ -1,0 +1,364 @@
+// kernels_hex.cu -- general (deformed) trilinear hexahedral meshes: Algorithm 1 as written
+// (P:311-360): gather the cell's nodal coordinates and u^e through the explicit node map
+// (Table 2 "node map", "read nodal position"), recompute J, det J, J^-1 at each of the 2x2x2
+// Gauss points, form grad u, the stress (scaled by w_q det J), P = sigma J^-T and
+// v_i += P grad^phi_i, and add v^e into v.  FP64.
+//
+// B200 form: one thread per cell, everything in registers.  The reference
+// gradients are applied in the Hadamard ("modal") basis of the trilinear space -- the 8 nodal
+// values of a field become 7 modal coefficients (23 adds), from which the derivative at each
+// Gauss point is 3 adds -- and the test contraction is accumulated in the same basis and
+// transformed back once per cell (22 adds per component).  J^-1 and det J are used through the
+// cofactor matrix: det(J) J^-T = cof(J), so P w det J = sigma cof(J) and one reciprocal per
+// point suffices.  Scatter: red.global.add.f64 into v (the paper's atomics; P:303 -- the
+// result is exact up to the summation order), constrained nodes skipped and then overwritten
+// by the identity rows y = x in a second kernel.
+//
+// Constants (derivation in DESIGN.md §5.5): with unnormalised modal sums c (c_m = sum_a u_a
+// prod_{d in m} s_ad) the reference derivative is d_e u(q) = (1/8)[c_e + g s_d1 c_ed1 +
+// g s_d2 c_ed2 + g^2 s_d1 s_d2 c_xyz] at q = g s_q, g = 1/sqrt(3).  J' = 8 J and G' = 8 grad^ u
+// drop the 1/8 (grad u = G' J'^-1 is invariant), det J = det J' / 512, cof J = cof J' / 64,
+// grad^ phi_a carries 1/8: v_a = (1/512) sum_q sum_e (sigma cof J')_{ce} s_ae prod(1 + ..g).
+#include <algorithm>
+
+#include "fem_internal.cuh"
+
+namespace fem {
+
+namespace {
+
+constexpr double kG = 0.57735026918962576451;   // 1/sqrt(3): Gauss point
+constexpr double kG2 = 1.0 / 3.0;               // g^2
+constexpr double kInv512 = 1.0 / 512.0;
+
+struct Modal {
+  double x, y, z, xy, xz, yz, xyz;  // the constant mode is not needed (no gradient)
+};
+
+// forward transform of 8 corner values in bit order (bit 0: x, bit 1: y, bit 2: z)
+__device__ __forceinline__ Modal hadamard(const double v[8]) {
+  const double s0 = v[0] + v[1], d0 = v[1] - v[0], s1 = v[2] + v[3], d1 = v[3] - v[2];
+  const double s2 = v[4] + v[5], d2 = v[5] - v[4], s3 = v[6] + v[7], d3 = v[7] - v[6];
+  const double ss0 = s0 + s1, y0 = s1 - s0, x0 = d0 + d1, xy0 = d1 - d0;
+  const double ss1 = s2 + s3, y1 = s3 - s2, x1 = d2 + d3, xy1 = d3 - d2;
+  Modal m;
+  m.x = x0 + x1; m.y = y0 + y1; m.xy = xy0 + xy1;
+  m.z = ss1 - ss0; m.xz = x1 - x0; m.yz = y1 - y0; m.xyz = xy1 - xy0;
+  return m;
+}
+
+// pre-scale the bilinear / trilinear coefficients by g, g^2 (Gauss point coordinates)
+__device__ __forceinline__ void prescale(Modal& m) {
+  m.xy *= kG; m.xz *= kG; m.yz *= kG; m.xyz *= kG2;
+}
+
+// reference gradient (x 8) of a field at the Gauss point with signs (sx, sy, sz)
+template <int SX, int SY, int SZ>
+__device__ __forceinline__ void dref(const Modal& m, double& dx, double& dy, double& dz) {
+  dx = m.x + (SY * m.xy + (SZ * m.xz + (SY * SZ) * m.xyz));
+  dy = m.y + (SX * m.xy + (SZ * m.yz + (SX * SZ) * m.xyz));
+  dz = m.z + (SX * m.xz + (SY * m.yz + (SX * SY) * m.xyz));
+}
+
+// transposed accumulation of P_{c,.} at the Gauss point (SX, SY, SZ) into the modal sums
+template <int SX, int SY, int SZ>
+__device__ __forceinline__ void accum(Modal& a, double p0, double p1, double p2) {
+  a.x += p0; a.y += p1; a.z += p2;
+  a.xy += SY * p0 + SX * p1;
+  a.xz += SZ * p0 + SX * p2;
+  a.yz += SZ * p1 + SY * p2;
+  a.xyz += (SY * SZ) * p0 + ((SX * SZ) * p1 + (SX * SY) * p2);
+}
+
+// inverse transform of the modal sums (constant mode 0) to the 8 corners, bit order
+__device__ __forceinline__ void inverse(const Modal& m, double v[8]) {
+  // z: A = x +- xz, B = y +- yz, C = xy +- xyz, D = +- z
+  const double Am = m.x - m.xz, Ap = m.x + m.xz, Bm = m.y - m.yz, Bp = m.y + m.yz;
+  const double Cm = m.xy - m.xyz, Cp = m.xy + m.xyz;
+  // y: E = D +- B, F = A +- C   (z = -1: D = -z; z = +1: D = +z)
+  const double Emm = -m.z - Bm, Emp = -m.z + Bm, Epm = m.z - Bp, Epp = m.z + Bp;
+  const double Fmm = Am - Cm, Fmp = Am + Cm, Fpm = Ap - Cp, Fpp = Ap + Cp;
+  // x: v = E +- F ; index = bx + 2 by + 4 bz
+  v[0] = Emm - Fmm; v[1] = Emm + Fmm;
+  v[2] = Emp - Fmp; v[3] = Emp + Fmp;
+  v[4] = Epm - Fpm; v[5] = Epm + Fpm;
+  v[6] = Epp - Fpp; v[7] = Epp + Fpp;
+}
+
+// one Gauss point: J' from the coordinate modes, cofactors, det; grad u, stress, P; transposed
+// accumulation; energy (u^T A_e u contribution, modes >= 1)
+template <int KIND, int C, int SX, int SY, int SZ>
+__device__ __forceinline__ void gauss_point(const Modal& mx, const Modal& my, const Modal& mz,
+                                            const Modal* mu, Modal* acc, double L, double M,
+                                            double& energy) {
+  double J[3][3];
+  dref<SX, SY, SZ>(mx, J[0][0], J[0][1], J[0][2]);
+  dref<SX, SY, SZ>(my, J[1][0], J[1][1], J[1][2]);
+  dref<SX, SY, SZ>(mz, J[2][0], J[2][1], J[2][2]);
+  double cf[3][3];  // cofactor matrix: det(J) J^-T
+  cf[0][0] = fma(J[1][1], J[2][2], -J[1][2] * J[2][1]);
+  cf[0][1] = fma(J[1][2], J[2][0], -J[1][0] * J[2][2]);
+  cf[0][2] = fma(J[1][0], J[2][1], -J[1][1] * J[2][0]);
+  cf[1][0] = fma(J[0][2], J[2][1], -J[0][1] * J[2][2]);
+  cf[1][1] = fma(J[0][0], J[2][2], -J[0][2] * J[2][0]);
+  cf[1][2] = fma(J[0][1], J[2][0], -J[0][0] * J[2][1]);
+  cf[2][0] = fma(J[0][1], J[1][2], -J[0][2] * J[1][1]);
+  cf[2][1] = fma(J[0][2], J[1][0], -J[0][0] * J[1][2]);
+  cf[2][2] = fma(J[0][0], J[1][1], -J[0][1] * J[1][0]);
+  const double det = fma(J[0][0], cf[0][0], fma(J[0][1], cf[0][1], J[0][2] * cf[0][2]));
+  const double rdet = __drcp_rn(det);
+  // Gt[c][d] = det * d u_c / d x_d = sum_e G'[c][e] cf[d][e]
+  double Gt[C][3];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    double g0, g1, g2;
+    dref<SX, SY, SZ>(mu[c], g0, g1, g2);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) Gt[c][d] = fma(g0, cf[d][0], fma(g1, cf[d][1], g2 * cf[d][2]));
+  }
+  if (KIND == 2) {
+    // sigma~ = det * sigma = lambda tr(Gt) I + mu (Gt + Gt^T)   (reading R4)
+    const double tr = Gt[0][0] + Gt[1][1] + Gt[2][2];
+    const double Lt = L * tr, M2 = M + M;
+    const double s00 = fma(M2, Gt[0][0], Lt), s11 = fma(M2, Gt[1][1], Lt), s22 = fma(M2, Gt[2][2], Lt);
+    const double e01 = Gt[0][1] + Gt[1][0], e02 = Gt[0][2] + Gt[2][0], e12 = Gt[1][2] + Gt[2][1];
+    const double s01 = M * e01, s02 = M * e02, s12 = M * e12;
+    energy = fma(rdet, fma(s00, Gt[0][0], fma(s11, Gt[1][1], fma(s22, Gt[2][2],
+                 fma(s01, e01, fma(s02, e02, s12 * e12))))), energy);
+    const double S[3][3] = {{s00 * rdet, s01 * rdet, s02 * rdet},
+                            {0.0, s11 * rdet, s12 * rdet},
+                            {0.0, 0.0, s22 * rdet}};
+    auto sg = [&](int a, int b) { return a <= b ? S[a][b] : S[b][a]; };
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double p[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) p[e] = fma(sg(c, 0), cf[0][e], fma(sg(c, 1), cf[1][e], sg(c, 2) * cf[2][e]));
+      accum<SX, SY, SZ>(acc[c], p[0], p[1], p[2]);
+    }
+  } else {
+    // Laplace (scalar / per component): flux = grad u; P = grad u cof(J)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      energy = fma(rdet, fma(Gt[c][0], Gt[c][0], fma(Gt[c][1], Gt[c][1], Gt[c][2] * Gt[c][2])), energy);
+      const double f0 = Gt[c][0] * rdet, f1 = Gt[c][1] * rdet, f2 = Gt[c][2] * rdet;
+      double p[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) p[e] = fma(f0, cf[0][e], fma(f1, cf[1][e], f2 * cf[2][e]));
+      accum<SX, SY, SZ>(acc[c], p[0], p[1], p[2]);
+    }
+  }
+}
+
+constexpr int kHexThreads = 128;
+
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(kHexThreads, 2)
+    hex_apply_kernel(const int4* __restrict__ cells, const double4* __restrict__ xyz,
+                     const double2* __restrict__ lm, const double* __restrict__ u,
+                     double* __restrict__ y, int64_t ncells, int bc, CgScalars* sc, Reduce red) {
+  constexpr int C = (KIND == 0) ? 1 : 3;
+  __shared__ double red_sh[32];
+  if (MODE >= 1 && sc->done) return;
+  double energy = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncells; e += stride) {
+    // gather (Alg. 1 line 1): node map -> coordinates and u^e (masked at constrained nodes)
+    const int4 lo = cells[2 * e], hi = cells[2 * e + 1];
+    const int raw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    int id[8];
+    bool fix[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      fix[a] = bc && raw[a] < 0;  // Dirichlet node of an operator with bc (mask P)
+      id[a] = raw[a] & 0x7fffffff;
+    }
+    Modal mx, my, mz;
+    {
+      double X[8], Y[8], Z[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const double4 p = xyz[id[a]];
+        X[a] = p.x; Y[a] = p.y; Z[a] = p.z;
+      }
+      mx = hadamard(X); my = hadamard(Y); mz = hadamard(Z);
+      prescale(mx); prescale(my); prescale(mz);
+    }
+    Modal mu[C], acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      double U[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) U[a] = fix[a] ? 0.0 : u[(int64_t)C * id[a] + c];
+      mu[c] = hadamard(U);
+      prescale(mu[c]);
+      acc[c] = Modal{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    }
+    double L = 0.0, M = 0.0;
+    if (KIND == 2) {
+      const double2 v = lm[e];
+      L = v.x; M = v.y;
+    }
+    double en = 0.0;
+    // the 8 Gauss points (Alg. 1 "for each quadrature point q")
+    gauss_point<KIND, C, -1, -1, -1>(mx, my, mz, mu, acc, L, M, en);
+    gauss_point<KIND, C, +1, -1, -1>(mx, my, mz, mu, acc, L, M, en);
+    gauss_point<KIND, C, -1, +1, -1>(mx, my, mz, mu, acc, L, M, en);
+    gauss_point<KIND, C, +1, +1, -1>(mx, my, mz, mu, acc, L, M, en);
+    gauss_point<KIND, C, -1, -1, +1>(mx, my, mz, mu, acc, L, M, en);
+    gauss_point<KIND, C, +1, -1, +1>(mx, my, mz, mu, acc, L, M, en);
+    gauss_point<KIND, C, -1, +1, +1>(mx, my, mz, mu, acc, L, M, en);
+    gauss_point<KIND, C, +1, +1, +1>(mx, my, mz, mu, acc, L, M, en);
+    energy += en;
+    // back to nodes and scatter-add (Alg. 1 last line)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      Modal& m = acc[c];
+      m.x *= kInv512; m.y *= kInv512; m.z *= kInv512;
+      m.xy *= kG * kInv512; m.xz *= kG * kInv512; m.yz *= kG * kInv512; m.xyz *= kG2 * kInv512;
+      double v[8];
+      inverse(m, v);
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+    }
+  }
+  if (MODE >= 1) {  // p.Ap of the masked operator part: sum of the element energies
+    double total;
+    if (last_block_reduce(block_sum(energy * kInv512, red_sh), red, red_sh, &total)) sc->pq = total;
+  }
+}
+
+// identity rows of the constrained nodes: y = x; mode 1 adds sum x_b^2 to p.Ap
+template <int MODE>
+__global__ void __launch_bounds__(256) hex_dirichlet_kernel(const int32_t* __restrict__ nodes, int64_t nb, int C,
+                                                            const double* __restrict__ x, double* __restrict__ y,
+                                                            CgScalars* sc, Reduce red) {
+  __shared__ double red_sh[32];
+  if (MODE >= 1 && sc->done) return;
+  double acc = 0.0;
+  const int64_t n = nb * C;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += stride) {
+    const int64_t i = (int64_t)nodes[t / C] * C + t % C;
+    const double v = x[i];
+    y[i] = v;
+    acc = fma(v, v, acc);
+  }
+  if (MODE >= 1) {
+    double total;
+    if (last_block_reduce(block_sum(acc, red_sh), red, red_sh, &total)) sc->pq += total;
+  }
+}
+
+// validation: node ids in range, det J > 0 at every Gauss point
+__global__ void __launch_bounds__(256) hex_check_kernel(const int4* __restrict__ cells,
+                                                        const double4* __restrict__ xyz, int64_t ncells,
+                                                        int64_t nnodes, unsigned long long* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncells; e += stride) {
+    const int4 lo = cells[2 * e], hi = cells[2 * e + 1];
+    const int raw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    bool ok = true;
+    double X[8], Y[8], Z[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int id = raw[a] & 0x7fffffff;
+      ok = ok && id < nnodes;
+      const double4 p = xyz[ok ? id : 0];
+      X[a] = p.x; Y[a] = p.y; Z[a] = p.z;
+    }
+    if (!ok) {
+      atomicAdd(&bad[0], 1ull);
+      continue;
+    }
+    Modal mx = hadamard(X), my = hadamard(Y), mz = hadamard(Z);
+    prescale(mx); prescale(my); prescale(mz);
+    bool pos = true;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double sx = (q & 1) ? 1.0 : -1.0, sy = (q & 2) ? 1.0 : -1.0, sz = (q & 4) ? 1.0 : -1.0;
+      double J[3][3];
+      const Modal* f[3] = {&mx, &my, &mz};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const Modal& m = *f[d];
+        J[d][0] = m.x + sy * m.xy + sz * m.xz + sy * sz * m.xyz;
+        J[d][1] = m.y + sx * m.xy + sz * m.yz + sx * sz * m.xyz;
+        J[d][2] = m.z + sx * m.xz + sy * m.yz + sx * sy * m.xyz;
+      }
+      const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                         J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                         J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      pos = pos && det > 0.0 && isfinite(det);
+    }
+    if (!pos) atomicAdd(&bad[1], 1ull);
+  }
+}
+
+// VTK corner order -> bit order (bit 0 x, bit 1 y, bit 2 z), Dirichlet flag in bit 31
+__global__ void hex_pack_cells_kernel(const int32_t* __restrict__ vtk, const uint8_t* __restrict__ dir,
+                                      int64_t ncells, int64_t nnodes, int* __restrict__ out,
+                                      unsigned long long* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ncells * 8; t += stride) {
+    const int64_t e = t >> 3;
+    const int bx = (int)(t & 1), by = (int)((t >> 1) & 1), bz = (int)((t >> 2) & 1);
+    const int vidx = 4 * bz + (by ? (bx ? 2 : 3) : bx);  // VTK index of this bit-order corner
+    const int id = vtk[e * 8 + vidx];
+    if (id < 0 || id >= nnodes) {
+      atomicAdd(&bad[0], 1ull);
+      out[t] = 0;
+      continue;
+    }
+    out[t] = (dir && dir[id]) ? (int)((unsigned)id | 0x80000000u) : id;
+  }
+}
+
+int grid_for(int64_t n, int threads, int sm_count, int per_sm) {
+  const int64_t want = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count * per_sm));
+}
+
+}  // namespace
+
+cudaError_t launch_hex_apply(int kind, int bc, const int4* cells, const double4* xyz, const double2* lm,
+                             const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
+                             Reduce red, cudaStream_t s, int sm_count) {
+  if (ncells <= 0) return cudaSuccess;
+  const int grid = grid_for(ncells, kHexThreads, sm_count, 8);
+  if (mode >= 1 && grid > red.capacity) return cudaErrorInvalidConfiguration;
+#define HEX_LAUNCH(K, M) hex_apply_kernel<K, M><<<grid, kHexThreads, 0, s>>>(cells, xyz, lm, x, y, ncells, bc, sc, red)
+  if (kind == 0) { if (mode) HEX_LAUNCH(0, 1); else HEX_LAUNCH(0, 0); }
+  else if (kind == 1) { if (mode) HEX_LAUNCH(1, 1); else HEX_LAUNCH(1, 0); }
+  else { if (mode) HEX_LAUNCH(2, 1); else HEX_LAUNCH(2, 0); }
+#undef HEX_LAUNCH
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hex_dirichlet(const int32_t* nodes, int64_t nb, int comps, const double* x, double* y,
+                                 int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  if (nb <= 0) return cudaSuccess;
+  const int grid = grid_for(nb * comps, 256, sm_count, 4);
+  if (mode) hex_dirichlet_kernel<1><<<grid, 256, 0, s>>>(nodes, nb, comps, x, y, sc, red);
+  else hex_dirichlet_kernel<0><<<grid, 256, 0, s>>>(nodes, nb, comps, x, y, sc, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hex_check(const int4* cells, const double4* xyz, int64_t ncells, int64_t nnodes,
+                             unsigned long long* bad, cudaStream_t s, int sm_count) {
+  hex_check_kernel<<<grid_for(ncells, 256, sm_count, 8), 256, 0, s>>>(cells, xyz, ncells, nnodes, bad);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hex_pack_cells(const int32_t* vtk, const uint8_t* dir, int64_t ncells, int64_t nnodes,
+                                  int* out, unsigned long long* bad, cudaStream_t s, int sm_count) {
+  hex_pack_cells_kernel<<<grid_for(ncells * 8, 256, sm_count, 8), 256, 0, s>>>(vtk, dir, ncells, nnodes, out, bad);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace fem

@@ -43,7 +43,8 @@ class CgInfo(ctypes.Structure):
 # every symbol include/fem.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fem_last_error", "fem_version", "fem_launch_count", "fem_get_unique_id", "fem_comm_create",
-    "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy", "fem_op_create",
+    "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy",
+    "fem_mesh_create_hex", "fem_mesh_info_hex", "fem_op_create",
     "fem_op_ndof", "fem_set_material", "fem_apply", "fem_dot", "fem_cg_solve", "fem_cg_begin",
     "fem_cg_iterate", "fem_cg_end", "fem_set_option", "fem_get_option", "fem_apply_time", "fem_op_destroy",
     "fem_csr_create", "fem_csr_info", "fem_csr_apply", "fem_csr_destroy",
@@ -79,6 +80,8 @@ def load(build_if_missing: bool = True):
         "fem_mesh_create": ([i64, i64, i64, dbl, vp, P(vp)], ctypes.c_int),
         "fem_mesh_local": ([vp, P(i64), P(i64), P(i64)], ctypes.c_int),
         "fem_mesh_destroy": ([vp], None),
+        "fem_mesh_create_hex": ([i64, i64, vp, vp, vp, P(vp)], ctypes.c_int),
+        "fem_mesh_info_hex": ([vp, P(i64), P(i64), P(i64)], ctypes.c_int),
         "fem_op_create": ([vp, i32, i32, P(vp)], ctypes.c_int),
         "fem_op_ndof": ([vp, P(i64), P(i64)], ctypes.c_int),
         "fem_set_material": ([vp, vp, vp, i64, i64], ctypes.c_int),
@@ -110,18 +113,18 @@ def _check(rc: int):
         raise FemError(rc, load().fem_last_error().decode())
 
 
-def _ptr(a):
+def _ptr(a, dtype: str = "float64"):
     """Raw pointer of a torch tensor (device or host) or numpy array; checks dtype/contiguity."""
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        if a.dtype != np.float64 or not a.flags.c_contiguous:
-            raise TypeError("numpy arrays must be contiguous float64")
+        if a.dtype != np.dtype(dtype) or not a.flags.c_contiguous:
+            raise TypeError(f"numpy arrays must be contiguous {dtype}")
         return a.ctypes.data
     import torch
     if isinstance(a, torch.Tensor):
-        if a.dtype != torch.float64 or not a.is_contiguous():
-            raise TypeError("tensors must be contiguous float64")
+        if a.dtype != getattr(torch, dtype) or not a.is_contiguous():
+            raise TypeError(f"tensors must be contiguous {dtype}")
         return a.data_ptr()
     raise TypeError(f"unsupported buffer type {type(a)}")
 
@@ -199,6 +202,35 @@ class Mesh:
             pass
 
 
+class HexMesh:
+    """General (deformed) hexahedral mesh: Alg. 1 input -- coordinates (n, 3) float64, node map
+    (ne, 8) int32 in VTK corner order, optional Dirichlet flags (n,) uint8 (include/fem.h)."""
+
+    def __init__(self, coords, cells, dirichlet=None):
+        n = int(coords.shape[0]) if hasattr(coords, "shape") else len(coords) // 3
+        ne = int(cells.shape[0]) if cells.ndim == 2 else int(cells.shape[0]) // 8
+        m = ctypes.c_void_p()
+        _check(load().fem_mesh_create_hex(n, ne, _ptr(coords), _ptr(cells, "int32"),
+                                          _ptr(dirichlet, "uint8"), ctypes.byref(m)))
+        self.h_ = m
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(load().fem_mesh_info_hex(m, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        self.n_nodes, self.n_cells, self.n_constrained = a.value, b.value, c.value
+        self.comm = None
+        self.plane_begin, self.plane_end, self.n_local_nodes = 0, 1, self.n_nodes
+
+    def close(self):
+        if self.h_:
+            load().fem_mesh_destroy(self.h_)
+            self.h_ = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Operator:
     def __init__(self, mesh: Mesh, kind: str | int, bc: str | int = "dirichlet"):
         self.mesh = mesh
@@ -215,7 +247,7 @@ class Operator:
     # -- material ---------------------------------------------------------------------------
     def set_material(self, lam, mu, layer_begin: int = 0, n_layers: int | None = None):
         if n_layers is None:
-            n_layers = self.mesh.nz - layer_begin
+            n_layers = 1 if isinstance(self.mesh, HexMesh) else self.mesh.nz - layer_begin
         _check(load().fem_set_material(self.h, _ptr(lam), _ptr(mu), layer_begin, n_layers))
 
     # -- operator ---------------------------------------------------------------------------
