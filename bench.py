@@ -68,6 +68,13 @@ def cg_apply_bytes(kind, nx, ny, nz, fused):
     return b
 
 
+# General-hex kernel (kernels_hex.cu): FP64 operations per cell of the per-cell body, counted
+# from the SASS (DADD + DMUL + 2 DFMA; tools/sass_mix.sh), CG mode (with the energy for p.Ap).
+HEX_FLOPS_PER_CELL = {"elastic": 635 + 337 + 2 * 609, "vector": 594 + 345 + 2 * 609,
+                      "scalar": 302 + 175 + 2 * 323}
+FP64_PEAK_TFLOPS = 2 * 17.08  # own DFMA microbenchmark, profiles/r01_microbench_fp64_hbm.txt
+
+
 def cg_vector_bytes(ndof, fused):
     # update: read x,p,r,q write x,r (48 B/DOF); unfused p-update: read r,p write p (24 B/DOF)
     return (48 if fused else 72) * ndof
@@ -142,21 +149,30 @@ def oracle_sample_dims(kind):
     return {"elastic": (96, 96, 96), "vector": (48, 48, 48), "scalar": (160, 160, 160)}[kind]
 
 
-def oracle_cg_rate(kind, iters=2):
+def oracle_cg_rate(kind, iters=2, hexmesh=False):
     from oracle import oracle as O
     nx, ny, nz = oracle_sample_dims(kind)
     h = 1.0 / nx
     g = I.rng(I.SEED_BASE + 77)
     lam, mu = I.materials(g, nx, ny, nz)
     b = I.interior_rhs(g, nx, ny, nz, I.ncomp(kind))
+    if hexmesh:
+        coords, cells, bnd = I.hex_box_mesh(nx, ny, nz, h=h, g=g, jitter=0.2)
+
+        def run(m):
+            O.cg_hex(kind, coords, cells, b, bnd, tol=0.0, maxit=m, lam=lam, mu=mu)
+    else:
+        def run(m):
+            O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=m, lam=lam, mu=mu)
     t0 = time.perf_counter()
-    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=0, lam=lam, mu=mu)
+    run(0)
     t1 = time.perf_counter()
-    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=iters, lam=lam, mu=mu)
+    run(iters)
     t2 = time.perf_counter()
     it_time = max((t2 - t1) - (t1 - t0), 1e-9) / iters
     cores = O.max_threads()
-    return b.size / it_time / 1e9, cores, f"oracle CG on {kind} {nx}x{ny}x{nz} (same recipe), " \
+    return b.size / it_time / 1e9, cores, f"oracle CG on {kind} {nx}x{ny}x{nz}" \
+        f"{' general hex (jittered)' if hexmesh else ''} (same recipe), " \
         f"{iters} iterations timed (init/true-residual applies subtracted), {b.size} DOF"
 
 
@@ -173,15 +189,24 @@ def run_reference(args, cfg):
     g = I.rng(I.SEED_BASE + 77)
     lam, mu = I.materials(g, nx, ny, nz)
     b = I.interior_rhs(g, nx, ny, nz, I.ncomp(kind))
+    hexmesh = cfg.get("mesh") == "hex"
+    if hexmesh:  # general-hex workload: the oracle's Alg. 1 path on a jittered sub-box
+        coords, cells, bnd = I.hex_box_mesh(nx, ny, nz, h=h, g=g, jitter=cfg["jitter"])
+
+        def run(m):
+            O.cg_hex(kind, coords, cells, b, bnd, tol=0.0, maxit=m, lam=lam, mu=mu)
+    else:
+        def run(m):
+            O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=m, lam=lam, mu=mu)
     # each step = one oracle CG iteration on the bounded sub-box
-    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=0, lam=lam, mu=mu)  # warm the library
+    run(0)  # warm the library
     ta = time.perf_counter()
-    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=0, lam=lam, mu=mu)
+    run(0)
     t_fixed = time.perf_counter() - ta
     for _ in range(args.warmup):
         pass  # the oracle has no warm-up state; warm-up steps are not re-run to bound the time
     t0 = time.perf_counter()
-    O.cg(kind, 1, nx, ny, nz, h, b, tol=0.0, maxit=args.steps, lam=lam, mu=mu)
+    run(args.steps)
     t = max(time.perf_counter() - t0 - t_fixed, 1e-9)
     value = b.size * args.steps / t / 1e9
     cores = O.max_threads()
@@ -190,7 +215,8 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak" if "planes_per_rank" in cfg else "strong",
+        "higher_is_better": True,
+        "scaling": "weak" if ("planes_per_rank" in cfg or cfg.get("mesh") == "hex") else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["name"], "kind": kind, "cells": list(I.config_cells(cfg, ws)),
                    "sample_cells": [nx, ny, nz], "bc": "dirichlet_box"},
@@ -220,16 +246,24 @@ def run_native(args, cfg):
     nx, ny, nz = I.config_cells(cfg, ws)
     h = 1.0 / nx
     c = I.ncomp(kind)
-    scaling = "weak" if "planes_per_rank" in cfg else "strong"
+    hexmesh = cfg.get("mesh") == "hex"
+    scaling = "weak" if ("planes_per_rank" in cfg or hexmesh) else "strong"
     comm = None
-    if ws > 1:
+    if ws > 1 and not hexmesh:
         uid = [fem.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = fem.Comm(ws, rank, uid[0])
-    mesh = fem.Mesh(nx, ny, nz, h, comm)
+    if hexmesh:  # single-GPU operator: N ranks run N independent replicas ("replicas only")
+        gm = I.rng(I.SEED_BASE + args.config + 2000)
+        coords, cells, bnd = I.hex_box_mesh(nx, ny, nz, h=h, g=gm, jitter=cfg["jitter"])
+        mesh = fem.HexMesh(torch.from_numpy(coords).cuda(), torch.from_numpy(cells).cuda(),
+                           torch.from_numpy(bnd).cuda())
+        del coords, cells, bnd
+    else:
+        mesh = fem.Mesh(nx, ny, nz, h, comm)
     op = fem.Operator(mesh, kind, "dirichlet")
-    ndof_global = op.n_global
-    k0, k1 = mesh.plane_begin, mesh.plane_end
+    ndof_global = op.n_global * (ws if hexmesh else 1)
+    k0, k1 = (0, nz + 1) if hexmesh else (mesh.plane_begin, mesh.plane_end)
     plane = (nx + 1) * (ny + 1)
 
     # ---- inputs (seeded, synthetic, SURVEY §8(d) recipe) ----
@@ -239,8 +273,11 @@ def run_native(args, cfg):
         lb = max(k0 - 1, 0)
         le = min(k1, nz)
         sl = slice(lb * nx * ny, le * nx * ny)
-        op.set_material(torch.from_numpy(lam[sl]).cuda(), torch.from_numpy(mu[sl]).cuda(),
-                        layer_begin=lb, n_layers=le - lb)
+        if hexmesh:
+            op.set_material(torch.from_numpy(lam).cuda(), torch.from_numpy(mu).cuda())
+        else:
+            op.set_material(torch.from_numpy(lam[sl]).cuda(), torch.from_numpy(mu[sl]).cuda(),
+                            layer_begin=lb, n_layers=le - lb)
         del lam, mu
     gb = I.rng(I.SEED_BASE + args.config + 1000)
     b_full = I.interior_rhs(gb, nx, ny, nz, c)
@@ -299,6 +336,9 @@ def run_native(args, cfg):
     # algorithmic bytes of one rank's apply launch: owned planes (+ its cell layers)
     alg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) * nloc_planes / (nz + 1)
     achieved = alg_bytes / (apply_ms / 1e3) / 1e9
+    if hexmesh:  # FP64-bound: flops of the per-cell body / apply time
+        hex_flops = HEX_FLOPS_PER_CELL[kind] * nx * ny * nz
+        achieved_tf = hex_flops / (apply_ms / 1e3) / 1e12
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}.json")
     if os.path.exists(tr_path) and ws == 1:
@@ -356,14 +396,14 @@ def run_native(args, cfg):
                "step": f"one fem_cg_solve call ({M} iterations) with pinned host b, x; per-rank bytes"}
 
     # ---- CSR SpMV baseline, same box (N = 1) ----
-    if ws == 1 and not args.no_csr:
+    if ws == 1 and not args.no_csr and not hexmesh:
         extra.update(csr_compare(fem, torch, kind, args))
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1) ----
     cpu = None
     if ws == 1 and rank == 0 and not args.no_cpu:
         try:
-            v, cores, sample = oracle_cg_rate(kind)
+            v, cores, sample = oracle_cg_rate(kind, hexmesh=hexmesh)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
@@ -376,16 +416,23 @@ def run_native(args, cfg):
             "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg["name"], "kind": kind, "cells": [nx, ny, nz],
+                       "mesh": ("general hex: explicit node map + coordinates, interior nodes jittered "
+                                f"U(-{cfg['jitter']}, {cfg['jitter']}) h" if hexmesh else "box"),
                        "ndof": ndof_global, "bc": "dirichlet_box",
                        "material": "E=10^U(0,2), nu=U(0.20,0.35) per cell" if kind == "elastic" else None,
                        "parallelism": f"z-slab x{ws}" if ws > 1 else "single GPU",
                        "l2": "inputs larger than L2 (vectors %.2f GB each)" % (ndof_global * 8 / 1e9)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": (f"{kind} fused CG apply (p = r + beta p_old, q = A p, p.q)" if fused
-                                    else f"{kind} apply (CG mode, fused p.Ap)"),
-                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-                         "frac_of_8TBps_nominal": achieved / 8000.0},
+            "roofline": ({"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": achieved / hbm_peak, "traffic": traffic,
+                          "kernel": (f"{kind} fused CG apply (p = r + beta p_old, q = A p, p.q)" if fused
+                                     else f"{kind} apply (CG mode, fused p.Ap)"),
+                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                          "frac_of_8TBps_nominal": achieved / 8000.0} if not hexmesh else
+                         {"bound": "alu", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS,
+                          "unit": "TFLOP/s", "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": None,
+                          "kernel": f"hex_apply_kernel<{kind}, CG mode> (Alg. 1, J per Gauss point)",
+                          "flops_per_cell": HEX_FLOPS_PER_CELL[kind],
+                          "peak_source": "FP64 DFMA microbenchmark x 2 (profiles/r01_microbench_fp64_hbm.txt)"}),
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": int(launches),

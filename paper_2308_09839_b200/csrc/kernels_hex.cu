@@ -153,7 +153,7 @@ __device__ __forceinline__ void gauss_point(const Modal& mx, const Modal& my, co
 constexpr int kHexThreads = 128;
 
 template <int KIND, int MODE>
-__global__ void __launch_bounds__(kHexThreads, 2)
+__global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
     hex_apply_kernel(const int4* __restrict__ cells, const double4* __restrict__ xyz,
                      const double2* __restrict__ lm, const double* __restrict__ u,
                      double* __restrict__ y, int64_t ncells, int bc, CgScalars* sc, Reduce red) {

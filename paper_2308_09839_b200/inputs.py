@@ -30,6 +30,12 @@ CONFIGS = {
             cg_iters=100),
     5: dict(name="C5b_elastic_weak", kind="elastic", n=(665, 665, None), planes_per_rank=94, bc=1,
             cg_iters=100),
+    # NEXT #2 of SURVEY §8(f): general (deformed) hexahedra, Alg. 1 as written -- explicit node
+    # map + coordinates, interior nodes jittered by U(-0.2, 0.2) h (non-affine cells)
+    6: dict(name="H1_elastic_hex_256", kind="elastic", n=(256, 256, 256), mesh="hex", jitter=0.2, bc=1,
+            cg_iters=100),
+    7: dict(name="H2_scalar_hex_256", kind="scalar", n=(256, 256, 256), mesh="hex", jitter=0.2, bc=1,
+            cg_iters=100),
 }
 
 
