@@ -179,6 +179,10 @@ void fem_op_destroy(fem_op_t op);
 int fem_csr_create(fem_op_t op, fem_csr_t* out);
 int fem_csr_info(fem_csr_t csr, int64_t* nrows, int64_t* nnz, int64_t* bytes);
 int fem_csr_apply(fem_csr_t csr, const double* x, double* y, void* stream);
+/* Copy the CSR arrays out (device or host destinations, any may be NULL): rowptr nrows + 1
+ * int64, col nnz int32, val nnz FP64.  Synchronises the stream.  Used to hand the identical
+ * matrix to a library SpMV (cuSPARSE) for the baseline comparison of bench.py. */
+int fem_csr_export(fem_csr_t csr, int64_t* rowptr, int32_t* col, double* val, void* stream);
 void fem_csr_destroy(fem_csr_t csr);
 
 #ifdef __cplusplus

@@ -1238,6 +1238,23 @@ int fem_csr_apply(fem_csr_t c, const double* x, double* y, void* stream) {
   return FEM_OK;
 }
 
+int fem_csr_export(fem_csr_t c, int64_t* rowptr, int32_t* col, double* val, void* stream) {
+  if (!c) return fail(FEM_EINVAL, "csr is NULL");
+  FEM_TRY(set_device(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> int {
+    if (!dst) return FEM_OK;
+    const cudaMemcpyKind k = is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, k, s));
+    return FEM_OK;
+  };
+  FEM_TRY(cp(rowptr, c->rowptr, (c->nrows + 1) * sizeof(int64_t)));
+  FEM_TRY(cp(col, c->col, c->nnz * sizeof(int32_t)));
+  FEM_TRY(cp(val, c->val, c->nnz * sizeof(double)));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return FEM_OK;
+}
+
 void fem_csr_destroy(fem_csr_t c) {
   if (!c) return;
   set_device(c->device);

@@ -47,7 +47,7 @@ EXPORTS = [
     "fem_mesh_create_hex", "fem_mesh_info_hex", "fem_op_create",
     "fem_op_ndof", "fem_set_material", "fem_apply", "fem_dot", "fem_cg_solve", "fem_cg_begin",
     "fem_cg_iterate", "fem_cg_end", "fem_set_option", "fem_get_option", "fem_apply_time", "fem_op_destroy",
-    "fem_csr_create", "fem_csr_info", "fem_csr_apply", "fem_csr_destroy",
+    "fem_csr_create", "fem_csr_info", "fem_csr_apply", "fem_csr_export", "fem_csr_destroy",
 ]
 
 _lib = None
@@ -98,6 +98,7 @@ def load(build_if_missing: bool = True):
         "fem_csr_create": ([vp, P(vp)], ctypes.c_int),
         "fem_csr_info": ([vp, P(i64), P(i64), P(i64)], ctypes.c_int),
         "fem_csr_apply": ([vp, vp, vp, vp], ctypes.c_int),
+        "fem_csr_export": ([vp, vp, vp, vp, vp], ctypes.c_int),
         "fem_csr_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
@@ -344,6 +345,11 @@ class Csr:
             y = torch.empty_like(x)
         _check(load().fem_csr_apply(self.h, _ptr(x), _ptr(y), _stream(stream)))
         return y
+
+    def export(self, rowptr, col, val, stream=None):
+        """Copy rowptr (int64), col (int32), val (float64) into the given buffers."""
+        _check(load().fem_csr_export(self.h, _ptr(rowptr, "int64"), _ptr(col, "int32"), _ptr(val),
+                                     _stream(stream)))
 
     def close(self):
         if self.h:
