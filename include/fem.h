@@ -162,7 +162,10 @@ int fem_cg_iterate(fem_op_t op, int32_t iters, void* stream);
 int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
 /* Options: "use_graph" (default 1), "check_every" (default 16 iterations between host
  * convergence polls in fem_cg_solve), "time_apply" (1: record CUDA events around every apply
- * launched by fem_cg_iterate; read back with fem_apply_time). */
+ * launched by fem_cg_iterate; read back with fem_apply_time), "partial_assembly" (general hex
+ * meshes only, else FEM_EUNSUPPORTED; 1: store the Gauss-point geometry once -- 6 values per
+ * point for the Laplace kinds, 9 for elasticity -- and apply from it, the paper's comparison
+ * method P:308-309 / Table 3; 0: matrix-free recomputation, the default). */
 int fem_set_option(fem_op_t op, const char* key, int64_t value);
 /* Read-only properties: "fused_cg" (1: CG iterations use the fused apply -- p = r + beta p_old
  * formed inside the TMA apply kernel -- and 2 kernels per iteration; 0: apply + update +

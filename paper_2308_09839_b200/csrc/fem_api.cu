@@ -119,6 +119,9 @@ struct fem_op_s {
   cudaGraphExec_t graph1 = nullptr, graphN = nullptr, graph1b = nullptr;
   // options
   int use_graph = 1, check_every = 16, time_apply = 0;
+  // general hex meshes: partial assembly (per-Gauss-point geometry stored once)
+  int use_pa = 0;
+  double* pa = nullptr;
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
 };
@@ -365,8 +368,11 @@ static int64_t pl_count(fem_op_s* op) { return op->nloc_planes * op->pl_pp; }  /
 static int apply_hex(fem_op_s* op, const double* x, double* y, int mode, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
   CUDA_TRY(cudaMemsetAsync(y, 0, op->n_local * sizeof(double), s));
-  cudaError_t e = launch_hex_apply(op->kind, op->bc, m->hx_cells, m->hx_xyz, op->lm, x, y, m->hx_ncells, mode, op->sc,
-                                   op->red, s, m->sm_count);
+  cudaError_t e = op->use_pa
+                      ? launch_hex_pa_apply(op->kind, op->bc, m->hx_cells, op->pa, op->lm, x, y, m->hx_ncells, mode,
+                                            op->sc, op->red, s, m->sm_count)
+                      : launch_hex_apply(op->kind, op->bc, m->hx_cells, m->hx_xyz, op->lm, x, y, m->hx_ncells, mode,
+                                         op->sc, op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "hex apply launch: %s", cudaGetErrorString(e));
   if (op->bc && m->hx_nb) {
     e = launch_hex_dirichlet(m->hx_bnodes, m->hx_nb, op->comps, x, y, mode, op->sc, op->red, s, m->sm_count);
@@ -625,6 +631,7 @@ static void op_free(fem_op_s* op) {
   if (op->graphN) cudaGraphExecDestroy(op->graphN);
   for (auto e : op->ev) cudaEventDestroy(e);
   cudaFree(op->lm);
+  cudaFree(op->pa);
   cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
   if (op->graph1b) cudaGraphExecDestroy(op->graph1b);
   cudaFree(op->ghost_lo); cudaFree(op->ghost_hi);
@@ -1143,7 +1150,23 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (value < 1) return fail(FEM_EINVAL, "check_every must be >= 1");
     op->check_every = (int)value;
   } else if (!std::strcmp(key, "time_apply")) op->time_apply = value != 0;
-  else return fail(FEM_EINVAL, "unknown option '%s'", key);
+  else if (!std::strcmp(key, "partial_assembly")) {
+    if (!op->mesh->hex) return fail(FEM_EUNSUPPORTED, "partial_assembly is an option of general hex meshes");
+    FEM_TRY(set_device(op->mesh->device));
+    if (value && !op->pa) {
+      const int64_t n = hex_pa_doubles(op->kind, op->mesh->hx_ncells);
+      FEM_TRY(dalloc(&op->pa, n));
+      cudaError_t e = launch_hex_pa_setup(op->kind, op->mesh->hx_cells, op->mesh->hx_xyz, op->pa,
+                                          op->mesh->hx_ncells, 0, op->mesh->sm_count);
+      if (e != cudaSuccess) return fail(FEM_ECUDA, "partial-assembly setup: %s", cudaGetErrorString(e));
+      CUDA_TRY(cudaDeviceSynchronize());
+    }
+    op->use_pa = value != 0;
+    // captured CG graphs hold the other kernel
+    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
+    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
+    if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
+  } else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }
 
@@ -1153,6 +1176,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "use_graph")) *value = op->use_graph;
   else if (!std::strcmp(key, "check_every")) *value = op->check_every;
   else if (!std::strcmp(key, "time_apply")) *value = op->time_apply;
+  else if (!std::strcmp(key, "partial_assembly")) *value = op->use_pa;
   else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }

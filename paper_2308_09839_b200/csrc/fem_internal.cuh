@@ -115,6 +115,14 @@ cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const 
 cudaError_t launch_hex_apply(int kind, int bc, const int4* cells, const double4* xyz, const double2* lm,
                              const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
                              Reduce red, cudaStream_t s, int sm_count);
+// partial assembly on general hex meshes: per-Gauss-point geometry stored once (setup), then
+// applied without recomputing J (Laplace kinds share the 6-value D'; elasticity 9-value B)
+int64_t hex_pa_doubles(int kind, int64_t ncells);
+cudaError_t launch_hex_pa_setup(int kind, const int4* cells, const double4* xyz, double* pa, int64_t ncells,
+                                cudaStream_t s, int sm_count);
+cudaError_t launch_hex_pa_apply(int kind, int bc, const int4* cells, const double* pa, const double2* lm,
+                                const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
+                                Reduce red, cudaStream_t s, int sm_count);
 // y = x on the constrained nodes; mode 1: sc->pq += sum x_b^2
 cudaError_t launch_hex_dirichlet(const int32_t* nodes, int64_t nb, int comps, const double* x, double* y,
                                  int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);

@@ -315,6 +315,185 @@ __global__ void hex_pack_cells_kernel(const int32_t* __restrict__ vtk, const uin
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Partial assembly (the paper's comparison method, Table 3): the geometry
+// of every Gauss point is computed once and stored; the apply then reads it instead of
+// recomputing J.  Stored per cell and point (SoA, [q][k][cell], coalesced):
+//   Laplace:    D' = cof(J')^T cof(J') / det J'   (6 values, the paper's "6 per qpt")
+//   elasticity: B  = cof(J') / sqrt(det J')         (9 values; the paper stores 21 with the
+//               material folded in -- here lambda, mu stay per cell, 2 values)
+// so that P' = G' D' (Laplace) or P' = sigma(G' B^T) B (elasticity) equal the matrix-free P'.
+template <int KIND>
+__global__ void __launch_bounds__(256) hex_pa_setup_kernel(const int4* __restrict__ cells,
+                                                           const double4* __restrict__ xyz,
+                                                           double* __restrict__ pa, int64_t ncells) {
+  constexpr int K = (KIND == 2) ? 9 : 6;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncells; e += stride) {
+    const int4 lo = cells[2 * e], hi = cells[2 * e + 1];
+    const int raw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    double X[8], Y[8], Z[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const double4 p = xyz[raw[a] & 0x7fffffff];
+      X[a] = p.x; Y[a] = p.y; Z[a] = p.z;
+    }
+    Modal mx = hadamard(X), my = hadamard(Y), mz = hadamard(Z);
+    prescale(mx); prescale(my); prescale(mz);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double sx = (q & 1) ? 1.0 : -1.0, sy = (q & 2) ? 1.0 : -1.0, sz = (q & 4) ? 1.0 : -1.0;
+      double J[3][3];
+      const Modal* f[3] = {&mx, &my, &mz};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const Modal& m = *f[d];
+        J[d][0] = m.x + (sy * m.xy + (sz * m.xz + (sy * sz) * m.xyz));
+        J[d][1] = m.y + (sx * m.xy + (sz * m.yz + (sx * sz) * m.xyz));
+        J[d][2] = m.z + (sx * m.xz + (sy * m.yz + (sx * sy) * m.xyz));
+      }
+      double cf[3][3];
+      cf[0][0] = fma(J[1][1], J[2][2], -J[1][2] * J[2][1]);
+      cf[0][1] = fma(J[1][2], J[2][0], -J[1][0] * J[2][2]);
+      cf[0][2] = fma(J[1][0], J[2][1], -J[1][1] * J[2][0]);
+      cf[1][0] = fma(J[0][2], J[2][1], -J[0][1] * J[2][2]);
+      cf[1][1] = fma(J[0][0], J[2][2], -J[0][2] * J[2][0]);
+      cf[1][2] = fma(J[0][1], J[2][0], -J[0][0] * J[2][1]);
+      cf[2][0] = fma(J[0][1], J[1][2], -J[0][2] * J[1][1]);
+      cf[2][1] = fma(J[0][2], J[1][0], -J[0][0] * J[1][2]);
+      cf[2][2] = fma(J[0][0], J[1][1], -J[0][1] * J[1][0]);
+      const double det = fma(J[0][0], cf[0][0], fma(J[0][1], cf[0][1], J[0][2] * cf[0][2]));
+      double* out = pa + (int64_t)q * K * ncells + e;
+      if (KIND == 2) {
+        const double rs = rsqrt(det);
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) out[(3 * d + k) * ncells] = cf[d][k] * rs;
+      } else {
+        const double rd = 1.0 / det;
+        // D'_{ef} = sum_d cf[d][e] cf[d][f] / det : (00, 01, 02, 11, 12, 22)
+        const int E[6] = {0, 0, 0, 1, 1, 2}, Fi[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+          out[k * ncells] =
+              fma(cf[0][E[k]], cf[0][Fi[k]], fma(cf[1][E[k]], cf[1][Fi[k]], cf[2][E[k]] * cf[2][Fi[k]])) * rd;
+      }
+    }
+  }
+}
+
+template <int KIND, int C, int SX, int SY, int SZ>
+__device__ __forceinline__ void pa_point(const double* __restrict__ g, int64_t ncells, const Modal* mu,
+                                         Modal* acc, double L, double M, double& energy) {
+  if (KIND == 2) {
+    double B[3][3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) B[k / 3][k % 3] = g[k * ncells];
+    double Gt[3][3];  // G' B^T = sqrt(det J') grad u
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double g0, g1, g2;
+      dref<SX, SY, SZ>(mu[c], g0, g1, g2);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) Gt[c][d] = fma(g0, B[d][0], fma(g1, B[d][1], g2 * B[d][2]));
+    }
+    const double tr = Gt[0][0] + Gt[1][1] + Gt[2][2];
+    const double Lt = L * tr, M2 = M + M;
+    const double s00 = fma(M2, Gt[0][0], Lt), s11 = fma(M2, Gt[1][1], Lt), s22 = fma(M2, Gt[2][2], Lt);
+    const double e01 = Gt[0][1] + Gt[1][0], e02 = Gt[0][2] + Gt[2][0], e12 = Gt[1][2] + Gt[2][1];
+    const double s01 = M * e01, s02 = M * e02, s12 = M * e12;
+    energy = fma(s00, Gt[0][0], fma(s11, Gt[1][1], fma(s22, Gt[2][2], fma(s01, e01, fma(s02, e02, fma(s12, e12, energy))))));
+    const double S[3][3] = {{s00, s01, s02}, {s01, s11, s12}, {s02, s12, s22}};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double p[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) p[e] = fma(S[c][0], B[0][e], fma(S[c][1], B[1][e], S[c][2] * B[2][e]));
+      accum<SX, SY, SZ>(acc[c], p[0], p[1], p[2]);
+    }
+  } else {
+    const double d00 = g[0], d01 = g[ncells], d02 = g[2 * ncells], d11 = g[3 * ncells],
+                 d12 = g[4 * ncells], d22 = g[5 * ncells];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      double g0, g1, g2;
+      dref<SX, SY, SZ>(mu[c], g0, g1, g2);
+      const double p0 = fma(d00, g0, fma(d01, g1, d02 * g2));
+      const double p1 = fma(d01, g0, fma(d11, g1, d12 * g2));
+      const double p2 = fma(d02, g0, fma(d12, g1, d22 * g2));
+      energy = fma(g0, p0, fma(g1, p1, fma(g2, p2, energy)));
+      accum<SX, SY, SZ>(acc[c], p0, p1, p2);
+    }
+  }
+}
+
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(128, (KIND == 0) ? 4 : 2)
+    hex_pa_apply_kernel(const int4* __restrict__ cells, const double* __restrict__ pa,
+                        const double2* __restrict__ lm, const double* __restrict__ u,
+                        double* __restrict__ y, int64_t ncells, int bc, CgScalars* sc, Reduce red) {
+  constexpr int C = (KIND == 0) ? 1 : 3;
+  constexpr int K = (KIND == 2) ? 9 : 6;
+  __shared__ double red_sh[32];
+  if (MODE >= 1 && sc->done) return;
+  double energy = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncells; e += stride) {
+    const int4 lo = cells[2 * e], hi = cells[2 * e + 1];
+    const int raw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    int id[8];
+    bool fix[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      fix[a] = bc && raw[a] < 0;
+      id[a] = raw[a] & 0x7fffffff;
+    }
+    Modal mu[C], acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      double U[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) U[a] = fix[a] ? 0.0 : u[(int64_t)C * id[a] + c];
+      mu[c] = hadamard(U);
+      prescale(mu[c]);
+      acc[c] = Modal{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    }
+    double L = 0.0, M = 0.0;
+    if (KIND == 2) {
+      const double2 v = lm[e];
+      L = v.x; M = v.y;
+    }
+    double en = 0.0;
+    const double* g = pa + e;
+    const int64_t qs = (int64_t)K * ncells;
+    pa_point<KIND, C, -1, -1, -1>(g + 0 * qs, ncells, mu, acc, L, M, en);
+    pa_point<KIND, C, +1, -1, -1>(g + 1 * qs, ncells, mu, acc, L, M, en);
+    pa_point<KIND, C, -1, +1, -1>(g + 2 * qs, ncells, mu, acc, L, M, en);
+    pa_point<KIND, C, +1, +1, -1>(g + 3 * qs, ncells, mu, acc, L, M, en);
+    pa_point<KIND, C, -1, -1, +1>(g + 4 * qs, ncells, mu, acc, L, M, en);
+    pa_point<KIND, C, +1, -1, +1>(g + 5 * qs, ncells, mu, acc, L, M, en);
+    pa_point<KIND, C, -1, +1, +1>(g + 6 * qs, ncells, mu, acc, L, M, en);
+    pa_point<KIND, C, +1, +1, +1>(g + 7 * qs, ncells, mu, acc, L, M, en);
+    energy += en;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      Modal& m = acc[c];
+      m.x *= kInv512; m.y *= kInv512; m.z *= kInv512;
+      m.xy *= kG * kInv512; m.xz *= kG * kInv512; m.yz *= kG * kInv512; m.xyz *= kG2 * kInv512;
+      double v[8];
+      inverse(m, v);
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+    }
+  }
+  if (MODE >= 1) {
+    double total;
+    if (last_block_reduce(block_sum(energy * kInv512, red_sh), red, red_sh, &total)) sc->pq = total;
+  }
+}
+
 int grid_for(int64_t n, int threads, int sm_count, int per_sm) {
   const int64_t want = (n + threads - 1) / threads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count * per_sm));
@@ -333,6 +512,32 @@ cudaError_t launch_hex_apply(int kind, int bc, const int4* cells, const double4*
   else if (kind == 1) { if (mode) HEX_LAUNCH(1, 1); else HEX_LAUNCH(1, 0); }
   else { if (mode) HEX_LAUNCH(2, 1); else HEX_LAUNCH(2, 0); }
 #undef HEX_LAUNCH
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+int64_t hex_pa_doubles(int kind, int64_t ncells) { return (int64_t)8 * ((kind == 2) ? 9 : 6) * ncells; }
+
+cudaError_t launch_hex_pa_setup(int kind, const int4* cells, const double4* xyz, double* pa, int64_t ncells,
+                                cudaStream_t s, int sm_count) {
+  const int grid = grid_for(ncells, 256, sm_count, 8);
+  if (kind == 2) hex_pa_setup_kernel<2><<<grid, 256, 0, s>>>(cells, xyz, pa, ncells);
+  else hex_pa_setup_kernel<0><<<grid, 256, 0, s>>>(cells, xyz, pa, ncells);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hex_pa_apply(int kind, int bc, const int4* cells, const double* pa, const double2* lm,
+                                const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
+                                Reduce red, cudaStream_t s, int sm_count) {
+  if (ncells <= 0) return cudaSuccess;
+  const int grid = grid_for(ncells, 128, sm_count, 8);
+  if (mode >= 1 && grid > red.capacity) return cudaErrorInvalidConfiguration;
+#define PA_LAUNCH(K, M) hex_pa_apply_kernel<K, M><<<grid, 128, 0, s>>>(cells, pa, lm, x, y, ncells, bc, sc, red)
+  if (kind == 0) { if (mode) PA_LAUNCH(0, 1); else PA_LAUNCH(0, 0); }
+  else if (kind == 1) { if (mode) PA_LAUNCH(1, 1); else PA_LAUNCH(1, 0); }
+  else { if (mode) PA_LAUNCH(2, 1); else PA_LAUNCH(2, 0); }
+#undef PA_LAUNCH
   add_launches(1);
   return cudaGetLastError();
 }

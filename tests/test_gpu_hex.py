@@ -166,3 +166,47 @@ def test_hex_errors(F):
     with pytest.raises(F.FemError) as e:
         op.apply_ghost(x, None, None)
     assert e.value.status == F.FEM_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_hex_partial_assembly_parity(F, oracle, kind, bc):
+    """Partial assembly (stored Gauss-point geometry) is the same operator: oracle parity and
+    agreement with the matrix-free kernel."""
+    coords, cells, bnd, lam, mu = make((7, 6, 5), 0.22, True, 31)
+    c = I.ncomp(kind)
+    x = np.random.default_rng(4).uniform(-1, 1, coords.shape[0] * c)
+    ref = oracle.apply_hex(kind, coords, cells, x, bnd if bc else None, lam, mu)
+    op = F.Operator(F.HexMesh(dev(coords), dev(cells), dev(bnd)), kind, bc)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    y_mf = op.apply(dev(x)).cpu().numpy()
+    op.set_option("partial_assembly", 1)
+    assert op.get_option("partial_assembly") == 1
+    y_pa = op.apply(dev(x)).cpu().numpy()
+    assert relerr(y_pa, ref) <= APPLY_TOL
+    assert relerr(y_pa, y_mf) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("kind", ["scalar", "elastic"])
+def test_hex_partial_assembly_cg(F, oracle, kind):
+    coords, cells, bnd, lam, mu = make((9, 8, 7), 0.2, True, 11)
+    c = I.ncomp(kind)
+    b = np.random.default_rng(21).uniform(-1, 1, coords.shape[0] * c)
+    b[np.repeat(bnd == 1, c)] = 0.0
+    ref = oracle.cg_hex(kind, coords, cells, b, bnd, tol=1e-14, maxit=3000, lam=lam, mu=mu)
+    op = F.Operator(F.HexMesh(dev(coords), dev(cells), dev(bnd)), kind, 1)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    op.set_option("partial_assembly", 1)
+    x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+    info = op.cg_solve(dev(b), x, tol=1e-14, maxit=3000)
+    assert info["converged"]
+    assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10 * max(1.0, np.abs(ref.x).max())
+
+
+def test_partial_assembly_box_unsupported(F):
+    op = F.Operator(F.Mesh(4, 4, 4, 0.25), "scalar", 1)
+    with pytest.raises(F.FemError) as e:
+        op.set_option("partial_assembly", 1)
+    assert e.value.status == F.FEM_EUNSUPPORTED
