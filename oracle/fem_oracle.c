@@ -79,10 +79,25 @@ void orc_basis_gradients(const double xi[3], double dphi[8][3]) {
   }
 }
 
-/* 2-point Gauss-Legendre per direction: +-1/sqrt(3), weight 1 (reading R1).
- * Quadrature point q uses the same corner pattern as node q. */
+/* Quadrature rule of every element matrix below (reading R1):
+ *   ORC_GAUSS (default): 2-point Gauss-Legendre per direction, +-1/sqrt(3), weight 1;
+ *   ORC_GLL: 2-point Gauss-Lobatto-Legendre, +-1 (the nodes), weight 1 -- the quadrature of the
+ *            CEED benchmark problems BP5/BP6 the paper names (SURVEY
+ *            §8(c) item 1), collocated with the Q1 nodes.
+ * A process-wide setting (the oracle is single-threaded at this level); orc_set_quadrature
+ * returns the previous rule. */
+#define ORC_GAUSS 0
+#define ORC_GLL 1
+static int g_rule = ORC_GAUSS;
+int orc_set_quadrature(int rule) {
+  const int old = g_rule;
+  g_rule = (rule == ORC_GLL) ? ORC_GLL : ORC_GAUSS;
+  return old;
+}
+
+/* Quadrature point q uses the same corner pattern as node q. */
 void orc_reference_element(double xq[8][3], double wq[8], double dphi[8][8][3], double phi[8][8]) {
-  const double g = 1.0 / sqrt(3.0);
+  const double g = (g_rule == ORC_GLL) ? 1.0 : 1.0 / sqrt(3.0);
   for (int q = 0; q < 8; ++q) {
     for (int d = 0; d < 3; ++d) xq[q][d] = (2.0 * CORNER[q][d] - 1.0) * g;
     wq[q] = 1.0;

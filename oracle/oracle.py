@@ -72,6 +72,8 @@ def lib():
         L.orc_cg_hex.argtypes = [ctypes.c_int, i64, i64, d, i32p, u8p, d, d, d, d, ctypes.c_double,
                                  ctypes.c_int, ctypes.POINTER(CgInfoC), d, ctypes.c_int]
         L.orc_cg_hex.restype = ctypes.c_int
+        L.orc_set_quadrature.argtypes = [ctypes.c_int]
+        L.orc_set_quadrature.restype = ctypes.c_int
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = ctypes.c_int
         _lib = L
@@ -259,6 +261,24 @@ def cg_hex(kind, coords, cells, b, dirichlet=None, x0=None, tol=0.0, maxit=50, l
                     breakdown_iter=info.breakdown_iter, status=info.status, r0_norm=info.r0_norm,
                     r_norm=info.r_norm, true_r_norm=info.true_r_norm,
                     res_hist=hist[: info.iterations + 1])
+
+
+QUAD = {"gauss": 0, "gll": 1}
+
+
+class quadrature:
+    """Context manager selecting the oracle's quadrature rule ("gauss" default, "gll")."""
+
+    def __init__(self, rule: str):
+        self.rule = QUAD[rule]
+
+    def __enter__(self):
+        self.old = lib().orc_set_quadrature(self.rule)
+        return self
+
+    def __exit__(self, *exc):
+        lib().orc_set_quadrature(self.old)
+        return False
 
 
 def max_threads() -> int:
