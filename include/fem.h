@@ -165,7 +165,11 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * launched by fem_cg_iterate; read back with fem_apply_time), "partial_assembly" (general hex
  * meshes only, else FEM_EUNSUPPORTED; 1: store the Gauss-point geometry once -- 6 values per
  * point for the Laplace kinds, 9 for elasticity -- and apply from it, the paper's comparison
- * method P:308-309 / Table 3; 0: matrix-free recomputation, the default). */
+ * method P:308-309 / Table 3; 0: matrix-free recomputation, the default), "quadrature" (0: the
+ * 2x2x2 Gauss-Legendre rule, default; 1: the 2x2x2 Gauss-Lobatto rule collocated with the nodes,
+ * the quadrature of the CEED benchmark problems BP5 / BP6 the paper names, P:581, P:638,
+ * a different operator (the 7-point stencil for Laplace on the box); applies to
+ * every kernel of the operator incl. fem_csr_create). */
 int fem_set_option(fem_op_t op, const char* key, int64_t value);
 /* Read-only properties: "fused_cg" (1: CG iterations use the fused apply -- p = r + beta p_old
  * formed inside the TMA apply kernel -- and 2 kernels per iteration; 0: apply + update +

@@ -122,6 +122,8 @@ struct fem_op_s {
   // general hex meshes: partial assembly (per-Gauss-point geometry stored once)
   int use_pa = 0;
   double* pa = nullptr;
+  int pa_quad = -1;  // rule the stored geometry was computed for
+  int quad = 0;      // 0: 2x2x2 Gauss-Legendre, 1: 2x2x2 Gauss-Lobatto (BP5/BP6; reading R1)
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
 };
@@ -173,8 +175,10 @@ static int dalloc(T** p, size_t count) {
 
 // unit-cube element matrices by the library's own 2x2x2 Gauss quadrature (h = 1), corner
 // index a = dx + 2 dy + 4 dz.  Eq. 4 (scalar) and Eq. 6 split into its lambda and mu parts.
-static void unit_element_matrices(double K[64], double Kl[576], double Km[576]) {
-  const double gp[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
+static void unit_element_matrices(double K[64], double Kl[576], double Km[576], int quad = 0) {
+  // 2-point rule on [0, 1]: Gauss-Legendre (default) or Gauss-Lobatto (quad 1: the nodes)
+  const double g = quad == 1 ? 1.0 : 1.0 / std::sqrt(3.0);
+  const double gp[2] = {0.5 - 0.5 * g, 0.5 + 0.5 * g};
   std::memset(K, 0, 64 * sizeof(double));
   std::memset(Kl, 0, 576 * sizeof(double));
   std::memset(Km, 0, 576 * sizeof(double));
@@ -336,7 +340,7 @@ static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* u
                         cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
   ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr,
-                 op->tm_interior ? 1 : 0};
+                 op->tm_interior ? 1 : 0, op->quad};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
@@ -369,10 +373,10 @@ static int apply_hex(fem_op_s* op, const double* x, double* y, int mode, cudaStr
   fem_mesh_s* m = op->mesh;
   CUDA_TRY(cudaMemsetAsync(y, 0, op->n_local * sizeof(double), s));
   cudaError_t e = op->use_pa
-                      ? launch_hex_pa_apply(op->kind, op->bc, m->hx_cells, op->pa, op->lm, x, y, m->hx_ncells, mode,
-                                            op->sc, op->red, s, m->sm_count)
-                      : launch_hex_apply(op->kind, op->bc, m->hx_cells, m->hx_xyz, op->lm, x, y, m->hx_ncells, mode,
-                                         op->sc, op->red, s, m->sm_count);
+                      ? launch_hex_pa_apply(op->kind, op->bc, op->quad, m->hx_cells, op->pa, op->lm, x, y,
+                                            m->hx_ncells, mode, op->sc, op->red, s, m->sm_count)
+                      : launch_hex_apply(op->kind, op->bc, op->quad, m->hx_cells, m->hx_xyz, op->lm, x, y,
+                                         m->hx_ncells, mode, op->sc, op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "hex apply launch: %s", cudaGetErrorString(e));
   if (op->bc && m->hx_nb) {
     e = launch_hex_dirichlet(m->hx_bnodes, m->hx_nb, op->comps, x, y, mode, op->sc, op->red, s, m->sm_count);
@@ -944,7 +948,7 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   }
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
                  parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
-                 op->tm_interior ? 1 : 0};
+                 op->tm_interior ? 1 : 0, op->quad};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc, op->red, s,
@@ -1143,6 +1147,18 @@ int fem_cg_solve(fem_op_t op, const double* b, double* x, double tol, int32_t ma
   return st;
 }
 
+// (re)compute the stored Gauss-point geometry when partial assembly is on and the rule changed
+static int pa_setup(fem_op_s* op) {
+  if (!op->use_pa || op->pa_quad == op->quad) return FEM_OK;
+  if (!op->pa) FEM_TRY(dalloc(&op->pa, hex_pa_doubles(op->kind, op->mesh->hx_ncells)));
+  cudaError_t e = launch_hex_pa_setup(op->kind, op->quad, op->mesh->hx_cells, op->mesh->hx_xyz, op->pa,
+                                      op->mesh->hx_ncells, 0, op->mesh->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "partial-assembly setup: %s", cudaGetErrorString(e));
+  CUDA_TRY(cudaDeviceSynchronize());
+  op->pa_quad = op->quad;
+  return FEM_OK;
+}
+
 int fem_set_option(fem_op_t op, const char* key, int64_t value) {
   if (!op || !key) return fail(FEM_EINVAL, "op/key is NULL");
   if (!std::strcmp(key, "use_graph")) op->use_graph = value != 0;
@@ -1153,16 +1169,17 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
   else if (!std::strcmp(key, "partial_assembly")) {
     if (!op->mesh->hex) return fail(FEM_EUNSUPPORTED, "partial_assembly is an option of general hex meshes");
     FEM_TRY(set_device(op->mesh->device));
-    if (value && !op->pa) {
-      const int64_t n = hex_pa_doubles(op->kind, op->mesh->hx_ncells);
-      FEM_TRY(dalloc(&op->pa, n));
-      cudaError_t e = launch_hex_pa_setup(op->kind, op->mesh->hx_cells, op->mesh->hx_xyz, op->pa,
-                                          op->mesh->hx_ncells, 0, op->mesh->sm_count);
-      if (e != cudaSuccess) return fail(FEM_ECUDA, "partial-assembly setup: %s", cudaGetErrorString(e));
-      CUDA_TRY(cudaDeviceSynchronize());
-    }
     op->use_pa = value != 0;
+    FEM_TRY(pa_setup(op));
     // captured CG graphs hold the other kernel
+    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
+    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
+    if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
+  } else if (!std::strcmp(key, "quadrature")) {
+    if (value != 0 && value != 1) return fail(FEM_EINVAL, "quadrature must be 0 (Gauss) or 1 (Gauss-Lobatto)");
+    op->quad = (int)value;
+    FEM_TRY(set_device(op->mesh->device));
+    FEM_TRY(pa_setup(op));
     if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
     if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
     if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
@@ -1177,6 +1194,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "check_every")) *value = op->check_every;
   else if (!std::strcmp(key, "time_apply")) *value = op->time_apply;
   else if (!std::strcmp(key, "partial_assembly")) *value = op->use_pa;
+  else if (!std::strcmp(key, "quadrature")) *value = op->quad;
   else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }
@@ -1234,7 +1252,14 @@ int fem_csr_create(fem_op_t op, fem_csr_t* out) {
     return fail(FEM_ENOMEM, "CSR needs %.1f GB, %.1f GB free", need / 1e9, fr / 1e9);
   }
   if ((st = dalloc(&c->col, nnz)) || (st = dalloc(&c->val, nnz))) { fem_csr_destroy(c); return st; }
-  e = launch_csr_fill(op->kind, op->bc, g, op->lm, c->rowptr, c->col, c->val, 0);
+  {  // unit element matrices of the operator's quadrature rule (constant memory, this device)
+    std::lock_guard<std::mutex> lk(g_unit_mu);
+    double K[64], Kl[576], Km[576];
+    unit_element_matrices(K, Kl, Km, op->quad);
+    e = upload_unit_matrices(K, Kl, Km);
+    if (e == cudaSuccess) e = launch_csr_fill(op->kind, op->bc, g, op->lm, c->rowptr, c->col, c->val, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { fem_csr_destroy(c); return fail(FEM_ECUDA, "csr fill: %s", cudaGetErrorString(e)); }
   *out = c;

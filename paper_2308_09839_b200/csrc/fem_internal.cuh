@@ -45,6 +45,7 @@ struct ApplyMaps {
   const double* pold;      // mode 2: p_old owned plane k0 (same layout as x)
   double* pnew;            // mode 2: p output owned plane k0 (same layout as x)
   int interior;            // 1: u tensor spans only the Dirichlet interior (zero fill = mask)
+  int quad;                // 0: 2x2x2 Gauss-Legendre (default), 1: 2x2x2 Gauss-Lobatto (BP5/BP6)
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).
@@ -112,15 +113,15 @@ cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const 
 // order, bit 31 = Dirichlet node), xyz = node coordinates (w unused), lm = (lambda, mu) per cell.
 // mode 0: y += A (P x) at unconstrained nodes (y zeroed by the caller); mode 1: + sc->pq = the
 // sum of the element energies (P x)^T A (P x).
-cudaError_t launch_hex_apply(int kind, int bc, const int4* cells, const double4* xyz, const double2* lm,
+cudaError_t launch_hex_apply(int kind, int bc, int quad, const int4* cells, const double4* xyz, const double2* lm,
                              const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
                              Reduce red, cudaStream_t s, int sm_count);
 // partial assembly on general hex meshes: per-Gauss-point geometry stored once (setup), then
 // applied without recomputing J (Laplace kinds share the 6-value D'; elasticity 9-value B)
 int64_t hex_pa_doubles(int kind, int64_t ncells);
-cudaError_t launch_hex_pa_setup(int kind, const int4* cells, const double4* xyz, double* pa, int64_t ncells,
-                                cudaStream_t s, int sm_count);
-cudaError_t launch_hex_pa_apply(int kind, int bc, const int4* cells, const double* pa, const double2* lm,
+cudaError_t launch_hex_pa_setup(int kind, int quad, const int4* cells, const double4* xyz, double* pa,
+                                int64_t ncells, cudaStream_t s, int sm_count);
+cudaError_t launch_hex_pa_apply(int kind, int bc, int quad, const int4* cells, const double* pa, const double2* lm,
                                 const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
                                 Reduce red, cudaStream_t s, int sm_count);
 // y = x on the constrained nodes; mode 1: sc->pq += sum x_b^2

@@ -34,7 +34,11 @@ __device__ __forceinline__ Face face_fwd(double u00, double u10, double u01, dou
 }
 }  // namespace
 
-template <bool TM, int MODE, int TY, int S>
+// GLL: 2-point Gauss-Lobatto quadrature (BP6-style, reading R1): the quadrature
+// moment w = <xi^2> is 1/3 under Gauss and 1 under Gauss-Lobatto.  Modal weights in terms of w:
+// linear modes 1; bilinear modes mu 3w, lambda w (the "Seta" groups) and mu w (the T group);
+// trilinear modes (4 mu + lambda) w^2.
+template <bool TM, int MODE, int TY, int S, bool GLL>
 __global__ void __launch_bounds__(32 * (TY + 1), 1)
     elastic_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
@@ -178,15 +182,17 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
       const double gux = fma(M2, ux, LS0), gvy = fma(M2, vy, LS0), gwz = fma(M2, wz, LS0);
       const double tuv = M0 * (uy + vx), tuw = M0 * (uz + wx), tvw = M0 * (vz + wy);
       const double guy = tuv, gvx = tuv, guz = tuw, gwx = tuw, gvz = tvw, gwy = tvw;
-      const double L1 = L0 * (1.0 / 3.0), M1 = M0 * (1.0 / 3.0);
+      const double L1 = GLL ? L0 : L0 * (1.0 / 3.0), M1 = GLL ? M0 : M0 * (1.0 / 3.0);
       const double Sxi = vxy + wxz, Seta = uxy + wyz, Szeta = uxz + vyz;
       const double LSxi = L1 * Sxi, LSeta = L1 * Seta, LSzeta = L1 * Szeta;
-      const double guxy = fma(M0, uxy, LSeta), gwyz = fma(M0, wyz, LSeta);
-      const double gvxy = fma(M0, vxy, LSxi), gwxz = fma(M0, wxz, LSxi);
-      const double guxz = fma(M0, uxz, LSzeta), gvyz = fma(M0, vyz, LSzeta);
+      // mu weight of these bilinear modes: 3 <xi^2> (1 under Gauss, 3 under Gauss-Lobatto)
+      const double MB = GLL ? 3.0 * M0 : M0;
+      const double guxy = fma(MB, uxy, LSeta), gwyz = fma(MB, wyz, LSeta);
+      const double gvxy = fma(MB, vxy, LSxi), gwxz = fma(MB, wxz, LSxi);
+      const double guxz = fma(MB, uxz, LSzeta), gvyz = fma(MB, vyz, LSzeta);
       const double T = uyz + vxz + wxy;
       const double guyz = M1 * (T + uyz), gvxz = M1 * (T + vxz), gwxy = M1 * (T + wxy);
-      const double K3 = fma(4.0, M0, L0) * (1.0 / 9.0);
+      const double K3 = GLL ? fma(4.0, M0, L0) : fma(4.0, M0, L0) * (1.0 / 9.0);
       const double guxyz = K3 * uxyz, gvxyz = K3 * vxyz, gwxyz = K3 * wxyz;
 
       // inverse z: face mode f at bottom = g_f - g_fz, top = g_f + g_fz (g_1 = 0);
@@ -287,13 +293,16 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   using Ring2 = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX, (TM ? 2 : 1)>;
   const size_t ring_bytes = mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META;
   const size_t smem = ring_bytes + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t);
-  auto kern = mode == 2 ? elastic_kernel<TM, (TM ? 2 : 1), TY, S>
-                        : (mode ? elastic_kernel<TM, 1, TY, S> : elastic_kernel<TM, 0, TY, S>);
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[mode]) {
+  const bool gll = maps.quad == 1;
+  auto kern = gll ? (mode == 2 ? elastic_kernel<TM, (TM ? 2 : 1), TY, S, true>
+                               : (mode ? elastic_kernel<TM, 1, TY, S, true> : elastic_kernel<TM, 0, TY, S, true>))
+                  : (mode == 2 ? elastic_kernel<TM, (TM ? 2 : 1), TY, S, false>
+                               : (mode ? elastic_kernel<TM, 1, TY, S, false> : elastic_kernel<TM, 0, TY, S, false>));
+  static bool attr_set[6] = {false, false, false, false, false, false};
+  if (!attr_set[mode + 3 * gll]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set[mode] = true;
+    attr_set[mode + 3 * gll] = true;
   }
   const int64_t xt = (g.nx + 1 + (TX - 1) - 1) / (TX - 1);
   const int64_t yt = (g.ny + 1 + (TY - 1) - 1) / (TY - 1);

@@ -48,8 +48,11 @@ __device__ __forceinline__ Modal hadamard(const double v[8]) {
 }
 
 // pre-scale the bilinear / trilinear coefficients by g, g^2 (Gauss point coordinates)
+// (GLL: the 2-point Gauss-Lobatto points are the nodes, g = 1; reading R1)
+template <bool GLL>
 __device__ __forceinline__ void prescale(Modal& m) {
-  m.xy *= kG; m.xz *= kG; m.yz *= kG; m.xyz *= kG2;
+  constexpr double g = GLL ? 1.0 : kG, g2 = GLL ? 1.0 : kG2;
+  m.xy *= g; m.xz *= g; m.yz *= g; m.xyz *= g2;
 }
 
 // reference gradient (x 8) of a field at the Gauss point with signs (sx, sy, sz)
@@ -152,7 +155,7 @@ __device__ __forceinline__ void gauss_point(const Modal& mx, const Modal& my, co
 
 constexpr int kHexThreads = 128;
 
-template <int KIND, int MODE>
+template <int KIND, int MODE, bool GLL>
 __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
     hex_apply_kernel(const int4* __restrict__ cells, const double4* __restrict__ xyz,
                      const double2* __restrict__ lm, const double* __restrict__ u,
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
         X[a] = p.x; Y[a] = p.y; Z[a] = p.z;
       }
       mx = hadamard(X); my = hadamard(Y); mz = hadamard(Z);
-      prescale(mx); prescale(my); prescale(mz);
+      prescale<GLL>(mx); prescale<GLL>(my); prescale<GLL>(mz);
     }
     Modal mu[C], acc[C];
 #pragma unroll
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
 #pragma unroll
       for (int a = 0; a < 8; ++a) U[a] = fix[a] ? 0.0 : u[(int64_t)C * id[a] + c];
       mu[c] = hadamard(U);
-      prescale(mu[c]);
+      prescale<GLL>(mu[c]);
       acc[c] = Modal{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     }
     double L = 0.0, M = 0.0;
@@ -215,7 +218,8 @@ __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
     for (int c = 0; c < C; ++c) {
       Modal& m = acc[c];
       m.x *= kInv512; m.y *= kInv512; m.z *= kInv512;
-      m.xy *= kG * kInv512; m.xz *= kG * kInv512; m.yz *= kG * kInv512; m.xyz *= kG2 * kInv512;
+      constexpr double g = GLL ? 1.0 : kG, g2 = GLL ? 1.0 : kG2;
+      m.xy *= g * kInv512; m.xz *= g * kInv512; m.yz *= g * kInv512; m.xyz *= g2 * kInv512;
       double v[8];
       inverse(m, v);
 #pragma unroll
@@ -272,11 +276,12 @@ __global__ void __launch_bounds__(256) hex_check_kernel(const int4* __restrict__
       atomicAdd(&bad[0], 1ull);
       continue;
     }
-    Modal mx = hadamard(X), my = hadamard(Y), mz = hadamard(Z);
-    prescale(mx); prescale(my); prescale(mz);
+    const Modal ux = hadamard(X), uy = hadamard(Y), uz = hadamard(Z);
     bool pos = true;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 16; ++q) {  // the 8 Gauss points, then the 8 Gauss-Lobatto points (nodes)
+      Modal mx = ux, my = uy, mz = uz;
+      if (q < 8) { prescale<false>(mx); prescale<false>(my); prescale<false>(mz); }
       const double sx = (q & 1) ? 1.0 : -1.0, sy = (q & 2) ? 1.0 : -1.0, sz = (q & 4) ? 1.0 : -1.0;
       double J[3][3];
       const Modal* f[3] = {&mx, &my, &mz};
@@ -323,7 +328,7 @@ __global__ void hex_pack_cells_kernel(const int32_t* __restrict__ vtk, const uin
 //   elasticity: B  = cof(J') / sqrt(det J')         (9 values; the paper stores 21 with the
 //               material folded in -- here lambda, mu stay per cell, 2 values)
 // so that P' = G' D' (Laplace) or P' = sigma(G' B^T) B (elasticity) equal the matrix-free P'.
-template <int KIND>
+template <int KIND, bool GLL>
 __global__ void __launch_bounds__(256) hex_pa_setup_kernel(const int4* __restrict__ cells,
                                                            const double4* __restrict__ xyz,
                                                            double* __restrict__ pa, int64_t ncells) {
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(256) hex_pa_setup_kernel(const int4* __restric
       X[a] = p.x; Y[a] = p.y; Z[a] = p.z;
     }
     Modal mx = hadamard(X), my = hadamard(Y), mz = hadamard(Z);
-    prescale(mx); prescale(my); prescale(mz);
+    prescale<GLL>(mx); prescale<GLL>(my); prescale<GLL>(mz);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const double sx = (q & 1) ? 1.0 : -1.0, sy = (q & 2) ? 1.0 : -1.0, sz = (q & 4) ? 1.0 : -1.0;
@@ -428,7 +433,7 @@ __device__ __forceinline__ void pa_point(const double* __restrict__ g, int64_t n
   }
 }
 
-template <int KIND, int MODE>
+template <int KIND, int MODE, bool GLL>
 __global__ void __launch_bounds__(128, (KIND == 0) ? 4 : 2)
     hex_pa_apply_kernel(const int4* __restrict__ cells, const double* __restrict__ pa,
                         const double2* __restrict__ lm, const double* __restrict__ u,
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(128, (KIND == 0) ? 4 : 2)
 #pragma unroll
       for (int a = 0; a < 8; ++a) U[a] = fix[a] ? 0.0 : u[(int64_t)C * id[a] + c];
       mu[c] = hadamard(U);
-      prescale(mu[c]);
+      prescale<GLL>(mu[c]);
       acc[c] = Modal{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     }
     double L = 0.0, M = 0.0;
@@ -480,7 +485,8 @@ __global__ void __launch_bounds__(128, (KIND == 0) ? 4 : 2)
     for (int c = 0; c < C; ++c) {
       Modal& m = acc[c];
       m.x *= kInv512; m.y *= kInv512; m.z *= kInv512;
-      m.xy *= kG * kInv512; m.xz *= kG * kInv512; m.yz *= kG * kInv512; m.xyz *= kG2 * kInv512;
+      constexpr double g = GLL ? 1.0 : kG, g2 = GLL ? 1.0 : kG2;
+      m.xy *= g * kInv512; m.xz *= g * kInv512; m.yz *= g * kInv512; m.xyz *= g2 * kInv512;
       double v[8];
       inverse(m, v);
 #pragma unroll
@@ -501,16 +507,18 @@ int grid_for(int64_t n, int threads, int sm_count, int per_sm) {
 
 }  // namespace
 
-cudaError_t launch_hex_apply(int kind, int bc, const int4* cells, const double4* xyz, const double2* lm,
+cudaError_t launch_hex_apply(int kind, int bc, int quad, const int4* cells, const double4* xyz, const double2* lm,
                              const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
                              Reduce red, cudaStream_t s, int sm_count) {
   if (ncells <= 0) return cudaSuccess;
   const int grid = grid_for(ncells, kHexThreads, sm_count, 8);
   if (mode >= 1 && grid > red.capacity) return cudaErrorInvalidConfiguration;
-#define HEX_LAUNCH(K, M) hex_apply_kernel<K, M><<<grid, kHexThreads, 0, s>>>(cells, xyz, lm, x, y, ncells, bc, sc, red)
-  if (kind == 0) { if (mode) HEX_LAUNCH(0, 1); else HEX_LAUNCH(0, 0); }
-  else if (kind == 1) { if (mode) HEX_LAUNCH(1, 1); else HEX_LAUNCH(1, 0); }
-  else { if (mode) HEX_LAUNCH(2, 1); else HEX_LAUNCH(2, 0); }
+#define HEX_LAUNCH(K, M, G) hex_apply_kernel<K, M, G><<<grid, kHexThreads, 0, s>>>(cells, xyz, lm, x, y, ncells, bc, sc, red)
+#define HEX_LAUNCH2(K, M) { if (quad == 1) HEX_LAUNCH(K, M, true); else HEX_LAUNCH(K, M, false); }
+  if (kind == 0) { if (mode) HEX_LAUNCH2(0, 1) else HEX_LAUNCH2(0, 0) }
+  else if (kind == 1) { if (mode) HEX_LAUNCH2(1, 1) else HEX_LAUNCH2(1, 0) }
+  else { if (mode) HEX_LAUNCH2(2, 1) else HEX_LAUNCH2(2, 0) }
+#undef HEX_LAUNCH2
 #undef HEX_LAUNCH
   add_launches(1);
   return cudaGetLastError();
@@ -518,25 +526,32 @@ cudaError_t launch_hex_apply(int kind, int bc, const int4* cells, const double4*
 
 int64_t hex_pa_doubles(int kind, int64_t ncells) { return (int64_t)8 * ((kind == 2) ? 9 : 6) * ncells; }
 
-cudaError_t launch_hex_pa_setup(int kind, const int4* cells, const double4* xyz, double* pa, int64_t ncells,
-                                cudaStream_t s, int sm_count) {
+cudaError_t launch_hex_pa_setup(int kind, int quad, const int4* cells, const double4* xyz, double* pa,
+                                int64_t ncells, cudaStream_t s, int sm_count) {
   const int grid = grid_for(ncells, 256, sm_count, 8);
-  if (kind == 2) hex_pa_setup_kernel<2><<<grid, 256, 0, s>>>(cells, xyz, pa, ncells);
-  else hex_pa_setup_kernel<0><<<grid, 256, 0, s>>>(cells, xyz, pa, ncells);
+  if (kind == 2) {
+    if (quad == 1) hex_pa_setup_kernel<2, true><<<grid, 256, 0, s>>>(cells, xyz, pa, ncells);
+    else hex_pa_setup_kernel<2, false><<<grid, 256, 0, s>>>(cells, xyz, pa, ncells);
+  } else {
+    if (quad == 1) hex_pa_setup_kernel<0, true><<<grid, 256, 0, s>>>(cells, xyz, pa, ncells);
+    else hex_pa_setup_kernel<0, false><<<grid, 256, 0, s>>>(cells, xyz, pa, ncells);
+  }
   add_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_hex_pa_apply(int kind, int bc, const int4* cells, const double* pa, const double2* lm,
+cudaError_t launch_hex_pa_apply(int kind, int bc, int quad, const int4* cells, const double* pa, const double2* lm,
                                 const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
                                 Reduce red, cudaStream_t s, int sm_count) {
   if (ncells <= 0) return cudaSuccess;
   const int grid = grid_for(ncells, 128, sm_count, 8);
   if (mode >= 1 && grid > red.capacity) return cudaErrorInvalidConfiguration;
-#define PA_LAUNCH(K, M) hex_pa_apply_kernel<K, M><<<grid, 128, 0, s>>>(cells, pa, lm, x, y, ncells, bc, sc, red)
-  if (kind == 0) { if (mode) PA_LAUNCH(0, 1); else PA_LAUNCH(0, 0); }
-  else if (kind == 1) { if (mode) PA_LAUNCH(1, 1); else PA_LAUNCH(1, 0); }
-  else { if (mode) PA_LAUNCH(2, 1); else PA_LAUNCH(2, 0); }
+#define PA_LAUNCH(K, M, G) hex_pa_apply_kernel<K, M, G><<<grid, 128, 0, s>>>(cells, pa, lm, x, y, ncells, bc, sc, red)
+#define PA_LAUNCH2(K, M) { if (quad == 1) PA_LAUNCH(K, M, true); else PA_LAUNCH(K, M, false); }
+  if (kind == 0) { if (mode) PA_LAUNCH2(0, 1) else PA_LAUNCH2(0, 0) }
+  else if (kind == 1) { if (mode) PA_LAUNCH2(1, 1) else PA_LAUNCH2(1, 0) }
+  else { if (mode) PA_LAUNCH2(2, 1) else PA_LAUNCH2(2, 0) }
+#undef PA_LAUNCH2
 #undef PA_LAUNCH
   add_launches(1);
   return cudaGetLastError();

@@ -18,7 +18,9 @@
 
 namespace fem {
 
-template <bool TM, int MODE, int C, int TX, int TY, int R, int S>
+// GLL: 2-point Gauss-Lobatto quadrature (BP5/BP6, reading R1): the 1-D mass is
+// lumped, M~ = [0, 3m, 0] instead of [1, 2m, 1]; K~ is exact under both rules.
+template <bool TM, int MODE, int C, int TX, int TY, int R, int S, bool GLL>
 __global__ void __launch_bounds__(TX*(TY + 1), 2)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
             xp = fma(beta, row2[2 * C + c], xp);
           }
           const double sn = xm + xp;
-          a[rr][c] = fma(2.0 * mx, x0, sn);
+          a[rr][c] = GLL ? (3.0 * mx) * x0 : fma(2.0 * mx, x0, sn);
           b[rr][c] = fma(mx, x0, -sn);
           if (rr >= 1 && rr <= R) xcw[1][rr - 1][c] = x0;
         }
@@ -126,8 +128,13 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
         for (int c = 0; c < C; ++c) {
           const double an = a[r][c] + a[r + 2][c];
           const double bn = b[r][c] + b[r + 2][c];
-          c1w[2][r][c] = fma(2.0 * my[r], a[r + 1][c], an);
-          c2w[2][r][c] = fma(2.0 * my[r], b[r + 1][c], bn) + fma(my[r], a[r + 1][c], -an);
+          if (GLL) {
+            c1w[2][r][c] = (3.0 * my[r]) * a[r + 1][c];
+            c2w[2][r][c] = fma(3.0 * my[r], b[r + 1][c], fma(my[r], a[r + 1][c], -an));
+          } else {
+            c1w[2][r][c] = fma(2.0 * my[r], a[r + 1][c], an);
+            c2w[2][r][c] = fma(2.0 * my[r], b[r + 1][c], bn) + fma(my[r], a[r + 1][c], -an);
+          }
         }
       // z-direction: output plane q = p-1
       const int64_t q = p - 1;
@@ -150,7 +157,10 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
               v = xv;
             } else {
               const double nb = (c2w[0][r][c] - c1w[0][r][c]) + (c2w[2][r][c] - c1w[2][r][c]);
-              v = h36 * fma(2.0 * mz, c2w[1][r][c], fma(mz, c1w[1][r][c], nb));
+              if (GLL)
+                v = h36 * fma(3.0 * mz, c2w[1][r][c], fma(mz, c1w[1][r][c], -(c1w[0][r][c] + c1w[2][r][c])));
+              else
+                v = h36 * fma(2.0 * mz, c2w[1][r][c], fma(mz, c1w[1][r][c], nb));
             }
             yq[off_y[r] + c] = v;
             if (mode == 2) pq_new[off_x[r] + c] = xv;
@@ -179,13 +189,18 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   using Ring1 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, 1>;
   using Ring2 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, (TM ? 2 : 1)>;
   const size_t smem = (mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META);
-  auto kern = mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S>
-                        : (mode ? laplace_kernel<TM, 1, C, TX, TY, R, S> : laplace_kernel<TM, 0, C, TX, TY, R, S>);
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[mode]) {
+  const bool gll = maps.quad == 1;
+  auto kern = gll ? (mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S, true>
+                               : (mode ? laplace_kernel<TM, 1, C, TX, TY, R, S, true>
+                                       : laplace_kernel<TM, 0, C, TX, TY, R, S, true>))
+                  : (mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S, false>
+                               : (mode ? laplace_kernel<TM, 1, C, TX, TY, R, S, false>
+                                       : laplace_kernel<TM, 0, C, TX, TY, R, S, false>));
+  static bool attr_set[6] = {false, false, false, false, false, false};
+  if (!attr_set[mode + 3 * gll]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set[mode] = true;
+    attr_set[mode + 3 * gll] = true;
   }
   const int64_t xt = (g.nx + 1 + TX - 1) / TX;
   const int64_t yt = (g.ny + 1 + TY * R - 1) / (TY * R);
