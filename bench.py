@@ -264,6 +264,8 @@ def run_native(args, cfg):
     op = fem.Operator(mesh, kind, "dirichlet")
     if hexmesh and args.pa:  # partial assembly: stored Gauss-point geometry (Table 3)
         op.set_option("partial_assembly", 1)
+    if args.gll:  # Gauss-Lobatto quadrature: the BP5 / BP6 operators (reading R1)
+        op.set_option("quadrature", 1)
     ndof_global = op.n_global * (ws if hexmesh else 1)
     k0, k1 = (0, nz + 1) if hexmesh else (mesh.plane_begin, mesh.plane_end)
     plane = (nx + 1) * (ny + 1)
@@ -489,6 +491,8 @@ def csr_compare(fem, torch, kind, args):
     try:
         mesh = fem.Mesh(n, n, n, 1.0 / n)
         op = fem.Operator(mesh, kind, "dirichlet")
+        if args.gll:
+            op.set_option("quadrature", 1)
         if kind == "elastic":
             g = I.rng(I.SEED_BASE + 55)
             lam, mu = I.materials(g, n, n, n)
@@ -528,6 +532,8 @@ def csr_compare(fem, torch, kind, args):
                 m = 176
                 mesh2 = fem.Mesh(m, m, m, 1.0 / m)
                 op2 = fem.Operator(mesh2, kind, "dirichlet")
+                if args.gll:
+                    op2.set_option("quadrature", 1)
                 if kind == "elastic":
                     g2 = I.rng(I.SEED_BASE + 56)
                     l2, m2 = I.materials(g2, m, m, m)
@@ -575,6 +581,8 @@ def main():
     ap.add_argument("--csr-n", type=int, default=0)
     ap.add_argument("--e2e-iters", type=int, default=100)
     ap.add_argument("--n", type=int, default=0, help="override cells per direction (debug)")
+    ap.add_argument("--gll", action="store_true",
+                    help="2x2x2 Gauss-Lobatto quadrature (the CEED BP5/BP6 operators) instead of Gauss")
     ap.add_argument("--pa", action="store_true",
                     help="general-hex configs (6/7): partial assembly instead of matrix-free")
     args = ap.parse_args()
@@ -586,6 +594,8 @@ def main():
         cfg["name"] += f"_n{args.n}"
     if args.pa and cfg.get("mesh") == "hex":
         cfg["name"] += "_pa"
+    if args.gll:
+        cfg["name"] += "_gll"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
