@@ -144,6 +144,13 @@ int fem_apply(fem_op_t op, const double* x, double* y, void* stream);
  * values each; NULL where the plane is outside the box).  x, y device, owned planes. */
 int fem_apply_ghost(fem_op_t op, const double* x, const double* ghost_lo, const double* ghost_hi,
                     double* y, void* stream);
+/* As fem_apply_ghost, but through the CG-internal padded layout and its TMA tensor maps (the
+ * path every fused CG iteration runs, including the material tensor at the slab offset), for
+ * single-process slab tests of that path: x and the ghost planes are packed into the library's
+ * padded x, the apply writes the padded q, which is unpacked into y.  Interrupts an active
+ * fem_cg_begin/iterate sequence (FEM_ESTATE on the next fem_cg_iterate). */
+int fem_apply_ghost_padded(fem_op_t op, const double* x, const double* ghost_lo, const double* ghost_hi,
+                           double* y, void* stream);
 /* Global sum_i a_i b_i over owned DOFs (Table 4 "ddot").  Deterministic for a
  * fixed rank count.  Result written to *result (host).  Collective. */
 int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void* stream);

@@ -850,6 +850,35 @@ int fem_apply_ghost(fem_op_t op, const double* x, const double* glo, const doubl
   return launch_apply(op, src, dense_out(op, y), nullptr, 0, (cudaStream_t)stream);
 }
 
+int fem_apply_ghost_padded(fem_op_t op, const double* x, const double* glo, const double* ghi, double* y,
+                           void* stream) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  FEM_TRY(check_vec(x, "x"));
+  FEM_TRY(check_vec(y, "y"));
+  if ((const void*)x == (const void*)y) return fail(FEM_EINVAL, "x and y alias");
+  if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
+  if (op->mesh->hex) return fail(FEM_EUNSUPPORTED, "fem_apply_ghost_padded: general hex meshes are single-GPU");
+  const Grid& g = op->mesh->g;
+  if ((g.k0 > 0 && !glo) || (g.k1 <= g.nz && !ghi))
+    return fail(FEM_EINVAL, "a ghost plane inside the box is NULL");
+  if (!is_device_ptr(x) || !is_device_ptr(y) || (glo && !is_device_ptr(glo)) || (ghi && !is_device_ptr(ghi)))
+    return fail(FEM_EINVAL, "fem_apply_ghost_padded needs device pointers");
+  FEM_TRY(set_device(op->mesh->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  op->cg_active = false;  // x_pl / q_pl are the CG workspace
+  FEM_TRY(pack(op, x, op->x_pl, 1, s));
+  const fem_mesh_s* m = op->mesh;
+  auto ghost = [&](const double* src, double* dst) -> int {
+    cudaError_t e = launch_pack(src, dst, op->pl_rp, op->pl_pp, 1, g.nx + 1, g.ny + 1, op->comps, 1, s, m->sm_count);
+    if (e != cudaSuccess) return fail(FEM_ECUDA, "ghost pack: %s", cudaGetErrorString(e));
+    return FEM_OK;
+  };
+  if (m->rank > 0 && glo) FEM_TRY(ghost(glo, op->x_pl + op->pl_lead));
+  if (m->rank < m->nranks - 1 && ghi) FEM_TRY(ghost(ghi, op->x_pl + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp));
+  FEM_TRY(launch_apply(op, pl_src(op, op->x_pl), pl_out(op, op->q_pl), op->tm_ok ? &op->tm_x : nullptr, 0, s));
+  return pack(op, y, op->q_pl, 0, s);
+}
+
 int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
   if (!op) return fail(FEM_EINVAL, "op is NULL");
   FEM_TRY(need_comm(op));

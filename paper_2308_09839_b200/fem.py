@@ -43,7 +43,7 @@ class CgInfo(ctypes.Structure):
 # every symbol include/fem.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fem_last_error", "fem_version", "fem_launch_count", "fem_get_unique_id", "fem_comm_create",
-    "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy",
+    "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_apply_ghost_padded", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy",
     "fem_mesh_create_hex", "fem_mesh_info_hex", "fem_op_create",
     "fem_op_ndof", "fem_set_material", "fem_apply", "fem_dot", "fem_cg_solve", "fem_cg_begin",
     "fem_cg_iterate", "fem_cg_end", "fem_set_option", "fem_get_option", "fem_apply_time", "fem_op_destroy",
@@ -77,6 +77,7 @@ def load(build_if_missing: bool = True):
         "fem_comm_destroy": ([vp], None),
         "fem_partition": ([i64, i32, i32, P(i64), P(i64)], ctypes.c_int),
         "fem_apply_ghost": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "fem_apply_ghost_padded": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "fem_mesh_create": ([i64, i64, i64, dbl, vp, P(vp)], ctypes.c_int),
         "fem_mesh_local": ([vp, P(i64), P(i64), P(i64)], ctypes.c_int),
         "fem_mesh_destroy": ([vp], None),
@@ -269,6 +270,15 @@ class Operator:
             y = torch.empty_like(x)
         _check(load().fem_apply_ghost(self.h, _ptr(x), _ptr(ghost_lo), _ptr(ghost_hi), _ptr(y),
                                       _stream(stream)))
+        return y
+
+    def apply_ghost_padded(self, x, ghost_lo, ghost_hi, y=None, stream=None):
+        """As apply_ghost, through the CG-internal padded layout and its TMA tensor maps."""
+        if y is None:
+            import torch
+            y = torch.empty_like(x)
+        _check(load().fem_apply_ghost_padded(self.h, _ptr(x), _ptr(ghost_lo), _ptr(ghost_hi), _ptr(y),
+                                             _stream(stream)))
         return y
 
     def dot(self, a, b, stream=None) -> float:

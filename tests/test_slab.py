@@ -120,7 +120,7 @@ def test_loopback_slabs_bitwise(kind, P):
         ref_op.set_material(lam, mu)
     ref = ref_op.apply(x)
     plane = (nx + 1) * (ny + 1) * c
-    outs = []
+    outs, outs_tma = [], []
     for r in range(P):
         comm = fem.Comm(P, r)  # virtual: partition only
         mesh = fem.Mesh(nx, ny, nz, h, comm)
@@ -134,8 +134,13 @@ def test_loopback_slabs_bitwise(kind, P):
         lo = x[(k0 - 1) * plane:k0 * plane].contiguous() if k0 > 0 else None
         hi = x[k1 * plane:(k1 + 1) * plane].contiguous() if k1 <= nz else None
         outs.append(op.apply_ghost(xl, lo, hi))
+        outs_tma.append(op.apply_ghost_padded(xl, lo, hi))  # the CG kernels' TMA path
         with pytest.raises(fem.FemError) as e:
             op.apply(xl)  # a virtual communicator cannot exchange
         assert e.value.status == fem.FEM_EUNSUPPORTED
     y = torch.cat(outs)
     assert torch.equal(y, ref)
+    # TMA (padded-layout) path: bitwise equal to its own P = 1 result across slabs
+    ref_tma = ref_op.apply_ghost_padded(x, None, None)
+    assert torch.equal(torch.cat(outs_tma), ref_tma)
+    assert float((ref_tma - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
