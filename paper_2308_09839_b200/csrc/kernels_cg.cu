@@ -106,13 +106,44 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __
   }
   const double alpha = sc->rr / pq;
   double acc = 0.0;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+  // 16-B vector accesses (the four vectors share one layout, hence one alignment); a leading
+  // unaligned element and a trailing odd element are handled by thread 0 / the last thread
+  const int64_t head = (reinterpret_cast<uintptr_t>(r) & 15) ? 1 : 0;
+  auto one = [&](int64_t i) {
     x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
     acc = fma(ri, ri, acc);
+  };
+  if (head && gtid == 0 && n > 0) one(0);
+  const int64_t n2 = (n - head) / 2;
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(x + head);
+  double2* __restrict__ r2 = reinterpret_cast<double2*>(r + head);
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p + head);
+  const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q + head);
+  int64_t i = gtid;
+  for (; i + stride < n2; i += 2 * stride) {  // two independent 16-B groups in flight per thread
+    const double2 pa = p2[i], pb = p2[i + stride], xa = x2[i], xb = x2[i + stride];
+    const double2 qa = q2[i], qb = q2[i + stride], ra = r2[i], rb = r2[i + stride];
+    x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
+    x2[i + stride] = make_double2(fma(alpha, pb.x, xb.x), fma(alpha, pb.y, xb.y));
+    const double2 na = make_double2(fma(-alpha, qa.x, ra.x), fma(-alpha, qa.y, ra.y));
+    const double2 nb = make_double2(fma(-alpha, qb.x, rb.x), fma(-alpha, qb.y, rb.y));
+    r2[i] = na;
+    r2[i + stride] = nb;
+    acc = fma(na.x, na.x, acc); acc = fma(na.y, na.y, acc);
+    acc = fma(nb.x, nb.x, acc); acc = fma(nb.y, nb.y, acc);
   }
+  for (; i < n2; i += stride) {
+    const double2 pa = p2[i], xa = x2[i], qa = q2[i], ra = r2[i];
+    x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
+    const double2 na = make_double2(fma(-alpha, qa.x, ra.x), fma(-alpha, qa.y, ra.y));
+    r2[i] = na;
+    acc = fma(na.x, na.x, acc); acc = fma(na.y, na.y, acc);
+  }
+  if (((n - head) & 1) && gtid == stride - 1) one(n - 1);
   double bs = block_sum(acc, sh);
   double tot;
   if (last_block_reduce(bs, red, sh, &tot)) {
