@@ -74,7 +74,13 @@ struct Reduce {
 constexpr int kMaxCtas = 1 << 16;
 
 // Tile shapes of the apply kernels (kernel templates and host tensor-map boxes must agree).
-constexpr int kLapTX = 32, kLapTY = 8, kLapR1 = 2, kLapR3 = 1;  // Laplace: C=1 / C=3 rows per thread
+#ifndef FEM_LAP_TY
+#define FEM_LAP_TY 7
+#endif
+#ifndef FEM_LAP_R1
+#define FEM_LAP_R1 3
+#endif
+constexpr int kLapTX = 32, kLapTY = FEM_LAP_TY, kLapR1 = FEM_LAP_R1, kLapR3 = 1;  // Laplace: C=1 / C=3 rows per thread
 #ifndef FEM_EL_TY
 #define FEM_EL_TY 15
 #endif
