@@ -39,7 +39,7 @@ __device__ __forceinline__ Face face_fwd(double u00, double u10, double u01, dou
 // linear modes 1; bilinear modes mu 3w, lambda w (the "Seta" groups) and mu w (the T group);
 // trilinear modes (4 mu + lambda) w^2.
 template <bool TM, int MODE, int TY, int S, bool GLL>
-__global__ void __launch_bounds__(32 * (TY + 1), 1)
+__global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
     elastic_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                    const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
@@ -307,8 +307,11 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   const int64_t xt = (g.nx + 1 + (TX - 1) - 1) / (TX - 1);
   const int64_t yt = (g.ny + 1 + (TY - 1) - 1) / (TY - 1);
   const int64_t nplanes = g.k1 - g.k0;
-  int64_t zc = (4LL * sm_count + xt * yt - 1) / (xt * yt);
-  zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / 8));
+  int64_t zc = ((kElTY <= 7 ? 8LL : 4LL) * sm_count + xt * yt - 1) / (xt * yt);
+  // chunks of >= 8 planes amortise the pipeline fill; a mesh too small to fill the GPU that
+  // way takes chunks down to 2 planes (latency: the z-march is the serial part of a CTA)
+  const int64_t minchunk = (xt * yt * (nplanes / 8) < sm_count) ? 2 : 8;
+  zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / minchunk));
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
@@ -328,7 +331,7 @@ cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMap
   if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
   if (maps.u) {
     if (mode == 2) return launch_cfg<true, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
-    return launch_cfg<true, kElTY, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    return launch_cfg<true, kElTY, (kElTY <= 7 ? 4 : 8)>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
   }
   return launch_cfg<false, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
 }

@@ -207,7 +207,10 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   const int64_t nplanes = g.k1 - g.k0;
   // z-chunks: about 4 resident waves of CTAs (2 per SM), chunks of >= 16 planes
   int64_t zc = (8LL * sm_count + xt * yt - 1) / (xt * yt);
-  zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / 16));
+  // chunks of >= 16 planes amortise the pipeline fill; a mesh too small to fill the GPU that
+  // way takes chunks down to 2 planes (latency: the z-march is the serial part of a CTA)
+  const int64_t minchunk = (xt * yt * (nplanes / 16) < sm_count) ? 2 : 16;
+  zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / minchunk));
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
