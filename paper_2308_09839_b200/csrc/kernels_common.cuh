@@ -130,8 +130,10 @@ struct WorkGrid {
 };
 
 // Host: choose the z-chunking so that the items (xt*yt*zc) spread evenly over `slots` resident
-// CTAs (minimise the idle fraction of the last round), with chunks of >= min_chunk planes.
-inline WorkGrid make_workgrid(int xt, int yt, int64_t nplanes, int64_t slots, int64_t min_chunk) {
+// CTAs (minimise the idle fraction of the last round), with chunks of >= min_chunk planes and at
+// least min_rounds rounds of CTAs when the mesh allows it.
+inline WorkGrid make_workgrid(int xt, int yt, int64_t nplanes, int64_t slots, int64_t min_chunk,
+                              int64_t min_rounds = 1) {
   WorkGrid best{xt, yt, 1, nplanes};
   double best_eff = -1.0;
   const int64_t tiles = (int64_t)xt * yt;
@@ -141,6 +143,7 @@ inline WorkGrid make_workgrid(int xt, int yt, int64_t nplanes, int64_t slots, in
     const int64_t z = (nplanes + kchunk - 1) / kchunk;
     const int64_t items = tiles * z;
     const int64_t rounds = (items + slots - 1) / slots;
+    if (rounds < min_rounds && zc < zmax) continue;  // keep enough CTAs to balance the SMs
     // useful work / (rounds * slots * chunk length incl. the 2-plane halo)
     const double eff = (double)nplanes * tiles / ((double)rounds * slots * (kchunk + 2));
     if (eff > best_eff + 1e-9) {

@@ -314,6 +314,11 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / minchunk));
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
+  if (minchunk > 2) {  // wave-quantisation aware chunking (1 resident CTAs per SM)
+    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, 1LL * sm_count, minchunk, 4);
+    zc = w.zc;
+    kchunk = w.kchunk;
+  }
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
   CUtensorMap um, um2;
