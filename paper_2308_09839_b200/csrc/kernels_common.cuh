@@ -121,8 +121,7 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
 
-// Persistent schedule: work item w = (tile x, tile y, z-chunk), CTAs take w = blockIdx.x,
-// blockIdx.x + gridDim.x, ... (consecutive items -> neighbouring tiles run together, L2 halo reuse).
+// Launch geometry of an apply: xt x yt tiles, zc z-chunks of kchunk node planes each.
 struct WorkGrid {
   int xt, yt, zc;      // tiles in x, y; z-chunks
   int64_t kchunk;      // node planes per z-chunk
