@@ -266,6 +266,8 @@ def run_native(args, cfg):
         op.set_option("partial_assembly", 1)
     if args.gll:  # Gauss-Lobatto quadrature: the BP5 / BP6 operators (reading R1)
         op.set_option("quadrature", 1)
+    if args.cgcg:  # Chronopoulos-Gear single-reduction CG (NEXT #1)
+        op.set_option("cg_variant", 1)
     ndof_global = op.n_global * (ws if hexmesh else 1)
     k0, k1 = (0, nz + 1) if hexmesh else (mesh.plane_begin, mesh.plane_end)
     plane = (nx + 1) * (ny + 1)
@@ -337,6 +339,9 @@ def run_native(args, cfg):
     hbm_peak, peak_src = measured_peaks()
     nloc_planes = k1 - k0
     fused = bool(op.get_option("fused_cg"))
+    cgcg = bool(op.get_option("cg_variant"))
+    if cgcg:  # apply reads r, writes w (16 B/DOF); update reads r,w,p,s,x writes p,s,x,r (72 B/DOF)
+        fused = False
     # algorithmic bytes of one rank's apply launch: owned planes (+ its cell layers)
     alg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) * nloc_planes / (nz + 1)
     achieved = alg_bytes / (apply_ms / 1e3) / 1e9
@@ -381,6 +386,7 @@ def run_native(args, cfg):
     extra["cg_bytes_per_dof_alg"] = cg_bytes / ndof_global
     extra["cg_iteration_gbs"] = cg_bytes / (ms / args.steps / 1e3) / 1e9
     extra["fused_cg"] = fused
+    extra["cg_variant"] = "chronopoulos-gear" if cgcg else "hestenes-stiefel"
     del xx, yy
 
     # ---- e2e: the public call a user makes, with pinned HOST buffers ----
@@ -435,7 +441,8 @@ def run_native(args, cfg):
             "roofline": ({"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": traffic,
                           "kernel": (f"{kind} fused CG apply (p = r + beta p_old, q = A p, p.q)" if fused
-                                     else f"{kind} apply (CG mode, fused p.Ap)"),
+                                     else (f"{kind} apply (single-reduction CG: w = A r, w.r, r.r)" if cgcg
+                                           else f"{kind} apply (CG mode, fused p.Ap)")),
                           "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                           "frac_of_8TBps_nominal": achieved / 8000.0} if not hexmesh else
                          {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -581,6 +588,8 @@ def main():
     ap.add_argument("--csr-n", type=int, default=0)
     ap.add_argument("--e2e-iters", type=int, default=100)
     ap.add_argument("--n", type=int, default=0, help="override cells per direction (debug)")
+    ap.add_argument("--cgcg", action="store_true",
+                    help="Chronopoulos-Gear single-reduction CG (one allreduce of 2 values per iteration)")
     ap.add_argument("--gll", action="store_true",
                     help="2x2x2 Gauss-Lobatto quadrature (the CEED BP5/BP6 operators) instead of Gauss")
     ap.add_argument("--pa", action="store_true",
@@ -596,6 +605,8 @@ def main():
         cfg["name"] += "_pa"
     if args.gll:
         cfg["name"] += "_gll"
+    if args.cgcg:
+        cfg["name"] += "_cgcg"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -124,6 +124,7 @@ struct fem_op_s {
   double* pa = nullptr;
   int pa_quad = -1;  // rule the stored geometry was computed for
   int quad = 0;      // 0: 2x2x2 Gauss-Legendre, 1: 2x2x2 Gauss-Lobatto (BP5/BP6; reading R1)
+  int cg_variant = 0;  // 0: fused Hestenes-Stiefel (Table 4), 1: Chronopoulos-Gear single reduction
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
 };
@@ -257,10 +258,10 @@ static int halo(fem_op_s* op, const double* owned, double* lo, double* hi, cudaS
   return halo_pitch(op, owned, lo, hi, op->plane_dofs, s);
 }
 
-static int allreduce1(fem_op_s* op, double* dev_scalar, cudaStream_t s) {
+static int allreduce1(fem_op_s* op, double* dev_scalar, cudaStream_t s, int count = 1) {
   fem_mesh_s* m = op->mesh;
   if (m->nranks == 1) return FEM_OK;
-  NCCL_TRY(ncclAllReduce(dev_scalar, dev_scalar, 1, ncclDouble, ncclSum, m->comm->nccl, s));
+  NCCL_TRY(ncclAllReduce(dev_scalar, dev_scalar, count, ncclDouble, ncclSum, m->comm->nccl, s));
   return FEM_OK;
 }
 
@@ -650,7 +651,7 @@ static int op_common_alloc(fem_op_s* op) {
   FEM_TRY(dalloc(&op->sc, 1));
   FEM_TRY(dalloc(&op->dot_dev, 1));
   FEM_TRY(dalloc(&op->bad, 1));
-  FEM_TRY(dalloc(&op->red.partials, kMaxCtas));
+  FEM_TRY(dalloc(&op->red.partials, 2 * kMaxCtas));  // (two sums: last_block_reduce2)
   FEM_TRY(dalloc(&op->red.ticket, 1));
   op->red.capacity = kMaxCtas;
   if (cudaMallocHost(&op->sc_host, sizeof(CgScalars)) != cudaSuccess ||
@@ -733,7 +734,7 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   OP_TRY(dalloc(&op->sc, 1));
   OP_TRY(dalloc(&op->dot_dev, 1));
   OP_TRY(dalloc(&op->bad, 1));
-  OP_TRY(dalloc(&op->red.partials, kMaxCtas));
+  OP_TRY(dalloc(&op->red.partials, 2 * kMaxCtas));
   OP_TRY(dalloc(&op->red.ticket, 1));
   op->red.capacity = kMaxCtas;
   if (cudaMallocHost(&op->sc_host, sizeof(CgScalars)) != cudaSuccess ||
@@ -998,7 +999,35 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   return FEM_OK;
 }
 
+// Chronopoulos-Gear iteration (option "cg_variant" = 1; TMA path): w = A r with delta = w.r and
+// gamma = r.r reduced together (one allreduce of 2 values), then one update kernel
+static int cg_cgcg_body(fem_op_s* op, cudaStream_t s, bool timed) {
+  fem_mesh_s* m = op->mesh;
+  if (timed) {
+    if (op->ev_used + 2 > op->ev.size()) {
+      for (int t = 0; t < 64; ++t) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        op->ev.push_back(e);
+      }
+    }
+    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used], s));
+  }
+  FEM_TRY(apply_pl(op, op->r_pl, &op->tm_r, 3, s));  // w (q_pl) = A r; pq = w.r, rr_new = r.r
+  if (timed) {
+    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used + 1], s));
+    op->ev_used += 2;
+  }
+  FEM_TRY(allreduce1(op, &op->sc->pq, s, 2));  // pq and rr_new are adjacent in CgScalars
+  cudaError_t e = launch_cg_cgcg_update(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, op->p_pl),
+                                        pl_owned(op, op->p2_pl), pl_owned(op, op->q_pl), pl_count(op), op->sc,
+                                        op->red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "cgcg update launch: %s", cudaGetErrorString(e));
+  return FEM_OK;
+}
+
 static int iteration(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
+  if (op->tm_ok && op->cg_variant == 1) return cg_cgcg_body(op, s, timed);
   return op->tm_ok ? cg_fused_body(op, parity, s, timed) : cg_iteration_body(op, s, timed);
 }
 
@@ -1204,6 +1233,13 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
     if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
     if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
+  } else if (!std::strcmp(key, "cg_variant")) {
+    if (value != 0 && value != 1) return fail(FEM_EINVAL, "cg_variant must be 0 (fused CG) or 1 (Chronopoulos-Gear)");
+    if (op->cg_active) return fail(FEM_ESTATE, "cg_variant cannot change during a CG solve");
+    op->cg_variant = (int)value;
+    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
+    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
+    if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
   } else if (!std::strcmp(key, "quadrature")) {
     if (value != 0 && value != 1) return fail(FEM_EINVAL, "quadrature must be 0 (Gauss) or 1 (Gauss-Lobatto)");
     op->quad = (int)value;
@@ -1224,6 +1260,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "time_apply")) *value = op->time_apply;
   else if (!std::strcmp(key, "partial_assembly")) *value = op->use_pa;
   else if (!std::strcmp(key, "quadrature")) *value = op->quad;
+  else if (!std::strcmp(key, "cg_variant")) *value = (op->tm_ok && op->cg_variant == 1) ? 1 : 0;
   else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }

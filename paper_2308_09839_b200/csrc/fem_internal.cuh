@@ -55,7 +55,7 @@ struct CgScalars {
   double rr_new;    // r.r after the update (global after allreduce)
   double rr0;       // r0.r0
   double stop_rr;   // tol^2 * rr0
-  double pad0;
+  double alpha;     // Chronopoulos-Gear CG: alpha of the last update
   int32_t done;     // 0 running, 1 converged, 2 breakdown, 3 maxit reached
   int32_t it;       // iterations completed
   int32_t maxit;
@@ -139,6 +139,11 @@ cudaError_t launch_hex_check(const int4* cells, const double4* xyz, int64_t ncel
 // VTK-ordered int32 node map (+ optional uint8 Dirichlet flags) -> internal cell records
 cudaError_t launch_hex_pack_cells(const int32_t* vtk, const uint8_t* dir, int64_t ncells, int64_t nnodes,
                                   int* out, unsigned long long* bad, cudaStream_t s, int sm_count);
+// Chronopoulos-Gear CG (single reduction, NEXT #1): with gamma = r.r and delta = w.r from the
+// apply (mode 3): beta = gamma / gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev);
+// p = r + beta p, s = w + beta s, x += alpha p, r -= alpha s (first step: p = r, s = w)
+cudaError_t launch_cg_cgcg_update(double* x, double* r, double* p, double* s, const double* w, int64_t n,
+                                  CgScalars* sc, Reduce red, cudaStream_t st, int sm_count);
 // deterministic dot -> *out (device)
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
                        cudaStream_t s, int sm_count);
@@ -215,6 +220,39 @@ __device__ __forceinline__ bool last_block_reduce(double partial, Reduce red, do
   double s = block_sum(v, sh);
   if (tid == 0) {
     *total = s;
+    *red.ticket = 0u;
+  }
+  return tid == 0;
+}
+
+// the same for two sums at once (partials of b at red.partials + red.capacity)
+__device__ __forceinline__ bool last_block_reduce2(double a, double b, Reduce red, double* sh,
+                                                   double* ta, double* tb) {
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nthr = blockDim.x * blockDim.y * blockDim.z;
+  const unsigned int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned int nblk = gridDim.x * gridDim.y * gridDim.z;
+  __shared__ unsigned int s_is_last2;
+  if (tid == 0) {
+    red.partials[bid] = a;
+    red.partials[red.capacity + bid] = b;
+    __threadfence();
+    unsigned int t = atomicAdd(red.ticket, 1u);
+    s_is_last2 = (t == nblk - 1);
+  }
+  __syncthreads();
+  if (!s_is_last2) return false;
+  __threadfence();
+  double va = 0.0, vb = 0.0;
+  for (unsigned int k = tid; k < nblk; k += nthr) {
+    va += ((volatile double*)red.partials)[k];
+    vb += ((volatile double*)red.partials)[red.capacity + k];
+  }
+  const double sa = block_sum(va, sh);
+  const double sb = block_sum(vb, sh);
+  if (tid == 0) {
+    *ta = sa;
+    *tb = sb;
     *red.ticket = 0u;
   }
   return tid == 0;

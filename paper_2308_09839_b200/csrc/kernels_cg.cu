@@ -157,6 +157,82 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __
   }
 }
 
+// Chronopoulos-Gear CG update (NEXT #1; single global reduction per iteration -- the apply
+// (mode 3) delivered delta = w.r in pq and gamma = r.r in rr_new, reduced together).  Recurrences:
+//   beta = gamma / gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev)  (first: beta = 0,
+//   alpha = gamma / delta); p = r + beta p; s = w + beta s; x += alpha p; r -= alpha s.
+// gamma is the residual of the iterate before this update, so convergence is decided here.
+__global__ void __launch_bounds__(kVecThreads) cg_cgcg_update_kernel(double* __restrict__ x, double* __restrict__ r,
+                                                                     double* __restrict__ p, double* __restrict__ s,
+                                                                     const double* __restrict__ w, int64_t n,
+                                                                     CgScalars* sc, Reduce red) {
+  __shared__ double sh[32];
+  if (sc->done) return;
+  const double gam = sc->rr_new, delta = sc->pq;
+  const bool first = sc->first != 0;
+  if (gam == 0.0 || gam <= sc->stop_rr) {  // converged at the current iterate (same test in every block)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc->rr = gam;
+      sc->done = 1;
+    }
+    return;
+  }
+  const double beta = first ? 0.0 : gam / sc->rr;
+  const double denom = first ? delta : delta - beta * gam / sc->alpha;
+  const double alpha = gam / denom;
+  if (!(denom > 0.0) || !isfinite(alpha)) {  // breakdown
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc->breakdown_iter = sc->it;
+      sc->rr = gam;
+      sc->done = 2;
+    }
+    return;
+  }
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto one = [&](int64_t i) {
+    const double ri = r[i], wi = w[i];
+    const double pi = first ? ri : fma(beta, p[i], ri);
+    const double si = first ? wi : fma(beta, s[i], wi);
+    p[i] = pi;
+    s[i] = si;
+    x[i] = fma(alpha, pi, x[i]);
+    r[i] = fma(-alpha, si, ri);
+  };
+  // 16-B accesses (the five vectors share one layout), head / tail elements scalar
+  const int64_t head = (reinterpret_cast<uintptr_t>(r) & 15) ? 1 : 0;
+  if (head && gtid == 0 && n > 0) one(0);
+  const int64_t n2 = (n - head) / 2;
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(x + head);
+  double2* __restrict__ r2 = reinterpret_cast<double2*>(r + head);
+  double2* __restrict__ p2 = reinterpret_cast<double2*>(p + head);
+  double2* __restrict__ s2 = reinterpret_cast<double2*>(s + head);
+  const double2* __restrict__ w2 = reinterpret_cast<const double2*>(w + head);
+  for (int64_t i = gtid; i < n2; i += stride) {
+    const double2 rv = r2[i], wv = w2[i], xv = x2[i];
+    double2 pv = rv, sv = wv;
+    if (!first) {
+      const double2 po = p2[i], so = s2[i];
+      pv = make_double2(fma(beta, po.x, rv.x), fma(beta, po.y, rv.y));
+      sv = make_double2(fma(beta, so.x, wv.x), fma(beta, so.y, wv.y));
+    }
+    p2[i] = pv;
+    s2[i] = sv;
+    x2[i] = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+    r2[i] = make_double2(fma(-alpha, sv.x, rv.x), fma(-alpha, sv.y, rv.y));
+  }
+  if (((n - head) & 1) && gtid == stride - 1) one(n - 1);
+  double tot;
+  if (last_block_reduce(0.0, red, sh, &tot)) {  // every block has read the scalars
+    sc->rr = gam;
+    sc->alpha = alpha;
+    sc->first = 0;
+    const int it = sc->it + 1;
+    sc->it = it;
+    if (it >= sc->maxit) sc->done = 3;
+  }
+}
+
 __global__ void __launch_bounds__(kVecThreads) cg_pupdate_kernel(const double* __restrict__ r,
                                                                  double* __restrict__ p, int64_t n,
                                                                  CgScalars* sc, Reduce red) {
@@ -233,6 +309,12 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
                                    CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   cg_update_fused_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_cgcg_update(double* x, double* r, double* p, double* s, const double* w, int64_t n,
+                                  CgScalars* sc, Reduce red, cudaStream_t st, int sm_count) {
+  cg_cgcg_update_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, st>>>(x, r, p, s, w, n, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -17,6 +17,7 @@
 // (independent of the tiling and of the z-chunk / slab boundaries).
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 
 #include "kernels_common.cuh"
 
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
   ring.init(tid, NT, TY);  // (fences + __syncthreads cover the hand-off barriers too)
   if (TM) ring.set_tshift(i0 - 1, uorg);
 
-  double pq = 0.0;
+  double pq = 0.0, rr2 = 0.0;  // (rr2: mode 3, sum of the input's squares)
   if (ty == TY) {
     ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, &mmap, mat_layer0, &umap2);
   } else {
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
               yp[c] = vv;
               if (mode == 2) pnb[c] = xv;
               if (mode >= 1) pq = fma(vv, xv, pq);
+              if (mode == 3) rr2 = fma(xv, xv, rr2);
             }
           }
           if (mode == 2) { ppb += x.ppitch; pnb += x.ppitch; }
@@ -272,7 +274,15 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
       }
     }
   }
-  if (mode >= 1) {
+  if (mode == 3) {  // single-reduction CG: delta = w.r and gamma = r.r in one pass
+    const double bd = block_sum(pq, red_sh);
+    const double bg = block_sum(rr2, red_sh);
+    double td, tg;
+    if (last_block_reduce2(bd, bg, red, red_sh, &td, &tg)) {
+      sc->pq = td;
+      sc->rr_new = tg;
+    }
+  } else if (mode >= 1) {
     double bsum = block_sum(pq, red_sh);
     double total;
     if (last_block_reduce(bsum, red, red_sh, &total)) {
@@ -294,15 +304,20 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   const size_t ring_bytes = mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META;
   const size_t smem = ring_bytes + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t);
   const bool gll = maps.quad == 1;
-  auto kern = gll ? (mode == 2 ? elastic_kernel<TM, (TM ? 2 : 1), TY, S, true>
-                               : (mode ? elastic_kernel<TM, 1, TY, S, true> : elastic_kernel<TM, 0, TY, S, true>))
-                  : (mode == 2 ? elastic_kernel<TM, (TM ? 2 : 1), TY, S, false>
-                               : (mode ? elastic_kernel<TM, 1, TY, S, false> : elastic_kernel<TM, 0, TY, S, false>));
-  static bool attr_set[6] = {false, false, false, false, false, false};
-  if (!attr_set[mode + 3 * gll]) {
+  if (mode == 3 && !TM) return cudaErrorInvalidValue;  // single-reduction CG: tensor path only
+  auto pick = [&](auto gl) {
+    constexpr bool G = decltype(gl)::value;
+    return mode == 3 ? elastic_kernel<TM, (TM ? 3 : 1), TY, S, G>
+         : mode == 2 ? elastic_kernel<TM, (TM ? 2 : 1), TY, S, G>
+         : mode == 1 ? elastic_kernel<TM, 1, TY, S, G>
+                     : elastic_kernel<TM, 0, TY, S, G>;
+  };
+  auto kern = gll ? pick(std::true_type{}) : pick(std::false_type{});
+  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  if (!attr_set[mode + 4 * gll]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set[mode + 3 * gll] = true;
+    attr_set[mode + 4 * gll] = true;
   }
   const int64_t xt = (g.nx + 1 + (TX - 1) - 1) / (TX - 1);
   const int64_t yt = (g.ny + 1 + (TY - 1) - 1) / (TY - 1);
@@ -334,6 +349,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
 cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int mode,
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
+  if (mode == 3 && !maps.u) return cudaErrorInvalidValue;
   if (maps.u) {
     if (mode == 2) return launch_cfg<true, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     return launch_cfg<true, kElTY, (kElTY <= 7 ? 4 : 8)>(g, x, y, maps, bc, mode, sc, red, s, sm_count);

@@ -13,6 +13,7 @@
 // the one-node xy halo from L2.  Vector Laplace (Eq. 8) is the same per component.
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 
 #include "kernels_common.cuh"
 
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
   ring.init(tid, NT, TY);
   if (TM) ring.set_tshift(i0 - 1, uorg);
 
-  double pq = 0.0;
+  double pq = 0.0, rr2 = 0.0;  // (rr2: mode 3, sum of the input's squares)
   if (ty == TY) {
     ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, nullptr, 0, &umap2);
   } else {
@@ -165,12 +166,21 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
             yq[off_y[r] + c] = v;
             if (mode == 2) pq_new[off_x[r] + c] = xv;
             if (mode >= 1) pq = fma(v, xv, pq);
+            if (mode == 3) rr2 = fma(xv, xv, rr2);
           }
         }
       }
     }
   }
-  if (mode >= 1) {
+  if (mode == 3) {  // single-reduction CG: delta = w.r and gamma = r.r in one pass
+    const double bd = block_sum(pq, red_sh);
+    const double bg = block_sum(rr2, red_sh);
+    double td, tg;
+    if (last_block_reduce2(bd, bg, red, red_sh, &td, &tg)) {
+      sc->pq = td;
+      sc->rr_new = tg;
+    }
+  } else if (mode >= 1) {
     double bsum = block_sum(pq, red_sh);
     double total;
     if (last_block_reduce(bsum, red, red_sh, &total)) {
@@ -189,18 +199,21 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   using Ring1 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, 1>;
   using Ring2 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, (TM ? 2 : 1)>;
   const size_t smem = (mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META);
+  if (mode == 3 && !TM) return cudaErrorInvalidValue;  // single-reduction CG: tensor path only
   const bool gll = maps.quad == 1;
-  auto kern = gll ? (mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S, true>
-                               : (mode ? laplace_kernel<TM, 1, C, TX, TY, R, S, true>
-                                       : laplace_kernel<TM, 0, C, TX, TY, R, S, true>))
-                  : (mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S, false>
-                               : (mode ? laplace_kernel<TM, 1, C, TX, TY, R, S, false>
-                                       : laplace_kernel<TM, 0, C, TX, TY, R, S, false>));
-  static bool attr_set[6] = {false, false, false, false, false, false};
-  if (!attr_set[mode + 3 * gll]) {
+  auto pick = [&](auto gl) {
+    constexpr bool G = decltype(gl)::value;
+    return mode == 3 ? laplace_kernel<TM, (TM ? 3 : 1), C, TX, TY, R, S, G>
+         : mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S, G>
+         : mode == 1 ? laplace_kernel<TM, 1, C, TX, TY, R, S, G>
+                     : laplace_kernel<TM, 0, C, TX, TY, R, S, G>;
+  };
+  auto kern = gll ? pick(std::true_type{}) : pick(std::false_type{});
+  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  if (!attr_set[mode + 4 * gll]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set[mode + 3 * gll] = true;
+    attr_set[mode + 4 * gll] = true;
   }
   const int64_t xt = (g.nx + 1 + TX - 1) / TX;
   const int64_t yt = (g.ny + 1 + TY * R - 1) / (TY * R);
@@ -232,6 +245,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
 cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps,
                            int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
+  if (mode == 3 && !maps.u) return cudaErrorInvalidValue;
   if (maps.u) {
     if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     if (mode == 2) return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);

@@ -265,3 +265,41 @@ def test_csr_parity(F, oracle, kind, dims, bc):
         full = (nx - 3) * (ny - 3) * (nz - 3)
         assert A.nnz >= full * 27 * c * c
         assert A.nnz <= n_int * 27 * c * c + (I.n_nodes(nx, ny, nz) - n_int) * c
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+def test_cg_chronopoulos_gear_parity(F, oracle, kind):
+    """Single-reduction CG (option cg_variant = 1): same Krylov iterates in exact arithmetic, so
+    the converged solution matches the oracle's Hestenes-Stiefel CG."""
+    nx, ny, nz = 12, 10, 9
+    h = 1.0 / 12
+    g = I.rng(I.SEED_BASE + 1400)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = I.interior_rhs(g, nx, ny, nz, I.ncomp(kind))
+    ref = oracle.cg(kind, 1, nx, ny, nz, h, b, tol=1e-14, maxit=500, lam=lam, mu=mu)
+    assert ref.converged
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 1)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    op.set_option("cg_variant", 1)
+    assert op.get_option("cg_variant") == 1
+    x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+    info = op.cg_solve(dev(b), x, tol=1e-14, maxit=500)
+    assert info["converged"]
+    assert abs(info["iterations"] - ref.iterations) <= 3
+    assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10 * max(1.0, np.abs(ref.x).max())
+    assert info["true_r_norm"] <= 1e-12 * info["r0_norm"]
+
+
+def test_cg_chronopoulos_gear_fixed_iterations(F, oracle):
+    """tol = 0: exactly maxit updates, iterate close to the Hestenes-Stiefel one (C1)."""
+    nx = ny = nz = 8
+    g = I.rng(I.SEED_BASE + 0)
+    b = I.interior_rhs(g, nx, ny, nz, 1)
+    ref = oracle.cg("scalar", 1, nx, ny, nz, 1 / 8, b, tol=0.0, maxit=50)
+    op = F.Operator(F.Mesh(nx, ny, nz, 1 / 8), "scalar", 1)
+    op.set_option("cg_variant", 1)
+    x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+    info = op.cg_solve(dev(b), x, tol=0.0, maxit=50)
+    assert info["iterations"] == ref.iterations
+    assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10
