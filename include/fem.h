@@ -151,6 +151,19 @@ int fem_apply_ghost(fem_op_t op, const double* x, const double* ghost_lo, const 
  * fem_cg_begin/iterate sequence (FEM_ESTATE on the next fem_cg_iterate). */
 int fem_apply_ghost_padded(fem_op_t op, const double* x, const double* ghost_lo, const double* ghost_hi,
                            double* y, void* stream);
+/* Single-process loopback of the peer halo ("peer_halo" option): this slab operator reads its
+ * ghost planes directly from the padded vectors of the operators of the slabs below (lo) and
+ * above (hi) -- NULL where the box ends -- which live in the same process on the same device.
+ * For tests of the peer-halo kernel path with virtual communicators (fem_apply_ghost_padded then
+ * takes NULL ghost planes); the cross-process version is fem_set_option(op, "peer_halo", 1). */
+int fem_op_link_peers(fem_op_t op, fem_op_t lo, fem_op_t hi);
+/* Peer halo across processes without NCCL for the handle exchange: fem_op_peer_info writes this
+ * slab operator's CUDA IPC handles of its CG vectors and its plane count (<= 320 bytes) into
+ * `info`; the caller sends it to both slab neighbours (any channel, e.g. torch.distributed) and
+ * each rank calls fem_op_open_peers with the infos of the slabs below / above (NULL at the box
+ * ends).  Equivalent to the "peer_halo" option, which does the same exchange over NCCL. */
+int fem_op_peer_info(fem_op_t op, void* info, int64_t bytes);
+int fem_op_open_peers(fem_op_t op, const void* lo_info, const void* hi_info);
 /* Global sum_i a_i b_i over owned DOFs (Table 4 "ddot").  Deterministic for a
  * fixed rank count.  Result written to *result (host).  Collective. */
 int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void* stream);
@@ -179,7 +192,11 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * every kernel of the operator incl. fem_csr_create), "cg_variant" (0: the fused
  * Hestenes-Stiefel CG of Table 4, default; 1: Chronopoulos-Gear single-reduction CG -- r.r and
  * w.r come out of the apply together, one allreduce of two values per iteration instead of two;
- * TMA path only, reads back 0 elsewhere). */
+ * TMA path only, reads back 0 elsewhere), "peer_halo" (1: collective over the slab ranks --
+ * every rank sets it -- exchanging CUDA IPC handles of the CG vectors with the neighbours over
+ * NCCL; the apply kernels then load the ghost node planes straight from the neighbours' memory
+ * over NVLink inside their TMA pipeline and the NCCL halo step disappears; the two CG allreduces
+ * order the cross-rank reads and writes; TMA path only, cannot be switched off). */
 int fem_set_option(fem_op_t op, const char* key, int64_t value);
 /* Read-only properties: "fused_cg" (1: CG iterations use the fused apply -- p = r + beta p_old
  * formed inside the TMA apply kernel -- and 2 kernels per iteration; 0: apply + update +

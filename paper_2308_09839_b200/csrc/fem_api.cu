@@ -125,6 +125,14 @@ struct fem_op_s {
   int pa_quad = -1;  // rule the stored geometry was computed for
   int quad = 0;      // 0: 2x2x2 Gauss-Legendre, 1: 2x2x2 Gauss-Lobatto (BP5/BP6; reading R1)
   int cg_variant = 0;  // 0: fused Hestenes-Stiefel (Table 4), 1: Chronopoulos-Gear single reduction
+  // peer halo: the neighbour ranks' padded vectors x, p, r, p2 (CUDA IPC or, for single-process
+  // tests, the other operator's buffers) and tensor maps over their ghost-plane sources
+  bool peer_on = false, peer_ipc = false;
+  double* nb_lo[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* nb_hi[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t nb_lo_nloc = 0;
+  CUtensorMap pm_lo[4]{}, pm_hi[4]{};
+  int64_t pm_klo = -(int64_t(1) << 62), pm_khi = -(int64_t(1) << 62);
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
 };
@@ -328,6 +336,35 @@ static int make_pl_maps(fem_op_s* op) {
   return FEM_OK;
 }
 
+// Peer halo: tensor maps over the neighbours' ghost-plane sources (their last / first owned node
+// plane), same origin, box and pitches as the local maps; ghost planes outside the operator's
+// tensor range (the Dirichlet faces of the Laplace interior tensor) stay zero-filled locally.
+static int build_peer_maps(fem_op_s* op) {
+  const Grid& g = op->mesh->g;
+  const int C = op->comps;
+  const bool interior = op->tm_interior;
+  const int64_t lo = interior ? 1 : 0;
+  const int64_t i1 = interior ? g.nx - 1 : g.nx, j1 = interior ? g.ny - 1 : g.ny;
+  const int64_t kmax = interior ? g.nz - 1 : g.nz;
+  unsigned bw, bh;
+  u_box(op->kind, &bw, &bh);
+  constexpr int64_t kNone = -(int64_t(1) << 62);  // never a plane index (planes start at -1)
+  op->pm_klo = (op->nb_lo[0] && g.k0 - 1 >= lo) ? g.k0 - 1 : kNone;
+  op->pm_khi = (op->nb_hi[0] && g.k1 <= kmax) ? g.k1 : kNone;
+  const int64_t off = op->pl_lead + lo * op->pl_rp + lo * C;
+  for (int v = 0; v < 4; ++v) {
+    if (op->pm_klo >= 0)
+      FEM_TRY(make_map3d(&op->pm_lo[v], op->nb_lo[v] + off + op->nb_lo_nloc * op->pl_pp,
+                         (uint64_t)((i1 - lo + 1) * C), (uint64_t)(j1 - lo + 1), 1, op->pl_rp * 8, op->pl_pp * 8,
+                         bw, bh));
+    if (op->pm_khi >= 0)
+      FEM_TRY(make_map3d(&op->pm_hi[v], op->nb_hi[v] + off + op->pl_pp, (uint64_t)((i1 - lo + 1) * C),
+                         (uint64_t)(j1 - lo + 1), 1, op->pl_rp * 8, op->pl_pp * 8, bw, bh));
+  }
+  op->peer_on = true;
+  return FEM_OK;
+}
+
 static int make_mat_map(fem_op_s* op) {
   const Grid& g = op->mesh->g;
   unsigned bw, bh;
@@ -337,11 +374,31 @@ static int make_mat_map(fem_op_s* op) {
 }
 
 // apply kernel dispatch
+static int vec_index(const fem_op_s* op, const double* v) {  // x, p, r, p2 -> 0..3
+  const double* b[4] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl};
+  for (int i = 0; i < 4; ++i)
+    if (b[i] == v) return i;
+  return -1;
+}
+
+// peer-halo maps of one launch: u = padded vector v, u2 = v2 (mode 2), or none
+static bool fill_peer(const fem_op_s* op, const double* v, const double* v2, PeerMaps* pm) {
+  const int i = vec_index(op, v), i2 = v2 ? vec_index(op, v2) : i;
+  if (!op->peer_on || i < 0 || i2 < 0) return false;
+  pm->lo = op->pm_lo[i]; pm->hi = op->pm_hi[i];
+  pm->lo2 = op->pm_lo[i2]; pm->hi2 = op->pm_hi[i2];
+  pm->klo = op->pm_klo; pm->khi = op->pm_khi;
+  pm->on = 1;
+  return true;
+}
+
 static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* umap, int mode,
-                        cudaStream_t s) {
+                        cudaStream_t s, const double* vsrc = nullptr) {
   fem_mesh_s* m = op->mesh;
+  static thread_local PeerMaps pm;
+  const bool peer = umap && vsrc && fill_peer(op, vsrc, nullptr, &pm);
   ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr,
-                 op->tm_interior ? 1 : 0, op->quad};
+                 op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
@@ -399,12 +456,12 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
 static int apply_pl(fem_op_s* op, double* v, const CUtensorMap* map, int mode, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
   if (m->hex) return apply_hex(op, pl_owned(op, v), pl_owned(op, op->q_pl), mode, s);
-  if (m->nranks > 1) {
+  if (m->nranks > 1 && !(op->peer_on && op->tm_ok)) {
     double* own = pl_owned(op, v);
     FEM_TRY(halo_pitch(op, own, v + op->pl_lead, v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp,
                        op->pl_pp, s));
   }
-  return launch_apply(op, pl_src(op, v), pl_out(op, op->q_pl), op->tm_ok ? map : nullptr, mode, s);
+  return launch_apply(op, pl_src(op, v), pl_out(op, op->q_pl), op->tm_ok ? map : nullptr, mode, s, v);
 }
 
 static int pack(fem_op_s* op, const double* dense, double* v, int to_padded, cudaStream_t s) {
@@ -635,6 +692,11 @@ static void op_free(fem_op_s* op) {
   if (op->graph1) cudaGraphExecDestroy(op->graph1);
   if (op->graphN) cudaGraphExecDestroy(op->graphN);
   for (auto e : op->ev) cudaEventDestroy(e);
+  if (op->peer_ipc)
+    for (int v = 0; v < 4; ++v) {
+      if (op->nb_lo[v]) cudaIpcCloseMemHandle(op->nb_lo[v]);
+      if (op->nb_hi[v]) cudaIpcCloseMemHandle(op->nb_hi[v]);
+    }
   cudaFree(op->lm);
   cudaFree(op->pa);
   cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
@@ -860,7 +922,7 @@ int fem_apply_ghost_padded(fem_op_t op, const double* x, const double* glo, cons
   if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
   if (op->mesh->hex) return fail(FEM_EUNSUPPORTED, "fem_apply_ghost_padded: general hex meshes are single-GPU");
   const Grid& g = op->mesh->g;
-  if ((g.k0 > 0 && !glo) || (g.k1 <= g.nz && !ghi))
+  if (!op->peer_on && ((g.k0 > 0 && !glo) || (g.k1 <= g.nz && !ghi)))
     return fail(FEM_EINVAL, "a ghost plane inside the box is NULL");
   if (!is_device_ptr(x) || !is_device_ptr(y) || (glo && !is_device_ptr(glo)) || (ghi && !is_device_ptr(ghi)))
     return fail(FEM_EINVAL, "fem_apply_ghost_padded needs device pointers");
@@ -874,10 +936,116 @@ int fem_apply_ghost_padded(fem_op_t op, const double* x, const double* glo, cons
     if (e != cudaSuccess) return fail(FEM_ECUDA, "ghost pack: %s", cudaGetErrorString(e));
     return FEM_OK;
   };
-  if (m->rank > 0 && glo) FEM_TRY(ghost(glo, op->x_pl + op->pl_lead));
-  if (m->rank < m->nranks - 1 && ghi) FEM_TRY(ghost(ghi, op->x_pl + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp));
-  FEM_TRY(launch_apply(op, pl_src(op, op->x_pl), pl_out(op, op->q_pl), op->tm_ok ? &op->tm_x : nullptr, 0, s));
+  if (!op->peer_on) {
+    if (m->rank > 0 && glo) FEM_TRY(ghost(glo, op->x_pl + op->pl_lead));
+    if (m->rank < m->nranks - 1 && ghi) FEM_TRY(ghost(ghi, op->x_pl + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp));
+  }
+  FEM_TRY(launch_apply(op, pl_src(op, op->x_pl), pl_out(op, op->q_pl), op->tm_ok ? &op->tm_x : nullptr, 0, s,
+                       op->x_pl));
   return pack(op, y, op->q_pl, 0, s);
+}
+
+int fem_op_link_peers(fem_op_t op, fem_op_t lo, fem_op_t hi) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  if (!op->tm_ok) return fail(FEM_EUNSUPPORTED, "peer halo needs the TMA (padded) path");
+  const Grid& g = op->mesh->g;
+  for (fem_op_s* nb : {lo, hi}) {
+    if (!nb) continue;
+    const Grid& h = nb->mesh->g;
+    if (nb->kind != op->kind || nb->bc != op->bc || h.nx != g.nx || h.ny != g.ny || h.nz != g.nz ||
+        nb->mesh->device != op->mesh->device || !nb->tm_ok)
+      return fail(FEM_EINVAL, "peer operator does not match (kind, bc, mesh, device)");
+  }
+  if ((lo && lo->mesh->g.k1 != g.k0) || (hi && hi->mesh->g.k0 != g.k1))
+    return fail(FEM_EINVAL, "peer slabs are not the neighbours of this slab");
+  if ((g.k0 > 0) != (lo != nullptr) || (g.k1 <= g.nz) != (hi != nullptr))
+    return fail(FEM_EINVAL, "a neighbour slab is missing (or given where there is none)");
+  FEM_TRY(set_device(op->mesh->device));
+  auto bufs = [](fem_op_s* o, double** b) { b[0] = o->x_pl; b[1] = o->p_pl; b[2] = o->r_pl; b[3] = o->p2_pl; };
+  if (lo) { bufs(lo, op->nb_lo); op->nb_lo_nloc = lo->nloc_planes; }
+  if (hi) bufs(hi, op->nb_hi);
+  op->cg_active = false;
+  return build_peer_maps(op);
+}
+
+// peer halo across processes: CUDA IPC handles of the padded vectors x, p, r, p2 + the slab's
+// owned plane count (fem_op_peer_info), opened by the neighbours (fem_op_open_peers)
+struct PeerInfo {
+  cudaIpcMemHandle_t h[4];
+  int64_t nloc;
+};
+static_assert(sizeof(PeerInfo) <= 320, "peer info exceeds the documented 320 bytes");
+
+int fem_op_peer_info(fem_op_t op, void* info, int64_t bytes) {
+  if (!op || !info) return fail(FEM_EINVAL, "op / info is NULL");
+  if (bytes < (int64_t)sizeof(PeerInfo)) return fail(FEM_EINVAL, "info buffer must hold %zu bytes", sizeof(PeerInfo));
+  if (!op->tm_ok) return fail(FEM_EUNSUPPORTED, "peer halo needs the TMA (padded) path");
+  FEM_TRY(set_device(op->mesh->device));
+  PeerInfo mine{};
+  double* b[4] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl};
+  for (int v = 0; v < 4; ++v) CUDA_TRY(cudaIpcGetMemHandle(&mine.h[v], b[v]));
+  mine.nloc = op->nloc_planes;
+  std::memcpy(info, &mine, sizeof(mine));
+  return FEM_OK;
+}
+
+int fem_op_open_peers(fem_op_t op, const void* lo_info, const void* hi_info) {
+  if (!op) return fail(FEM_EINVAL, "op is NULL");
+  if (!op->tm_ok) return fail(FEM_EUNSUPPORTED, "peer halo needs the TMA (padded) path");
+  if (op->peer_on) return fail(FEM_ESTATE, "peers already linked");
+  const Grid& g = op->mesh->g;
+  if ((g.k0 > 0) != (lo_info != nullptr) || (g.k1 <= g.nz) != (hi_info != nullptr))
+    return fail(FEM_EINVAL, "a neighbour's info is missing (or given where there is none)");
+  FEM_TRY(set_device(op->mesh->device));
+  PeerInfo nb[2]{};
+  if (lo_info) std::memcpy(&nb[0], lo_info, sizeof(PeerInfo));
+  if (hi_info) std::memcpy(&nb[1], hi_info, sizeof(PeerInfo));
+  for (int v = 0; v < 4; ++v) {
+    void* p = nullptr;
+    if (lo_info) {
+      CUDA_TRY(cudaIpcOpenMemHandle(&p, nb[0].h[v], cudaIpcMemLazyEnablePeerAccess));
+      op->nb_lo[v] = static_cast<double*>(p);
+    }
+    if (hi_info) {
+      CUDA_TRY(cudaIpcOpenMemHandle(&p, nb[1].h[v], cudaIpcMemLazyEnablePeerAccess));
+      op->nb_hi[v] = static_cast<double*>(p);
+    }
+  }
+  op->nb_lo_nloc = nb[0].nloc;
+  op->peer_ipc = true;
+  op->cg_active = false;
+  return build_peer_maps(op);
+}
+
+// the same exchange over the operator's NCCL communicator (option "peer_halo")
+static int peer_halo_ipc(fem_op_s* op) {
+  fem_mesh_s* m = op->mesh;
+  if (m->nranks == 1) return FEM_OK;
+  if (!m->comm || !m->comm->nccl) return fail(FEM_EUNSUPPORTED, "peer halo across processes needs an NCCL communicator");
+  PeerInfo mine{};
+  FEM_TRY(fem_op_peer_info(op, &mine, sizeof(mine)));
+  char* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, 3 * sizeof(PeerInfo)));
+  CUDA_TRY(cudaMemcpy(d, &mine, sizeof(PeerInfo), cudaMemcpyHostToDevice));
+  cudaStream_t s = 0;
+  ncclComm_t c = m->comm->nccl;
+  ncclResult_t r = ncclGroupStart();
+  if (m->rank > 0) {
+    if (r == ncclSuccess) r = ncclSend(d, sizeof(PeerInfo), ncclChar, m->rank - 1, c, s);
+    if (r == ncclSuccess) r = ncclRecv(d + sizeof(PeerInfo), sizeof(PeerInfo), ncclChar, m->rank - 1, c, s);
+  }
+  if (m->rank < m->nranks - 1) {
+    if (r == ncclSuccess) r = ncclSend(d, sizeof(PeerInfo), ncclChar, m->rank + 1, c, s);
+    if (r == ncclSuccess) r = ncclRecv(d + 2 * sizeof(PeerInfo), sizeof(PeerInfo), ncclChar, m->rank + 1, c, s);
+  }
+  if (r == ncclSuccess) r = ncclGroupEnd();
+  PeerInfo nb[2];
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaMemcpy(nb, d + sizeof(PeerInfo), 2 * sizeof(PeerInfo), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (r != ncclSuccess) return fail(FEM_ENCCL, "peer handle exchange: %s", ncclGetErrorString(r));
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "peer handle exchange: %s", cudaGetErrorString(e));
+  return fem_op_open_peers(op, m->rank > 0 ? &nb[0] : nullptr, m->rank < m->nranks - 1 ? &nb[1] : nullptr);
 }
 
 int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
@@ -961,7 +1129,9 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
   double* pold = parity ? op->p2_pl : op->p_pl;
   double* pnew = parity ? op->p_pl : op->p2_pl;
-  if (m->nranks > 1) {
+  static thread_local PeerMaps pm;
+  const bool peer = fill_peer(op, op->r_pl, pold, &pm);
+  if (m->nranks > 1 && !peer) {
     for (double* v : {op->r_pl, pold})
       FEM_TRY(halo_pitch(op, pl_owned(op, v), v + op->pl_lead,
                          v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp, op->pl_pp, s));
@@ -978,7 +1148,7 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   }
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
                  parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
-                 op->tm_interior ? 1 : 0, op->quad};
+                 op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc, op->red, s,
@@ -1023,6 +1193,8 @@ static int cg_cgcg_body(fem_op_s* op, cudaStream_t s, bool timed) {
                                         pl_owned(op, op->p2_pl), pl_owned(op, op->q_pl), pl_count(op), op->sc,
                                         op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "cgcg update launch: %s", cudaGetErrorString(e));
+  // peer halo: the next apply reads the neighbours' r -- wait for their updates
+  if (op->peer_on && m->nranks > 1) FEM_TRY(allreduce1(op, op->dot_dev, s));
   return FEM_OK;
 }
 
@@ -1063,6 +1235,8 @@ static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGrap
 static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, int maxit, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
   FEM_TRY(pack(op, x, op->x_pl, 1, s));
+  // peer halo: the neighbours must have packed their x0 before this rank's apply reads it
+  if (op->peer_on && m->nranks > 1) FEM_TRY(allreduce1(op, op->dot_dev, s));
   FEM_TRY(apply_pl(op, op->x_pl, &op->tm_x, 0, s));  // q = A x0
   FEM_TRY(pack(op, b, op->r_pl, 1, s));              // r = b
   cudaError_t e = launch_cg_init(pl_owned(op, op->r_pl), pl_owned(op, op->q_pl), pl_owned(op, op->r_pl),
@@ -1233,6 +1407,17 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
     if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
     if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
+  } else if (!std::strcmp(key, "peer_halo")) {
+    // collective over the slab ranks (every rank must set it): ghost planes read in the apply
+    // kernels straight from the neighbours' memory (CUDA IPC over NVLink), no NCCL halo
+    if (!value) return fail(FEM_EINVAL, "peer_halo cannot be switched off once on");
+    if (!op->tm_ok) return fail(FEM_EUNSUPPORTED, "peer halo needs the TMA (padded) path");
+    if (op->cg_active) return fail(FEM_ESTATE, "peer_halo cannot change during a CG solve");
+    FEM_TRY(set_device(op->mesh->device));
+    if (!op->peer_on) FEM_TRY(peer_halo_ipc(op));
+    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
+    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
+    if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
   } else if (!std::strcmp(key, "cg_variant")) {
     if (value != 0 && value != 1) return fail(FEM_EINVAL, "cg_variant must be 0 (fused CG) or 1 (Chronopoulos-Gear)");
     if (op->cg_active) return fail(FEM_ESTATE, "cg_variant cannot change during a CG solve");
@@ -1261,6 +1446,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "partial_assembly")) *value = op->use_pa;
   else if (!std::strcmp(key, "quadrature")) *value = op->quad;
   else if (!std::strcmp(key, "cg_variant")) *value = (op->tm_ok && op->cg_variant == 1) ? 1 : 0;
+  else if (!std::strcmp(key, "peer_halo")) *value = op->peer_on ? 1 : 0;
   else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }

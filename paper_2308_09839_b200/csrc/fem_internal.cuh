@@ -33,6 +33,17 @@ struct OutVec {
   int64_t rpitch, ppitch;
 };
 
+// Peer halo (option "peer_halo"): tensor maps over the NEIGHBOUR ranks' padded
+// vectors (CUDA IPC over NVLink / NVSwitch) for the ghost planes klo = k0-1 and khi = k1, so the
+// apply's producer warp loads them straight from peer memory -- no separate halo exchange.
+// on = 0: the ghost planes come from the local padded buffer (NCCL halo).
+struct __align__(64) PeerMaps {
+  CUtensorMap lo, hi;    // u ghost planes
+  CUtensorMap lo2, hi2;  // u2 (mode 2: p_old) ghost planes
+  int64_t klo, khi;      // global plane index served by lo / hi (-2^62: none)
+  int on;
+};
+
 // TMA tensor maps of one apply launch (u plane: padded layout; material: interleaved lambda/mu)
 // mode 2 (fused CG): the operator input is p = r + beta p_old formed in the kernel; u is r,
 // u2 is p_old, p is written to pnew (owned nodes, padded layout of x).
@@ -46,6 +57,7 @@ struct ApplyMaps {
   double* pnew;            // mode 2: p output owned plane k0 (same layout as x)
   int interior;            // 1: u tensor spans only the Dirichlet interior (zero fill = mask)
   int quad;                // 0: 2x2x2 Gauss-Legendre (default), 1: 2x2x2 Gauss-Lobatto (BP5/BP6)
+  const PeerMaps* peer;    // ghost planes from peer memory (nullptr / on = 0: local)
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).

@@ -233,7 +233,8 @@ struct PlaneRing {
                                           int64_t ilo, int64_t jlo, int bc, int lane,
                                           const CUtensorMap* umap, TmaOrigin uorg,
                                           const CUtensorMap* mmap, int64_t mlayer0,
-                                          const CUtensorMap* umap2 = nullptr, int tbase = 0) {
+                                          const CUtensorMap* umap2 = nullptr, int tbase = 0,
+                                          const PeerMaps* peer = nullptr) {
     if (lane == 0) {
       if (TM) tma_prefetch_desc(umap);
       if (NU == 2) tma_prefetch_desc(umap2);
@@ -277,8 +278,14 @@ struct PlaneRing {
       if (TM) {
         if (lane == 0) {
           mbar_arrive_expect_tx(&full[s], NU * UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
-          tma_load_3d(slot, umap, ux, uy, (int)(p - uorg.t_k0), &full[s]);
-          if (NU == 2) tma_load_3d(slot + UDBL, umap2, ux, uy, (int)(p - uorg.t_k0), &full[s]);
+          const CUtensorMap *m1 = umap, *m2 = umap2;
+          int z = (int)(p - uorg.t_k0);
+          if (peer && peer->on) {  // ghost planes straight from the neighbour's memory
+            if (p == peer->klo) { m1 = &peer->lo; m2 = &peer->lo2; z = 0; }
+            else if (p == peer->khi) { m1 = &peer->hi; m2 = &peer->hi2; z = 0; }
+          }
+          tma_load_3d(slot, m1, ux, uy, z, &full[s]);
+          if (NU == 2) tma_load_3d(slot + UDBL, m2, ux, uy, z, &full[s]);
           if (MROWS > 0) tma_load_3d(slot + NU * UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
         }
         continue;

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
     elastic_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                    const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
-                   int bc, int64_t kchunk, CgScalars* sc, Reduce red) {
+                   int bc, int64_t kchunk, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer) {
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   // TY consumer warps (lane = cell column, warp = cell row) + 1 producer warp
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
 
   double pq = 0.0, rr2 = 0.0;  // (rr2: mode 3, sum of the input's squares)
   if (ty == TY) {
-    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, &mmap, mat_layer0, &umap2);
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, &mmap, mat_layer0, &umap2, 0, &peer);
   } else {
     const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + ty;
     const double hs = g.h * (1.0 / 16.0);
@@ -340,8 +340,10 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
   if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
+  PeerMaps pm;
+  if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
   kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
-                                 bc, kchunk, sc, red);
+                                 bc, kchunk, sc, red, pm);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -25,7 +25,8 @@ template <bool TM, int MODE, int C, int TX, int TY, int R, int S, bool GLL>
 __global__ void __launch_bounds__(TX*(TY + 1), 2)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
-                   double* pnew, int bc, int tmint, int64_t kchunk, CgScalars* sc, Reduce red) {
+                   double* pnew, int bc, int tmint, int64_t kchunk, CgScalars* sc, Reduce red,
+                   const __grid_constant__ PeerMaps peer) {
   (void)tmint;  // Laplace uses interior-only tensors with the Dirichlet box (zero fill = mask)
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
 
   double pq = 0.0, rr2 = 0.0;  // (rr2: mode 3, sum of the input's squares)
   if (ty == TY) {
-    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, nullptr, 0, &umap2);
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, nullptr, 0, &umap2, 0, &peer);
   } else {
     const int64_t i = i0 + tx;
     const double h36 = g.h * (1.0 / 36.0);
@@ -237,7 +238,9 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
   if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
-  kern<<<grid, block, smem, s>>>(g, x, y, um, org, um2, maps.pold, maps.pnew, bc, maps.interior, kchunk, sc, red);
+  PeerMaps pm;
+  if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, um2, maps.pold, maps.pnew, bc, maps.interior, kchunk, sc, red, pm);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -43,7 +43,8 @@ class CgInfo(ctypes.Structure):
 # every symbol include/fem.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fem_last_error", "fem_version", "fem_launch_count", "fem_get_unique_id", "fem_comm_create",
-    "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_apply_ghost_padded", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy",
+    "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_apply_ghost_padded", "fem_op_link_peers",
+    "fem_op_peer_info", "fem_op_open_peers", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy",
     "fem_mesh_create_hex", "fem_mesh_info_hex", "fem_op_create",
     "fem_op_ndof", "fem_set_material", "fem_apply", "fem_dot", "fem_cg_solve", "fem_cg_begin",
     "fem_cg_iterate", "fem_cg_end", "fem_set_option", "fem_get_option", "fem_apply_time", "fem_op_destroy",
@@ -78,6 +79,9 @@ def load(build_if_missing: bool = True):
         "fem_partition": ([i64, i32, i32, P(i64), P(i64)], ctypes.c_int),
         "fem_apply_ghost": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "fem_apply_ghost_padded": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "fem_op_link_peers": ([vp, vp, vp], ctypes.c_int),
+        "fem_op_peer_info": ([vp, vp, i64], ctypes.c_int),
+        "fem_op_open_peers": ([vp, vp, vp], ctypes.c_int),
         "fem_mesh_create": ([i64, i64, i64, dbl, vp, P(vp)], ctypes.c_int),
         "fem_mesh_local": ([vp, P(i64), P(i64), P(i64)], ctypes.c_int),
         "fem_mesh_destroy": ([vp], None),
@@ -271,6 +275,20 @@ class Operator:
         _check(load().fem_apply_ghost(self.h, _ptr(x), _ptr(ghost_lo), _ptr(ghost_hi), _ptr(y),
                                       _stream(stream)))
         return y
+
+    def link_peers(self, lo: "Operator | None", hi: "Operator | None"):
+        """Single-process loopback of the peer halo (ghost planes from the neighbours' buffers)."""
+        _check(load().fem_op_link_peers(self.h, lo.h if lo else None, hi.h if hi else None))
+
+    def peer_info(self) -> bytes:
+        buf = ctypes.create_string_buffer(320)
+        _check(load().fem_op_peer_info(self.h, buf, 320))
+        return buf.raw
+
+    def open_peers(self, lo_info: bytes | None, hi_info: bytes | None):
+        lo = ctypes.create_string_buffer(lo_info, 320) if lo_info else None
+        hi = ctypes.create_string_buffer(hi_info, 320) if hi_info else None
+        _check(load().fem_op_open_peers(self.h, lo, hi))
 
     def apply_ghost_padded(self, x, ghost_lo, ghost_hi, y=None, stream=None):
         """As apply_ghost, through the CG-internal padded layout and its TMA tensor maps."""

@@ -144,3 +144,105 @@ def test_loopback_slabs_bitwise(kind, P):
     ref_tma = ref_op.apply_ghost_padded(x, None, None)
     assert torch.equal(torch.cat(outs_tma), ref_tma)
     assert float((ref_tma - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_peer_halo_bitwise(kind, P):
+    """Peer halo: every slab operator reads its ghost planes from the neighbour operators' padded
+    buffers inside the TMA pipeline (fem_op_link_peers), reproducing P = 1 bitwise."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2308_09839_b200 import fem
+    nx, ny, nz, h = 37, 30, 23, 0.04
+    c = I.ncomp(kind)
+    g = I.rng(I.SEED_BASE + 510)
+    x = torch.from_numpy(I.uniform_vector(g, nx, ny, nz, c)).cuda()
+    lam, mu = I.materials(g, nx, ny, nz)
+    ref_op = fem.Operator(fem.Mesh(nx, ny, nz, h), kind, 1)
+    if kind == "elastic":
+        ref_op.set_material(lam, mu)
+    ref = ref_op.apply_ghost_padded(x, None, None)
+    plane = (nx + 1) * (ny + 1) * c
+    ops, xs, keep = [], [], []
+    for r in range(P):
+        comm = fem.Comm(P, r)
+        mesh = fem.Mesh(nx, ny, nz, h, comm)
+        k0, k1 = mesh.plane_begin, mesh.plane_end
+        op = fem.Operator(mesh, kind, 1)
+        if kind == "elastic":
+            lb, le = max(k0 - 1, 0), min(k1, nz)
+            op.set_material(np.ascontiguousarray(lam[lb * nx * ny:le * nx * ny]),
+                            np.ascontiguousarray(mu[lb * nx * ny:le * nx * ny]), lb, le - lb)
+        ops.append(op); xs.append(x[k0 * plane:k1 * plane].contiguous()); keep.append((comm, mesh))
+    for r, op in enumerate(ops):
+        op.link_peers(ops[r - 1] if r > 0 else None, ops[r + 1] if r < P - 1 else None)
+        assert op.get_option("peer_halo") == 1
+    for r, op in enumerate(ops):  # first pass stages every slab's x in its padded buffer
+        op.apply_ghost_padded(xs[r], None, None)
+    y = torch.cat([op.apply_ghost_padded(xs[r], None, None) for r, op in enumerate(ops)])
+    assert torch.equal(y, ref)
+
+
+def _ipc_worker(rank, world, port, kind, q):
+    import torch.distributed as dist
+    from paper_2308_09839_b200 import fem
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        nx, ny, nz, h = 37, 30, 23, 0.04
+        c = I.ncomp(kind)
+        g = I.rng(I.SEED_BASE + 520)
+        xfull = I.uniform_vector(g, nx, ny, nz, c)
+        lam, mu = I.materials(g, nx, ny, nz)
+        comm = fem.Comm(world, rank)  # virtual: the partition; the exchange goes through IPC
+        mesh = fem.Mesh(nx, ny, nz, h, comm)
+        k0, k1 = mesh.plane_begin, mesh.plane_end
+        op = fem.Operator(mesh, kind, 1)
+        if kind == "elastic":
+            lb, le = max(k0 - 1, 0), min(k1, nz)
+            op.set_material(np.ascontiguousarray(lam[lb * nx * ny:le * nx * ny]),
+                            np.ascontiguousarray(mu[lb * nx * ny:le * nx * ny]), lb, le - lb)
+        infos = [None] * world
+        dist.all_gather_object(infos, op.peer_info())
+        op.open_peers(infos[rank - 1] if rank > 0 else None, infos[rank + 1] if rank < world - 1 else None)
+        plane = (nx + 1) * (ny + 1) * c
+        xl = torch.from_numpy(xfull[k0 * plane:k1 * plane].copy()).cuda()
+        op.apply_ghost_padded(xl, None, None)  # stage x in the padded buffer the neighbours read
+        torch.cuda.synchronize(); dist.barrier()
+        y = op.apply_ghost_padded(xl, None, None)
+        torch.cuda.synchronize(); dist.barrier()
+        outs = [None] * world
+        dist.all_gather_object(outs, y.cpu().numpy())
+        if rank == 0:
+            ref_op = fem.Operator(fem.Mesh(nx, ny, nz, h), kind, 1)
+            if kind == "elastic":
+                ref_op.set_material(lam, mu)
+            ref = ref_op.apply_ghost_padded(torch.from_numpy(xfull).cuda(), None, None).cpu().numpy()
+            q.put(bool(np.array_equal(np.concatenate(outs), ref)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as ex:  # reported to the parent
+        q.put(repr(ex))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["scalar", "elastic"])
+def test_ipc_peer_halo_two_processes(kind):
+    """Two processes on one GPU exchange CUDA IPC handles (fem_op_peer_info / fem_op_open_peers,
+    bytes sent over gloo); each slab's apply loads its ghost planes from the other process's
+    memory inside the TMA pipeline; the slabs reproduce P = 1 bitwise."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert res is True, res
