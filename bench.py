@@ -268,6 +268,8 @@ def run_native(args, cfg):
         op.set_option("quadrature", 1)
     if args.cgcg:  # Chronopoulos-Gear single-reduction CG (NEXT #1)
         op.set_option("cg_variant", 1)
+    if args.peer_halo and ws > 1 and not hexmesh:  # ghost planes over NVLink inside the apply (NEXT #3)
+        op.set_option("peer_halo", 1)
     ndof_global = op.n_global * (ws if hexmesh else 1)
     k0, k1 = (0, nz + 1) if hexmesh else (mesh.plane_begin, mesh.plane_end)
     plane = (nx + 1) * (ny + 1)
@@ -436,7 +438,8 @@ def run_native(args, cfg):
                                 f"U(-{cfg['jitter']}, {cfg['jitter']}) h" if hexmesh else "box"),
                        "ndof": ndof_global, "bc": "dirichlet_box",
                        "material": "E=10^U(0,2), nu=U(0.20,0.35) per cell" if kind == "elastic" else None,
-                       "parallelism": f"z-slab x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": (f"z-slab x{ws}" + (" peer-halo" if args.peer_halo else " nccl-halo"))
+                                      if ws > 1 else "single GPU",
                        "l2": "inputs larger than L2 (vectors %.2f GB each)" % (ndof_global * 8 / 1e9)},
             "roofline": ({"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": traffic,
@@ -588,6 +591,8 @@ def main():
     ap.add_argument("--csr-n", type=int, default=0)
     ap.add_argument("--e2e-iters", type=int, default=100)
     ap.add_argument("--n", type=int, default=0, help="override cells per direction (debug)")
+    ap.add_argument("--peer-halo", action="store_true",
+                    help="N > 1: ghost planes read by the apply kernels from the neighbours' memory (CUDA IPC)")
     ap.add_argument("--cgcg", action="store_true",
                     help="Chronopoulos-Gear single-reduction CG (one allreduce of 2 values per iteration)")
     ap.add_argument("--gll", action="store_true",
