@@ -189,7 +189,8 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * 2x2x2 Gauss-Legendre rule, default; 1: the 2x2x2 Gauss-Lobatto rule collocated with the nodes,
  * the quadrature of the CEED benchmark problems BP5 / BP6 the paper names, P:581, P:638,
  * a different operator (the 7-point stencil for Laplace on the box); applies to
- * every kernel of the operator incl. fem_csr_create), "cg_variant" (0: the fused
+ * every kernel of the operator incl. fem_csr_create; on a general hex mesh, switching to 1
+ * checks det J > 0 at the nodes, FEM_EINVAL otherwise), "cg_variant" (0: the fused
  * Hestenes-Stiefel CG of Table 4, default; 1: Chronopoulos-Gear single-reduction CG -- r.r and
  * w.r come out of the apply together, one allreduce of two values per iteration instead of two;
  * TMA path only, reads back 0 elsewhere), "peer_halo" (1: collective over the slab ranks --

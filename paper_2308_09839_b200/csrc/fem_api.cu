@@ -644,7 +644,7 @@ int fem_mesh_create_hex(int64_t n_nodes, int64_t n_cells, const double* coords, 
   }
   if (launch_hex_pack_cells(d_vtk, d_dir, n_cells, n_nodes, reinterpret_cast<int*>(m->hx_cells), d_bad, 0,
                             m->sm_count) != cudaSuccess ||
-      launch_hex_check(m->hx_cells, m->hx_xyz, n_cells, n_nodes, d_bad, 0, m->sm_count) != cudaSuccess)
+      launch_hex_check(m->hx_cells, m->hx_xyz, n_cells, n_nodes, 0, d_bad, 0, m->sm_count) != cudaSuccess)
     return bail(fail(FEM_ECUDA, "mesh validation launch failed"));
   unsigned long long bad[2] = {0, 0};
   if (cudaMemcpy(bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost) != cudaSuccess)
@@ -1427,6 +1427,20 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
   } else if (!std::strcmp(key, "quadrature")) {
     if (value != 0 && value != 1) return fail(FEM_EINVAL, "quadrature must be 0 (Gauss) or 1 (Gauss-Lobatto)");
+    if (value == 1 && op->mesh->hex) {  // the Lobatto points are the nodes: det J > 0 there too
+      FEM_TRY(set_device(op->mesh->device));
+      unsigned long long* d_bad = nullptr;
+      FEM_TRY(dalloc(&d_bad, 2));
+      unsigned long long bad[2] = {0, 0};
+      cudaError_t e = cudaMemset(d_bad, 0, sizeof(bad));
+      if (e == cudaSuccess)
+        e = launch_hex_check(op->mesh->hx_cells, op->mesh->hx_xyz, op->mesh->hx_ncells, op->mesh->hx_nodes, 1, d_bad,
+                             0, op->mesh->sm_count);
+      if (e == cudaSuccess) e = cudaMemcpy(bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost);
+      cudaFree(d_bad);
+      if (e != cudaSuccess) return fail(FEM_ECUDA, "mesh check: %s", cudaGetErrorString(e));
+      if (bad[1]) return fail(FEM_EINVAL, "%llu cells have det J <= 0 at a node (Gauss-Lobatto point)", bad[1]);
+    }
     op->quad = (int)value;
     FEM_TRY(set_device(op->mesh->device));
     FEM_TRY(pa_setup(op));

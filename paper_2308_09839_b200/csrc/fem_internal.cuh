@@ -145,8 +145,9 @@ cudaError_t launch_hex_pa_apply(int kind, int bc, int quad, const int4* cells, c
 // y = x on the constrained nodes; mode 1: sc->pq += sum x_b^2
 cudaError_t launch_hex_dirichlet(const int32_t* nodes, int64_t nb, int comps, const double* x, double* y,
                                  int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
-// bad[0] += cells with an out-of-range node, bad[1] += cells with det J <= 0 at a Gauss point
-cudaError_t launch_hex_check(const int4* cells, const double4* xyz, int64_t ncells, int64_t nnodes,
+// bad[0] += cells with an out-of-range node, bad[1] += cells with det J <= 0 at a point of the
+// rule (0: the 2x2x2 Gauss points, 1: the Gauss-Lobatto points = the nodes)
+cudaError_t launch_hex_check(const int4* cells, const double4* xyz, int64_t ncells, int64_t nnodes, int rule,
                              unsigned long long* bad, cudaStream_t s, int sm_count);
 // VTK-ordered int32 node map (+ optional uint8 Dirichlet flags) -> internal cell records
 cudaError_t launch_hex_pack_cells(const int32_t* vtk, const uint8_t* dir, int64_t ncells, int64_t nnodes,

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) hex_dirichlet_kernel(const int32_t* __res
 // validation: node ids in range, det J > 0 at every Gauss point
 __global__ void __launch_bounds__(256) hex_check_kernel(const int4* __restrict__ cells,
                                                         const double4* __restrict__ xyz, int64_t ncells,
-                                                        int64_t nnodes, unsigned long long* bad) {
+                                                        int64_t nnodes, int rule, unsigned long long* bad) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncells; e += stride) {
     const int4 lo = cells[2 * e], hi = cells[2 * e + 1];
@@ -279,9 +279,9 @@ __global__ void __launch_bounds__(256) hex_check_kernel(const int4* __restrict__
     const Modal ux = hadamard(X), uy = hadamard(Y), uz = hadamard(Z);
     bool pos = true;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {  // the 8 Gauss points, then the 8 Gauss-Lobatto points (nodes)
+    for (int q = 0; q < 8; ++q) {  // the 8 points of the rule: Gauss (0) or Gauss-Lobatto = nodes (1)
       Modal mx = ux, my = uy, mz = uz;
-      if (q < 8) { prescale<false>(mx); prescale<false>(my); prescale<false>(mz); }
+      if (rule == 0) { prescale<false>(mx); prescale<false>(my); prescale<false>(mz); }
       const double sx = (q & 1) ? 1.0 : -1.0, sy = (q & 2) ? 1.0 : -1.0, sz = (q & 4) ? 1.0 : -1.0;
       double J[3][3];
       const Modal* f[3] = {&mx, &my, &mz};
@@ -567,9 +567,9 @@ cudaError_t launch_hex_dirichlet(const int32_t* nodes, int64_t nb, int comps, co
   return cudaGetLastError();
 }
 
-cudaError_t launch_hex_check(const int4* cells, const double4* xyz, int64_t ncells, int64_t nnodes,
+cudaError_t launch_hex_check(const int4* cells, const double4* xyz, int64_t ncells, int64_t nnodes, int rule,
                              unsigned long long* bad, cudaStream_t s, int sm_count) {
-  hex_check_kernel<<<grid_for(ncells, 256, sm_count, 8), 256, 0, s>>>(cells, xyz, ncells, nnodes, bad);
+  hex_check_kernel<<<grid_for(ncells, 256, sm_count, 8), 256, 0, s>>>(cells, xyz, ncells, nnodes, rule, bad);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -11,6 +11,9 @@ timeout 300 python bench.py --config 1 --no-cpu > $OUT/bench_c2.json 2> $OUT/ben
 timeout 300 python bench.py --config 2 --no-cpu > $OUT/bench_c3.json 2> $OUT/bench_c3.err
 timeout 300 python bench.py --config 0 --no-cpu --no-csr > $OUT/bench_c1.json 2> $OUT/bench_c1.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+for c in 4 5 6 7; do timeout 400 python bench.py --config $c --no-cpu > $OUT/bench_x$c.json 2> $OUT/bench_x$c.err; done
+timeout 300 python bench.py --config 6 --pa --no-cpu > $OUT/bench_x6pa.json 2> $OUT/bench_x6pa.err
+for c in 1 2; do timeout 300 python bench.py --config $c --gll --no-cpu --no-e2e > $OUT/bench_gll$c.json 2> $OUT/bench_gll$c.err; done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c4.csv \
   python bench.py --steps 3 --warmup 3 --no-e2e --no-csr --no-cpu > $OUT/ncu_launch.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:elastic_kernel -s 6 -c 1 \
