@@ -1361,7 +1361,9 @@ int fem_cg_solve(fem_op_t op, const double* b, double* x, double tol, int32_t ma
   if (!xd) { CUDA_TRY(cudaMemcpyAsync(op->stage_a, x, bytes, cudaMemcpyHostToDevice, s)); xs = op->stage_a; }
   FEM_TRY(cg_begin_dev(op, bs, xs, tol, maxit, s));
   int done_it = 0;
-  const int chunk = std::max(1, op->check_every);
+  // tol == 0 runs exactly maxit iterations unless r.r == 0 / breakdown, which the kernels stop on
+  // by themselves (done flag): no intermediate host polls needed
+  const int chunk = tol == 0.0 ? std::max(1, maxit) : std::max(1, op->check_every);
   while (done_it < maxit) {
     const int n = std::min(chunk, maxit - done_it);
     FEM_TRY(cg_iterate_dev(op, n, s));
