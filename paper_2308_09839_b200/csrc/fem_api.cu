@@ -773,7 +773,9 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   // padded layout: even row pitch, lead so that the tensor origin node is 16-B aligned
   op->pl_rp = ((g.nx + 1) * op->comps + 1) & ~1LL;
   op->pl_pp = op->pl_rp * (g.ny + 1);
-  op->tm_interior = bc && kind != FEM_ELASTICITY;
+  // Laplace tensors span the whole box like elasticity's (mask in registers, identity rows from
+  // the staged planes); FEM_LAP_INTERIOR=1 restores interior-only tensors (zero fill = mask)
+  op->tm_interior = FEM_LAP_INTERIOR && bc && kind != FEM_ELASTICITY;
   op->pl_lead = op->tm_interior ? (op->comps & 1) : 0;  // tensor-origin node 16-B aligned
   op->pl_n = (op->pl_lead + (op->nloc_planes + 2) * op->pl_pp + 1) & ~1LL;
   op->pl_off = op->pl_lead + op->pl_pp;

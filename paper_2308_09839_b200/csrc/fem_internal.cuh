@@ -93,6 +93,9 @@ constexpr int kMaxCtas = 1 << 16;
 #define FEM_LAP_R1 3
 #endif
 constexpr int kLapTX = 32, kLapTY = FEM_LAP_TY, kLapR1 = FEM_LAP_R1, kLapR3 = 1;  // Laplace: C=1 / C=3 rows per thread
+#ifndef FEM_LAP_INTERIOR
+#define FEM_LAP_INTERIOR 0  // 1: Laplace CG tensors span the Dirichlet interior only (round-1 layout)
+#endif
 #ifndef FEM_EL_TY
 #define FEM_EL_TY 15
 #endif

@@ -153,6 +153,15 @@ inline WorkGrid make_workgrid(int xt, int yt, int64_t nplanes, int64_t slots, in
   return best;
 }
 
+// Host: cover n nodes with tiles of at most tmax, all tiles (but possibly the last) equally wide:
+// returns the tile count, *per = nodes per tile.  (257 nodes at tmax 32 -> 9 tiles of 29 instead
+// of 8 x 32 + a 1-node sliver that streams every plane for one column.)
+inline int64_t balanced_tiles(int64_t n, int tmax, int* per) {
+  const int64_t tiles = (n + tmax - 1) / tmax;
+  *per = (int)((n + tiles - 1) / tiles);
+  return (n + *per - 1) / *per;
+}
+
 // Tensor-map coordinates of a tile: box origin = node (ilo, jlo) of plane k, relative to the
 // tensor origin (node (t_i0, t_j0) of plane t_k0).  Out-of-range coordinates zero-fill.
 struct TmaOrigin {

@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
     elastic_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                    const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
-                   int bc, int64_t kchunk, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer) {
+                   int bc, int64_t kchunk, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
+                   int txa, int tya) {
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   // TY consumer warps (lane = cell column, warp = cell row) + 1 producer warp
@@ -70,11 +71,12 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
-  // output tile: nodes i0 .. i0+TX-2, j0 .. j0+TY-2; thread (tx,ty) owns cell (i0-1+tx, j0-1+ty)
-  // and outputs node (i0-1+tx, j0+ty) (when tx >= 1, ty <= TY-2) from its top corners + the
-  // bottom corners handed down by the warp above
-  const int64_t i0 = (int64_t)blockIdx.x * (TX - 1);
-  const int64_t j0 = (int64_t)blockIdx.y * (TY - 1);
+  // output tile: nodes i0 .. i0+txa-1, j0 .. j0+tya-1 (txa <= TX-1, tya <= TY-1, balanced over
+  // the mesh by the launcher); thread (tx,ty) owns cell (i0-1+tx, j0-1+ty) and outputs node
+  // (i0-1+tx, j0+ty) (when 1 <= tx <= txa, ty < tya) from its top corners + the bottom corners
+  // handed down by the warp above
+  const int64_t i0 = (int64_t)blockIdx.x * txa;
+  const int64_t j0 = (int64_t)blockIdx.y * tya;
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;  // planes kb-1 .. ke (cell layers kb-1 .. ke-1)
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
     // Dirichlet mask flags of the cell's node columns ci, ci+1 and rows cj, cj+1 (TMA path)
     const bool mc0 = bc && (ci == 0 || ci == g.nx), mc1 = bc && (ci + 1 == 0 || ci + 1 == g.nx);
     const bool mr0 = bc && (cj == 0 || cj == g.ny), mr1 = bc && (cj + 1 == 0 || cj + 1 == g.ny);
-    const bool owner = tx >= 1 && ty <= TY - 2 && ci <= g.nx && nj <= g.ny;
+    const bool owner = tx >= 1 && tx <= txa && ty < tya && ci <= g.nx && nj <= g.ny;
     const bool bnode_xy = bc && (ci == 0 || ci == g.nx || nj == 0 || nj == g.ny);
     // output / boundary-read pointers, advanced by one plane per output plane
     double* yp = yo.y + (kb - g.k0) * yo.ppitch + (owner ? nj * yo.rpitch + ci * 3 : 0);
@@ -319,8 +321,9 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
     if (e != cudaSuccess) return e;
     attr_set[mode + 4 * gll] = true;
   }
-  const int64_t xt = (g.nx + 1 + (TX - 1) - 1) / (TX - 1);
-  const int64_t yt = (g.ny + 1 + (TY - 1) - 1) / (TY - 1);
+  int txa, tya;
+  const int64_t xt = balanced_tiles(g.nx + 1, TX - 1, &txa);
+  const int64_t yt = balanced_tiles(g.ny + 1, TY - 1, &tya);
   const int64_t nplanes = g.k1 - g.k0;
   int64_t zc = ((kElTY <= 7 ? 8LL : 4LL) * sm_count + xt * yt - 1) / (xt * yt);
   // chunks of >= 8 planes amortise the pipeline fill; a mesh too small to fill the GPU that
@@ -343,7 +346,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   PeerMaps pm;
   if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
   kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
-                                 bc, kchunk, sc, red, pm);
+                                 bc, kchunk, sc, red, pm, txa, tya);
   add_launches(1);
   return cudaGetLastError();
 }

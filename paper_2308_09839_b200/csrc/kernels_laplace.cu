@@ -26,8 +26,10 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
                    double* pnew, int bc, int tmint, int64_t kchunk, CgScalars* sc, Reduce red,
-                   const __grid_constant__ PeerMaps peer) {
-  (void)tmint;  // Laplace uses interior-only tensors with the Dirichlet box (zero fill = mask)
+                   const __grid_constant__ PeerMaps peer, int txa, int rya) {
+  // tmint = 1: the u tensor spans only the Dirichlet interior (TMA zero fill = the mask P, the
+  // identity rows read x from global memory); 0: the tensor spans the whole box, the mask is
+  // applied in registers and the identity rows use the staged values (no global loads).
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   // TY consumer warps (one node column per lane, R node rows each) + 1 producer warp
@@ -46,8 +48,10 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
-  const int64_t i0 = (int64_t)blockIdx.x * TX;
-  const int64_t j0 = (int64_t)blockIdx.y * (TY * R);
+  // tile = txa <= TX node columns x rya <= TY*R node rows: the launcher balances the tiles over
+  // the mesh (e.g. 257 columns = 9 x 29, not 8 x 32 + 1) so no CTA streams planes for a sliver
+  const int64_t i0 = (int64_t)blockIdx.x * txa;
+  const int64_t j0 = (int64_t)blockIdx.y * rya;
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;
@@ -69,11 +73,25 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
     for (int r = 0; r < R; ++r) {
       const int64_t j = j0 + ty * R + r;
       my[r] = (double)((j > 0) + (j < g.ny));
-      active[r] = (i <= g.nx) && (j <= g.ny);
+      active[r] = (i <= g.nx) && (j <= g.ny) && tx < txa && ty * R + r < rya;
       bnode_xy[r] = bc && (i == 0 || i == g.nx || j == 0 || j == g.ny);
       off_y[r] = j * yo.rpitch + i * C;
       off_x[r] = j * x.rpitch + i * C;
     }
+    // Dirichlet mask of the full-box tensor (TM && !tmint): node columns i-1, i, i+1 and the
+    // R+2 node rows this thread reads; warp-uniform `wedge` selects the masked x-filter
+    const bool rmask = TM && bc && !tmint;
+    const bool cmm = rmask && (i - 1 == 0 || i - 1 == g.nx), cm0 = rmask && (i == 0 || i == g.nx);
+    const bool cmp = rmask && (i + 1 == 0 || i + 1 == g.nx);
+    bool rmk[R + 2];
+    bool anym = cmm || cm0 || cmp;
+#pragma unroll
+    for (int rr = 0; rr < R + 2; ++rr) {
+      const int64_t jr = j0 + ty * R + rr - 1;
+      rmk[rr] = rmask && (jr == 0 || jr == g.ny);
+      anym = anym || rmk[rr];
+    }
+    const bool wedge = __any_sync(0xffffffffu, anym);
     // windows: c1, c2 and the centre value for planes p-2, p-1, p
     double c1w[3][R][C], c2w[3][R][C], xcw[2][R][C];
 #pragma unroll
@@ -104,24 +122,36 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
         }
       // x-direction filters for the R+2 rows this thread needs
       double a[R + 2][C], b[R + 2][C];
+      auto xfilter = [&](auto masked) {
+        constexpr bool MK = decltype(masked)::value;
+        const bool pm = MK && (p == 0 || p == g.nz);  // Dirichlet face plane
 #pragma unroll
-      for (int rr = 0; rr < R + 2; ++rr) {
-        const double* row = ring.row_ptr(slot, ty * R + rr) + tx * C;
-        const double* row2 = row + Ring::UDBL;  // mode 2: p_old box
+        for (int rr = 0; rr < R + 2; ++rr) {
+          const double* row = ring.row_ptr(slot, ty * R + rr) + tx * C;
+          const double* row2 = row + Ring::UDBL;  // mode 2: p_old box
+          const bool rz = MK && (pm || rmk[rr]);
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          double xm = row[c], x0 = row[C + c], xp = row[2 * C + c];
-          if (mode == 2) {
-            xm = fma(beta, row2[c], xm);
-            x0 = fma(beta, row2[C + c], x0);
-            xp = fma(beta, row2[2 * C + c], xp);
+          for (int c = 0; c < C; ++c) {
+            double xm = row[c], x0 = row[C + c], xp = row[2 * C + c];
+            if (mode == 2) {
+              xm = fma(beta, row2[c], xm);
+              x0 = fma(beta, row2[C + c], x0);
+              xp = fma(beta, row2[2 * C + c], xp);
+            }
+            if (rr >= 1 && rr <= R) xcw[1][rr - 1][c] = x0;  // unmasked (identity rows)
+            if (MK) {
+              xm = (rz || cmm) ? 0.0 : xm;
+              x0 = (rz || cm0) ? 0.0 : x0;
+              xp = (rz || cmp) ? 0.0 : xp;
+            }
+            const double sn = xm + xp;
+            a[rr][c] = GLL ? (3.0 * mx) * x0 : fma(2.0 * mx, x0, sn);
+            b[rr][c] = fma(mx, x0, -sn);
           }
-          const double sn = xm + xp;
-          a[rr][c] = GLL ? (3.0 * mx) * x0 : fma(2.0 * mx, x0, sn);
-          b[rr][c] = fma(mx, x0, -sn);
-          if (rr >= 1 && rr <= R) xcw[1][rr - 1][c] = x0;
         }
-      }
+      };
+      if (rmask && (wedge || p == 0 || p == g.nz)) xfilter(std::true_type{});
+      else xfilter(std::false_type{});
       ring.release(slot, tx);
       // y-direction
 #pragma unroll
@@ -154,8 +184,10 @@ __global__ void __launch_bounds__(TX*(TY + 1), 2)
           for (int c = 0; c < C; ++c) {
             double v, xv = xcw[0][r][c];
             if (qface || bnode_xy[r]) {
-              xv = xq[off_x[r] + c];
-              if (mode == 2) xv = fma(beta, pq_old[off_x[r] + c], xv);
+              if (!rmask) {  // interior tensor / row path: boundary values are not staged
+                xv = xq[off_x[r] + c];
+                if (mode == 2) xv = fma(beta, pq_old[off_x[r] + c], xv);
+              }
               v = xv;
             } else {
               const double nb = (c2w[0][r][c] - c1w[0][r][c]) + (c2w[2][r][c] - c1w[2][r][c]);
@@ -216,8 +248,9 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
     if (e != cudaSuccess) return e;
     attr_set[mode + 4 * gll] = true;
   }
-  const int64_t xt = (g.nx + 1 + TX - 1) / TX;
-  const int64_t yt = (g.ny + 1 + TY * R - 1) / (TY * R);
+  int txa, rya;
+  const int64_t xt = balanced_tiles(g.nx + 1, TX, &txa);
+  const int64_t yt = balanced_tiles(g.ny + 1, TY * R, &rya);
   const int64_t nplanes = g.k1 - g.k0;
   // z-chunks: about 4 resident waves of CTAs (2 per SM), chunks of >= 16 planes
   int64_t zc = (8LL * sm_count + xt * yt - 1) / (xt * yt);
@@ -240,7 +273,8 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
   PeerMaps pm;
   if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
-  kern<<<grid, block, smem, s>>>(g, x, y, um, org, um2, maps.pold, maps.pnew, bc, maps.interior, kchunk, sc, red, pm);
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, um2, maps.pold, maps.pnew, bc, maps.interior, kchunk, sc, red, pm,
+                                 txa, rya);
   add_launches(1);
   return cudaGetLastError();
 }
