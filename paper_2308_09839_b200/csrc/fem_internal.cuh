@@ -92,7 +92,14 @@ constexpr int kMaxCtas = 1 << 16;
 #ifndef FEM_LAP_R1
 #define FEM_LAP_R1 3
 #endif
+#ifndef FEM_LAP_MINB
+#define FEM_LAP_MINB 2  // resident CTAs per SM the Laplace apply is compiled for (register cap)
+#endif
+#ifndef FEM_LAP_S1
+#define FEM_LAP_S1 8  // ring stages of the scalar fused CG apply
+#endif
 constexpr int kLapTX = 32, kLapTY = FEM_LAP_TY, kLapR1 = FEM_LAP_R1, kLapR3 = 1;  // Laplace: C=1 / C=3 rows per thread
+constexpr int kLapMinB = FEM_LAP_MINB, kLapS1 = FEM_LAP_S1;
 #ifndef FEM_LAP_INTERIOR
 #define FEM_LAP_INTERIOR 0  // 1: Laplace CG tensors span the Dirichlet interior only (round-1 layout)
 #endif
@@ -100,13 +107,26 @@ constexpr int kLapTX = 32, kLapTY = FEM_LAP_TY, kLapR1 = FEM_LAP_R1, kLapR3 = 1;
 #define FEM_EL_TY 15
 #endif
 constexpr int kElTY = FEM_EL_TY;                                      // elasticity consumer warps
+#ifndef FEM_EL_CY
+#define FEM_EL_CY 2  // cell rows per thread of the elasticity apply (1: elastic_kernel, 2: elastic2_kernel)
+#endif
+#ifndef FEM_EL2_TY
+#define FEM_EL2_TY 7  // consumer warps of elastic2_kernel (2 cell rows each)
+#endif
+#ifndef FEM_EL2_S
+#define FEM_EL2_S 4  // ring stages of elastic2_kernel in fused CG (x2 for one input box)
+#endif
+constexpr int kElCY = FEM_EL_CY, kEl2TY = FEM_EL2_TY, kEl2S = FEM_EL2_S;
+constexpr int kElCellRows = kElCY == 2 ? 2 * kEl2TY : kElTY;  // cell rows per TMA tile (= u box rows - 1)
+// material box rows: shared by elastic2_kernel (TMA path) and elastic_kernel (caller vectors)
+constexpr int kElMatRows = kElCellRows > kElTY ? kElCellRows : kElTY;
 // u-plane TMA box (doubles x rows) per kind: width = (((cols * C) + 1) & ~1) + 2
 inline void u_box(int kind, unsigned* w, unsigned* h) {
   if (kind == 0) { *w = ((((kLapTX + 2) * 1) + 1) & ~1) + 2; *h = kLapTY * kLapR1 + 2; }
   else if (kind == 1) { *w = ((((kLapTX + 2) * 3) + 1) & ~1) + 2; *h = kLapTY * kLapR3 + 2; }
-  else { *w = ((((32 + 1) * 3) + 1) & ~1) + 2; *h = kElTY + 1; }
+  else { *w = ((((32 + 1) * 3) + 1) & ~1) + 2; *h = kElCellRows + 1; }
 }
-inline void mat_box(unsigned* w, unsigned* h) { *w = 2 * 32; *h = kElTY; }
+inline void mat_box(unsigned* w, unsigned* h) { *w = 2 * 32; *h = kElMatRows; }
 
 // ---- launchers (return cudaError_t of the launch) -----------------------------------------
 // mode: 0 plain apply (y = A_c x), 1 CG apply (also pq partial -> sc->pq; skips if sc->done),

@@ -55,7 +55,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
   constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
   constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
   constexpr int TPART = 4 * TY * TX * 3;  // y hand-off buffers (ring of 4)
-  using Ring = PlaneRing<TM, ROWS, COLS, 3, S, TY, TX, NU>;
+  using Ring = PlaneRing<TM, ROWS, COLS, 3, S, kElMatRows, TX, NU>;
+  static_assert(kElMatRows >= TY, "material box covers the tile's cell rows");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
@@ -297,12 +298,372 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
   }
 }
 
+// ---- two cell rows per thread (FEM_EL_CY = 2) -------------------------------
+// One cell layer of the modal closed form: (bottom face fb, top face ft, lambda h/16, mu h/16)
+// -> complete face F at the bottom plane (carried top face cb of the layer below + this layer's
+// bottom face), cbo <- this layer's top face.  Same arithmetic as the loop body of elastic_kernel.
+template <bool GLL>
+__device__ __forceinline__ void elastic_layer(const Face* fb, const Face* ft, double L0, double M0,
+                                              const double* cb, double* cbo, double* F) {
+  const double ux = fb[0].x + ft[0].x, uy = fb[0].y + ft[0].y, uxy = fb[0].xy + ft[0].xy;
+  const double uz = ft[0].s - fb[0].s, uxz = ft[0].x - fb[0].x, uyz = ft[0].y - fb[0].y, uxyz = ft[0].xy - fb[0].xy;
+  const double vx = fb[1].x + ft[1].x, vy = fb[1].y + ft[1].y, vxy = fb[1].xy + ft[1].xy;
+  const double vz = ft[1].s - fb[1].s, vxz = ft[1].x - fb[1].x, vyz = ft[1].y - fb[1].y, vxyz = ft[1].xy - fb[1].xy;
+  const double wx = fb[2].x + ft[2].x, wy = fb[2].y + ft[2].y, wxy = fb[2].xy + ft[2].xy;
+  const double wz = ft[2].s - fb[2].s, wxz = ft[2].x - fb[2].x, wyz = ft[2].y - fb[2].y, wxyz = ft[2].xy - fb[2].xy;
+  const double M2 = M0 + M0;
+  const double S0 = ux + vy + wz;
+  const double LS0 = L0 * S0;
+  const double gux = fma(M2, ux, LS0), gvy = fma(M2, vy, LS0), gwz = fma(M2, wz, LS0);
+  const double tuv = M0 * (uy + vx), tuw = M0 * (uz + wx), tvw = M0 * (vz + wy);
+  const double guy = tuv, gvx = tuv, guz = tuw, gwx = tuw, gvz = tvw, gwy = tvw;
+  const double L1 = GLL ? L0 : L0 * (1.0 / 3.0), M1 = GLL ? M0 : M0 * (1.0 / 3.0);
+  const double Sxi = vxy + wxz, Seta = uxy + wyz, Szeta = uxz + vyz;
+  const double LSxi = L1 * Sxi, LSeta = L1 * Seta, LSzeta = L1 * Szeta;
+  const double MB = GLL ? 3.0 * M0 : M0;
+  const double guxy = fma(MB, uxy, LSeta), gwyz = fma(MB, wyz, LSeta);
+  const double gvxy = fma(MB, vxy, LSxi), gwxz = fma(MB, wxz, LSxi);
+  const double guxz = fma(MB, uxz, LSzeta), gvyz = fma(MB, vyz, LSzeta);
+  const double T = uyz + vxz + wxy;
+  const double guyz = M1 * (T + uyz), gvxz = M1 * (T + vxz), gwxy = M1 * (T + wxy);
+  const double K3 = GLL ? fma(4.0, M0, L0) : fma(4.0, M0, L0) * (1.0 / 9.0);
+  const double guxyz = K3 * uxyz, gvxyz = K3 * vxyz, gwxyz = K3 * wxyz;
+  const double gx[3] = {gux, gvx, gwx}, gy[3] = {guy, gvy, gwy}, gxy[3] = {guxy, gvxy, gwxy};
+  const double gz[3] = {guz, gvz, gwz}, gxz[3] = {guxz, gvxz, gwxz}, gyz[3] = {guyz, gvyz, gwyz};
+  const double gxyz[3] = {guxyz, gvxyz, gwxyz};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    F[4 * c + 0] = cb[4 * c + 0] - gz[c];
+    F[4 * c + 1] = cb[4 * c + 1] + (gx[c] - gxz[c]);
+    F[4 * c + 2] = cb[4 * c + 2] + (gy[c] - gyz[c]);
+    F[4 * c + 3] = cb[4 * c + 3] + (gxy[c] - gxyz[c]);
+    cbo[4 * c + 0] = gz[c];
+    cbo[4 * c + 1] = gx[c] + gxz[c];
+    cbo[4 * c + 2] = gy[c] + gyz[c];
+    cbo[4 * c + 3] = gxy[c] + gxyz[c];
+  }
+}
+
+// corner values of a complete face F (4 modes x 3 comps): c00, c10, c01, c11 per component
+__device__ __forceinline__ void face_corners(const double* F, int c, double& c00, double& c10, double& c01,
+                                             double& c11) {
+  const double G1 = F[4 * c + 0], Gx = F[4 * c + 1], Gy = F[4 * c + 2], Gxy = F[4 * c + 3];
+  const double es = G1 - Gy, ed = Gx - Gxy, fs = G1 + Gy, fd = Gx + Gxy;
+  c00 = es - ed; c10 = es + ed; c01 = fs - fd; c11 = fs + fd;
+}
+
+// Thread (tx, ty) owns the two cells (i0-1+tx, j0-1+2ty) ("A") and (i0-1+tx, j0+2ty) ("B"): the
+// node row between them (nA = j0+2ty) is summed in registers, the row above B (nB) with the
+// bottom corners handed down by warp ty+1.  Per cell: 9 instead of 12 staged node values, one
+// y hand-off per two cells, the x butterflies of the shared node row computed once.  Per node the
+// summation order is the one of elastic_kernel: ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j)).
+template <bool TM, int MODE, int TY, int S, bool GLL>
+__global__ void __launch_bounds__(32 * (TY + 1), 1)
+    elastic2_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
+                    TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
+                    const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
+                    int bc, int64_t kchunk, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
+                    int txa, int tya) {
+  constexpr int mode = MODE;
+  constexpr int NU = (MODE == 2) ? 2 : 1;
+  constexpr int TX = 32;
+  constexpr int NT = TX * (TY + 1);
+  constexpr int ROWS = 2 * TY + 1;  // node rows j0-1 .. j0+2TY-1
+  constexpr int COLS = TX + 1;      // node cols i0-1 .. i0+TX-1
+  constexpr int TPART = 4 * TY * TX * 3;
+  using Ring = PlaneRing<TM, ROWS, COLS, 3, S, kElMatRows, TX, NU>;
+  static_assert(kElMatRows >= 2 * TY, "material box covers the tile's cell rows");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double red_sh[32];
+  Ring ring;
+  double* tpart = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // [4][TY][TX][3]
+  uint64_t* tfull = reinterpret_cast<uint64_t*>(tpart + TPART);        // [4][TY]
+  uint64_t* tempty = tfull + 4 * TY;                                    // [4][TY]
+  ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + 4 * TY));
+  const uint32_t tfull_a = smem_u32(tfull), tempty_a = smem_u32(tempty);
+
+  if (mode >= 1 && sc->done) return;
+  const double beta = (mode == 2) ? (sc->first ? 0.0 : sc->rr_new / sc->rr) : 0.0;
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = tx + TX * ty;
+  // output tile: nodes i0 .. i0+txa-1 (txa <= TX-1), j0 .. j0+tya-1 (tya <= 2TY-1)
+  const int64_t i0 = (int64_t)blockIdx.x * txa;
+  const int64_t j0 = (int64_t)blockIdx.y * tya;
+  const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
+  const int64_t ke = min(g.k1, kb + kchunk);
+  const int64_t pfirst = kb - 1;
+  if (tid < 4 * TY) {
+    mbar_init(&tfull[tid], 1);
+    mbar_init(&tempty[tid], 1);
+  }
+  ring.init(tid, NT, TY);
+  if (TM) ring.set_tshift(i0 - 1, uorg);
+
+  double pq = 0.0, rr2 = 0.0;
+  if (ty == TY) {
+    ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, &mmap, mat_layer0, &umap2, 0, &peer);
+  } else {
+    const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + 2 * ty;  // cell A = (ci, cj), cell B = (ci, cj+1)
+    const double hs = g.h * (1.0 / 16.0);
+    const int64_t nA = cj + 1, nB = cj + 2;  // node rows this thread outputs
+    const bool mc0 = bc && (ci == 0 || ci == g.nx), mc1 = bc && (ci + 1 == 0 || ci + 1 == g.nx);
+    const bool mr0 = bc && (cj == 0 || cj == g.ny), mr1 = bc && (cj + 1 == 0 || cj + 1 == g.ny);
+    const bool mr2 = bc && (cj + 2 == 0 || cj + 2 == g.ny);
+    const bool colok = tx >= 1 && tx <= txa && ci <= g.nx;
+    const bool ownA = colok && 2 * ty < tya && nA <= g.ny;
+    const bool ownB = colok && 2 * ty + 1 < tya && nB <= g.ny;
+    const bool bnA_xy = bc && (ci == 0 || ci == g.nx || nA == 0 || nA == g.ny);
+    const bool bnB_xy = bc && (ci == 0 || ci == g.nx || nB == 0 || nB == g.ny);
+    const bool own = ownA || ownB;  // (ownB implies nA is a mesh row too)
+    double* yp = yo.y + (kb - g.k0) * yo.ppitch + (own ? nA * yo.rpitch + ci * 3 : 0);
+    const int64_t xoff0 = (kb - g.k0) * x.ppitch + (own ? nA * x.rpitch + ci * 3 : 0);
+    const double* xpb = x.main + xoff0;
+    const double* ppb = (mode == 2) ? pold + xoff0 : nullptr;
+    double* pnb = (mode == 2) ? pnew + xoff0 : nullptr;
+    const int nplane = (int)(ke - pfirst + 1);
+    const int qface0 = bc ? (int)(0 - kb) : -1000000;
+    const int qface1 = bc ? (int)(g.nz - kb) : -1000000;
+    double* const tw0 = tpart + (ty * TX + tx) * 3;
+    const double* const tr0 = tpart + ((ty + 1) * TX + tx) * 3;
+    const uint32_t tfw0 = tfull_a + 8u * ty, tew0 = tempty_a + 8u * ty;
+    const uint32_t tfr0 = tfull_a + 8u * (ty + 1), ter0 = tempty_a + 8u * (ty + 1);
+
+    // loop state in two register sets (ping-pong: the z-march is unrolled by two, so nothing is
+    // moved at the back edge): faces of cells A, B at a node plane, carried top faces, the node
+    // values of rows nA, nB, and the material of the cell layer above the plane (x h/16)
+    Face fA[2][3], fB[2][3];
+    double cA[2][12], cB[2][12];
+    double xA[2][3], xB[2][3];
+    double LA[2], MA[2], LB[2], MB[2];
+#pragma unroll
+    for (int t = 0; t < 12; ++t) { cA[0][t] = 0.0; cB[0][t] = 0.0; }
+
+    auto load_plane = [&](int t, Face* fA, Face* fB, double* xA, double* xB, double& LA, double& MA,
+                          double& LB, double& MB) {
+      const int slot = t & (S - 1);
+      ring.wait(slot, (uint32_t)((t / S) & 1));
+      const double2 lmA = ring.mat(slot, 2 * ty, tx), lmB = ring.mat(slot, 2 * ty + 1, tx);
+      const double* r0 = ring.row_ptr(slot, 2 * ty) + tx * 3;
+      const double* r1 = ring.row_ptr(slot, 2 * ty + 1) + tx * 3;
+      const double* r2 = ring.row_ptr(slot, 2 * ty + 2) + tx * 3;
+      const int64_t pl = pfirst + t;
+      const bool pface = TM && bc && (pl == 0 || pl == g.nz);
+      const bool m00 = pface || mc0 || mr0, m10 = pface || mc1 || mr0;
+      const bool m01 = pface || mc0 || mr1, m11 = pface || mc1 || mr1;
+      const bool m02 = pface || mc0 || mr2, m12 = pface || mc1 || mr2;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double a00 = r0[c], a10 = r0[3 + c], a01 = r1[c], a11 = r1[3 + c], a02 = r2[c], a12 = r2[3 + c];
+        if (mode == 2) {  // p = r + beta p_old (second box)
+          const double* q0 = r0 + Ring::UDBL;
+          const double* q1 = r1 + Ring::UDBL;
+          const double* q2 = r2 + Ring::UDBL;
+          a00 = fma(beta, q0[c], a00);
+          a10 = fma(beta, q0[3 + c], a10);
+          a01 = fma(beta, q1[c], a01);
+          a11 = fma(beta, q1[3 + c], a11);
+          a02 = fma(beta, q2[c], a02);
+          a12 = fma(beta, q2[3 + c], a12);
+        }
+        xA[c] = a01;  // node (ci, nA), unmasked
+        xB[c] = a02;  // node (ci, nB)
+        if (TM && bc && (m00 || m10 || m01 || m11 || m02 || m12)) {
+          a00 = m00 ? 0.0 : a00;
+          a10 = m10 ? 0.0 : a10;
+          a01 = m01 ? 0.0 : a01;
+          a11 = m11 ? 0.0 : a11;
+          a02 = m02 ? 0.0 : a02;
+          a12 = m12 ? 0.0 : a12;
+        }
+        // x butterflies per node row (the middle row is shared by the two faces)
+        const double s0 = a00 + a10, d0 = a10 - a00, s1 = a01 + a11, d1 = a11 - a01;
+        const double s2 = a02 + a12, d2 = a12 - a02;
+        fA[c] = Face{s0 + s1, s1 - s0, d0 + d1, d1 - d0};
+        fB[c] = Face{s1 + s2, s2 - s1, d1 + d2, d2 - d1};
+      }
+      ring.release(slot, tx);
+      LA = lmA.x * hs;
+      MA = lmA.y * hs;
+      LB = lmB.x * hs;
+      MB = lmB.y * hs;
+    };
+    load_plane(0, fA[0], fB[0], xA[0], xB[0], LA[0], MA[0], LB[0], MB[0]);
+
+    // one step of the z-march: plane t arrives in set V; the cell layer between planes t-1 (set
+    // U) and t is applied; node plane t-2 is completed and written
+    auto step = [&](int t, auto uc) {
+      constexpr int U = decltype(uc)::value, V = 1 - U;
+      load_plane(t, fA[V], fB[V], xA[V], xB[V], LA[V], MA[V], LB[V], MB[V]);
+      double FA[12], FB[12];
+      elastic_layer<GLL>(fA[U], fA[V], LA[U], MA[U], cA[U], cA[V], FA);
+      elastic_layer<GLL>(fB[U], fB[V], LB[U], MB[U], cB[U], cB[V], FB);
+      const double* xs_A = xA[U];  // node values at plane t-1 (= the output plane)
+      const double* xs_B = xB[U];
+        if (t >= 2) {  // node plane q = kb + t - 2 is complete
+          const int qo = t - 2;
+          const int b = qo & 3;
+          const uint32_t n = (uint32_t)(qo >> 2);
+          double BA[3], vA[3], TB[3];
+  #pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double a00, a10, a01, a11, b00, b10, b01, b11;
+            face_corners(FA, c, a00, a10, a01, a11);
+            face_corners(FB, c, b00, b10, b01, b11);
+            const double a10l = __shfl_up_sync(0xffffffffu, a10, 1);  // from cell i-1
+            const double a11l = __shfl_up_sync(0xffffffffu, a11, 1);
+            const double b10l = __shfl_up_sync(0xffffffffu, b10, 1);
+            const double b11l = __shfl_up_sync(0xffffffffu, b11, 1);
+            BA[c] = a10l + a00;                     // node row cj (cells row cj): to warp ty-1
+            vA[c] = (a11l + a01) + (b10l + b00);    // node row nA: cells row cj, then row cj+1
+            TB[c] = b11l + b01;                     // node row nB, cells row cj+1
+          }
+          if (ty >= 1) {
+            if (n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
+            double* dst = tw0 + b * (TY * TX * 3);
+            dst[0] = BA[0]; dst[1] = BA[1]; dst[2] = BA[2];
+            __syncwarp();
+            if (tx == 0) mbar_arrive_a(tfw0 + 8u * TY * b);
+          }
+          const bool qf = qo == qface0 || qo == qface1;
+          if (ownA) {
+            const bool bnode = bnA_xy || qf;
+  #pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              double vv = vA[c], xv = xs_A[c];
+              if (bnode) {
+                if (!TM) {
+                  xv = xpb[c];
+                  if (mode == 2) xv = fma(beta, ppb[c], xv);
+                }
+                vv = xv;
+              }
+              yp[c] = vv;
+              if (mode == 2) pnb[c] = xv;
+              if (mode >= 1) pq = fma(vv, xv, pq);
+              if (mode == 3) rr2 = fma(xv, xv, rr2);
+            }
+          }
+          if (ty < TY - 1) {
+            mbar_wait_a(tfr0 + 8u * TY * b, n & 1);
+            const double* src = tr0 + b * (TY * TX * 3);
+            double v[3];
+  #pragma unroll
+            for (int c = 0; c < 3; ++c) v[c] = TB[c] + src[c];
+            __syncwarp();
+            if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
+            if (ownB) {
+              const bool bnode = bnB_xy || qf;
+  #pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                double vv = v[c], xv = xs_B[c];
+                if (bnode) {
+                  if (!TM) {
+                    xv = xpb[x.rpitch + c];
+                    if (mode == 2) xv = fma(beta, ppb[x.rpitch + c], xv);
+                  }
+                  vv = xv;
+                }
+                yp[yo.rpitch + c] = vv;
+                if (mode == 2) pnb[x.rpitch + c] = xv;
+                if (mode >= 1) pq = fma(vv, xv, pq);
+                if (mode == 3) rr2 = fma(xv, xv, rr2);
+              }
+            }
+          }
+          if (mode == 2) { ppb += x.ppitch; pnb += x.ppitch; }
+          yp += yo.ppitch;
+          xpb += x.ppitch;
+        }
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+#pragma unroll 1
+    for (int t = 1; t < nplane; t += 2) {
+      step(t, I0{});
+      if (t + 1 >= nplane) break;
+      step(t + 1, I1{});
+    }
+  }
+  if (mode == 3) {
+    const double bd = block_sum(pq, red_sh);
+    const double bg = block_sum(rr2, red_sh);
+    double td, tg;
+    if (last_block_reduce2(bd, bg, red, red_sh, &td, &tg)) {
+      sc->pq = td;
+      sc->rr_new = tg;
+    }
+  } else if (mode >= 1) {
+    double bsum = block_sum(pq, red_sh);
+    double total;
+    if (last_block_reduce(bsum, red, red_sh, &total)) {
+      sc->pq = total;
+      if (mode == 2) {
+        sc->rr = sc->rr_new;
+        sc->first = 0;
+      }
+    }
+  }
+}
+
+template <bool TM, int TY, int S>
+static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int bc, int mode,
+                               CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
+  constexpr int TX = 32;
+  using Ring1 = PlaneRing<TM, 2 * TY + 1, TX + 1, 3, S, kElMatRows, TX, 1>;
+  using Ring2 = PlaneRing<TM, 2 * TY + 1, TX + 1, 3, S, kElMatRows, TX, (TM ? 2 : 1)>;
+  const size_t ring_bytes = mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META;
+  const size_t smem = ring_bytes + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t);
+  const bool gll = maps.quad == 1;
+  if (mode == 3 && !TM) return cudaErrorInvalidValue;
+  auto pick = [&](auto gl) {
+    constexpr bool G = decltype(gl)::value;
+    return mode == 3 ? elastic2_kernel<TM, (TM ? 3 : 1), TY, S, G>
+         : mode == 2 ? elastic2_kernel<TM, (TM ? 2 : 1), TY, S, G>
+         : mode == 1 ? elastic2_kernel<TM, 1, TY, S, G>
+                     : elastic2_kernel<TM, 0, TY, S, G>;
+  };
+  auto kern = gll ? pick(std::true_type{}) : pick(std::false_type{});
+  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  if (!attr_set[mode + 4 * gll]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set[mode + 4 * gll] = true;
+  }
+  int txa, tya;
+  const int64_t xt = balanced_tiles(g.nx + 1, TX - 1, &txa);
+  const int64_t yt = balanced_tiles(g.ny + 1, 2 * TY - 1, &tya);
+  const int64_t nplanes = g.k1 - g.k0;
+  int64_t zc = (4LL * sm_count + xt * yt - 1) / (xt * yt);
+  const int64_t minchunk = (xt * yt * (nplanes / 8) < sm_count) ? 2 : 8;
+  zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / minchunk));
+  int64_t kchunk = (nplanes + zc - 1) / zc;
+  zc = (nplanes + kchunk - 1) / kchunk;
+  if (minchunk > 2) {  // wave-quantisation aware chunking (1 resident CTA per SM)
+    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, 1LL * sm_count, minchunk, 4);
+    zc = w.zc;
+    kchunk = w.kchunk;
+  }
+  if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
+  CUtensorMap um, um2;
+  if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
+  if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
+  TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
+  PeerMaps pm;
+  if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
+  kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
+                                 bc, kchunk, sc, red, pm, txa, tya);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
 template <bool TM, int TY, int S>
 static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int bc, int mode,
                               CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   constexpr int TX = 32;
-  using Ring1 = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX, 1>;
-  using Ring2 = PlaneRing<TM, TY + 1, TX + 1, 3, S, TY, TX, (TM ? 2 : 1)>;
+  using Ring1 = PlaneRing<TM, TY + 1, TX + 1, 3, S, kElMatRows, TX, 1>;
+  using Ring2 = PlaneRing<TM, TY + 1, TX + 1, 3, S, kElMatRows, TX, (TM ? 2 : 1)>;
   const size_t ring_bytes = mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META;
   const size_t smem = ring_bytes + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t);
   const bool gll = maps.quad == 1;
@@ -355,6 +716,12 @@ cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMap
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
   if (mode == 3 && !maps.u) return cudaErrorInvalidValue;
+  // CG vectors (tensor maps): two cell rows per thread; caller vectors (bulk-row staging, one copy
+  // per ring row): one cell row per thread, 16 rows per copy batch (measured faster there)
+  if (kElCY == 2 && maps.u) {
+    if (mode == 2) return launch_cfg2<true, kEl2TY, kEl2S>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    return launch_cfg2<true, kEl2TY, 2 * kEl2S>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  }
   if (maps.u) {
     if (mode == 2) return launch_cfg<true, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     return launch_cfg<true, kElTY, (kElTY <= 7 ? 4 : 8)>(g, x, y, maps, bc, mode, sc, red, s, sm_count);

@@ -22,7 +22,7 @@ namespace fem {
 // GLL: 2-point Gauss-Lobatto quadrature (BP5/BP6, reading R1): the 1-D mass is
 // lumped, M~ = [0, 3m, 0] instead of [1, 2m, 1]; K~ is exact under both rules.
 template <bool TM, int MODE, int C, int TX, int TY, int R, int S, bool GLL>
-__global__ void __launch_bounds__(TX*(TY + 1), 2)
+__global__ void __launch_bounds__(TX*(TY + 1), kLapMinB)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
                    double* pnew, int bc, int tmint, int64_t kchunk, CgScalars* sc, Reduce red,
@@ -253,7 +253,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   const int64_t yt = balanced_tiles(g.ny + 1, TY * R, &rya);
   const int64_t nplanes = g.k1 - g.k0;
   // z-chunks: about 4 resident waves of CTAs (2 per SM), chunks of >= 16 planes
-  int64_t zc = (8LL * sm_count + xt * yt - 1) / (xt * yt);
+  int64_t zc = (4LL * kLapMinB * sm_count + xt * yt - 1) / (xt * yt);
   // chunks of >= 16 planes amortise the pipeline fill; a mesh too small to fill the GPU that
   // way takes chunks down to 2 planes (latency: the z-march is the serial part of a CTA)
   const int64_t minchunk = (xt * yt * (nplanes / 16) < sm_count) ? 2 : 16;
@@ -261,7 +261,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (minchunk > 2) {  // wave-quantisation aware chunking (2 resident CTAs per SM)
-    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, 2LL * sm_count, minchunk, 4);
+    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, (int64_t)kLapMinB * sm_count, minchunk, 4);
     zc = w.zc;
     kchunk = w.kchunk;
   }
@@ -284,6 +284,7 @@ cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec 
   if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
   if (mode == 3 && !maps.u) return cudaErrorInvalidValue;
   if (maps.u) {
+    if (comps == 1 && mode == 2) return launch_cfg<true, 1, kLapTX, kLapTY, kLapR1, kLapS1>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     if (mode == 2) return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
