@@ -197,7 +197,11 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * every rank sets it -- exchanging CUDA IPC handles of the CG vectors with the neighbours over
  * NCCL; the apply kernels then load the ghost node planes straight from the neighbours' memory
  * over NVLink inside their TMA pipeline and the NCCL halo step disappears; the two CG allreduces
- * order the cross-rank reads and writes; TMA path only, cannot be switched off). */
+ * order the cross-rank reads and writes; TMA path only, cannot be switched off), "direct_tma"
+ * (1, default: fem_apply on a single-rank box operator stages caller vectors whose rows are
+ * 16-B multiples -- (nx+1)*comps even -- and whose base is 16-B aligned through a tensor map
+ * straight over the caller's memory, one TMA box per node plane; 0 or any other vector: one
+ * bulk copy per row; results are identical). */
 int fem_set_option(fem_op_t op, const char* key, int64_t value);
 /* Read-only properties: "fused_cg" (1: CG iterations use the fused apply -- p = r + beta p_old
  * formed inside the TMA apply kernel -- and 2 kernels per iteration; 0: apply + update +

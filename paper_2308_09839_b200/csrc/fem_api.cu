@@ -119,6 +119,7 @@ struct fem_op_s {
   cudaGraphExec_t graph1 = nullptr, graphN = nullptr, graph1b = nullptr;
   // options
   int use_graph = 1, check_every = 16, time_apply = 0;
+  int direct_tm = 1;  // fem_apply on 16-B-strided caller vectors: tensor map straight over x
   // general hex meshes: partial assembly (per-Gauss-point geometry stored once)
   int use_pa = 0;
   double* pa = nullptr;
@@ -446,6 +447,22 @@ static int apply_hex(fem_op_s* op, const double* x, double* y, int mode, cudaStr
 // y = A_c x for a DEVICE dense owned vector x (halo via op ghost buffers)
 static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s) {
   if (op->mesh->hex) return apply_hex(op, x, y, 0, s);
+  fem_mesh_s* m = op->mesh;
+  const Grid& g = m->g;
+  const int64_t rp = (g.nx + 1) * op->comps;
+  // A caller vector whose rows are 16-B multiples ((nx+1) c even) and whose base is 16-B aligned
+  // is described by a tensor map directly (full box, like the CG vectors), so the apply stages ONE
+  // TMA box per plane instead of one bulk copy per row.  Single rank: the ghost planes of a slab
+  // are not adjacent to the caller's memory.
+  if (op->direct_tm && m->nranks == 1 && op->tm_ok && !op->tm_interior && (rp & 1) == 0 &&
+      ((uintptr_t)x & 15) == 0) {
+    unsigned bw, bh;
+    u_box(op->kind, &bw, &bh);
+    CUtensorMap map;
+    FEM_TRY(make_map3d(&map, x, (uint64_t)rp, (uint64_t)(g.ny + 1), (uint64_t)(g.nz + 1), (uint64_t)rp * 8,
+                       (uint64_t)(g.plane * op->comps) * 8, bw, bh));
+    return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), &map, 0, s);
+  }
   FEM_TRY(halo(op, x, op->ghost_lo, op->ghost_hi, s));
   PlaneSrc src = dense_src(op, x, op->mesh->rank > 0 ? op->ghost_lo : nullptr,
                            op->mesh->rank < op->mesh->nranks - 1 ? op->ghost_hi : nullptr);
@@ -1402,6 +1419,7 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (value < 1) return fail(FEM_EINVAL, "check_every must be >= 1");
     op->check_every = (int)value;
   } else if (!std::strcmp(key, "time_apply")) op->time_apply = value != 0;
+  else if (!std::strcmp(key, "direct_tma")) op->direct_tm = value != 0;
   else if (!std::strcmp(key, "partial_assembly")) {
     if (!op->mesh->hex) return fail(FEM_EUNSUPPORTED, "partial_assembly is an option of general hex meshes");
     FEM_TRY(set_device(op->mesh->device));
@@ -1461,6 +1479,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "use_graph")) *value = op->use_graph;
   else if (!std::strcmp(key, "check_every")) *value = op->check_every;
   else if (!std::strcmp(key, "time_apply")) *value = op->time_apply;
+  else if (!std::strcmp(key, "direct_tma")) *value = op->direct_tm;
   else if (!std::strcmp(key, "partial_assembly")) *value = op->use_pa;
   else if (!std::strcmp(key, "quadrature")) *value = op->quad;
   else if (!std::strcmp(key, "cg_variant")) *value = (op->tm_ok && op->cg_variant == 1) ? 1 : 0;
