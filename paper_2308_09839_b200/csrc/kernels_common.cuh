@@ -61,7 +61,24 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // Wait for phase `parity` of an mbarrier.  The suspend-time hint lets the hardware park the warp
 // until the phase completes instead of spinning on issue slots (warps that run ahead of the
 // slowest consumer otherwise burn the issue bandwidth the slow warps need).
+#ifndef FEM_WAIT_HINT
+#define FEM_WAIT_HINT 1
+#endif
 __device__ __forceinline__ void mbar_wait_a(uint32_t addr, uint32_t parity) {
+#if !FEM_WAIT_HINT
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
