@@ -111,12 +111,16 @@ constexpr int kElTY = FEM_EL_TY;                                      // elastic
 #define FEM_EL_CY 2  // cell rows per thread of the elasticity apply (1: elastic_kernel, 2: elastic2_kernel)
 #endif
 #ifndef FEM_EL2_TY
-#define FEM_EL2_TY 7  // consumer warps of elastic2_kernel (2 cell rows each)
+#define FEM_EL2_TY 8  // consumer warps of elastic2_kernel (2 cell rows each)
 #endif
 #ifndef FEM_EL2_S
 #define FEM_EL2_S 4  // ring stages of elastic2_kernel in fused CG (x2 for one input box)
 #endif
+#ifndef FEM_EL2_SELF
+#define FEM_EL2_SELF 1  // elastic2_kernel without producer warp: consumer warp 0 issues the TMA loads
+#endif
 constexpr int kElCY = FEM_EL_CY, kEl2TY = FEM_EL2_TY, kEl2S = FEM_EL2_S;
+constexpr bool kEl2Self = FEM_EL2_SELF != 0;
 constexpr int kElCellRows = kElCY == 2 ? 2 * kEl2TY : kElTY;  // cell rows per TMA tile (= u box rows - 1)
 // material box rows: shared by elastic2_kernel (TMA path) and elastic_kernel (caller vectors)
 constexpr int kElMatRows = kElCellRows > kElTY ? kElCellRows : kElTY;

@@ -251,6 +251,29 @@ struct PlaneRing {
     __syncthreads();
   }
 
+  // TM, one thread: load plane p (u box(es) + material layer) into ring position t.  (ux, uy):
+  // u box origin (set_tshift), (mx, my): material box origin.
+  __device__ __forceinline__ void issue_tm(int t, int64_t p, int ux, int uy, int mx, int my, TmaOrigin uorg,
+                                           const CUtensorMap* umap, const CUtensorMap* umap2,
+                                           const CUtensorMap* mmap, int64_t mlayer0, const PeerMaps* peer) {
+    const int s = t & (S - 1);
+    double* slot = buf + (size_t)s * SLOT;
+    mbar_arrive_expect_tx(&full[s], NU * UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
+    const CUtensorMap *m1 = umap, *m2 = umap2;
+    int z = (int)(p - uorg.t_k0);
+    if (peer && peer->on) {  // ghost planes straight from the neighbour's memory
+      if (p == peer->klo) { m1 = &peer->lo; m2 = &peer->lo2; z = 0; }
+      else if (p == peer->khi) { m1 = &peer->hi; m2 = &peer->hi2; z = 0; }
+    }
+    tma_load_3d(slot, m1, ux, uy, z, &full[s]);
+    if (NU == 2) tma_load_3d(slot + UDBL, m2, ux, uy, z, &full[s]);
+    if (MROWS > 0) tma_load_3d(slot + NU * UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
+  }
+  // TM: wait until every consumer warp released ring position t (slot t % S)
+  __device__ __forceinline__ void wait_released(int t) {
+    mbar_wait_a(empty_a + 8u * (t & (S - 1)), (uint32_t)((t / S) & 1));
+  }
+
   // producer warp: stream planes pfirst .. plast (and material layers) through the ring.
   //   ilo, jlo: global node index of tile column 0 / row 0 (may be -1); material tile cells
   //   start at cell (ilo, jlo).  umap / uorg used when TM; mmap: material tensor (or nullptr).
@@ -302,18 +325,7 @@ struct PlaneRing {
       if (t >= S) mbar_wait_a(empty_a + 8u * s, (uint32_t)(((t / S) - 1) & 1));
       double* slot = buf + (size_t)s * SLOT;
       if (TM) {
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&full[s], NU * UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
-          const CUtensorMap *m1 = umap, *m2 = umap2;
-          int z = (int)(p - uorg.t_k0);
-          if (peer && peer->on) {  // ghost planes straight from the neighbour's memory
-            if (p == peer->klo) { m1 = &peer->lo; m2 = &peer->lo2; z = 0; }
-            else if (p == peer->khi) { m1 = &peer->hi; m2 = &peer->hi2; z = 0; }
-          }
-          tma_load_3d(slot, m1, ux, uy, z, &full[s]);
-          if (NU == 2) tma_load_3d(slot + UDBL, m2, ux, uy, z, &full[s]);
-          if (MROWS > 0) tma_load_3d(slot + NU * UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
-        }
+        if (lane == 0) issue_tm(t, p, ux, uy, mx, my, uorg, umap, umap2, mmap, mlayer0, peer);
         continue;
       }
       fence_proxy_async();

@@ -358,7 +358,7 @@ __device__ __forceinline__ void face_corners(const double* F, int c, double& c00
 // y hand-off per two cells, the x butterflies of the shared node row computed once.  Per node the
 // summation order is the one of elastic_kernel: ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j)).
 template <bool TM, int MODE, int TY, int S, bool GLL>
-__global__ void __launch_bounds__(32 * (TY + 1), 1)
+__global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     elastic2_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                     TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                     const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
@@ -367,7 +367,10 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   constexpr int TX = 32;
-  constexpr int NT = TX * (TY + 1);
+  // SELF: no producer warp -- consumer warp 0 (the bottom of the y hand-off chain, hence the last
+  // warp through every plane) refills the slot of plane t with plane t+S right after reading t
+  constexpr bool SELF = TM && kEl2Self;
+  constexpr int NT = TX * (TY + (SELF ? 0 : 1));
   constexpr int ROWS = 2 * TY + 1;  // node rows j0-1 .. j0+2TY-1
   constexpr int COLS = TX + 1;      // node cols i0-1 .. i0+TX-1
   constexpr int TPART = 4 * TY * TX * 3;
@@ -398,10 +401,19 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
     mbar_init(&tempty[tid], 1);
   }
   ring.init(tid, NT, TY);
-  if (TM) ring.set_tshift(i0 - 1, uorg);
+  const int tux = TM ? ring.set_tshift(i0 - 1, uorg) : 0, tuy = (int)(j0 - 1 - uorg.t_j0);
+  const int tmx = (int)(2 * (i0 - 1)), tmy = (int)(j0 - 1);
+  const int nplane = (int)(ke - pfirst + 1);  // planes kb-1 .. ke
+  if (SELF && tid == 0) {  // prologue: the first S planes
+    tma_prefetch_desc(&umap);
+    if (MODE == 2) tma_prefetch_desc(&umap2);
+    tma_prefetch_desc(&mmap);
+    for (int t = 0; t < S && t < nplane; ++t)
+      ring.issue_tm(t, pfirst + t, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0, &peer);
+  }
 
   double pq = 0.0, rr2 = 0.0;
-  if (ty == TY) {
+  if (!SELF && ty == TY) {
     ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, &mmap, mat_layer0, &umap2, 0, &peer);
   } else {
     const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + 2 * ty;  // cell A = (ci, cj), cell B = (ci, cj+1)
@@ -421,7 +433,6 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
     const double* xpb = x.main + xoff0;
     const double* ppb = (mode == 2) ? pold + xoff0 : nullptr;
     double* pnb = (mode == 2) ? pnew + xoff0 : nullptr;
-    const int nplane = (int)(ke - pfirst + 1);
     const int qface0 = bc ? (int)(0 - kb) : -1000000;
     const int qface1 = bc ? (int)(g.nz - kb) : -1000000;
     double* const tw0 = tpart + (ty * TX + tx) * 3;
@@ -483,6 +494,11 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
         fB[c] = Face{s1 + s2, s2 - s1, d1 + d2, d2 - d1};
       }
       ring.release(slot, tx);
+      if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
+        ring.wait_released(t);
+        if (tx == 0)
+          ring.issue_tm(t + S, pfirst + t + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0, &peer);
+      }
       LA = lmA.x * hs;
       MA = lmA.y * hs;
       LB = lmB.x * hs;
@@ -645,7 +661,7 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
     kchunk = w.kchunk;
   }
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
+  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + ((TM && kEl2Self) ? 0 : 1));
   CUtensorMap um, um2;
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
   if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
