@@ -96,10 +96,17 @@ constexpr int kMaxCtas = 1 << 16;
 #define FEM_LAP_MINB 2  // resident CTAs per SM the Laplace apply is compiled for (register cap)
 #endif
 #ifndef FEM_LAP_S1
-#define FEM_LAP_S1 8  // ring stages of the scalar fused CG apply
+#define FEM_LAP_S1 4  // ring stages of the scalar fused CG apply
 #endif
 constexpr int kLapTX = 32, kLapTY = FEM_LAP_TY, kLapR1 = FEM_LAP_R1, kLapR3 = 1;  // Laplace: C=1 / C=3 rows per thread
-constexpr int kLapMinB = FEM_LAP_MINB, kLapS1 = FEM_LAP_S1;
+#ifndef FEM_LAP_SELF1
+#define FEM_LAP_SELF1 1  // scalar TMA path without producer warp (consumer warp 0 issues the loads)
+#endif
+#ifndef FEM_LAP_TY1
+#define FEM_LAP_TY1 8  // consumer warps of the scalar TMA path
+#endif
+constexpr int kLapMinB = FEM_LAP_MINB, kLapS1 = FEM_LAP_S1, kLapTY1 = FEM_LAP_TY1;
+constexpr bool kLapSelf1 = FEM_LAP_SELF1 != 0;
 #ifndef FEM_LAP_INTERIOR
 #define FEM_LAP_INTERIOR 0  // 1: Laplace CG tensors span the Dirichlet interior only (round-1 layout)
 #endif
@@ -126,7 +133,7 @@ constexpr int kElCellRows = kElCY == 2 ? 2 * kEl2TY : kElTY;  // cell rows per T
 constexpr int kElMatRows = kElCellRows > kElTY ? kElCellRows : kElTY;
 // u-plane TMA box (doubles x rows) per kind: width = (((cols * C) + 1) & ~1) + 2
 inline void u_box(int kind, unsigned* w, unsigned* h) {
-  if (kind == 0) { *w = ((((kLapTX + 2) * 1) + 1) & ~1) + 2; *h = kLapTY * kLapR1 + 2; }
+  if (kind == 0) { *w = ((((kLapTX + 2) * 1) + 1) & ~1) + 2; *h = kLapTY1 * kLapR1 + 2; }
   else if (kind == 1) { *w = ((((kLapTX + 2) * 3) + 1) & ~1) + 2; *h = kLapTY * kLapR3 + 2; }
   else { *w = ((((32 + 1) * 3) + 1) & ~1) + 2; *h = kElCellRows + 1; }
 }

@@ -22,7 +22,7 @@ namespace fem {
 // GLL: 2-point Gauss-Lobatto quadrature (BP5/BP6, reading R1): the 1-D mass is
 // lumped, M~ = [0, 3m, 0] instead of [1, 2m, 1]; K~ is exact under both rules.
 template <bool TM, int MODE, int C, int TX, int TY, int R, int S, bool GLL>
-__global__ void __launch_bounds__(TX*(TY + 1), kLapMinB)
+__global__ void __launch_bounds__(TX*(TY + ((TM && C == 1 && kLapSelf1) ? 0 : 1)), kLapMinB)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
                    double* pnew, int bc, int tmint, int64_t kchunk, CgScalars* sc, Reduce red,
@@ -33,7 +33,10 @@ __global__ void __launch_bounds__(TX*(TY + 1), kLapMinB)
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   // TY consumer warps (one node column per lane, R node rows each) + 1 producer warp
-  constexpr int NT = TX * (TY + 1);
+  // SELF: no producer warp -- consumer warp 0 refills the slot of plane t with plane t+S once
+  // every warp released t (the ring's `empty` barrier)
+  constexpr bool SELF = TM && C == 1 && kLapSelf1;
+  constexpr int NT = TX * (TY + (SELF ? 0 : 1));
   constexpr int ROWS = TY * R + 2;
   constexpr int COLS = TX + 2;
   using Ring = PlaneRing<TM, ROWS, COLS, C, S, 0, 0, NU>;
@@ -56,10 +59,17 @@ __global__ void __launch_bounds__(TX*(TY + 1), kLapMinB)
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;
   ring.init(tid, NT, TY);
-  if (TM) ring.set_tshift(i0 - 1, uorg);
+  const int tux = TM ? ring.set_tshift(i0 - 1, uorg) : 0, tuy = (int)(j0 - 1 - uorg.t_j0);
+  const int nplane = (int)(ke - pfirst + 1);
+  if (SELF && tid == 0) {  // prologue: the first S planes
+    tma_prefetch_desc(&umap);
+    if (MODE == 2) tma_prefetch_desc(&umap2);
+    for (int t = 0; t < S && t < nplane; ++t)
+      ring.issue_tm(t, pfirst + t, tux, tuy, 0, 0, uorg, &umap, &umap2, nullptr, 0, &peer);
+  }
 
   double pq = 0.0, rr2 = 0.0;  // (rr2: mode 3, sum of the input's squares)
-  if (ty == TY) {
+  if (!SELF && ty == TY) {
     ring.produce(x, g, pfirst, ke, i0 - 1, j0 - 1, bc, tx, &umap, uorg, nullptr, 0, &umap2, 0, &peer);
   } else {
     const int64_t i = i0 + tx;
@@ -142,6 +152,10 @@ __global__ void __launch_bounds__(TX*(TY + 1), kLapMinB)
       if (rmask && (wedge || p == 0 || p == g.nz)) xfilter(std::true_type{});
       else xfilter(std::false_type{});
       ring.release(slot, tx);
+      if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
+        ring.wait_released(t);
+        if (tx == 0) ring.issue_tm(t + S, p + S, tux, tuy, 0, 0, uorg, &umap, &umap2, nullptr, 0, &peer);
+      }
       // y-direction
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -281,7 +295,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
     kchunk = w.kchunk;
   }
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
+  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + ((TM && C == 1 && kLapSelf1) ? 0 : 1));
   CUtensorMap um, um2;
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
   if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
@@ -299,8 +313,8 @@ cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec 
   if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
   if (mode == 3 && !maps.u) return cudaErrorInvalidValue;
   if (maps.u) {
-    if (comps == 1 && mode == 2) return launch_cfg<true, 1, kLapTX, kLapTY, kLapR1, kLapS1>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
-    if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    if (comps == 1 && mode == 2) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, kLapS1>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     if (mode == 2) return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
   }
