@@ -86,6 +86,10 @@ struct Reduce {
 constexpr int kMaxCtas = 1 << 16;
 
 // Tile shapes of the apply kernels (kernel templates and host tensor-map boxes must agree).
+#ifndef FEM_HEX_PREFETCH
+#define FEM_HEX_PREFETCH 1  // general-hex apply: persistent grid + cp.async gather pipeline
+#endif
+constexpr bool kHexPrefetch = FEM_HEX_PREFETCH != 0;
 #ifndef FEM_LAP_TY
 #define FEM_LAP_TY 7
 #endif

@@ -204,7 +204,7 @@ struct PlaneRing {
   static constexpr size_t META = 2 * S * sizeof(uint64_t) + ((S + 1) * ROWS + 2 * S) * sizeof(int);
   static constexpr uint32_t UBOX_BYTES = ROWS * BOXW * 8;
   static constexpr uint32_t MBOX_BYTES = MROWS * MPITCH * 8;
-  static_assert(ROWS <= 32, "one producer lane per row");
+  static_assert(TM || ROWS <= 32, "one producer lane per row (row path)");
   static_assert((S & (S - 1)) == 0, "S must be a power of two");
   static_assert(ROWS <= 256 && BOXW <= 256 && MPITCH <= 256, "TMA box dims <= 256");
 

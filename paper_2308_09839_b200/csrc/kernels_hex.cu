@@ -233,6 +233,143 @@ __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
   }
 }
 
+// ---- software-pipelined variant (FEM_HEX_PREFETCH) ---------------------------
+// Same per-cell arithmetic; a persistent grid (one CTA per resident slot) and a two-deep
+// cp.async pipeline per thread: while cell e is computed, the node ids of cell e + 2 stride and
+// the coordinates / u / material of cell e + stride (gathered through the ids already staged)
+// travel into this thread's shared-memory staging area, so the gather latency (ncu: the top
+// stall of the one-shot kernel, 1.97 warps per issue on long_scoreboard) overlaps the FP64 work.
+__device__ __forceinline__ void hex_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void hex_cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void hex_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void hex_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <int C>
+constexpr size_t hex_pf_smem(int T) {
+  return (size_t)T * (8 * 32 + 8 * C * 8 + 4 * 16 + 16);
+}
+
+template <int KIND, int MODE, bool GLL>
+__global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
+    hex_apply_pf_kernel(const int4* __restrict__ cells, const double4* __restrict__ xyz,
+                        const double2* __restrict__ lm, const double* __restrict__ u,
+                        double* __restrict__ y, int64_t ncells, int bc, CgScalars* sc, Reduce red) {
+  constexpr int C = (KIND == 0) ? 1 : 3;
+  constexpr int T = kHexThreads;
+  __shared__ double red_sh[32];
+  extern __shared__ __align__(16) unsigned char hsm[];
+  double4* sxyz = reinterpret_cast<double4*>(hsm);         // [8][T]
+  double* su = reinterpret_cast<double*>(sxyz + 8 * T);    // [8 C][T]
+  int4* sid = reinterpret_cast<int4*>(su + 8 * C * T);     // [2 slots][2][T]
+  double2* slm = reinterpret_cast<double2*>(sid + 4 * T);  // [T]
+  if (MODE >= 1 && sc->done) return;
+  const int tid = threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * T;
+  auto stage_ids = [&](int64_t c, int slot) {
+    hex_cp16(&sid[(slot * 2 + 0) * T + tid], &cells[2 * c]);
+    hex_cp16(&sid[(slot * 2 + 1) * T + tid], &cells[2 * c + 1]);
+  };
+  auto stage_cell = [&](int64_t c, int slot) {  // gathers through the ids staged in `slot`
+    const int4 lo = sid[(slot * 2 + 0) * T + tid], hi = sid[(slot * 2 + 1) * T + tid];
+    const int raw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int64_t n = raw[a] & 0x7fffffff;
+      const double* src = reinterpret_cast<const double*>(xyz + n);
+      hex_cp16(&sxyz[a * T + tid], src);
+      hex_cp16(reinterpret_cast<double*>(&sxyz[a * T + tid]) + 2, src + 2);
+#pragma unroll
+      for (int k = 0; k < C; ++k) hex_cp8(&su[(a * C + k) * T + tid], u + (int64_t)C * n + k);
+    }
+    if (KIND == 2) hex_cp16(&slm[tid], &lm[c]);
+  };
+  double energy = 0.0;
+  int64_t e = blockIdx.x * (int64_t)T + tid;
+  if (e < ncells) stage_ids(e, 0);
+  if (e + stride < ncells) stage_ids(e + stride, 1);
+  hex_commit();
+  hex_wait_all();
+  if (e < ncells) stage_cell(e, 0);
+  hex_commit();
+  int slot = 0;
+#pragma unroll 1
+  for (; e < ncells; e += stride, slot ^= 1) {
+    hex_wait_all();  // cell e's gathers and the ids of e + stride have landed
+    const int4 lo = sid[(slot * 2 + 0) * T + tid], hi = sid[(slot * 2 + 1) * T + tid];
+    const int raw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    int id[8];
+    bool fix[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      fix[a] = bc && raw[a] < 0;
+      id[a] = raw[a] & 0x7fffffff;
+    }
+    Modal mx, my, mz, mu[C], acc[C];
+    {
+      double X[8], Y[8], Z[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const double4 p = sxyz[a * T + tid];
+        X[a] = p.x; Y[a] = p.y; Z[a] = p.z;
+      }
+      mx = hadamard(X); my = hadamard(Y); mz = hadamard(Z);
+      prescale<GLL>(mx); prescale<GLL>(my); prescale<GLL>(mz);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      double U[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) U[a] = fix[a] ? 0.0 : su[(a * C + c) * T + tid];
+      mu[c] = hadamard(U);
+      prescale<GLL>(mu[c]);
+      acc[c] = Modal{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    }
+    double L = 0.0, M = 0.0;
+    if (KIND == 2) {
+      const double2 v = slm[tid];
+      L = v.x; M = v.y;
+    }
+    // the staged values are in registers now: refill the staging area for the next cell
+    const int64_t en = e + stride;
+    if (en < ncells) stage_cell(en, slot ^ 1);
+    if (en + stride < ncells) stage_ids(en + stride, slot);
+    hex_commit();
+    double en_q = 0.0;
+    gauss_point<KIND, C, -1, -1, -1>(mx, my, mz, mu, acc, L, M, en_q);
+    gauss_point<KIND, C, +1, -1, -1>(mx, my, mz, mu, acc, L, M, en_q);
+    gauss_point<KIND, C, -1, +1, -1>(mx, my, mz, mu, acc, L, M, en_q);
+    gauss_point<KIND, C, +1, +1, -1>(mx, my, mz, mu, acc, L, M, en_q);
+    gauss_point<KIND, C, -1, -1, +1>(mx, my, mz, mu, acc, L, M, en_q);
+    gauss_point<KIND, C, +1, -1, +1>(mx, my, mz, mu, acc, L, M, en_q);
+    gauss_point<KIND, C, -1, +1, +1>(mx, my, mz, mu, acc, L, M, en_q);
+    gauss_point<KIND, C, +1, +1, +1>(mx, my, mz, mu, acc, L, M, en_q);
+    energy += en_q;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      Modal& m = acc[c];
+      m.x *= kInv512; m.y *= kInv512; m.z *= kInv512;
+      constexpr double g = GLL ? 1.0 : kG, g2 = GLL ? 1.0 : kG2;
+      m.xy *= g * kInv512; m.xz *= g * kInv512; m.yz *= g * kInv512; m.xyz *= g2 * kInv512;
+      double v[8];
+      inverse(m, v);
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+    }
+  }
+  hex_wait_all();
+  if (MODE >= 1) {
+    double total;
+    if (last_block_reduce(block_sum(energy * kInv512, red_sh), red, red_sh, &total)) sc->pq = total;
+  }
+}
+
 // identity rows of the constrained nodes: y = x; mode 1 adds sum x_b^2 to p.Ap
 template <int MODE>
 __global__ void __launch_bounds__(256) hex_dirichlet_kernel(const int32_t* __restrict__ nodes, int64_t nb, int C,
@@ -511,6 +648,34 @@ cudaError_t launch_hex_apply(int kind, int bc, int quad, const int4* cells, cons
                              const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
                              Reduce red, cudaStream_t s, int sm_count) {
   if (ncells <= 0) return cudaSuccess;
+  // measured: the pipelined kernel wins for the elasticity CG apply (2.87 ->
+  // 2.67 ms at H1) but not for the plain elasticity apply (2.43 -> 2.49) nor the scalar kind
+  if (kHexPrefetch && kind == 2 && mode >= 1) {  // persistent grid: one CTA per resident slot
+    const int per_sm = kind == 0 ? 3 : 2;
+    const int64_t want = (ncells + kHexThreads - 1) / kHexThreads;
+    const int grid = (int)std::min<int64_t>(want, (int64_t)per_sm * sm_count);
+    if (mode >= 1 && grid > red.capacity) return cudaErrorInvalidConfiguration;
+#define PF_LAUNCH(K, M, G)                                                                               \
+  {                                                                                                       \
+    constexpr size_t sm = hex_pf_smem<(K == 0) ? 1 : 3>(kHexThreads);                                     \
+    static bool set = false;                                                                              \
+    if (!set) {                                                                                           \
+      cudaError_t e = cudaFuncSetAttribute(hex_apply_pf_kernel<K, M, G>,                                  \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);          \
+      if (e != cudaSuccess) return e;                                                                     \
+      set = true;                                                                                         \
+    }                                                                                                     \
+    hex_apply_pf_kernel<K, M, G><<<grid, kHexThreads, sm, s>>>(cells, xyz, lm, x, y, ncells, bc, sc, red); \
+  }
+#define PF_LAUNCH2(K, M) { if (quad == 1) PF_LAUNCH(K, M, true) else PF_LAUNCH(K, M, false) }
+    if (kind == 0) { if (mode) PF_LAUNCH2(0, 1) else PF_LAUNCH2(0, 0) }
+    else if (kind == 1) { if (mode) PF_LAUNCH2(1, 1) else PF_LAUNCH2(1, 0) }
+    else { if (mode) PF_LAUNCH2(2, 1) else PF_LAUNCH2(2, 0) }
+#undef PF_LAUNCH2
+#undef PF_LAUNCH
+    add_launches(1);
+    return cudaGetLastError();
+  }
   const int grid = grid_for(ncells, kHexThreads, sm_count, 8);
   if (mode >= 1 && grid > red.capacity) return cudaErrorInvalidConfiguration;
 #define HEX_LAUNCH(K, M, G) hex_apply_kernel<K, M, G><<<grid, kHexThreads, 0, s>>>(cells, xyz, lm, x, y, ncells, bc, sc, red)
