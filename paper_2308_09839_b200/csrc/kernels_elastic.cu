@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   constexpr int TX = 32;
   // SELF: no producer warp -- consumer warp 0 (the bottom of the y hand-off chain, hence the last
   // warp through every plane) refills the slot of plane t with plane t+S right after reading t
+  static_assert(TM, "elastic2_kernel: TMA path only (caller vectors use elastic_kernel)");
   constexpr bool SELF = TM && kEl2Self;
   constexpr int NT = TX * (TY + (SELF ? 0 : 1));
   constexpr int ROWS = 2 * TY + 1;  // node rows j0-1 .. j0+2TY-1
@@ -430,8 +431,6 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     const bool own = ownA || ownB;  // (ownB implies nA is a mesh row too)
     double* yp = yo.y + (kb - g.k0) * yo.ppitch + (own ? nA * yo.rpitch + ci * 3 : 0);
     const int64_t xoff0 = (kb - g.k0) * x.ppitch + (own ? nA * x.rpitch + ci * 3 : 0);
-    const double* xpb = x.main + xoff0;
-    const double* ppb = (mode == 2) ? pold + xoff0 : nullptr;
     double* pnb = (mode == 2) ? pnew + xoff0 : nullptr;
     const int qface0 = bc ? (int)(0 - kb) : -1000000;
     const int qface1 = bc ? (int)(g.nz - kb) : -1000000;
@@ -548,10 +547,6 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
             for (int c = 0; c < 3; ++c) {
               double vv = vA[c], xv = xs_A[c];
               if (bnode) {
-                if (!TM) {
-                  xv = xpb[c];
-                  if (mode == 2) xv = fma(beta, ppb[c], xv);
-                }
                 vv = xv;
               }
               yp[c] = vv;
@@ -574,10 +569,6 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
               for (int c = 0; c < 3; ++c) {
                 double vv = v[c], xv = xs_B[c];
                 if (bnode) {
-                  if (!TM) {
-                    xv = xpb[x.rpitch + c];
-                    if (mode == 2) xv = fma(beta, ppb[x.rpitch + c], xv);
-                  }
                   vv = xv;
                 }
                 yp[yo.rpitch + c] = vv;
@@ -587,9 +578,8 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
               }
             }
           }
-          if (mode == 2) { ppb += x.ppitch; pnb += x.ppitch; }
+          if (mode == 2) pnb += x.ppitch;
           yp += yo.ppitch;
-          xpb += x.ppitch;
         }
     };
     using I0 = std::integral_constant<int, 0>;
