@@ -640,13 +640,15 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   const int64_t xt = balanced_tiles(g.nx + 1, TX - 1, &txa);
   const int64_t yt = balanced_tiles(g.ny + 1, 2 * TY - 1, &tya);
   const int64_t nplanes = g.k1 - g.k0;
-  int64_t zc = (4LL * sm_count + xt * yt - 1) / (xt * yt);
+  // resident CTAs per SM at ~255 registers per thread: 65536 / (32 (TY [+1]) 255)
+  constexpr int kRes = (TY + ((TM && kEl2Self) ? 0 : 1)) <= 4 ? 2 : 1;
+  int64_t zc = (4LL * kRes * sm_count + xt * yt - 1) / (xt * yt);
   const int64_t minchunk = (xt * yt * (nplanes / 8) < sm_count) ? 2 : 8;
   zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / minchunk));
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (minchunk > 2) {  // wave-quantisation aware chunking (1 resident CTA per SM)
-    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, 1LL * sm_count, minchunk, 4);
+    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, (int64_t)kRes * sm_count, minchunk, 4);
     zc = w.zc;
     kchunk = w.kchunk;
   }
