@@ -133,3 +133,81 @@ def test_fullsize_symmetry(F, idx):
     ab = op.dot(a, op.apply(b))
     ba = op.dot(b, op.apply(a))
     assert abs(ab - ba) <= 1e-12 * abs(ab), (cfg["name"], ab, ba)
+
+
+# ---- general hexahedra at the bench sizes (H1 elasticity / H2 scalar, 256^3 jittered) ------------
+HEX_CASES = [6, 7]
+
+
+def _hex_setup(F, idx):
+    cfg = I.CONFIGS[idx]
+    kind = cfg["kind"]
+    nx, ny, nz = I.config_cells(cfg)
+    h = 1.0 / nx
+    gm = I.rng(I.SEED_BASE + idx + 2000)  # bench.py's mesh
+    coords, cells, bnd = I.hex_box_mesh(nx, ny, nz, h=h, g=gm, jitter=cfg["jitter"])
+    g = I.rng(I.SEED_BASE + idx)
+    lam, mu = (I.materials(g, nx, ny, nz) if kind == "elastic" else (None, None))
+    op = F.Operator(F.HexMesh(torch.from_numpy(coords).cuda(), torch.from_numpy(cells).cuda(),
+                              torch.from_numpy(bnd).cuda()), kind, "dirichlet")
+    if kind == "elastic":
+        op.set_material(torch.from_numpy(lam).cuda(), torch.from_numpy(mu).cuda())
+    return cfg, kind, (nx, ny, nz), coords, cells, bnd, lam, mu, op
+
+
+@pytest.mark.parametrize("idx", HEX_CASES)
+def test_fullsize_hex_apply_sampled(F, oracle, idx):
+    """(A_c x) at sampled nodes: the oracle's Alg. 1 path on the <= 8 cells around each node
+    (a sub-mesh carrying the global Dirichlet flags), against the full GPU apply."""
+    cfg, kind, (nx, ny, nz), coords, cells, bnd, lam, mu, op = _hex_setup(F, idx)
+    c = I.ncomp(kind)
+    g = I.rng(I.SEED_BASE + 600 + idx)
+    x = g.uniform(-1, 1, coords.shape[0] * c)
+    y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy().reshape(-1, c)
+    nodes = _sample_nodes(nx, ny, nz, g, count=120)
+    errs, scale = [], 0.0
+    for n in nodes:
+        i, j, k = n % (nx + 1), (n // (nx + 1)) % (ny + 1), n // ((nx + 1) * (ny + 1))
+        es = [ci + nx * (cj + ny * ck) for ck in (k - 1, k) for cj in (j - 1, j) for ci in (i - 1, i)
+              if 0 <= ci < nx and 0 <= cj < ny and 0 <= ck < nz]
+        sub = cells[es]
+        ids, inv = np.unique(sub, return_inverse=True)
+        sub_cells = inv.reshape(sub.shape).astype(np.int32)
+        xs = x.reshape(-1, c)[ids].ravel()
+        ref = oracle.apply_hex(kind, coords[ids], sub_cells, xs, bnd[ids],
+                               None if lam is None else lam[es], None if mu is None else mu[es])
+        loc = int(np.searchsorted(ids, n))
+        r = ref.reshape(-1, c)[loc]
+        errs.append(np.abs(y[n] - r).max())
+        scale = max(scale, np.abs(r).max())
+    err = max(errs) / scale
+    assert err <= APPLY_TOL, (cfg["name"], err)
+
+
+@pytest.mark.parametrize("idx", HEX_CASES)
+def test_fullsize_hex_cg(F, idx):
+    """the CG kernels bench.py times (elasticity: the pipelined gather kernel) against textbook CG
+    around fem_apply, 3 iterations, elementwise"""
+    cfg, kind, (nx, ny, nz), coords, cells, bnd, lam, mu, op = _hex_setup(F, idx)
+    c = I.ncomp(kind)
+    gb = I.rng(I.SEED_BASE + idx + 1000)
+    b = torch.from_numpy(I.interior_rhs(gb, nx, ny, nz, c)).cuda()
+    iters = 3
+    x = torch.zeros_like(b)
+    op.cg_begin(b, x, tol=0.0, maxit=iters)
+    op.cg_iterate(iters)
+    assert op.cg_end()["iterations"] == iters
+    xr = torch.zeros_like(b)
+    r = b.clone()
+    p = r.clone()
+    rr = torch.dot(r, r)
+    for _ in range(iters):
+        q = op.apply(p)
+        alpha = rr / torch.dot(p, q)
+        xr += alpha * p
+        r -= alpha * q
+        rr_new = torch.dot(r, r)
+        p = r + (rr_new / rr) * p
+        rr = rr_new
+    d = float((x - xr).abs().max() / xr.abs().max())
+    assert d <= 1e-11, (cfg["name"], d)
