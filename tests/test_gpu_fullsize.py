@@ -76,17 +76,22 @@ def _setup(F, idx):
     return cfg, kind, (nx, ny, nz, h), lam, mu, op
 
 
+@pytest.mark.parametrize("quad", ["gauss", "gll"])
 @pytest.mark.parametrize("idx", CASES)
-def test_fullsize_apply_sampled(F, oracle, idx):
+def test_fullsize_apply_sampled(F, oracle, idx, quad):
+    """quad "gll": the 2x2x2 Gauss-Lobatto rule of the BP5 / BP6 operators (reading R1)"""
     cfg, kind, (nx, ny, nz, h), lam, mu, op = _setup(F, idx)
+    if quad == "gll":
+        op.set_option("quadrature", 1)
     c = I.ncomp(kind)
     g = I.rng(I.SEED_BASE + 500 + idx)
     x = I.uniform_vector(g, nx, ny, nz, c)
     y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy().reshape(-1, c)
     nodes = _sample_nodes(nx, ny, nz, g)
-    ref = oracle.apply_nodes(kind, 1, nx, ny, nz, h, x, nodes, lam=lam, mu=mu)
+    with oracle.quadrature(quad):
+        ref = oracle.apply_nodes(kind, 1, nx, ny, nz, h, x, nodes, lam=lam, mu=mu)
     err = np.abs(y[nodes] - ref).max() / np.abs(ref).max()
-    assert err <= APPLY_TOL, (cfg["name"], err)
+    assert err <= APPLY_TOL, (cfg["name"], quad, err)
 
 
 @pytest.mark.parametrize("idx", CASES)
