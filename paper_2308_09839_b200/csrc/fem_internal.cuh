@@ -90,6 +90,12 @@ constexpr int kMaxCtas = 1 << 16;
 #define FEM_HEX_PREFETCH 1  // general-hex apply: persistent grid + cp.async gather pipeline
 #endif
 constexpr bool kHexPrefetch = FEM_HEX_PREFETCH != 0;
+#ifndef FEM_LAP_MINCHUNK
+#define FEM_LAP_MINCHUNK 16  // Laplace z-chunks: minimum planes per chunk
+#endif
+#ifndef FEM_LAP_ROUNDS
+#define FEM_LAP_ROUNDS 4  // Laplace z-chunks: minimum rounds of resident CTAs
+#endif
 #ifndef FEM_LAP_TY
 #define FEM_LAP_TY 7
 #endif

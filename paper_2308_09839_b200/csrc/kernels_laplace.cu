@@ -285,12 +285,12 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   int64_t zc = (4LL * kLapMinB * sm_count + xt * yt - 1) / (xt * yt);
   // chunks of >= 16 planes amortise the pipeline fill; a mesh too small to fill the GPU that
   // way takes chunks down to 2 planes (latency: the z-march is the serial part of a CTA)
-  const int64_t minchunk = (xt * yt * (nplanes / 16) < sm_count) ? 2 : 16;
+  const int64_t minchunk = (xt * yt * (nplanes / 16) < sm_count) ? 2 : FEM_LAP_MINCHUNK;
   zc = std::max<int64_t>(1, std::min<int64_t>(zc, nplanes / minchunk));
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (minchunk > 2) {  // wave-quantisation aware chunking (2 resident CTAs per SM)
-    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, (int64_t)kLapMinB * sm_count, minchunk, 4);
+    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, (int64_t)kLapMinB * sm_count, minchunk, FEM_LAP_ROUNDS);
     zc = w.zc;
     kchunk = w.kchunk;
   }
