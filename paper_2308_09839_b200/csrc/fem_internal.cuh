@@ -117,6 +117,14 @@ constexpr int kLapTX = 32, kLapTY = FEM_LAP_TY, kLapR1 = FEM_LAP_R1, kLapR3 = 1;
 #endif
 constexpr int kLapMinB = FEM_LAP_MINB, kLapS1 = FEM_LAP_S1, kLapTY1 = FEM_LAP_TY1;
 constexpr bool kLapSelf1 = FEM_LAP_SELF1 != 0;
+#ifndef FEM_LAP_SELF3
+#define FEM_LAP_SELF3 0  // vector TMA path without producer warp
+#endif
+#ifndef FEM_LAP_TY3
+#define FEM_LAP_TY3 7  // consumer warps of the vector TMA path
+#endif
+constexpr bool kLapSelf3 = FEM_LAP_SELF3 != 0;
+constexpr int kLapTY3 = FEM_LAP_TY3;
 #ifndef FEM_LAP_INTERIOR
 #define FEM_LAP_INTERIOR 0  // 1: Laplace CG tensors span the Dirichlet interior only (round-1 layout)
 #endif
@@ -144,7 +152,7 @@ constexpr int kElMatRows = kElCellRows > kElTY ? kElCellRows : kElTY;
 // u-plane TMA box (doubles x rows) per kind: width = (((cols * C) + 1) & ~1) + 2
 inline void u_box(int kind, unsigned* w, unsigned* h) {
   if (kind == 0) { *w = ((((kLapTX + 2) * 1) + 1) & ~1) + 2; *h = kLapTY1 * kLapR1 + 2; }
-  else if (kind == 1) { *w = ((((kLapTX + 2) * 3) + 1) & ~1) + 2; *h = kLapTY * kLapR3 + 2; }
+  else if (kind == 1) { *w = ((((kLapTX + 2) * 3) + 1) & ~1) + 2; *h = kLapTY3 * kLapR3 + 2; }
   else { *w = ((((32 + 1) * 3) + 1) & ~1) + 2; *h = kElCellRows + 1; }
 }
 inline void mat_box(unsigned* w, unsigned* h) { *w = 2 * 32; *h = kElMatRows; }

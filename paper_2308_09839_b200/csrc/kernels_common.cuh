@@ -213,6 +213,7 @@ struct PlaneRing {
   uint64_t* empty;  // S mbarriers
   int* lead;        // (S+1) * ROWS     (!TM)
   int* valid;       // S               (!TM)
+  unsigned* cnt;    // S release counters (refill by the last consumer warp, no producer warp)
   int tshift = 0;   // TM: 1 if the tile's first element sits at an odd offset of the tensor
   uint32_t full_a = 0, empty_a = 0;  // shared-window addresses of full[0], empty[0]
 
@@ -231,6 +232,7 @@ struct PlaneRing {
     empty_a = smem_u32(empty);
     lead = reinterpret_cast<int*>(empty + S);
     valid = lead + (S + 1) * ROWS;
+    cnt = reinterpret_cast<unsigned*>(valid + S);
   }
 
   // all threads: zero the ring (row path), init barriers; ends with __syncthreads
@@ -240,6 +242,7 @@ struct PlaneRing {
       for (int t = tid; t < NSLOT * SLOT / 2; t += nthreads) b2[t] = make_double2(0.0, 0.0);
       for (int t = tid; t < (S + 1) * ROWS; t += nthreads) lead[t] = 2;
     }
+    if (tid < S) cnt[tid] = 0u;
     if (tid == 0) {
       for (int s = 0; s < S; ++s) {
         mbar_init(&full[s], TM ? 1 : ROWS + 1);
@@ -366,6 +369,21 @@ struct PlaneRing {
 
   // consumers: wait until slot s holds its plane (phase parity ph)
   __device__ __forceinline__ void wait(int s, uint32_t ph) { mbar_wait_a(full_a + 8u * s, ph); }
+
+  // consumer warp, no-producer rings: count this warp's release of slot s; true in the warp whose
+  // release was the last of the nwarps consumers (it refills the slot: fence_proxy_async, then
+  // issue_tm).  The acq_rel atomic orders every warp's reads of the slot before the refill.
+  __device__ __forceinline__ bool release_last(int s, int lane, int nwarps) {
+    __syncwarp();
+    unsigned last = 0;
+    if (lane == 0) {
+      unsigned old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n"
+                   : "=r"(old) : "r"(smem_u32(cnt + s)) : "memory");
+      last = ((old + 1) % (unsigned)nwarps) == 0u;
+    }
+    return __shfl_sync(0xffffffffu, last, 0) != 0u;
+  }
 
   // consumer warp: release slot s after its last read
   __device__ __forceinline__ void release(int s, int lane) {

@@ -22,7 +22,7 @@ namespace fem {
 // GLL: 2-point Gauss-Lobatto quadrature (BP5/BP6, reading R1): the 1-D mass is
 // lumped, M~ = [0, 3m, 0] instead of [1, 2m, 1]; K~ is exact under both rules.
 template <bool TM, int MODE, int C, int TX, int TY, int R, int S, bool GLL>
-__global__ void __launch_bounds__(TX*(TY + ((TM && C == 1 && kLapSelf1) ? 0 : 1)), kLapMinB)
+__global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSelf3)) ? 0 : 1)), kLapMinB)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
                    double* pnew, int bc, int tmint, int64_t kchunk, CgScalars* sc, Reduce red,
@@ -33,9 +33,9 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && C == 1 && kLapSelf1) ? 0 : 1)
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   // TY consumer warps (one node column per lane, R node rows each) + 1 producer warp
-  // SELF: no producer warp -- consumer warp 0 refills the slot of plane t with plane t+S once
-  // every warp released t (the ring's `empty` barrier)
-  constexpr bool SELF = TM && C == 1 && kLapSelf1;
+  // SELF: no producer warp -- the consumer warp that releases the slot of plane t last refills
+  // it with plane t+S (Ring::release_last)
+  constexpr bool SELF = TM && (C == 1 ? kLapSelf1 : kLapSelf3);
   constexpr int NT = TX * (TY + (SELF ? 0 : 1));
   constexpr int ROWS = TY * R + 2;
   constexpr int COLS = TX + 2;
@@ -151,10 +151,13 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && C == 1 && kLapSelf1) ? 0 : 1)
       };
       if (rmask && (wedge || p == 0 || p == g.nz)) xfilter(std::true_type{});
       else xfilter(std::false_type{});
-      ring.release(slot, tx);
-      if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
-        ring.wait_released(t);
-        if (tx == 0) ring.issue_tm(t + S, p + S, tux, tuy, 0, 0, uorg, &umap, &umap2, nullptr, 0, &peer);
+      if (SELF) {
+        if (ring.release_last(slot, tx, TY) && t + S < nplane && tx == 0) {  // refill: plane t+S
+          fence_proxy_async();
+          ring.issue_tm(t + S, p + S, tux, tuy, 0, 0, uorg, &umap, &umap2, nullptr, 0, &peer);
+        }
+      } else {
+        ring.release(slot, tx);
       }
       // y-direction
 #pragma unroll
@@ -295,7 +298,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
     kchunk = w.kchunk;
   }
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + ((TM && C == 1 && kLapSelf1) ? 0 : 1));
+  dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + ((TM && (C == 1 ? kLapSelf1 : kLapSelf3)) ? 0 : 1));
   CUtensorMap um, um2;
   if (TM) um = *maps.u; else std::memset(&um, 0, sizeof(um));
   if (TM && mode == 2) um2 = *maps.u2; else std::memset(&um2, 0, sizeof(um2));
@@ -315,8 +318,8 @@ cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec 
   if (maps.u) {
     if (comps == 1 && mode == 2) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, kLapS1>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
-    if (mode == 2) return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
-    return launch_cfg<true, 3, kLapTX, kLapTY, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    if (mode == 2) return launch_cfg<true, 3, kLapTX, kLapTY3, kLapR3, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    return launch_cfg<true, 3, kLapTX, kLapTY3, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
   }
   if (comps == 1) return launch_cfg<false, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
   return launch_cfg<false, 3, kLapTX, kLapTY, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
