@@ -331,3 +331,43 @@ def test_cg_chronopoulos_gear_fixed_iterations(F, oracle):
     info = op.cg_solve(dev(b), x, tol=0.0, maxit=50)
     assert info["iterations"] == ref.iterations
     assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10
+
+
+# Tile-seam sweep: node counts around the tile widths of every kernel (Laplace 32/29 columns x
+# 24/21 (scalar) or 7 (vector) rows; elasticity 31/30 x 15 (CG kernel) or 14 (caller-vector
+# kernel)), odd and even rows (caller vectors with 16-B rows take the tensor-map path), both the
+# apply (against the oracle) and the fused CG kernels (against textbook CG around fem_apply).
+SEAM_MESHES = [(29, 14, 3), (30, 15, 4), (31, 16, 3), (32, 13, 2), (33, 23, 3), (61, 29, 2), (62, 30, 3)]
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("dims", SEAM_MESHES)
+def test_tile_seams(F, oracle, kind, dims):
+    nx, ny, nz = dims
+    h = 1.0 / nx
+    g = I.rng(I.SEED_BASE + 700 + nx + 7 * ny + 31 * nz)
+    c = I.ncomp(kind)
+    x = I.uniform_vector(g, nx, ny, nz, c)
+    lam, mu = I.materials(g, nx, ny, nz)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 1)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    ref = oracle.apply(kind, 1, nx, ny, nz, h, x, lam=lam, mu=mu)
+    y = op.apply(dev(x)).cpu().numpy()
+    assert relerr(y, ref) <= APPLY_TOL
+    b = dev(I.interior_rhs(g, nx, ny, nz, c))
+    iters = 4
+    xg = torch.zeros_like(b)
+    op.cg_begin(b, xg, tol=0.0, maxit=iters)
+    op.cg_iterate(iters)
+    assert op.cg_end()["iterations"] == iters
+    xr = torch.zeros_like(b); r = b.clone(); p = r.clone(); rr = torch.dot(r, r)
+    for _ in range(iters):
+        q = op.apply(p)
+        alpha = rr / torch.dot(p, q)
+        xr += alpha * p
+        r -= alpha * q
+        rr_new = torch.dot(r, r)
+        p = r + (rr_new / rr) * p
+        rr = rr_new
+    assert float((xg - xr).abs().max() / xr.abs().max()) <= 1e-11
