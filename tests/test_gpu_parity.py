@@ -120,6 +120,28 @@ def test_apply_deterministic(F):
 
 
 @pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+def test_fused_cg_deterministic(F, kind):
+    """the producer-less TMA kernels (ring refilled by a consumer warp, mbarrier hand-offs) give
+    bitwise identical CG iterates run after run -- the race check racecheck cannot do (DESIGN 8a)"""
+    nx, ny, nz = 70, 45, 61
+    g = I.rng(I.SEED_BASE + 203)
+    c = I.ncomp(kind)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = dev(I.interior_rhs(g, nx, ny, nz, c))
+    op = F.Operator(F.Mesh(nx, ny, nz, 1.0 / nx), kind, 1)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    xs = []
+    for _ in range(3):
+        x = torch.zeros_like(b)
+        op.cg_begin(b, x, tol=0.0, maxit=25)
+        op.cg_iterate(25)
+        op.cg_end()
+        xs.append(x)
+    assert torch.equal(xs[0], xs[1]) and torch.equal(xs[0], xs[2])
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
 def test_null_space_and_symmetry_gpu(F, kind):
     """Properties that hold at any size, checked on the GPU alone (no oracle)."""
     nx, ny, nz, h = 37, 29, 23, 0.05
