@@ -201,7 +201,10 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * (1, default: fem_apply on a single-rank box operator stages caller vectors whose rows are
  * 16-B multiples -- (nx+1)*comps even -- and whose base is 16-B aligned through a tensor map
  * straight over the caller's memory, one TMA box per node plane; 0 or any other vector: one
- * bulk copy per row; results are identical). */
+ * bulk copy per row; results are identical; with the Dirichlet box, Laplace kinds and odd rows
+ * a "row-pair" tensor view -- two TMA boxes per plane -- is used when the caller's allocation
+ * extends one row past the vector).  Read-only "last_apply_path": staging of the last fem_apply
+ * (0 bulk rows, 1 tensor map, 2 row-pair tensor map). */
 int fem_set_option(fem_op_t op, const char* key, int64_t value);
 /* Read-only properties: "fused_cg" (1: CG iterations use the fused apply -- p = r + beta p_old
  * formed inside the TMA apply kernel -- and 2 kernels per iteration; 0: apply + update +

@@ -120,6 +120,7 @@ struct fem_op_s {
   // options
   int use_graph = 1, check_every = 16, time_apply = 0;
   int direct_tm = 1;  // fem_apply on 16-B-strided caller vectors: tensor map straight over x
+  int last_path = 0;  // staging of the last fem_apply: 0 bulk rows, 1 tensor map, 2 row-pair tensor map
   // general hex meshes: partial assembly (per-Gauss-point geometry stored once)
   int use_pa = 0;
   double* pa = nullptr;
@@ -394,12 +395,12 @@ static bool fill_peer(const fem_op_s* op, const double* v, const double* v2, Pee
 }
 
 static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* umap, int mode,
-                        cudaStream_t s, const double* vsrc = nullptr) {
+                        cudaStream_t s, const double* vsrc = nullptr, const PairGeom* pair = nullptr) {
   fem_mesh_s* m = op->mesh;
   static thread_local PeerMaps pm;
   const bool peer = umap && vsrc && fill_peer(op, vsrc, nullptr, &pm);
   ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr,
-                 op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr};
+                 op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr, pair};
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
@@ -445,6 +446,23 @@ static int apply_hex(fem_op_s* op, const double* x, double* y, int mode, cudaStr
 }
 
 // y = A_c x for a DEVICE dense owned vector x (halo via op ghost buffers)
+// true if [p, p + bytes) lies inside one device allocation (the caller's cudaMalloc segment)
+static bool alloc_extends(const void* p, size_t bytes) {
+  using PFN = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static PFN fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+      return false;
+    fn = reinterpret_cast<PFN>(f);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS) return false;
+  return (uintptr_t)p + bytes <= (uintptr_t)base + size;
+}
+
 static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s) {
   if (op->mesh->hex) return apply_hex(op, x, y, 0, s);
   fem_mesh_s* m = op->mesh;
@@ -461,8 +479,30 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
     CUtensorMap map;
     FEM_TRY(make_map3d(&map, x, (uint64_t)rp, (uint64_t)(g.ny + 1), (uint64_t)(g.nz + 1), (uint64_t)rp * 8,
                        (uint64_t)(g.plane * op->comps) * 8, bw, bh));
+    op->last_path = 1;
     return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), &map, 0, s);
   }
+  // Odd rows (Laplace kinds, Dirichlet box): the row-pair view (kernels_common.cuh, PairGeom) --
+  // dim 0 spans two rows plus the plane parity, dims 1 / 2 step by row pairs / plane pairs (16-B
+  // strides) -- so the apply still stages two TMA boxes per plane.  Boxes read up to one row and
+  // two box widths past the vector's end (last plane): taken only when the caller's allocation
+  // extends that far (cuMemGetAddressRange), else the bulk-row path.
+  if (op->direct_tm && m->nranks == 1 && op->tm_ok && !op->tm_interior && op->bc && (rp & 1) &&
+      op->kind != FEM_ELASTICITY && ((uintptr_t)x & 15) == 0) {
+    unsigned bw, bh;
+    u_box(op->kind, &bw, &bh);
+    const int64_t lp = g.plane * op->comps;
+    const size_t need = (size_t)(op->n_local + rp + 2 * (int64_t)bw) * sizeof(double);
+    if (alloc_extends(x, need)) {
+      const PairGeom pg{rp, lp, g.nz};
+      CUtensorMap map;
+      FEM_TRY(make_map3d(&map, x, (uint64_t)(lp + 2 * rp), (uint64_t)((g.ny + 2) / 2), (uint64_t)((g.nz + 2) / 2),
+                         (uint64_t)(2 * rp) * 8, (uint64_t)(2 * lp) * 8, bw, (bh + 1) / 2));
+      op->last_path = 2;
+      return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), &map, 0, s, nullptr, &pg);
+    }
+  }
+  op->last_path = 0;
   FEM_TRY(halo(op, x, op->ghost_lo, op->ghost_hi, s));
   PlaneSrc src = dense_src(op, x, op->mesh->rank > 0 ? op->ghost_lo : nullptr,
                            op->mesh->rank < op->mesh->nranks - 1 ? op->ghost_hi : nullptr);
@@ -1480,6 +1520,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "check_every")) *value = op->check_every;
   else if (!std::strcmp(key, "time_apply")) *value = op->time_apply;
   else if (!std::strcmp(key, "direct_tma")) *value = op->direct_tm;
+  else if (!std::strcmp(key, "last_apply_path")) *value = op->last_path;
   else if (!std::strcmp(key, "partial_assembly")) *value = op->use_pa;
   else if (!std::strcmp(key, "quadrature")) *value = op->quad;
   else if (!std::strcmp(key, "cg_variant")) *value = (op->tm_ok && op->cg_variant == 1) ? 1 : 0;

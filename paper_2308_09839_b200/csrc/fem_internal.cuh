@@ -44,6 +44,12 @@ struct __align__(64) PeerMaps {
   int on;
 };
 
+// Row-pair view of a dense caller vector with odd rows (PlaneRing PAIR, kernels_common.cuh)
+struct PairGeom {
+  int64_t lr, lp;  // row / plane length of the caller vector in elements
+  int64_t nz;      // last node plane
+};
+
 // TMA tensor maps of one apply launch (u plane: padded layout; material: interleaved lambda/mu)
 // mode 2 (fused CG): the operator input is p = r + beta p_old formed in the kernel; u is r,
 // u2 is p_old, p is written to pnew (owned nodes, padded layout of x).
@@ -58,6 +64,7 @@ struct ApplyMaps {
   int interior;            // 1: u tensor spans only the Dirichlet interior (zero fill = mask)
   int quad;                // 0: 2x2x2 Gauss-Legendre (default), 1: 2x2x2 Gauss-Lobatto (BP5/BP6)
   const PeerMaps* peer;    // ghost planes from peer memory (nullptr / on = 0: local)
+  const PairGeom* pair = nullptr;  // u is a row-pair view of a caller vector (kernels_common.cuh)
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).

@@ -188,13 +188,25 @@ struct TmaOrigin {
 // Ring of S plane slots.  Slot: u region ROWS x PITCH doubles (+ material MROWS x MPITCH).
 //   TM:  PITCH = BOXW (box width, doubles); data at row r, element col*C + comp.
 //   !TM: PITCH even >= COLS*C + 4, row data start at lead[slot][row] in {2,3}; slot S = zeros.
-template <bool TM, int ROWS, int COLS, int C, int S, int MROWS = 0, int MCOLS = 0, int NU = 1>
+// PAIR (TM only): the u tensor is a "row-pair" view of a dense caller vector whose rows are NOT
+// 16-B multiples (odd (nx+1) C): dim 0 = elements of two consecutive rows plus the plane parity
+// (extent Lp + 2 Lr), dim 1 = row pairs (stride 2 Lr), dim 2 = plane pairs (stride 2 Lp), so all
+// strides are 16-B multiples.  A plane tile is TWO boxes: the rows of the parity of row jlo and
+// the rows of the other parity, each HR = ceil(ROWS / 2) rows; ring row r lives in box r & 1 at
+// box row r >> 1, shifted by the box's 8-B misalignment (set_pair_plane).  Columns / rows past the
+// box edge read the neighbouring row: only the Dirichlet identity rows see them (bc = 1 only).
+// (PairGeom: fem_internal.cuh)
+
+template <bool TM, int ROWS, int COLS, int C, int S, int MROWS = 0, int MCOLS = 0, int NU = 1,
+          bool PAIR = false>
 struct PlaneRing {
   // box width: COLS*C rounded to even, +2 so the box can start one element early (the box x
   // origin must be 16-B aligned: odd element offsets are shifted, see tshift)
   static constexpr int BOXW = (((COLS * C) + 1) & ~1) + 2;
   static constexpr int PITCH = TM ? BOXW : (((COLS * C + 4) + 1) & ~1);
-  static constexpr int UDBL = ((ROWS * PITCH) + 15) & ~15;          // 128-B multiple
+  static constexpr int HR = (ROWS + 1) / 2;                          // PAIR: rows per half box
+  static constexpr int HALF = ((HR * BOXW) + 15) & ~15;             // PAIR: half-box stride (128 B)
+  static constexpr int UDBL = (((PAIR ? 2 * HALF : ROWS * PITCH)) + 15) & ~15;  // 128-B multiple
   static constexpr int MPITCH = 2 * MCOLS;                           // doubles per material row
   static constexpr int MDBL = ((MROWS * MPITCH) + 15) & ~15;
   static constexpr int SLOT = NU * UDBL + MDBL;                      // doubles, 128-B multiple
@@ -202,7 +214,8 @@ struct PlaneRing {
   static constexpr int NSLOT = TM ? S : S + 1;
   static constexpr size_t BYTES = (size_t)NSLOT * SLOT * sizeof(double);
   static constexpr size_t META = 2 * S * sizeof(uint64_t) + ((S + 1) * ROWS + 2 * S) * sizeof(int);
-  static constexpr uint32_t UBOX_BYTES = ROWS * BOXW * 8;
+  static constexpr uint32_t UBOX_BYTES = (PAIR ? 2 * HR : ROWS) * BOXW * 8;
+  static_assert(!PAIR || (TM && NU == 1), "row-pair staging: tensor path, one input box");
   static constexpr uint32_t MBOX_BYTES = MROWS * MPITCH * 8;
   static_assert(TM || ROWS <= 32, "one producer lane per row (row path)");
   static_assert((S & (S - 1)) == 0, "S must be a power of two");
@@ -215,6 +228,9 @@ struct PlaneRing {
   int* valid;       // S               (!TM)
   unsigned* cnt;    // S release counters (refill by the last consumer warp, no producer warp)
   int tshift = 0;   // TM: 1 if the tile's first element sits at an odd offset of the tensor
+  int psh0 = 0, psh1 = 0;  // PAIR: 8-B shift of the two half boxes of the current plane
+  int64_t pilo = 0, pjlo = 0;  // PAIR: tile origin (node column / row of ring column / row 0)
+  PairGeom pg{};
   uint32_t full_a = 0, empty_a = 0;  // shared-window addresses of full[0], empty[0]
 
   // TM: the box must start at an even element (16 B); returns the (even) x coordinate
@@ -262,6 +278,18 @@ struct PlaneRing {
     const int s = t & (S - 1);
     double* slot = buf + (size_t)s * SLOT;
     mbar_arrive_expect_tx(&full[s], NU * UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
+    if (PAIR) {  // two half boxes (row parities); planes outside [0, nz] read as zeros
+      const bool in = p >= 0 && p <= pg.nz;
+      const int z = in ? (int)(p >> 1) : -1;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int64_t j = pjlo + b;
+        const int64_t d0 = pilo * C + (j & 1) * pg.lr + (p & 1) * pg.lp;
+        tma_load_3d(slot + b * HALF, umap, (int)(d0 & ~(int64_t)1), (int)(j >> 1), z, &full[s]);
+      }
+      if (MROWS > 0) tma_load_3d(slot + UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
+      return;
+    }
     const CUtensorMap *m1 = umap, *m2 = umap2;
     int z = (int)(p - uorg.t_k0);
     if (peer && peer->on) {  // ghost planes straight from the neighbour's memory
@@ -392,7 +420,16 @@ struct PlaneRing {
   }
 
   // base of row r of slot s for reading the u plane
+  // PAIR: tile origin and geometry (all threads), then the shifts of each plane before reading it
+  __device__ __forceinline__ void set_pair_tile(int64_t ilo, int64_t jlo, const PairGeom& g) {
+    pilo = ilo; pjlo = jlo; pg = g;
+  }
+  __device__ __forceinline__ void set_pair_plane(int64_t p) {
+    psh0 = (int)((pilo * C + (pjlo & 1) * pg.lr + (p & 1) * pg.lp) & 1);
+    psh1 = (int)((pilo * C + ((pjlo + 1) & 1) * pg.lr + (p & 1) * pg.lp) & 1);
+  }
   __device__ __forceinline__ const double* row_ptr(int s, int r) const {
+    if (PAIR) return buf + (size_t)s * SLOT + (r & 1) * HALF + (r >> 1) * BOXW + ((r & 1) ? psh1 : psh0);
     if (TM) return buf + (size_t)s * SLOT + r * PITCH + tshift;  // (second box: + UDBL)
     const int ss = valid[s] ? s : S;
     return buf + (size_t)ss * SLOT + r * PITCH + lead[ss * ROWS + r];

@@ -21,12 +21,12 @@ namespace fem {
 
 // GLL: 2-point Gauss-Lobatto quadrature (BP5/BP6, reading R1): the 1-D mass is
 // lumped, M~ = [0, 3m, 0] instead of [1, 2m, 1]; K~ is exact under both rules.
-template <bool TM, int MODE, int C, int TX, int TY, int R, int S, bool GLL>
+template <bool TM, int MODE, int C, int TX, int TY, int R, int S, bool GLL, bool PAIR = false>
 __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSelf3)) ? 0 : 1)), kLapMinB)
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
                    double* pnew, int bc, int tmint, int64_t kchunk, CgScalars* sc, Reduce red,
-                   const __grid_constant__ PeerMaps peer, int txa, int rya) {
+                   const __grid_constant__ PeerMaps peer, int txa, int rya, PairGeom pg) {
   // tmint = 1: the u tensor spans only the Dirichlet interior (TMA zero fill = the mask P, the
   // identity rows read x from global memory); 0: the tensor spans the whole box, the mask is
   // applied in registers and the identity rows use the staged values (no global loads).
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
   constexpr int NT = TX * (TY + (SELF ? 0 : 1));
   constexpr int ROWS = TY * R + 2;
   constexpr int COLS = TX + 2;
-  using Ring = PlaneRing<TM, ROWS, COLS, C, S, 0, 0, NU>;
+  using Ring = PlaneRing<TM, ROWS, COLS, C, S, 0, 0, NU, PAIR>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;
   ring.init(tid, NT, TY);
+  if (PAIR) ring.set_pair_tile(i0 - 1, j0 - 1, pg);
   const int tux = TM ? ring.set_tshift(i0 - 1, uorg) : 0, tuy = (int)(j0 - 1 - uorg.t_j0);
   const int nplane = (int)(ke - pfirst + 1);
   if (SELF && tid == 0) {  // prologue: the first S planes
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
       const int t = (int)(p - pfirst);
       const int slot = t & (S - 1);
       ring.wait(slot, (uint32_t)((t / S) & 1));
+      if (PAIR) ring.set_pair_plane(p);
       // x-direction filters for the R+2 rows this thread needs
       double a[R + 2][C], b[R + 2][C];
       auto xfilter = [&](auto masked) {
@@ -258,20 +260,22 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
   }
 }
 
-template <bool TM, int C, int TX, int TY, int R, int S>
+template <bool TM, int C, int TX, int TY, int R, int S, bool PAIR = false>
 static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int bc, int mode,
                               CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
-  using Ring1 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, 1>;
+  using Ring1 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, 1, PAIR>;
   using Ring2 = PlaneRing<TM, TY * R + 2, TX + 2, C, S, 0, 0, (TM ? 2 : 1)>;
   const size_t smem = (mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META);
   if (mode == 3 && !TM) return cudaErrorInvalidValue;  // single-reduction CG: tensor path only
   const bool gll = maps.quad == 1;
   auto pick = [&](auto gl) {
     constexpr bool G = decltype(gl)::value;
-    return mode == 3 ? laplace_kernel<TM, (TM ? 3 : 1), C, TX, TY, R, S, G>
-         : mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S, G>
-         : mode == 1 ? laplace_kernel<TM, 1, C, TX, TY, R, S, G>
-                     : laplace_kernel<TM, 0, C, TX, TY, R, S, G>;
+    if constexpr (PAIR) return laplace_kernel<TM, 0, C, TX, TY, R, S, G, true>;  // fem_apply only
+    else
+      return mode == 3 ? laplace_kernel<TM, (TM ? 3 : 1), C, TX, TY, R, S, G>
+           : mode == 2 ? laplace_kernel<TM, (TM ? 2 : 1), C, TX, TY, R, S, G>
+           : mode == 1 ? laplace_kernel<TM, 1, C, TX, TY, R, S, G>
+                       : laplace_kernel<TM, 0, C, TX, TY, R, S, G>;
   };
   auto kern = gll ? pick(std::true_type{}) : pick(std::false_type{});
   static bool attr_set[8] = {false, false, false, false, false, false, false, false};
@@ -305,8 +309,9 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
   PeerMaps pm;
   if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
+  const PairGeom pg = maps.pair ? *maps.pair : PairGeom{0, 0, 0};
   kern<<<grid, block, smem, s>>>(g, x, y, um, org, um2, maps.pold, maps.pnew, bc, maps.interior, kchunk, sc, red, pm,
-                                 txa, rya);
+                                 txa, rya, pg);
   add_launches(1);
   return cudaGetLastError();
 }
@@ -315,6 +320,11 @@ cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec 
                            int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   if (mode == 2 && (!maps.u || !maps.u2)) return cudaErrorInvalidValue;  // fused CG needs TMA maps
   if (mode == 3 && !maps.u) return cudaErrorInvalidValue;
+  if (maps.pair) {  // caller vector with odd rows through a row-pair tensor (fem_apply)
+    if (mode != 0 || !bc) return cudaErrorInvalidValue;
+    if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, 8, true>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    return launch_cfg<true, 3, kLapTX, kLapTY3, kLapR3, 8, true>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  }
   if (maps.u) {
     if (comps == 1 && mode == 2) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, kLapS1>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);

@@ -68,6 +68,38 @@ def test_apply_direct_tma(F, oracle, kind, bc, quad, dims):
         assert relerr(y1, ref) <= APPLY_TOL
 
 
+# odd rows ((nx+1) c odd) with the Dirichlet box: the Laplace kinds stage caller vectors through
+# the row-pair tensor view (two boxes per plane); equal to the bulk-row path (bitwise under Gauss)
+@pytest.mark.parametrize("kind", ["scalar", "vector"])
+@pytest.mark.parametrize("quad", [0, 1])
+@pytest.mark.parametrize("dims", [(4, 7, 9), (32, 17, 12), (64, 40, 21), (2, 2, 2), (30, 45, 3)])
+def test_apply_row_pairs(F, oracle, kind, quad, dims):
+    nx, ny, nz = dims
+    assert (nx + 1) % 2 == 1
+    h = 1.0 / max(dims)
+    g = I.rng(I.SEED_BASE + 400 + nx + 7 * ny + 31 * nz)
+    c = I.ncomp(kind)
+    x = I.uniform_vector(g, nx, ny, nz, c)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 1)
+    op.set_option("quadrature", quad)
+    xd = torch.empty(x.size + 4096, dtype=torch.float64, device="cuda")[:x.size]  # room past the end
+    xd.copy_(torch.from_numpy(x))
+    y1 = op.apply(xd).cpu().numpy()
+    assert op.get_option("last_apply_path") == 2
+    op.set_option("direct_tma", 0)
+    y0 = op.apply(xd).cpu().numpy()
+    assert op.get_option("last_apply_path") == 0
+    if quad == 0:
+        assert np.array_equal(y1, y0)
+        ref = oracle.apply(kind, 1, nx, ny, nz, h, x)
+        assert relerr(y1, ref) <= APPLY_TOL
+    else:  # the Gauss-Lobatto filters contract into FMAs differently per kernel instance: 1 ulp
+        assert relerr(y1, y0) <= 4e-16
+        with oracle.quadrature("gll"):
+            ref = oracle.apply(kind, 1, nx, ny, nz, h, x)
+        assert relerr(y1, ref) <= APPLY_TOL
+
+
 @pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
 @pytest.mark.parametrize("bc", [0, 1])
 @pytest.mark.parametrize("dims", MESHES)
