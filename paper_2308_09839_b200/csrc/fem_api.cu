@@ -482,13 +482,13 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
     op->last_path = 1;
     return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), &map, 0, s);
   }
-  // Odd rows (Laplace kinds, Dirichlet box): the row-pair view (kernels_common.cuh, PairGeom) --
+  // Odd rows (Dirichlet box): the row-pair view (kernels_common.cuh, PairGeom) --
   // dim 0 spans two rows plus the plane parity, dims 1 / 2 step by row pairs / plane pairs (16-B
   // strides) -- so the apply still stages two TMA boxes per plane.  Boxes read up to one row and
   // two box widths past the vector's end (last plane): taken only when the caller's allocation
   // extends that far (cuMemGetAddressRange), else the bulk-row path.
   if (op->direct_tm && m->nranks == 1 && op->tm_ok && !op->tm_interior && op->bc && (rp & 1) &&
-      op->kind != FEM_ELASTICITY && ((uintptr_t)x & 15) == 0) {
+      (op->kind != FEM_ELASTICITY || kElCY == 2) && ((uintptr_t)x & 15) == 0) {
     unsigned bw, bh;
     u_box(op->kind, &bw, &bh);
     const int64_t lp = g.plane * op->comps;

@@ -357,13 +357,13 @@ __device__ __forceinline__ void face_corners(const double* F, int c, double& c00
 // bottom corners handed down by warp ty+1.  Per cell: 9 instead of 12 staged node values, one
 // y hand-off per two cells, the x butterflies of the shared node row computed once.  Per node the
 // summation order is the one of elastic_kernel: ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j)).
-template <bool TM, int MODE, int TY, int S, bool GLL>
+template <bool TM, int MODE, int TY, int S, bool GLL, bool PAIR = false>
 __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     elastic2_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                     TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                     const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
                     int bc, int64_t kchunk, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
-                    int txa, int tya) {
+                    int txa, int tya, PairGeom pg) {
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   constexpr int TX = 32;
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   constexpr int ROWS = 2 * TY + 1;  // node rows j0-1 .. j0+2TY-1
   constexpr int COLS = TX + 1;      // node cols i0-1 .. i0+TX-1
   constexpr int TPART = 4 * TY * TX * 3;
-  using Ring = PlaneRing<TM, ROWS, COLS, 3, S, kElMatRows, TX, NU>;
+  using Ring = PlaneRing<TM, ROWS, COLS, 3, S, kElMatRows, TX, NU, PAIR>;
   static_assert(kElMatRows >= 2 * TY, "material box covers the tile's cell rows");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     mbar_init(&tempty[tid], 1);
   }
   ring.init(tid, NT, TY);
+  if (PAIR) ring.set_pair_tile(i0 - 1, j0 - 1, pg);
   const int tux = TM ? ring.set_tshift(i0 - 1, uorg) : 0, tuy = (int)(j0 - 1 - uorg.t_j0);
   const int tmx = (int)(2 * (i0 - 1)), tmy = (int)(j0 - 1);
   const int nplane = (int)(ke - pfirst + 1);  // planes kb-1 .. ke
@@ -453,6 +454,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
                           double& LB, double& MB) {
       const int slot = t & (S - 1);
       ring.wait(slot, (uint32_t)((t / S) & 1));
+      if (PAIR) ring.set_pair_plane(pfirst + t);
       const double2 lmA = ring.mat(slot, 2 * ty, tx), lmB = ring.mat(slot, 2 * ty + 1, tx);
       const double* r0 = ring.row_ptr(slot, 2 * ty) + tx * 3;
       const double* r1 = ring.row_ptr(slot, 2 * ty + 1) + tx * 3;
@@ -612,11 +614,11 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   }
 }
 
-template <bool TM, int TY, int S>
+template <bool TM, int TY, int S, bool PAIR = false>
 static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps maps, int bc, int mode,
                                CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
   constexpr int TX = 32;
-  using Ring1 = PlaneRing<TM, 2 * TY + 1, TX + 1, 3, S, kElMatRows, TX, 1>;
+  using Ring1 = PlaneRing<TM, 2 * TY + 1, TX + 1, 3, S, kElMatRows, TX, 1, PAIR>;
   using Ring2 = PlaneRing<TM, 2 * TY + 1, TX + 1, 3, S, kElMatRows, TX, (TM ? 2 : 1)>;
   const size_t ring_bytes = mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META;
   const size_t smem = ring_bytes + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t);
@@ -624,10 +626,12 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   if (mode == 3 && !TM) return cudaErrorInvalidValue;
   auto pick = [&](auto gl) {
     constexpr bool G = decltype(gl)::value;
-    return mode == 3 ? elastic2_kernel<TM, (TM ? 3 : 1), TY, S, G>
-         : mode == 2 ? elastic2_kernel<TM, (TM ? 2 : 1), TY, S, G>
-         : mode == 1 ? elastic2_kernel<TM, 1, TY, S, G>
-                     : elastic2_kernel<TM, 0, TY, S, G>;
+    if constexpr (PAIR) return elastic2_kernel<TM, 0, TY, S, G, true>;  // fem_apply only
+    else
+      return mode == 3 ? elastic2_kernel<TM, (TM ? 3 : 1), TY, S, G>
+           : mode == 2 ? elastic2_kernel<TM, (TM ? 2 : 1), TY, S, G>
+           : mode == 1 ? elastic2_kernel<TM, 1, TY, S, G>
+                       : elastic2_kernel<TM, 0, TY, S, G>;
   };
   auto kern = gll ? pick(std::true_type{}) : pick(std::false_type{});
   static bool attr_set[8] = {false, false, false, false, false, false, false, false};
@@ -661,7 +665,7 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   PeerMaps pm;
   if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
   kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
-                                 bc, kchunk, sc, red, pm, txa, tya);
+                                 bc, kchunk, sc, red, pm, txa, tya, maps.pair ? *maps.pair : PairGeom{0, 0, 0});
   add_launches(1);
   return cudaGetLastError();
 }
@@ -726,6 +730,10 @@ cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMap
   if (mode == 3 && !maps.u) return cudaErrorInvalidValue;
   // CG vectors (tensor maps): two cell rows per thread; caller vectors (bulk-row staging, one copy
   // per ring row): one cell row per thread, 16 rows per copy batch (measured faster there)
+  if (maps.pair) {  // caller vector with odd rows through a row-pair tensor (fem_apply)
+    if (mode != 0 || !bc) return cudaErrorInvalidValue;
+    return launch_cfg2<true, kEl2TY, 2 * kEl2S, true>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+  }
   if (kElCY == 2 && maps.u) {
     if (mode == 2) return launch_cfg2<true, kEl2TY, kEl2S>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     return launch_cfg2<true, kEl2TY, 2 * kEl2S>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
