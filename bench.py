@@ -381,6 +381,11 @@ def run_native(args, cfg):
     ams = max_over_ranks(a0.elapsed_time(a1) / R)
     extra["apply_only_gdofs"] = ndof_global / (ams / 1e3) / 1e9
     extra["apply_only_ms"] = ams
+    if not hexmesh:  # fem_apply on the caller's vectors: algorithmic bytes / time vs the HBM peak
+        ab = algorithmic_apply_bytes(kind, nx, ny, nz) * nloc_planes / (nz + 1)
+        extra["apply_only_gbs"] = ab / (ams / 1e3) / 1e9
+        extra["apply_only_frac"] = extra["apply_only_gbs"] / hbm_peak
+        extra["apply_only_path"] = ["bulk rows", "tensor map", "row-pair tensor map"][op.get_option("last_apply_path")]
     extra["apply_in_cg_ms"] = apply_ms
     extra["apply_share_of_step"] = share
     extra["cg_iteration_ms"] = ms / args.steps
