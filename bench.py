@@ -471,6 +471,13 @@ def run_native(args, cfg):
             "extra": extra,
         }
         print(json.dumps(line), flush=True)
+    # release the library objects in dependency order (operator -> mesh -> communicator) before
+    # the process group goes away, instead of leaving it to interpreter-exit garbage collection
+    torch.cuda.synchronize()
+    op.close()
+    mesh.close()
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.destroy_process_group()
 
