@@ -51,7 +51,6 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
   // TY consumer warps (lane = cell column, warp = cell row) + 1 producer warp
   constexpr int TX = 32;
   constexpr int NT = TX * (TY + 1);
-  constexpr int NC = TX * TY;   // consumer threads
   constexpr int ROWS = TY + 1;  // node rows j0-1 .. j0+TY-1
   constexpr int COLS = TX + 1;  // node cols i0-1 .. i0+TX-1
   constexpr int TPART = 4 * TY * TX * 3;  // y hand-off buffers (ring of 4)
