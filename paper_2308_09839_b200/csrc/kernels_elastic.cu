@@ -511,77 +511,89 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     auto step = [&](int t, auto uc) {
       constexpr int U = decltype(uc)::value, V = 1 - U;
       load_plane(t, fA[V], fB[V], xA[V], xB[V], LA[V], MA[V], LB[V], MB[V]);
-      double FA[12], FB[12];
-      elastic_layer<GLL>(fA[U], fA[V], LA[U], MA[U], cA[U], cA[V], FA);
-      elastic_layer<GLL>(fB[U], fB[V], LB[U], MB[U], cB[U], cB[V], FB);
+      // cell A's layer and corners first, then cell B's (A's face array is dead before B's is
+      // formed); per-node sums in the fixed order ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j))
+      double BA[3], TA[3], vA[3], TB[3];
+      {
+        double FA[12];
+        elastic_layer<GLL>(fA[U], fA[V], LA[U], MA[U], cA[U], cA[V], FA);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double a00, a10, a01, a11;
+          face_corners(FA, c, a00, a10, a01, a11);
+          const double a10l = __shfl_up_sync(0xffffffffu, a10, 1);  // from cell i-1
+          const double a11l = __shfl_up_sync(0xffffffffu, a11, 1);
+          BA[c] = a10l + a00;  // node row cj (cells row cj): to warp ty-1
+          TA[c] = a11l + a01;  // node row nA, cells row cj
+        }
+      }
+      {
+        double FB[12];
+        elastic_layer<GLL>(fB[U], fB[V], LB[U], MB[U], cB[U], cB[V], FB);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double b00, b10, b01, b11;
+          face_corners(FB, c, b00, b10, b01, b11);
+          const double b10l = __shfl_up_sync(0xffffffffu, b10, 1);
+          const double b11l = __shfl_up_sync(0xffffffffu, b11, 1);
+          vA[c] = TA[c] + (b10l + b00);  // node row nA: cells row cj, then row cj+1
+          TB[c] = b11l + b01;            // node row nB, cells row cj+1
+        }
+      }
       const double* xs_A = xA[U];  // node values at plane t-1 (= the output plane)
       const double* xs_B = xB[U];
-        if (t >= 2) {  // node plane q = kb + t - 2 is complete
-          const int qo = t - 2;
-          const int b = qo & 3;
-          const uint32_t n = (uint32_t)(qo >> 2);
-          double BA[3], vA[3], TB[3];
-  #pragma unroll
+      if (t >= 2) {  // node plane q = kb + t - 2 is complete
+        const int qo = t - 2;
+        const int b = qo & 3;
+        const uint32_t n = (uint32_t)(qo >> 2);
+        if (ty >= 1) {
+          if (n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
+          double* dst = tw0 + b * (TY * TX * 3);
+          dst[0] = BA[0]; dst[1] = BA[1]; dst[2] = BA[2];
+          __syncwarp();
+          if (tx == 0) mbar_arrive_a(tfw0 + 8u * TY * b);
+        }
+        const bool qf = qo == qface0 || qo == qface1;
+        if (ownA) {
+          const bool bnode = bnA_xy || qf;
+#pragma unroll
           for (int c = 0; c < 3; ++c) {
-            double a00, a10, a01, a11, b00, b10, b01, b11;
-            face_corners(FA, c, a00, a10, a01, a11);
-            face_corners(FB, c, b00, b10, b01, b11);
-            const double a10l = __shfl_up_sync(0xffffffffu, a10, 1);  // from cell i-1
-            const double a11l = __shfl_up_sync(0xffffffffu, a11, 1);
-            const double b10l = __shfl_up_sync(0xffffffffu, b10, 1);
-            const double b11l = __shfl_up_sync(0xffffffffu, b11, 1);
-            BA[c] = a10l + a00;                     // node row cj (cells row cj): to warp ty-1
-            vA[c] = (a11l + a01) + (b10l + b00);    // node row nA: cells row cj, then row cj+1
-            TB[c] = b11l + b01;                     // node row nB, cells row cj+1
+            double vv = vA[c], xv = xs_A[c];
+            if (bnode) {
+              vv = xv;
+            }
+            yp[c] = vv;
+            if (mode == 2) pnb[c] = xv;
+            if (mode >= 1) pq = fma(vv, xv, pq);
+            if (mode == 3) rr2 = fma(xv, xv, rr2);
           }
-          if (ty >= 1) {
-            if (n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
-            double* dst = tw0 + b * (TY * TX * 3);
-            dst[0] = BA[0]; dst[1] = BA[1]; dst[2] = BA[2];
-            __syncwarp();
-            if (tx == 0) mbar_arrive_a(tfw0 + 8u * TY * b);
-          }
-          const bool qf = qo == qface0 || qo == qface1;
-          if (ownA) {
-            const bool bnode = bnA_xy || qf;
-  #pragma unroll
+        }
+        if (ty < TY - 1) {
+          mbar_wait_a(tfr0 + 8u * TY * b, n & 1);
+          const double* src = tr0 + b * (TY * TX * 3);
+          double v[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) v[c] = TB[c] + src[c];
+          __syncwarp();
+          if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
+          if (ownB) {
+            const bool bnode = bnB_xy || qf;
+#pragma unroll
             for (int c = 0; c < 3; ++c) {
-              double vv = vA[c], xv = xs_A[c];
+              double vv = v[c], xv = xs_B[c];
               if (bnode) {
                 vv = xv;
               }
-              yp[c] = vv;
-              if (mode == 2) pnb[c] = xv;
+              yp[yo.rpitch + c] = vv;
+              if (mode == 2) pnb[x.rpitch + c] = xv;
               if (mode >= 1) pq = fma(vv, xv, pq);
               if (mode == 3) rr2 = fma(xv, xv, rr2);
             }
           }
-          if (ty < TY - 1) {
-            mbar_wait_a(tfr0 + 8u * TY * b, n & 1);
-            const double* src = tr0 + b * (TY * TX * 3);
-            double v[3];
-  #pragma unroll
-            for (int c = 0; c < 3; ++c) v[c] = TB[c] + src[c];
-            __syncwarp();
-            if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
-            if (ownB) {
-              const bool bnode = bnB_xy || qf;
-  #pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                double vv = v[c], xv = xs_B[c];
-                if (bnode) {
-                  vv = xv;
-                }
-                yp[yo.rpitch + c] = vv;
-                if (mode == 2) pnb[x.rpitch + c] = xv;
-                if (mode >= 1) pq = fma(vv, xv, pq);
-                if (mode == 3) rr2 = fma(xv, xv, rr2);
-              }
-            }
-          }
-          if (mode == 2) pnb += x.ppitch;
-          yp += yo.ppitch;
         }
+        if (mode == 2) pnb += x.ppitch;
+        yp += yo.ppitch;
+      }
     };
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;
