@@ -307,9 +307,17 @@ def run_native(args, cfg):
         return float(t.item())
 
     # ---- warm-up (W CG steps) ----
+    # time_apply: the K timed iterations run as ONE CUDA graph whose event-record nodes bracket
+    # every apply launch (fem_cg_iterate), so the per-apply durations are measured inside the
+    # timed, graph-replayed region itself; the warm-up replays that graph shape once.
     op.set_option("time_apply", 1)
     op.cg_begin(b, x, tol=0.0, maxit=1 << 30)
     op.cg_iterate(args.warmup)
+    if args.warmup % 2:  # even parity: the timed region replays the graph captured below
+        op.cg_iterate(1)
+    op.cg_iterate(args.steps)  # captures (and runs once) the K-iteration timed graph
+    if args.steps % 2:
+        op.cg_iterate(1)
     torch.cuda.synchronize()
     op.apply_time()  # discard warm-up events
 
@@ -334,6 +342,17 @@ def run_native(args, cfg):
     ms = max_over_ranks(e0.elapsed_time(e1))
     apply_ms_total, n_apply = op.apply_time()
     apply_ms = max_over_ranks(apply_ms_total / max(n_apply, 1))
+    # the same K iterations from the plain CG graphs (no event nodes): the event nodes' cost
+    op.set_option("time_apply", 0)
+    op.cg_iterate(2)
+    torch.cuda.synchronize()
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    op.cg_iterate(args.steps)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ms_plain = max_over_ranks(f0.elapsed_time(f1))
     info = op.cg_end()
     value = ndof_global * args.steps / (ms / 1e3) / 1e9
 
@@ -387,6 +406,8 @@ def run_native(args, cfg):
         extra["apply_only_frac"] = extra["apply_only_gbs"] / hbm_peak
         extra["apply_only_path"] = ["bulk rows", "tensor map", "row-pair tensor map"][op.get_option("last_apply_path")]
     extra["apply_in_cg_ms"] = apply_ms
+    extra["apply_launches_timed"] = n_apply
+    extra["cg_iteration_ms_plain_graph"] = ms_plain / args.steps
     extra["apply_share_of_step"] = share
     extra["cg_iteration_ms"] = ms / args.steps
     cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused)
@@ -432,6 +453,14 @@ def run_native(args, cfg):
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
                    "sample": f"failed: {ex}"}
 
+    l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size
+    vec_bytes = 8 * op.n_local
+    if 2 * vec_bytes > l2_bytes:
+        l2_label = ("inputs larger than L2 (vectors %.3f GB each per rank, L2 %.0f MB)"
+                    % (vec_bytes / 1e9, l2_bytes / 1e6))
+    else:
+        l2_label = ("L2-resident (vectors %.2f MB each per rank, L2 %.0f MB): latency-bound, "
+                    "not a roofline number" % (vec_bytes / 1e6, l2_bytes / 1e6))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -445,7 +474,7 @@ def run_native(args, cfg):
                        "material": "E=10^U(0,2), nu=U(0.20,0.35) per cell" if kind == "elastic" else None,
                        "parallelism": (f"z-slab x{ws}" + (" peer-halo" if args.peer_halo else " nccl-halo"))
                                       if ws > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (vectors %.2f GB each)" % (ndof_global * 8 / 1e9)},
+                       "l2": l2_label},
             "roofline": ({"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": traffic,
                           "kernel": (f"{kind} fused CG apply (p = r + beta p_old, q = A p, p.q)" if fused
@@ -589,6 +618,26 @@ def csr_compare(fem, torch, kind, args):
     return out
 
 
+def relaunch_multi_gpu(args):
+    """--gpus N > 1 outside torchrun: start N ranks (one per GPU) under torch.distributed.run on
+    this node, or fail loudly if fewer than N GPUs are visible.  Rank 0's JSON line is the output."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} GPUs; "
+                          f"{have} visible", "n_gpus": args.gpus}), flush=True)
+        sys.exit(2)
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -624,9 +673,14 @@ def main():
         cfg["name"] += "_gll"
     if args.cgcg:
         cfg["name"] += "_cgcg"
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_multi_gpu(args)
     else:
+        if ws != args.gpus and "WORLD_SIZE" in os.environ:
+            print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
         run_native(args, cfg)
 
 

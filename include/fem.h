@@ -71,7 +71,10 @@ typedef struct {
   int32_t breakdown_iter;  /* iteration at which p.Ap <= 0 / non-finite was seen, else -1       */
   int32_t status;          /* FEM_OK or FEM_EBREAKDOWN                                          */
   double r0_norm;          /* ||b - A x0||_2 (global)                                           */
-  double r_norm;           /* recurrence residual norm sqrt(r.r) at exit                        */
+  double r_norm;           /* recurrence residual norm sqrt(r.r) of the last residual the
+                              recurrence computed: the exit iterate's (Hestenes-Stiefel); with
+                              cg_variant 1 the iterate the last update started from, unless
+                              converged (then the exit iterate's)                              */
   double true_r_norm;      /* ||b - A x||_2 recomputed at exit (one extra apply)                */
 } fem_cg_info;
 
@@ -90,6 +93,17 @@ int fem_get_unique_id(void* id_out, int64_t id_bytes /* >= 128 */);
  * it only defines the slab partition (for single-process tests with fem_apply_ghost); calls that
  * need an exchange (fem_apply, fem_dot, fem_cg_*) then return FEM_EUNSUPPORTED. */
 int fem_comm_create(int32_t nranks, int32_t rank, const void* id, fem_comm_t* out);
+/* In-process loopback communicator: creates `nranks` (1..64) communicators out[0..nranks-1] of
+ * one group on the calling thread's current device, with no NCCL.  Each is used by ONE host
+ * thread (the rank), every rank with its own stream, all on that device.  The library's
+ * collectives (node-plane halo, allreduce of the CG scalars, the peer-halo exchange) become
+ * device copies and a rank-ordered sum kernel, ordered across the ranks' streams by CUDA events
+ * the ranks exchange through a host rendezvous; so fem_apply, fem_dot, fem_cg_* and the
+ * "peer_halo" option run the multi-rank code paths of the slab decomposition on one GPU (tests;
+ * DESIGN.md §7).  Every rank must enter the same collectives in the same order (as with NCCL); a
+ * rank missing for 120 s makes the others fail with FEM_ESTATE.  CG iterations are launched
+ * eagerly (no CUDA graph: the rendezvous is on the host).  Destroy every returned communicator. */
+int fem_comm_create_loopback(int32_t nranks, fem_comm_t* out);
 /* Slab partition (pure host function, no CUDA): the nz+1 node planes split as evenly as
  * possible, rank r owns [plane_begin, plane_end); the first (nz+1) % nranks ranks get one more. */
 int fem_partition(int64_t nz, int32_t nranks, int32_t rank, int64_t* plane_begin,

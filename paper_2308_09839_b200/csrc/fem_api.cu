@@ -8,7 +8,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -23,6 +25,30 @@ namespace fem {
 cudaError_t upload_unit_matrices(const double* K, const double* Kl, const double* Km);
 static std::atomic<int64_t> g_launches{0};
 void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+struct SmemAttr {
+  const void* fn;
+  int dev, smem;
+};
+static std::vector<SmemAttr> g_smem_attr;
+static std::mutex g_smem_mu;
+cudaError_t ensure_smem_attr(const void* kernel, int smem) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_smem_mu);
+  for (const SmemAttr& a : g_smem_attr)
+    if (a.fn == kernel && a.dev == dev && a.smem >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  for (SmemAttr& a : g_smem_attr)
+    if (a.fn == kernel && a.dev == dev) {
+      a.smem = smem;
+      return cudaSuccess;
+    }
+  g_smem_attr.push_back(SmemAttr{kernel, dev, smem});
+  return cudaSuccess;
+}
 }  // namespace fem
 
 using namespace fem;
@@ -67,9 +93,34 @@ static int fail(int code, const char* fmt, ...) {
 // ------------------------------------------------------------------------------------------
 // handles
 // ------------------------------------------------------------------------------------------
+// In-process loopback group (fem_comm_create_loopback): the P slab ranks of one
+// process on one device, each driven by its own host thread and stream.  Every NCCL call site
+// (halo_pitch, allreduce1, the peer-halo handle exchange) has a loopback branch: stream-ordered
+// device copies / a fixed-order sum kernel, ordered across the ranks' streams by CUDA events that
+// the ranks exchange through a host rendezvous.  Like NCCL, every collective is entered by every
+// rank in the same order.
+struct LoopRec {
+  const void* p = nullptr;  // halo: owned base of the published vector; peer exchange: fem_op_s*
+  int64_t np = 0, pitch = 0;
+};
+struct LoopGroup {
+  static constexpr int K = 64;  // event / record ring per rank (>= P: see loop_publish)
+  static constexpr int KR = 4;  // allreduce staging ring
+  static constexpr int MAXC = 8;  // values per allreduce
+  int P = 0, device = 0, refs = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<int64_t> seq;       // [P] collectives published by each rank
+  std::vector<LoopRec> rec;       // [P][K]
+  std::vector<cudaEvent_t> ev;    // [P][K]
+  double* red = nullptr;          // device [KR][P][MAXC] allreduce contributions
+};
+
 struct fem_comm_s {
   int nranks = 1, rank = 0, device = 0;
   ncclComm_t nccl = nullptr;
+  LoopGroup* loop = nullptr;  // loopback group (no NCCL)
+  int64_t loop_seq = 0, loop_ar = 0;  // this rank's collective / allreduce counters
 };
 
 struct fem_mesh_s {
@@ -137,6 +188,22 @@ struct fem_op_s {
   int64_t pm_klo = -(int64_t(1) << 62), pm_khi = -(int64_t(1) << 62);
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
+  bool ev_capture = false;   // events are being captured as graph nodes
+  struct MapEnt {
+    const void* p = nullptr;
+    unsigned long long id = 0;
+    int path = 0;
+    CUtensorMap map{};
+  };
+  std::vector<MapEnt> map_cache;  // fem_apply tensor maps over caller vectors
+  size_t map_next = 0;
+  // time_apply with graphs: one graph of exactly graphT_iters iterations (from parity
+  // graphT_parity) with event-record nodes around every apply
+  struct TimedGraph {
+    cudaGraphExec_t exec = nullptr;
+    int iters = 0, parity = 0;
+  };
+  std::vector<TimedGraph> graphT;  // up to 4 (iteration count, parity) shapes
 };
 
 struct fem_csr_s {
@@ -150,14 +217,49 @@ struct fem_csr_s {
 // ------------------------------------------------------------------------------------------
 // helpers
 // ------------------------------------------------------------------------------------------
-static bool is_device_ptr(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
+// One driver query per caller pointer: memory type, the allocation it lies in and that
+// allocation's unique id (cuPointerGetAttributes, no error for plain host pointers).
+struct PtrInfo {
+  bool device = false;
+  unsigned long long id = 0;  // CU_POINTER_ATTRIBUTE_BUFFER_ID (0: not a CUDA allocation)
+  uintptr_t base = 0;         // allocation range
+  size_t size = 0;
+};
+static PtrInfo ptr_info(const void* p) {
+  using PFN = CUresult (*)(unsigned int, CUpointer_attribute*, void**, CUdeviceptr);
+  static PFN fn = nullptr;
+  PtrInfo r;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttributes", &f, cudaEnableDefault, &q) != cudaSuccess || !f) {
+      cudaGetLastError();
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return r;
+      }
+      r.device = a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+      return r;
+    }
+    fn = reinterpret_cast<PFN>(f);
   }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  unsigned int mtype = 0, managed = 0;
+  CUdeviceptr start = 0;
+  size_t size = 0;
+  unsigned long long id = 0;
+  CUpointer_attribute at[5] = {CU_POINTER_ATTRIBUTE_MEMORY_TYPE, CU_POINTER_ATTRIBUTE_IS_MANAGED,
+                               CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, CU_POINTER_ATTRIBUTE_RANGE_SIZE,
+                               CU_POINTER_ATTRIBUTE_BUFFER_ID};
+  void* data[5] = {&mtype, &managed, &start, &size, &id};
+  if (fn(5, at, data, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS) return r;
+  r.device = mtype == CU_MEMORYTYPE_DEVICE || managed;
+  r.id = id;
+  r.base = (uintptr_t)start;
+  r.size = size;
+  return r;
 }
+static bool is_device_ptr(const void* p) { return ptr_info(p).device; }
 
 static int check_vec(const void* p, const char* name) {
   if (!p) return fail(FEM_EINVAL, "%s is NULL", name);
@@ -239,8 +341,83 @@ static int ensure_unit_matrices(int dev) {
 
 static int need_comm(fem_op_s* op) {
   fem_mesh_s* m = op->mesh;
-  if (m->nranks > 1 && (!m->comm || !m->comm->nccl))
+  if (m->nranks > 1 && (!m->comm || (!m->comm->nccl && !m->comm->loop)))
     return fail(FEM_EUNSUPPORTED, "virtual communicator: use fem_apply_ghost (no exchange available)");
+  return FEM_OK;
+}
+
+// ---- loopback collectives ------------------------------------------------------------------
+// Publish this rank's record (+ an event recorded on its stream) for its next collective and wait
+// until the ranks `who` have published theirs; their records / events are returned.
+// Ring reuse: a rank re-records its slot of collective n at n + K only after the rendezvous of
+// n + K - 1, by which every rank within distance K - 1 in the slab chain has published n + 1,
+// i.e. finished consuming collective n (K = 64 >= P, fem_comm_create_loopback).
+static int loop_publish(fem_comm_s* c, const LoopRec& mine, cudaStream_t s, const int* who, int nwho,
+                        LoopRec* out, cudaEvent_t* out_ev) {
+  LoopGroup* G = c->loop;
+  const int64_t n = c->loop_seq++;
+  const int slot = (int)(n % LoopGroup::K);
+  const int me = c->rank;
+  CUDA_TRY(cudaEventRecord(G->ev[me * LoopGroup::K + slot], s));
+  std::unique_lock<std::mutex> lk(G->mu);
+  G->rec[me * LoopGroup::K + slot] = mine;
+  G->seq[me] = n + 1;
+  G->cv.notify_all();
+  const bool ok = G->cv.wait_for(lk, std::chrono::seconds(120), [&] {
+    for (int t = 0; t < nwho; ++t)
+      if (G->seq[who[t]] <= n) return false;
+    return true;
+  });
+  if (!ok) return fail(FEM_ESTATE, "loopback collective %lld: a rank did not arrive within 120 s", (long long)n);
+  for (int t = 0; t < nwho; ++t) {
+    out[t] = G->rec[who[t] * LoopGroup::K + slot];
+    out_ev[t] = G->ev[who[t] * LoopGroup::K + slot];
+  }
+  return FEM_OK;
+}
+
+// halo: (1) publish the owned vector, copy the neighbours' boundary planes after their producers;
+// (2) publish "consumed", and the neighbours' streams wait for it before they can overwrite the
+// planes this rank read (the synchronising semantics of ncclSend / ncclRecv)
+static int loop_halo(fem_mesh_s* m, const double* owned, double* lo, double* hi, int64_t pitch,
+                     cudaStream_t s) {
+  fem_comm_s* c = m->comm;
+  int who[2], nw = 0;
+  if (m->rank > 0) who[nw++] = m->rank - 1;
+  if (m->rank < m->nranks - 1) who[nw++] = m->rank + 1;
+  LoopRec rec[2];
+  cudaEvent_t ev[2];
+  FEM_TRY(loop_publish(c, LoopRec{owned, m->g.k1 - m->g.k0, pitch}, s, who, nw, rec, ev));
+  for (int t = 0; t < nw; ++t) {
+    const double* src = static_cast<const double*>(rec[t].p);
+    const bool below = who[t] < m->rank;
+    const double* plane = below ? src + (rec[t].np - 1) * rec[t].pitch : src;
+    CUDA_TRY(cudaStreamWaitEvent(s, ev[t], 0));
+    CUDA_TRY(cudaMemcpyAsync(below ? lo : hi, plane, (size_t)pitch * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  FEM_TRY(loop_publish(c, LoopRec{}, s, who, nw, rec, ev));
+  for (int t = 0; t < nw; ++t) CUDA_TRY(cudaStreamWaitEvent(s, ev[t], 0));
+  return FEM_OK;
+}
+
+// allreduce(sum) of `count` device doubles: contributions staged in the group's ring, summed by
+// every rank in rank order (bitwise the same result on every rank)
+static int loop_allreduce(fem_mesh_s* m, double* dev, int count, cudaStream_t s) {
+  fem_comm_s* c = m->comm;
+  LoopGroup* G = c->loop;
+  if (count > LoopGroup::MAXC) return fail(FEM_EINVAL, "loopback allreduce of more than %d values", LoopGroup::MAXC);
+  double* stage = G->red + (c->loop_ar++ % LoopGroup::KR) * G->P * LoopGroup::MAXC;
+  CUDA_TRY(cudaMemcpyAsync(stage + m->rank * LoopGroup::MAXC, dev, count * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s));
+  std::vector<int> who(G->P);
+  for (int q = 0; q < G->P; ++q) who[q] = q;
+  std::vector<LoopRec> rec(G->P);
+  std::vector<cudaEvent_t> ev(G->P);
+  FEM_TRY(loop_publish(c, LoopRec{}, s, who.data(), G->P, rec.data(), ev.data()));
+  for (int q = 0; q < G->P; ++q)
+    if (q != m->rank) CUDA_TRY(cudaStreamWaitEvent(s, ev[q], 0));
+  cudaError_t e = launch_loop_sum(stage, G->P, LoopGroup::MAXC, count, dev, s);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "loopback sum: %s", cudaGetErrorString(e));
   return FEM_OK;
 }
 
@@ -249,6 +426,7 @@ static int halo_pitch(fem_op_s* op, const double* owned, double* lo, double* hi,
                       cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
   if (m->nranks == 1) return FEM_OK;
+  if (m->comm->loop) return loop_halo(m, owned, lo, hi, pitch, s);
   const size_t cnt = (size_t)pitch;
   const int64_t np = m->g.k1 - m->g.k0;
   ncclComm_t c = m->comm->nccl;
@@ -271,6 +449,7 @@ static int halo(fem_op_s* op, const double* owned, double* lo, double* hi, cudaS
 static int allreduce1(fem_op_s* op, double* dev_scalar, cudaStream_t s, int count = 1) {
   fem_mesh_s* m = op->mesh;
   if (m->nranks == 1) return FEM_OK;
+  if (m->comm->loop) return loop_allreduce(m, dev_scalar, count, s);
   NCCL_TRY(ncclAllReduce(dev_scalar, dev_scalar, count, ncclDouble, ncclSum, m->comm->nccl, s));
   return FEM_OK;
 }
@@ -445,25 +624,26 @@ static int apply_hex(fem_op_s* op, const double* x, double* y, int mode, cudaStr
   return FEM_OK;
 }
 
-// y = A_c x for a DEVICE dense owned vector x (halo via op ghost buffers)
-// true if [p, p + bytes) lies inside one device allocation (the caller's cudaMalloc segment)
-static bool alloc_extends(const void* p, size_t bytes) {
-  using PFN = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
-  static PFN fn = nullptr;
-  if (!fn) {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
-      return false;
-    fn = reinterpret_cast<PFN>(f);
-  }
-  CUdeviceptr base = 0;
-  size_t size = 0;
-  if (fn(&base, &size, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS) return false;
-  return (uintptr_t)p + bytes <= (uintptr_t)base + size;
+// Tensor maps over caller vectors, cached per (pointer, allocation id, staging path): fem_apply
+// on the same buffers (the usual case: a solver's work vectors) re-encodes nothing.
+static const CUtensorMap* cached_map(fem_op_s* op, const void* p, unsigned long long id, int path) {
+  for (const auto& e : op->map_cache)
+    if (e.p == p && e.id == id && e.path == path && id != 0) return &e.map;
+  return nullptr;
+}
+static CUtensorMap* new_map_slot(fem_op_s* op, const void* p, unsigned long long id, int path) {
+  constexpr size_t kSlots = 8;
+  if (op->map_cache.size() < kSlots) op->map_cache.emplace_back();
+  auto& e = op->map_cache[op->map_next++ % op->map_cache.size()];
+  e.p = p;
+  e.id = id;
+  e.path = path;
+  return &e.map;
 }
 
-static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s) {
+// y = A_c x for a DEVICE dense owned vector x (halo via op ghost buffers); xi describes x's
+// allocation (ptr_info)
+static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s, const PtrInfo& xi) {
   if (op->mesh->hex) return apply_hex(op, x, y, 0, s);
   fem_mesh_s* m = op->mesh;
   const Grid& g = m->g;
@@ -474,13 +654,17 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
   // are not adjacent to the caller's memory.
   if (op->direct_tm && m->nranks == 1 && op->tm_ok && !op->tm_interior && (rp & 1) == 0 &&
       ((uintptr_t)x & 15) == 0) {
-    unsigned bw, bh;
-    u_box(op->kind, &bw, &bh);
-    CUtensorMap map;
-    FEM_TRY(make_map3d(&map, x, (uint64_t)rp, (uint64_t)(g.ny + 1), (uint64_t)(g.nz + 1), (uint64_t)rp * 8,
-                       (uint64_t)(g.plane * op->comps) * 8, bw, bh));
+    const CUtensorMap* map = cached_map(op, x, xi.id, 1);
+    if (!map) {
+      unsigned bw, bh;
+      u_box(op->kind, &bw, &bh);
+      CUtensorMap* slot = new_map_slot(op, x, xi.id, 1);
+      FEM_TRY(make_map3d(slot, x, (uint64_t)rp, (uint64_t)(g.ny + 1), (uint64_t)(g.nz + 1), (uint64_t)rp * 8,
+                         (uint64_t)(g.plane * op->comps) * 8, bw, bh));
+      map = slot;
+    }
     op->last_path = 1;
-    return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), &map, 0, s);
+    return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), map, 0, s);
   }
   // Odd rows (Dirichlet box): the row-pair view (kernels_common.cuh, PairGeom) --
   // dim 0 spans two rows plus the plane parity, dims 1 / 2 step by row pairs / plane pairs (16-B
@@ -493,13 +677,17 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
     u_box(op->kind, &bw, &bh);
     const int64_t lp = g.plane * op->comps;
     const size_t need = (size_t)(op->n_local + rp + 2 * (int64_t)bw) * sizeof(double);
-    if (alloc_extends(x, need)) {
+    if (xi.id && (uintptr_t)x + need <= xi.base + xi.size) {
       const PairGeom pg{rp, lp, g.nz};
-      CUtensorMap map;
-      FEM_TRY(make_map3d(&map, x, (uint64_t)(lp + 2 * rp), (uint64_t)((g.ny + 2) / 2), (uint64_t)((g.nz + 2) / 2),
-                         (uint64_t)(2 * rp) * 8, (uint64_t)(2 * lp) * 8, bw, (bh + 1) / 2));
+      const CUtensorMap* map = cached_map(op, x, xi.id, 2);
+      if (!map) {
+        CUtensorMap* slot = new_map_slot(op, x, xi.id, 2);
+        FEM_TRY(make_map3d(slot, x, (uint64_t)(lp + 2 * rp), (uint64_t)((g.ny + 2) / 2), (uint64_t)((g.nz + 2) / 2),
+                           (uint64_t)(2 * rp) * 8, (uint64_t)(2 * lp) * 8, bw, (bh + 1) / 2));
+        map = slot;
+      }
       op->last_path = 2;
-      return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), &map, 0, s, nullptr, &pg);
+      return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), map, 0, s, nullptr, &pg);
     }
   }
   op->last_path = 0;
@@ -598,9 +786,58 @@ int fem_comm_create(int32_t nranks, int32_t rank, const void* id, fem_comm_t* ou
   return FEM_OK;
 }
 
+int fem_comm_create_loopback(int32_t nranks, fem_comm_t* out) {
+  if (!out) return fail(FEM_EINVAL, "out is NULL");
+  if (nranks < 1 || nranks > LoopGroup::K) return fail(FEM_EINVAL, "loopback nranks must be in [1, %d]", LoopGroup::K);
+  for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+  auto* G = new (std::nothrow) LoopGroup();
+  if (!G) return fail(FEM_ENOMEM, "host allocation failed");
+  G->P = nranks;
+  cudaGetDevice(&G->device);
+  G->seq.assign(nranks, 0);
+  G->rec.resize((size_t)nranks * LoopGroup::K);
+  G->ev.assign((size_t)nranks * LoopGroup::K, nullptr);
+  auto bail = [&](int st) {
+    for (cudaEvent_t e : G->ev)
+      if (e) cudaEventDestroy(e);
+    cudaFree(G->red);
+    for (int r = 0; r < nranks; ++r) { delete out[r]; out[r] = nullptr; }
+    delete G;
+    return st;
+  };
+  for (auto& e : G->ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(FEM_ECUDA, "cudaEventCreate failed"));
+  if (dalloc(&G->red, (size_t)LoopGroup::KR * nranks * LoopGroup::MAXC) != FEM_OK) return bail(FEM_ENOMEM);
+  for (int r = 0; r < nranks; ++r) {
+    out[r] = new (std::nothrow) fem_comm_s();
+    if (!out[r]) return bail(fail(FEM_ENOMEM, "host allocation failed"));
+    out[r]->nranks = nranks;
+    out[r]->rank = r;
+    out[r]->device = G->device;
+    out[r]->loop = G;
+  }
+  G->refs = nranks;
+  return FEM_OK;
+}
+
 void fem_comm_destroy(fem_comm_t c) {
   if (!c) return;
   if (c->nccl) ncclCommDestroy(c->nccl);
+  if (LoopGroup* G = c->loop) {
+    bool last;
+    {
+      std::lock_guard<std::mutex> lk(G->mu);
+      last = --G->refs == 0;
+    }
+    if (last) {
+      set_device(G->device);
+      for (cudaEvent_t e : G->ev)
+        if (e) cudaEventDestroy(e);
+      cudaFree(G->red);
+      delete G;
+    }
+  }
   delete c;
 }
 
@@ -758,6 +995,7 @@ static void op_free(fem_op_s* op) {
   cudaFree(op->pa);
   cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
   if (op->graph1b) cudaGraphExecDestroy(op->graph1b);
+  for (const auto& t : op->graphT) cudaGraphExecDestroy(t.exec);
   cudaFree(op->ghost_lo); cudaFree(op->ghost_hi);
   cudaFree(op->stage_a); cudaFree(op->stage_b);
   cudaFree(op->sc); cudaFree(op->dot_dev); cudaFree(op->bad);
@@ -1080,6 +1318,22 @@ int fem_op_open_peers(fem_op_t op, const void* lo_info, const void* hi_info) {
 static int peer_halo_ipc(fem_op_s* op) {
   fem_mesh_s* m = op->mesh;
   if (m->nranks == 1) return FEM_OK;
+  if (m->comm && m->comm->loop) {  // same process and device: link the neighbours' operators
+    int who[2], nw = 0;
+    if (m->rank > 0) who[nw++] = m->rank - 1;
+    if (m->rank < m->nranks - 1) who[nw++] = m->rank + 1;
+    LoopRec rec[2];
+    cudaEvent_t ev[2];
+    FEM_TRY(loop_publish(m->comm, LoopRec{op, 0, 0}, 0, who, nw, rec, ev));
+    fem_op_s* lo = nullptr;
+    fem_op_s* hi = nullptr;
+    for (int t = 0; t < nw; ++t)
+      (who[t] < m->rank ? lo : hi) = static_cast<fem_op_s*>(const_cast<void*>(rec[t].p));
+    const int st = fem_op_link_peers(op, lo, hi);
+    // the neighbours hold this operator's pointer: nobody returns before everyone has linked
+    FEM_TRY(loop_publish(m->comm, LoopRec{}, 0, who, nw, rec, ev));
+    return st;
+  }
   if (!m->comm || !m->comm->nccl) return fail(FEM_EUNSUPPORTED, "peer halo across processes needs an NCCL communicator");
   PeerInfo mine{};
   FEM_TRY(fem_op_peer_info(op, &mine, sizeof(mine)));
@@ -1116,8 +1370,9 @@ int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
   if (op->kind == FEM_ELASTICITY && !op->has_mat) return fail(FEM_ESTATE, "material not set");
   FEM_TRY(set_device(op->mesh->device));
   cudaStream_t s = (cudaStream_t)stream;
-  const bool xd = is_device_ptr(x), yd = is_device_ptr(y);
-  if (xd && yd) return apply_device(op, x, y, s);
+  const PtrInfo xi = ptr_info(x);
+  const bool xd = xi.device, yd = is_device_ptr(y);
+  if (xd && yd) return apply_device(op, x, y, s, xi);
   FEM_TRY(ensure_stage(op));
   const size_t bytes = op->n_local * sizeof(double);
   const double* xs = x;
@@ -1126,7 +1381,7 @@ int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
     xs = op->stage_a;
   }
   double* ys = yd ? y : op->stage_b;
-  FEM_TRY(apply_device(op, xs, ys, s));
+  FEM_TRY(apply_device(op, xs, ys, s, xd ? xi : ptr_info(xs)));
   if (!yd) {
     CUDA_TRY(cudaMemcpyAsync(y, ys, bytes, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1154,24 +1409,31 @@ int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void*
 }
 
 // ---- CG -----------------------------------------------------------------------------------
+// option time_apply: CUDA events around every apply launch of the CG iterations (read back by
+// fem_apply_time).  Inside a stream capture they become event-record nodes of the graph
+// (cudaEventRecordExternal), so the graph-replayed iteration is timed as it runs.
+static int ensure_events(fem_op_s* op, size_t n) {
+  while (op->ev.size() < n) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    op->ev.push_back(e);
+  }
+  return FEM_OK;
+}
+static int apply_event(fem_op_s* op, int end, cudaStream_t s) {
+  if (!end) FEM_TRY(ensure_events(op, op->ev_used + 2));
+  cudaEvent_t e = op->ev[op->ev_used + end];
+  CUDA_TRY(cudaEventRecordWithFlags(e, s, op->ev_capture ? cudaEventRecordExternal : cudaEventRecordDefault));
+  if (end) op->ev_used += 2;
+  return FEM_OK;
+}
+
 static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
   const int64_t n = pl_count(op);
-  if (timed) {
-    if (op->ev_used + 2 > op->ev.size()) {
-      for (int t = 0; t < 64; ++t) {
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreate(&e));
-        op->ev.push_back(e);
-      }
-    }
-    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used], s));
-  }
+  if (timed) FEM_TRY(apply_event(op, 0, s));
   FEM_TRY(apply_pl(op, op->p_pl, &op->tm_p, 1, s));  // q = A p, pq (halo inside when P > 1)
-  if (timed) {
-    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used + 1], s));
-    op->ev_used += 2;
-  }
+  if (timed) FEM_TRY(apply_event(op, 1, s));
   FEM_TRY(allreduce1(op, &op->sc->pq, s));
   cudaError_t e = launch_cg_update(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, op->p_pl),
                                    pl_owned(op, op->q_pl), n, op->sc, op->red, s, m->sm_count);
@@ -1195,16 +1457,7 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
       FEM_TRY(halo_pitch(op, pl_owned(op, v), v + op->pl_lead,
                          v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp, op->pl_pp, s));
   }
-  if (timed) {
-    if (op->ev_used + 2 > op->ev.size()) {
-      for (int t = 0; t < 64; ++t) {
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreate(&e));
-        op->ev.push_back(e);
-      }
-    }
-    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used], s));
-  }
+  if (timed) FEM_TRY(apply_event(op, 0, s));
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
                  parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
                  op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr};
@@ -1216,10 +1469,7 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
     e = launch_laplace(op->comps, op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc,
                        op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "fused apply launch: %s", cudaGetErrorString(e));
-  if (timed) {
-    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used + 1], s));
-    op->ev_used += 2;
-  }
+  if (timed) FEM_TRY(apply_event(op, 1, s));
   FEM_TRY(allreduce1(op, &op->sc->pq, s));
   e = launch_cg_update_fused(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, pnew),
                              pl_owned(op, op->q_pl), pl_count(op), op->sc, op->red, s, m->sm_count);
@@ -1232,21 +1482,9 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
 // gamma = r.r reduced together (one allreduce of 2 values), then one update kernel
 static int cg_cgcg_body(fem_op_s* op, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
-  if (timed) {
-    if (op->ev_used + 2 > op->ev.size()) {
-      for (int t = 0; t < 64; ++t) {
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreate(&e));
-        op->ev.push_back(e);
-      }
-    }
-    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used], s));
-  }
+  if (timed) FEM_TRY(apply_event(op, 0, s));
   FEM_TRY(apply_pl(op, op->r_pl, &op->tm_r, 3, s));  // w (q_pl) = A r; pq = w.r, rr_new = r.r
-  if (timed) {
-    CUDA_TRY(cudaEventRecord(op->ev[op->ev_used + 1], s));
-    op->ev_used += 2;
-  }
+  if (timed) FEM_TRY(apply_event(op, 1, s));
   FEM_TRY(allreduce1(op, &op->sc->pq, s, 2));  // pq and rr_new are adjacent in CgScalars
   cudaError_t e = launch_cg_cgcg_update(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, op->p_pl),
                                         pl_owned(op, op->p2_pl), pl_owned(op, op->q_pl), pl_count(op), op->sc,
@@ -1262,14 +1500,22 @@ static int iteration(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   return op->tm_ok ? cg_fused_body(op, parity, s, timed) : cg_iteration_body(op, s, timed);
 }
 
-static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGraphExec_t* out) {
+static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGraphExec_t* out,
+                   bool timed = false) {
   // capture on a private stream (legacy stream 0 cannot be captured)
+  if (timed) {
+    op->ev_used = 0;
+    FEM_TRY(ensure_events(op, 2 * (size_t)iters));
+  }
   cudaStream_t cs;
   CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   const int64_t before = g_launches.load();
   int st = FEM_OK;
-  for (int t = 0; t < iters && st == FEM_OK; ++t) st = iteration(op, (parity + t) & 1, cs, false);
+  op->ev_capture = timed;
+  for (int t = 0; t < iters && st == FEM_OK; ++t) st = iteration(op, (parity + t) & 1, cs, timed);
+  op->ev_capture = false;
+  if (timed) op->ev_used = 0;  // set at each replay
   g_launches.store(before);  // captured launches are counted at replay
   cudaGraph_t graph;
   cudaError_t e = cudaStreamEndCapture(cs, &graph);
@@ -1314,7 +1560,29 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
 static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
   const int per_iter_launches =
       op->tm_ok ? 2 : (op->mesh->hex ? 3 + ((op->bc && op->mesh->hx_nb) ? 1 : 0) : 3);
-  if (op->time_apply || !op->use_graph) {
+  // loopback ranks rendezvous on the host inside every collective: not capturable, run eagerly
+  const bool loop = op->mesh->comm && op->mesh->comm->loop && op->mesh->nranks > 1;
+  if (op->time_apply && op->use_graph && !loop && iters > 0) {
+    // timed AND graph-replayed: one graph of exactly `iters` iterations whose event-record nodes
+    // bracket every apply (the events of the last replay are read by fem_apply_time)
+    cudaGraphExec_t ge = nullptr;
+    for (const auto& t : op->graphT)
+      if (t.iters == iters && t.parity == op->cg_parity) ge = t.exec;
+    if (!ge) {
+      if (op->graphT.size() >= 4) {
+        cudaGraphExecDestroy(op->graphT.front().exec);
+        op->graphT.erase(op->graphT.begin());
+      }
+      FEM_TRY(capture(op, iters, op->cg_parity, s, &ge, true));
+      op->graphT.push_back({ge, iters, op->cg_parity});
+    }
+    CUDA_TRY(cudaGraphLaunch(ge, s));
+    add_launches((int64_t)iters * per_iter_launches);
+    op->ev_used = 2 * (size_t)iters;
+    op->cg_parity ^= (iters & 1);
+    return FEM_OK;
+  }
+  if (op->time_apply || !op->use_graph || loop) {
     for (int t = 0; t < iters; ++t) {
       FEM_TRY(iteration(op, op->cg_parity, s, op->time_apply != 0));
       op->cg_parity ^= 1;
@@ -1349,11 +1617,13 @@ static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
   int status = (h.done == 2) ? FEM_EBREAKDOWN : FEM_OK;
   if (info) {
     info->iterations = h.it;
-    info->converged = (h.done == 1) || (h.rr == 0.0) || (h.rr <= h.stop_rr);
+    info->converged = (h.done == 1) || (h.rr_new == 0.0) || (h.rr_new <= h.stop_rr);
     info->breakdown_iter = h.breakdown_iter;
     info->status = status;
     info->r0_norm = std::sqrt(h.rr0);
-    info->r_norm = std::sqrt(h.rr);
+    // rr_new is the last residual the recurrence computed (fused CG: the update's r.r; unfused:
+    // equal to rr; single-reduction CG: gamma = r.r of the iterate the last update started from)
+    info->r_norm = std::sqrt(h.rr_new);
     // true residual ||b - A x||
     FEM_TRY(apply_pl(op, op->x_pl, &op->tm_x, 0, s));
     FEM_TRY(pack(op, op->cg_b, op->r_pl, 1, s));
@@ -1440,6 +1710,17 @@ int fem_cg_solve(fem_op_t op, const double* b, double* x, double tol, int32_t ma
   return st;
 }
 
+// captured CG graphs hold the kernels / options of their capture
+static void drop_graphs(fem_op_s* op) {
+  for (cudaGraphExec_t* g : {&op->graph1, &op->graphN, &op->graph1b})
+    if (*g) {
+      cudaGraphExecDestroy(*g);
+      *g = nullptr;
+    }
+  for (const auto& t : op->graphT) cudaGraphExecDestroy(t.exec);
+  op->graphT.clear();
+}
+
 // (re)compute the stored Gauss-point geometry when partial assembly is on and the rule changed
 static int pa_setup(fem_op_s* op) {
   if (!op->use_pa || op->pa_quad == op->quad) return FEM_OK;
@@ -1466,9 +1747,7 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     op->use_pa = value != 0;
     FEM_TRY(pa_setup(op));
     // captured CG graphs hold the other kernel
-    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
-    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
-    if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
+    drop_graphs(op);
   } else if (!std::strcmp(key, "peer_halo")) {
     // collective over the slab ranks (every rank must set it): ghost planes read in the apply
     // kernels straight from the neighbours' memory (CUDA IPC over NVLink), no NCCL halo
@@ -1477,16 +1756,12 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (op->cg_active) return fail(FEM_ESTATE, "peer_halo cannot change during a CG solve");
     FEM_TRY(set_device(op->mesh->device));
     if (!op->peer_on) FEM_TRY(peer_halo_ipc(op));
-    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
-    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
-    if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
+    drop_graphs(op);
   } else if (!std::strcmp(key, "cg_variant")) {
     if (value != 0 && value != 1) return fail(FEM_EINVAL, "cg_variant must be 0 (fused CG) or 1 (Chronopoulos-Gear)");
     if (op->cg_active) return fail(FEM_ESTATE, "cg_variant cannot change during a CG solve");
     op->cg_variant = (int)value;
-    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
-    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
-    if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
+    drop_graphs(op);
   } else if (!std::strcmp(key, "quadrature")) {
     if (value != 0 && value != 1) return fail(FEM_EINVAL, "quadrature must be 0 (Gauss) or 1 (Gauss-Lobatto)");
     if (value == 1 && op->mesh->hex) {  // the Lobatto points are the nodes: det J > 0 there too
@@ -1506,9 +1781,7 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     op->quad = (int)value;
     FEM_TRY(set_device(op->mesh->device));
     FEM_TRY(pa_setup(op));
-    if (op->graph1) { cudaGraphExecDestroy(op->graph1); op->graph1 = nullptr; }
-    if (op->graphN) { cudaGraphExecDestroy(op->graphN); op->graphN = nullptr; }
-    if (op->graph1b) { cudaGraphExecDestroy(op->graph1b); op->graph1b = nullptr; }
+    drop_graphs(op);
   } else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }

@@ -216,6 +216,8 @@ cudaError_t launch_hex_pack_cells(const int32_t* vtk, const uint8_t* dir, int64_
 // p = r + beta p, s = w + beta s, x += alpha p, r -= alpha s (first step: p = r, s = w)
 cudaError_t launch_cg_cgcg_update(double* x, double* r, double* p, double* s, const double* w, int64_t n,
                                   CgScalars* sc, Reduce red, cudaStream_t st, int sm_count);
+// loopback allreduce: out[i] = sum over ranks q = 0..P-1 (in order) of stage[q * stride + i]
+cudaError_t launch_loop_sum(const double* stage, int P, int stride, int count, double* out, cudaStream_t s);
 // deterministic dot -> *out (device)
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
                        cudaStream_t s, int sm_count);
@@ -235,6 +237,9 @@ cudaError_t launch_csr_spmv(int comps, int64_t nrows, const int64_t* rowptr, con
                             int sm_count);
 
 void add_launches(int64_t n);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, smem) once per (kernel, current device): the
+// attribute belongs to the device context, so a process driving several GPUs sets it on each.
+cudaError_t ensure_smem_attr(const void* kernel, int smem);
 
 }  // namespace fem
 

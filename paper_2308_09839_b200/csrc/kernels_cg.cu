@@ -170,11 +170,10 @@ __global__ void __launch_bounds__(kVecThreads) cg_cgcg_update_kernel(double* __r
   if (sc->done) return;
   const double gam = sc->rr_new, delta = sc->pq;
   const bool first = sc->first != 0;
+  // Early exits write only `done` / `breakdown_iter`: other blocks may still be reading rr, alpha
+  // and first to take the same decision (the reported residual is rr_new, fem_cg_end).
   if (gam == 0.0 || gam <= sc->stop_rr) {  // converged at the current iterate (same test in every block)
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      sc->rr = gam;
-      sc->done = 1;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->done = 1;
     return;
   }
   const double beta = first ? 0.0 : gam / sc->rr;
@@ -183,7 +182,6 @@ __global__ void __launch_bounds__(kVecThreads) cg_cgcg_update_kernel(double* __r
   if (!(denom > 0.0) || !isfinite(alpha)) {  // breakdown
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       sc->breakdown_iter = sc->it;
-      sc->rr = gam;
       sc->done = 2;
     }
     return;
@@ -269,6 +267,15 @@ __global__ void __launch_bounds__(kVecThreads) dot_kernel(const double* __restri
   if (last_block_reduce(bs, red, sh, &tot)) *out = tot;
 }
 
+__global__ void loop_sum_kernel(const double* __restrict__ stage, int P, int stride, int count,
+                                double* __restrict__ out) {
+  const int i = threadIdx.x;
+  if (i >= count) return;
+  double v = 0.0;
+  for (int q = 0; q < P; ++q) v += stage[q * stride + i];
+  out[i] = v;
+}
+
 __global__ void sub_kernel(const double* __restrict__ b, const double* __restrict__ ax,
                            double* __restrict__ out, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -327,6 +334,11 @@ cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* 
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
                        cudaStream_t s, int sm_count) {
   dot_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(a, b, n, out, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_loop_sum(const double* stage, int P, int stride, int count, double* out, cudaStream_t s) {
+  loop_sum_kernel<<<1, 32, 0, s>>>(stage, P, stride, count, out);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -658,12 +658,10 @@ cudaError_t launch_hex_apply(int kind, int bc, int quad, const int4* cells, cons
 #define PF_LAUNCH(K, M, G)                                                                               \
   {                                                                                                       \
     constexpr size_t sm = hex_pf_smem<(K == 0) ? 1 : 3>(kHexThreads);                                     \
-    static bool set = false;                                                                              \
-    if (!set) {                                                                                           \
-      cudaError_t e = cudaFuncSetAttribute(hex_apply_pf_kernel<K, M, G>,                                  \
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);          \
+    {                                                                                                     \
+      const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(hex_apply_pf_kernel<K, M, G>),  \
+                                             (int)sm);                                                    \
       if (e != cudaSuccess) return e;                                                                     \
-      set = true;                                                                                         \
     }                                                                                                     \
     hex_apply_pf_kernel<K, M, G><<<grid, kHexThreads, sm, s>>>(cells, xyz, lm, x, y, ncells, bc, sc, red); \
   }

@@ -278,11 +278,9 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
                        : laplace_kernel<TM, 0, C, TX, TY, R, S, G>;
   };
   auto kern = gll ? pick(std::true_type{}) : pick(std::false_type{});
-  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
-  if (!attr_set[mode + 4 * gll]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set[mode + 4 * gll] = true;
   }
   int txa, rya;
   const int64_t xt = balanced_tiles(g.nx + 1, TX, &txa);

@@ -43,6 +43,7 @@ class CgInfo(ctypes.Structure):
 # every symbol include/fem.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fem_last_error", "fem_version", "fem_launch_count", "fem_get_unique_id", "fem_comm_create",
+    "fem_comm_create_loopback",
     "fem_comm_destroy", "fem_partition", "fem_apply_ghost", "fem_apply_ghost_padded", "fem_op_link_peers",
     "fem_op_peer_info", "fem_op_open_peers", "fem_mesh_create", "fem_mesh_local", "fem_mesh_destroy",
     "fem_mesh_create_hex", "fem_mesh_info_hex", "fem_op_create",
@@ -75,6 +76,7 @@ def load(build_if_missing: bool = True):
         "fem_launch_count": ([], i64),
         "fem_get_unique_id": ([vp, i64], ctypes.c_int),
         "fem_comm_create": ([i32, i32, vp, P(vp)], ctypes.c_int),
+        "fem_comm_create_loopback": ([i32, P(vp)], ctypes.c_int),
         "fem_comm_destroy": ([vp], None),
         "fem_partition": ([i64, i32, i32, P(i64), P(i64)], ctypes.c_int),
         "fem_apply_ghost": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
@@ -119,20 +121,30 @@ def _check(rc: int):
         raise FemError(rc, load().fem_last_error().decode())
 
 
-def _ptr(a, dtype: str = "float64"):
-    """Raw pointer of a torch tensor (device or host) or numpy array; checks dtype/contiguity."""
+def _numel(a) -> int:
+    return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
+
+
+def _ptr(a, dtype: str = "float64", n: int | None = None, name: str = "buffer"):
+    """Raw pointer of a torch tensor (device or host) or numpy array; checks dtype, contiguity
+    and, when `n` is given, the element count (the C ABI receives only the pointer, so a short
+    buffer would be over-read / over-written by the library)."""
     if a is None:
         return None
     if isinstance(a, np.ndarray):
         if a.dtype != np.dtype(dtype) or not a.flags.c_contiguous:
             raise TypeError(f"numpy arrays must be contiguous {dtype}")
-        return a.ctypes.data
-    import torch
-    if isinstance(a, torch.Tensor):
+        ptr = a.ctypes.data
+    else:
+        import torch
+        if not isinstance(a, torch.Tensor):
+            raise TypeError(f"unsupported buffer type {type(a)}")
         if a.dtype != getattr(torch, dtype) or not a.is_contiguous():
             raise TypeError(f"tensors must be contiguous {dtype}")
-        return a.data_ptr()
-    raise TypeError(f"unsupported buffer type {type(a)}")
+        ptr = a.data_ptr()
+    if n is not None and _numel(a) != n:
+        raise ValueError(f"{name} has {_numel(a)} elements, the operator needs {n}")
+    return ptr
 
 
 def _stream(stream):
@@ -174,6 +186,19 @@ class Comm:
         _check(load().fem_comm_create(nranks, rank, idbuf, ctypes.byref(h)))
         self.h = h
 
+    @classmethod
+    def loopback(cls, nranks: int) -> "list[Comm]":
+        """`nranks` in-process slab ranks on the current device (fem_comm_create_loopback): drive
+        each from its own thread and stream; the library's collectives run as device copies."""
+        arr = (ctypes.c_void_p * nranks)()
+        _check(load().fem_comm_create_loopback(nranks, arr))
+        out = []
+        for r in range(nranks):
+            c = cls.__new__(cls)
+            c.nranks, c.rank, c.h = nranks, r, ctypes.c_void_p(arr[r])
+            out.append(c)
+        return out
+
     def close(self):
         if self.h:
             load().fem_comm_destroy(self.h)
@@ -213,11 +238,14 @@ class HexMesh:
     (ne, 8) int32 in VTK corner order, optional Dirichlet flags (n,) uint8 (include/fem.h)."""
 
     def __init__(self, coords, cells, dirichlet=None):
-        n = int(coords.shape[0]) if hasattr(coords, "shape") else len(coords) // 3
-        ne = int(cells.shape[0]) if cells.ndim == 2 else int(cells.shape[0]) // 8
+        if tuple(coords.shape[1:]) != (3,) or coords.ndim != 2:
+            raise ValueError(f"coords must have shape (n, 3), got {tuple(coords.shape)}")
+        if tuple(cells.shape[1:]) != (8,) or cells.ndim != 2:
+            raise ValueError(f"cells must have shape (n_cells, 8), got {tuple(cells.shape)}")
+        n, ne = int(coords.shape[0]), int(cells.shape[0])
         m = ctypes.c_void_p()
         _check(load().fem_mesh_create_hex(n, ne, _ptr(coords), _ptr(cells, "int32"),
-                                          _ptr(dirichlet, "uint8"), ctypes.byref(m)))
+                                          _ptr(dirichlet, "uint8", n, "dirichlet"), ctypes.byref(m)))
         self.h_ = m
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(load().fem_mesh_info_hex(m, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
@@ -250,11 +278,23 @@ class Operator:
         _check(load().fem_op_ndof(o, ctypes.byref(nl), ctypes.byref(ng)))
         self.n_local, self.n_global = nl.value, ng.value
 
+    def _plane_dofs(self) -> int | None:
+        if isinstance(self.mesh, HexMesh):  # no node planes (the library rejects ghost applies)
+            return None
+        return (self.mesh.nx + 1) * (self.mesh.ny + 1) * self.comps
+
     # -- material ---------------------------------------------------------------------------
     def set_material(self, lam, mu, layer_begin: int = 0, n_layers: int | None = None):
-        if n_layers is None:
-            n_layers = 1 if isinstance(self.mesh, HexMesh) else self.mesh.nz - layer_begin
-        _check(load().fem_set_material(self.h, _ptr(lam), _ptr(mu), layer_begin, n_layers))
+        if isinstance(self.mesh, HexMesh):
+            if n_layers is None:
+                n_layers = 1
+            cnt = self.mesh.n_cells
+        else:
+            if n_layers is None:
+                n_layers = self.mesh.nz - layer_begin
+            cnt = self.mesh.nx * self.mesh.ny * n_layers
+        _check(load().fem_set_material(self.h, _ptr(lam, n=cnt, name="lambda"), _ptr(mu, n=cnt, name="mu"),
+                                       layer_begin, n_layers))
 
     # -- operator ---------------------------------------------------------------------------
     def apply(self, x, y=None, stream=None):
@@ -264,7 +304,8 @@ class Operator:
             else:
                 import torch
                 y = torch.empty_like(x)
-        _check(load().fem_apply(self.h, _ptr(x), _ptr(y), _stream(stream)))
+        n = self.n_local
+        _check(load().fem_apply(self.h, _ptr(x, n=n, name="x"), _ptr(y, n=n, name="y"), _stream(stream)))
         return y
 
     def apply_ghost(self, x, ghost_lo, ghost_hi, y=None, stream=None):
@@ -272,13 +313,17 @@ class Operator:
         if y is None:
             import torch
             y = torch.empty_like(x)
-        _check(load().fem_apply_ghost(self.h, _ptr(x), _ptr(ghost_lo), _ptr(ghost_hi), _ptr(y),
+        n, pd = self.n_local, self._plane_dofs()
+        _check(load().fem_apply_ghost(self.h, _ptr(x, n=n, name="x"), _ptr(ghost_lo, n=pd, name="ghost_lo"),
+                                      _ptr(ghost_hi, n=pd, name="ghost_hi"), _ptr(y, n=n, name="y"),
                                       _stream(stream)))
         return y
 
     def link_peers(self, lo: "Operator | None", hi: "Operator | None"):
-        """Single-process loopback of the peer halo (ghost planes from the neighbours' buffers)."""
+        """Single-process loopback of the peer halo (ghost planes from the neighbours' buffers).
+        The neighbours' device buffers are read by this operator's kernels: keep them alive."""
         _check(load().fem_op_link_peers(self.h, lo.h if lo else None, hi.h if hi else None))
+        self._peers = (lo, hi)
 
     def peer_info(self) -> bytes:
         buf = ctypes.create_string_buffer(320)
@@ -295,18 +340,23 @@ class Operator:
         if y is None:
             import torch
             y = torch.empty_like(x)
-        _check(load().fem_apply_ghost_padded(self.h, _ptr(x), _ptr(ghost_lo), _ptr(ghost_hi), _ptr(y),
+        n, pd = self.n_local, self._plane_dofs()
+        _check(load().fem_apply_ghost_padded(self.h, _ptr(x, n=n, name="x"), _ptr(ghost_lo, n=pd, name="ghost_lo"),
+                                             _ptr(ghost_hi, n=pd, name="ghost_hi"), _ptr(y, n=n, name="y"),
                                              _stream(stream)))
         return y
 
     def dot(self, a, b, stream=None) -> float:
         out = ctypes.c_double()
-        _check(load().fem_dot(self.h, _ptr(a), _ptr(b), ctypes.byref(out), _stream(stream)))
+        n = self.n_local
+        _check(load().fem_dot(self.h, _ptr(a, n=n, name="a"), _ptr(b, n=n, name="b"), ctypes.byref(out),
+                              _stream(stream)))
         return out.value
 
     def cg_solve(self, b, x, tol: float = 0.0, maxit: int = 100, stream=None, check=True):
         info = CgInfo()
-        rc = load().fem_cg_solve(self.h, _ptr(b), _ptr(x), float(tol), int(maxit),
+        n = self.n_local
+        rc = load().fem_cg_solve(self.h, _ptr(b, n=n, name="b"), _ptr(x, n=n, name="x"), float(tol), int(maxit),
                                  ctypes.byref(info), _stream(stream))
         if check and rc not in (FEM_OK, FEM_EBREAKDOWN):
             _check(rc)
@@ -315,7 +365,8 @@ class Operator:
         return d
 
     def cg_begin(self, b, x, tol: float = 0.0, maxit: int = 1 << 30, stream=None):
-        _check(load().fem_cg_begin(self.h, _ptr(b), _ptr(x), float(tol), int(maxit),
+        n = self.n_local
+        _check(load().fem_cg_begin(self.h, _ptr(b, n=n, name="b"), _ptr(x, n=n, name="x"), float(tol), int(maxit),
                                    _stream(stream)))
 
     def cg_iterate(self, iters: int, stream=None):
@@ -371,12 +422,14 @@ class Csr:
         if y is None:
             import torch
             y = torch.empty_like(x)
-        _check(load().fem_csr_apply(self.h, _ptr(x), _ptr(y), _stream(stream)))
+        n = self.nrows
+        _check(load().fem_csr_apply(self.h, _ptr(x, n=n, name="x"), _ptr(y, n=n, name="y"), _stream(stream)))
         return y
 
     def export(self, rowptr, col, val, stream=None):
         """Copy rowptr (int64), col (int32), val (float64) into the given buffers."""
-        _check(load().fem_csr_export(self.h, _ptr(rowptr, "int64"), _ptr(col, "int32"), _ptr(val),
+        _check(load().fem_csr_export(self.h, _ptr(rowptr, "int64", self.nrows + 1, "rowptr"),
+                                     _ptr(col, "int32", self.nnz, "col"), _ptr(val, n=self.nnz, name="val"),
                                      _stream(stream)))
 
     def close(self):

@@ -80,3 +80,19 @@ def test_binding_has_no_cpu_fallback():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in src.replace("oracle/", "").lower() or fn == "inputs.py", fn
+
+
+def test_binding_checks_buffer_lengths():
+    """The ABI receives bare pointers: the binding rejects buffers of the wrong length (a short
+    y would be written past its end, a short x over-read)."""
+    import numpy as np
+    import pytest
+    a = np.zeros(4)
+    assert F._ptr(a, n=4) == a.ctypes.data
+    with pytest.raises(ValueError):
+        F._ptr(np.zeros(3), n=4, name="x")
+    with pytest.raises(ValueError):
+        F._ptr(np.zeros(5), n=4, name="x")
+    with pytest.raises(TypeError):
+        F._ptr(np.zeros(4, dtype=np.float32), n=4)
+    assert _status(F.load().fem_comm_create_loopback(0, None)) == "FEM_EINVAL"

@@ -271,6 +271,33 @@ def test_cg_elastic_parity(F, oracle, dims, iters):
     assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10 * max(1.0, np.abs(ref.x).max())
 
 
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_cg_r_norm_is_exit_residual(F, kind, variant):
+    """fem_cg_info.r_norm is the recurrence residual of the exit iterate: after a
+    fixed number of unconverged iterations it equals ||b - A x|| up to rounding (the recurrence
+    and the true residual agree long before convergence).  Single-reduction CG reports the
+    residual of the iterate its last update started from (include/fem.h), so one iteration more
+    gives the comparison point there."""
+    nx, ny, nz, h = 11, 10, 9, 0.1
+    g = I.rng(I.SEED_BASE + 31)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = I.interior_rhs(g, nx, ny, nz, I.ncomp(kind))
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 1)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    op.set_option("cg_variant", variant)
+    x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+    info = op.cg_solve(dev(b), x, tol=0.0, maxit=6)
+    if variant == 0:
+        assert abs(info["r_norm"] - info["true_r_norm"]) <= 1e-9 * info["true_r_norm"]
+    else:  # r_norm belongs to iterate 5: run 5 iterations and compare its true residual
+        x5 = torch.zeros_like(x)
+        i5 = op.cg_solve(dev(b), x5, tol=0.0, maxit=5)
+        assert abs(info["r_norm"] - i5["true_r_norm"]) <= 1e-9 * i5["true_r_norm"]
+    assert info["r_norm"] < info["r0_norm"]
+
+
 def test_cg_vector_host_pointers(F, oracle):
     nx, ny, nz, h = 10, 9, 8, 0.1
     g = I.rng(I.SEED_BASE + 2)
