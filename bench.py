@@ -268,6 +268,8 @@ def run_native(args, cfg):
         op.set_option("quadrature", 1)
     if args.cgcg:  # Chronopoulos-Gear single-reduction CG (NEXT #1)
         op.set_option("cg_variant", 1)
+    if args.dot != "fused":  # the dot ablation: separate dot kernels / atomic partials
+        op.set_option("dot_mode", {"separate": 1, "atomic": 2}[args.dot])
     if args.peer_halo and ws > 1 and not hexmesh:  # ghost planes over NVLink inside the apply (NEXT #3)
         op.set_option("peer_halo", 1)
     ndof_global = op.n_global * (ws if hexmesh else 1)
@@ -415,6 +417,7 @@ def run_native(args, cfg):
     extra["cg_iteration_gbs"] = cg_bytes / (ms / args.steps / 1e3) / 1e9
     extra["fused_cg"] = fused
     extra["cg_variant"] = "chronopoulos-gear" if cgcg else "hestenes-stiefel"
+    extra["dot_mode"] = "single reduction (CG-CG)" if cgcg else args.dot
     del xx, yy
 
     # ---- e2e: the public call a user makes, with pinned HOST buffers ----
@@ -656,6 +659,8 @@ def main():
                     help="N > 1: ghost planes read by the apply kernels from the neighbours' memory (CUDA IPC)")
     ap.add_argument("--cgcg", action="store_true",
                     help="Chronopoulos-Gear single-reduction CG (one allreduce of 2 values per iteration)")
+    ap.add_argument("--dot", default="fused", choices=["fused", "separate", "atomic"],
+                    help="how the fused CG forms p.Ap and r.r (option dot_mode; P:714-728 ablation)")
     ap.add_argument("--gll", action="store_true",
                     help="2x2x2 Gauss-Lobatto quadrature (the CEED BP5/BP6 operators) instead of Gauss")
     ap.add_argument("--pa", action="store_true",
@@ -673,6 +678,8 @@ def main():
         cfg["name"] += "_gll"
     if args.cgcg:
         cfg["name"] += "_cgcg"
+    if args.dot != "fused":
+        cfg["name"] += "_dot-" + args.dot
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -207,7 +207,13 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * checks det J > 0 at the nodes, FEM_EINVAL otherwise), "cg_variant" (0: the fused
  * Hestenes-Stiefel CG of Table 4, default; 1: Chronopoulos-Gear single-reduction CG -- r.r and
  * w.r come out of the apply together, one allreduce of two values per iteration instead of two;
- * TMA path only, reads back 0 elsewhere), "peer_halo" (1: collective over the slab ranks --
+ * TMA path only, reads back 0 elsewhere), "dot_mode" (how the fused Hestenes-Stiefel CG
+ * forms its two dots -- the dot-implementation ablation of P:714-728: 0, default, in the
+ * epilogue of the producing kernel (p.Ap in the apply, r.r in the update) by a block tree plus a
+ * last-block pass over the CTA partials in block order (deterministic); 1 by separate dot
+ * kernels after the apply and the update, re-reading p, q and r (+24 B/DOF, +2 launches per
+ * iteration); 2 in the epilogue with the CTA partials added by FP64 atomics (summation order
+ * varies from run to run); TMA path, cg_variant 0 only), "peer_halo" (1: collective over the slab ranks --
  * every rank sets it -- exchanging CUDA IPC handles of the CG vectors with the neighbours over
  * NCCL; the apply kernels then load the ghost node planes straight from the neighbours' memory
  * over NVLink inside their TMA pipeline and the NCCL halo step disappears; the two CG allreduces

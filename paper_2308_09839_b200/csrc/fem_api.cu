@@ -178,6 +178,7 @@ struct fem_op_s {
   int pa_quad = -1;  // rule the stored geometry was computed for
   int quad = 0;      // 0: 2x2x2 Gauss-Legendre, 1: 2x2x2 Gauss-Lobatto (BP5/BP6; reading R1)
   int cg_variant = 0;  // 0: fused Hestenes-Stiefel (Table 4), 1: Chronopoulos-Gear single reduction
+  int dot_mode = 0;    // fused Hestenes-Stiefel dots: 0 epilogue, 1 separate kernels, 2 atomics
   // peer halo: the neighbour ranks' padded vectors x, p, r, p2 (CUDA IPC or, for single-process
   // tests, the other operator's buffers) and tensor maps over their ghost-plane sources
   bool peer_on = false, peer_ipc = false;
@@ -1461,19 +1462,31 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
                  parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
                  op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr};
+  // the two dots per option "dot_mode" (Reduce::dot_mode; the paper's dot ablation)
+  Reduce rd = op->red;
+  rd.dot_mode = op->dot_mode;
   cudaError_t e;
   if (op->kind == FEM_ELASTICITY)
-    e = launch_elastic(op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc, op->red, s,
+    e = launch_elastic(op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc, rd, s,
                        m->sm_count);
   else
     e = launch_laplace(op->comps, op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc,
-                       op->red, s, m->sm_count);
+                       rd, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "fused apply launch: %s", cudaGetErrorString(e));
   if (timed) FEM_TRY(apply_event(op, 1, s));
+  const int64_t n = pl_count(op);
+  if (op->dot_mode == 1) {  // p.q by a separate kernel re-reading p and q
+    e = launch_cg_dot(pl_owned(op, pnew), pl_owned(op, op->q_pl), n, 0, op->sc, op->red, s, m->sm_count);
+    if (e != cudaSuccess) return fail(FEM_ECUDA, "dot launch: %s", cudaGetErrorString(e));
+  }
   FEM_TRY(allreduce1(op, &op->sc->pq, s));
   e = launch_cg_update_fused(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, pnew),
-                             pl_owned(op, op->q_pl), pl_count(op), op->sc, op->red, s, m->sm_count);
+                             pl_owned(op, op->q_pl), n, op->sc, rd, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
+  if (op->dot_mode == 1) {  // r.r by a separate kernel re-reading r
+    e = launch_cg_dot(pl_owned(op, op->r_pl), pl_owned(op, op->r_pl), n, 1, op->sc, op->red, s, m->sm_count);
+    if (e != cudaSuccess) return fail(FEM_ECUDA, "dot launch: %s", cudaGetErrorString(e));
+  }
   FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
   return FEM_OK;
 }
@@ -1559,7 +1572,8 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
 
 static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
   const int per_iter_launches =
-      op->tm_ok ? 2 : (op->mesh->hex ? 3 + ((op->bc && op->mesh->hx_nb) ? 1 : 0) : 3);
+      op->tm_ok ? ((op->cg_variant == 0 && op->dot_mode == 1) ? 4 : 2)
+                : (op->mesh->hex ? 3 + ((op->bc && op->mesh->hx_nb) ? 1 : 0) : 3);
   // loopback ranks rendezvous on the host inside every collective: not capturable, run eagerly
   const bool loop = op->mesh->comm && op->mesh->comm->loop && op->mesh->nranks > 1;
   if (op->time_apply && op->use_graph && !loop && iters > 0) {
@@ -1699,7 +1713,8 @@ int fem_cg_solve(fem_op_t op, const double* b, double* x, double tol, int32_t ma
     done_it += n;
     CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    if (op->sc_host->done) break;
+    const CgScalars& h = *op->sc_host;  // rr_new is rank-global here (after its allreduce)
+    if (h.done || h.rr_new == 0.0 || h.rr_new <= h.stop_rr) break;
   }
   fem_cg_info tmp;
   int st = cg_end_dev(op, info ? info : &tmp, s);
@@ -1762,6 +1777,11 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (op->cg_active) return fail(FEM_ESTATE, "cg_variant cannot change during a CG solve");
     op->cg_variant = (int)value;
     drop_graphs(op);
+  } else if (!std::strcmp(key, "dot_mode")) {
+    if (value < 0 || value > 2) return fail(FEM_EINVAL, "dot_mode must be 0 (fused epilogue), 1 (separate dot kernels) or 2 (atomic partials)");
+    if (op->cg_active) return fail(FEM_ESTATE, "dot_mode cannot change during a CG solve");
+    op->dot_mode = (int)value;
+    drop_graphs(op);
   } else if (!std::strcmp(key, "quadrature")) {
     if (value != 0 && value != 1) return fail(FEM_EINVAL, "quadrature must be 0 (Gauss) or 1 (Gauss-Lobatto)");
     if (value == 1 && op->mesh->hex) {  // the Lobatto points are the nodes: det J > 0 there too
@@ -1798,6 +1818,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "quadrature")) *value = op->quad;
   else if (!std::strcmp(key, "cg_variant")) *value = (op->tm_ok && op->cg_variant == 1) ? 1 : 0;
   else if (!std::strcmp(key, "peer_halo")) *value = op->peer_on ? 1 : 0;
+  else if (!std::strcmp(key, "dot_mode")) *value = op->dot_mode;
   else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }

@@ -75,6 +75,7 @@ struct CgScalars {
   double rr0;       // r0.r0
   double stop_rr;   // tol^2 * rr0
   double alpha;     // Chronopoulos-Gear CG: alpha of the last update
+  double rr_acc;    // dot_mode 2: atomic accumulator of the update's r.r
   int32_t done;     // 0 running, 1 converged, 2 breakdown, 3 maxit reached
   int32_t it;       // iterations completed
   int32_t maxit;
@@ -88,6 +89,12 @@ struct Reduce {
   double* partials;       // >= max CTAs of any reducing launch
   unsigned int* ticket;   // zero-initialised, reset by the last block
   int64_t capacity;
+  // how the fused Hestenes-Stiefel CG computes its two dots (option "dot_mode"; the paper's dot
+  // ablation): 0 in the producing kernel's epilogue (block tree + last-block pass over
+  // the CTA partials, deterministic); 1 none in the producing kernel -- separate dot kernels
+  // re-read the vectors; 2 in the epilogue, CTA partials added with FP64 atomics (run-order
+  // dependent).  Kernels other than the fused apply / update always use 0.
+  int dot_mode = 0;
 };
 
 constexpr int kMaxCtas = 1 << 16;
@@ -151,6 +158,7 @@ constexpr int kElTY = FEM_EL_TY;                                      // elastic
 #ifndef FEM_EL2_SELF
 #define FEM_EL2_SELF 1  // elastic2_kernel without producer warp: consumer warp 0 issues the TMA loads
 #endif
+constexpr int kEl2HW = 3;  // doubles per thread per y hand-off of elastic2_kernel
 constexpr int kElCY = FEM_EL_CY, kEl2TY = FEM_EL2_TY, kEl2S = FEM_EL2_S;
 constexpr bool kEl2Self = FEM_EL2_SELF != 0;
 constexpr int kElCellRows = kElCY == 2 ? 2 * kEl2TY : kElTY;  // cell rows per TMA tile (= u box rows - 1)
@@ -218,6 +226,10 @@ cudaError_t launch_cg_cgcg_update(double* x, double* r, double* p, double* s, co
                                   CgScalars* sc, Reduce red, cudaStream_t st, int sm_count);
 // loopback allreduce: out[i] = sum over ranks q = 0..P-1 (in order) of stage[q * stride + i]
 cudaError_t launch_loop_sum(const double* stage, int P, int stride, int count, double* out, cudaStream_t s);
+// dot_mode 1 of the fused CG: which = 0: sc->pq = a.b, then roll rr = rr_new, first = 0;
+// which = 1: sc->rr_new = a.b, it++, maxit -> done = 3 (the update kernel's bookkeeping)
+cudaError_t launch_cg_dot(const double* a, const double* b, int64_t n, int which, CgScalars* sc, Reduce red,
+                          cudaStream_t s, int sm_count);
 // deterministic dot -> *out (device)
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
                        cudaStream_t s, int sm_count);
@@ -300,6 +312,34 @@ __device__ __forceinline__ bool last_block_reduce(double partial, Reduce red, do
     *red.ticket = 0u;
   }
   return tid == 0;
+}
+
+// Epilogue of a CG apply (mode 1 / 2): p.Ap of this CTA's nodes -> sc->pq, per red.dot_mode.
+// roll (fused CG, mode 2): once every CTA has read rr / rr_new / first (i.e. in the last CTA),
+// advance the recurrence rr = rr_new, first = 0 -- dot_mode 1 leaves that to the dot kernel.
+__device__ __forceinline__ void cg_apply_epilogue(double pq, bool roll, CgScalars* sc, Reduce red, double* sh) {
+  if (red.dot_mode == 1) return;  // separate dot kernel (launch_cg_dot) after this kernel
+  const double bsum = block_sum(pq, sh);
+  if (red.dot_mode == 2) {
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    if (tid == 0) atomicAdd(&sc->pq, bsum);  // zeroed by the previous update's last CTA
+    if (!roll) return;
+    double unused;
+    if (last_block_reduce(0.0, red, sh, &unused)) {  // ticket only: the last CTA rolls
+      sc->rr = sc->rr_new;
+      sc->first = 0;
+      sc->rr_acc = 0.0;  // the update's atomic target
+    }
+    return;
+  }
+  double total;
+  if (last_block_reduce(bsum, red, sh, &total)) {
+    sc->pq = total;
+    if (roll) {  // every block has read rr / rr_new / first: roll the recurrence
+      sc->rr = sc->rr_new;
+      sc->first = 0;
+    }
+  }
 }
 
 // the same for two sums at once (partials of b at red.partials + red.capacity)

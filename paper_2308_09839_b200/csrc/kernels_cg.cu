@@ -48,11 +48,12 @@ __global__ void cg_finish_init_kernel(CgScalars* sc, double tol, int maxit) {
   sc->rr0 = rr;
   sc->stop_rr = tol * tol * rr;
   sc->pq = 0.0;
+  sc->rr_acc = 0.0;
   sc->it = 0;
   sc->maxit = maxit;
   sc->breakdown_iter = -1;
   sc->first = 1;
-  sc->done = (rr == 0.0) ? 1 : (maxit <= 0 ? 3 : 0);
+  sc->done = (rr == 0.0 || rr <= sc->stop_rr) ? 1 : (maxit <= 0 ? 3 : 0);
 }
 
 __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restrict__ x,
@@ -96,6 +97,13 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __
                                                                       Reduce red) {
   __shared__ double sh[32];
   if (sc->done) return;
+  // convergence of the current iterate: rr_new is the allreduced (rank-global) r.r of the
+  // previous update, so every rank decides alike (the apply before this kernel was wasted work)
+  const double rrc = sc->rr_new;
+  if (rrc == 0.0 || rrc <= sc->stop_rr) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->done = 1;
+    return;
+  }
   const double pq = sc->pq;
   if (!(pq > 0.0) || !isfinite(pq)) {  // breakdown: same decision in every block
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -144,16 +152,28 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __
     acc = fma(na.x, na.x, acc); acc = fma(na.y, na.y, acc);
   }
   if (((n - head) & 1) && gtid == stride - 1) one(n - 1);
+  if (red.dot_mode == 1) return;  // r.r and the bookkeeping: launch_cg_dot(which = 1)
   double bs = block_sum(acc, sh);
+  if (red.dot_mode == 2) {
+    if (threadIdx.x == 0) atomicAdd(&sc->rr_acc, bs);  // zeroed by the apply's last CTA
+    double unused;
+    if (last_block_reduce(0.0, red, sh, &unused)) {  // ticket only: the last CTA publishes
+      sc->rr_new = sc->rr_acc;
+      sc->pq = 0.0;  // the next apply's atomic target
+      const int it = sc->it + 1;
+      sc->it = it;
+      if (it >= sc->maxit) sc->done = 3;
+    }
+    return;
+  }
   double tot;
   if (last_block_reduce(bs, red, sh, &tot)) {
+    // tot is this rank's partial of r.r: the allreduce that follows makes rr_new global, so the
+    // convergence test runs at the start of the next fused apply (every rank, the same value)
     sc->rr_new = tot;
     const int it = sc->it + 1;
     sc->it = it;
-    if (tot == 0.0 || tot <= sc->stop_rr)
-      sc->done = 1;
-    else if (it >= sc->maxit)
-      sc->done = 3;
+    if (it >= sc->maxit) sc->done = 3;
   }
 }
 
@@ -267,6 +287,42 @@ __global__ void __launch_bounds__(kVecThreads) dot_kernel(const double* __restri
   if (last_block_reduce(bs, red, sh, &tot)) *out = tot;
 }
 
+// dot_mode 1 (separate dot kernels): 16-B loads like the update kernel, deterministic reduction
+__global__ void __launch_bounds__(kVecThreads) cg_dot_kernel(const double* __restrict__ a,
+                                                             const double* __restrict__ b, int64_t n,
+                                                             int which, CgScalars* sc, Reduce red) {
+  __shared__ double sh[32];
+  if (sc->done) return;
+  double acc = 0.0;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t head = (reinterpret_cast<uintptr_t>(a) & 15) ? 1 : 0;
+  if (head && gtid == 0 && n > 0) acc = a[0] * b[0];
+  const int64_t n2 = (n - head) / 2;
+  const double2* __restrict__ a2 = reinterpret_cast<const double2*>(a + head);
+  const double2* __restrict__ b2 = reinterpret_cast<const double2*>(b + head);
+  for (int64_t i = gtid; i < n2; i += stride) {
+    const double2 u = a2[i], v = b2[i];
+    acc = fma(u.x, v.x, acc);
+    acc = fma(u.y, v.y, acc);
+  }
+  if (((n - head) & 1) && gtid == stride - 1) acc = fma(a[n - 1], b[n - 1], acc);
+  const double bs = block_sum(acc, sh);
+  double tot;
+  if (last_block_reduce(bs, red, sh, &tot)) {
+    if (which == 0) {  // p.q; the apply has finished reading rr / rr_new / first
+      sc->pq = tot;
+      sc->rr = sc->rr_new;
+      sc->first = 0;
+    } else {  // r.r of the update (local partial: the allreduce follows)
+      sc->rr_new = tot;
+      const int it = sc->it + 1;
+      sc->it = it;
+      if (it >= sc->maxit) sc->done = 3;
+    }
+  }
+}
+
 __global__ void loop_sum_kernel(const double* __restrict__ stage, int P, int stride, int count,
                                 double* __restrict__ out) {
   const int i = threadIdx.x;
@@ -334,6 +390,14 @@ cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* 
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* out, Reduce red,
                        cudaStream_t s, int sm_count) {
   dot_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(a, b, n, out, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_dot(const double* a, const double* b, int64_t n, int which, CgScalars* sc, Reduce red,
+                          cudaStream_t s, int sm_count) {
+  Reduce r = red;
+  r.dot_mode = 0;
+  cg_dot_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(a, b, n, which, sc, r);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -285,15 +285,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
       sc->rr_new = tg;
     }
   } else if (mode >= 1) {
-    double bsum = block_sum(pq, red_sh);
-    double total;
-    if (last_block_reduce(bsum, red, red_sh, &total)) {
-      sc->pq = total;
-      if (mode == 2) {  // every block has read rr / rr_new / first: roll the recurrence
-        sc->rr = sc->rr_new;
-        sc->first = 0;
-      }
-    }
+    cg_apply_epilogue(pq, mode == 2, sc, red, red_sh);
   }
 }
 
@@ -343,6 +335,13 @@ __device__ __forceinline__ void elastic_layer(const Face* fb, const Face* ft, do
   }
 }
 
+// Depth of elastic2_kernel's y hand-off ring: 4 planes when it fits in shared memory beside the
+// plane ring (227 KB per CTA), else 2 (the 8-stage row-pair ring of fem_apply)
+template <int TY, size_t RING>
+constexpr int el2_handoff_depth() {
+  return RING + 4ull * TY * (32 * kEl2HW * sizeof(double) + 2 * sizeof(uint64_t)) + 1024 <= 232448 ? 4 : 2;
+}
+
 // corner values of a complete face F (4 modes x 3 comps): c00, c10, c01, c11 per component
 __device__ __forceinline__ void face_corners(const double* F, int c, double& c00, double& c10, double& c01,
                                              double& c11) {
@@ -373,19 +372,22 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   constexpr int NT = TX * (TY + (SELF ? 0 : 1));
   constexpr int ROWS = 2 * TY + 1;  // node rows j0-1 .. j0+2TY-1
   constexpr int COLS = TX + 1;      // node cols i0-1 .. i0+TX-1
-  constexpr int TPART = 4 * TY * TX * 3;
+  constexpr int HW = kEl2HW;        // doubles per thread and y hand-off (3 corner sums)
   using Ring = PlaneRing<TM, ROWS, COLS, 3, S, kElMatRows, TX, NU, PAIR>;
+  constexpr int HD = el2_handoff_depth<TY, Ring::BYTES + Ring::META>();  // y hand-off ring depth
+  constexpr int TPART = HD * TY * TX * HW;
   static_assert(kElMatRows >= 2 * TY, "material box covers the tile's cell rows");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red_sh[32];
   Ring ring;
-  double* tpart = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // [4][TY][TX][3]
-  uint64_t* tfull = reinterpret_cast<uint64_t*>(tpart + TPART);        // [4][TY]
-  uint64_t* tempty = tfull + 4 * TY;                                    // [4][TY]
-  ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + 4 * TY));
+  double* tpart = reinterpret_cast<double*>(smem_raw + Ring::BYTES);  // [HD][TY][TX][HW]
+  uint64_t* tfull = reinterpret_cast<uint64_t*>(tpart + TPART);        // [HD][TY]
+  uint64_t* tempty = tfull + HD * TY;                                   // [HD][TY]
+  ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + HD * TY));
   const uint32_t tfull_a = smem_u32(tfull), tempty_a = smem_u32(tempty);
 
   if (mode >= 1 && sc->done) return;
+  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
   const double beta = (mode == 2) ? (sc->first ? 0.0 : sc->rr_new / sc->rr) : 0.0;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(g.k1, kb + kchunk);
   const int64_t pfirst = kb - 1;
-  if (tid < 4 * TY) {
+  if (tid < HD * TY) {
     mbar_init(&tfull[tid], 1);
     mbar_init(&tempty[tid], 1);
   }
@@ -420,189 +422,188 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     const int64_t ci = i0 - 1 + tx, cj = j0 - 1 + 2 * ty;  // cell A = (ci, cj), cell B = (ci, cj+1)
     const double hs = g.h * (1.0 / 16.0);
     const int64_t nA = cj + 1, nB = cj + 2;  // node rows this thread outputs
-    const bool mc0 = bc && (ci == 0 || ci == g.nx), mc1 = bc && (ci + 1 == 0 || ci + 1 == g.nx);
-    const bool mr0 = bc && (cj == 0 || cj == g.ny), mr1 = bc && (cj + 1 == 0 || cj + 1 == g.ny);
-    const bool mr2 = bc && (cj + 2 == 0 || cj + 2 == g.ny);
     const bool colok = tx >= 1 && tx <= txa && ci <= g.nx;
     const bool ownA = colok && 2 * ty < tya && nA <= g.ny;
     const bool ownB = colok && 2 * ty + 1 < tya && nB <= g.ny;
-    const bool bnA_xy = bc && (ci == 0 || ci == g.nx || nA == 0 || nA == g.ny);
-    const bool bnB_xy = bc && (ci == 0 || ci == g.nx || nB == 0 || nB == g.ny);
     const bool own = ownA || ownB;  // (ownB implies nA is a mesh row too)
     double* yp = yo.y + (kb - g.k0) * yo.ppitch + (own ? nA * yo.rpitch + ci * 3 : 0);
     const int64_t xoff0 = (kb - g.k0) * x.ppitch + (own ? nA * x.rpitch + ci * 3 : 0);
     double* pnb = (mode == 2) ? pnew + xoff0 : nullptr;
-    const int qface0 = bc ? (int)(0 - kb) : -1000000;
-    const int qface1 = bc ? (int)(g.nz - kb) : -1000000;
-    double* const tw0 = tpart + (ty * TX + tx) * 3;
-    const double* const tr0 = tpart + ((ty + 1) * TX + tx) * 3;
+    double* const tw0 = tpart + (ty * TX + tx) * HW;
+    const double* const tr0 = tpart + ((ty + 1) * TX + tx) * HW;
     const uint32_t tfw0 = tfull_a + 8u * ty, tew0 = tempty_a + 8u * ty;
     const uint32_t tfr0 = tfull_a + 8u * (ty + 1), ter0 = tempty_a + 8u * (ty + 1);
+    // Dirichlet box: only CTAs whose tile or z-chunk touches a box face need the mask P
+    // and the identity rows; all others run the same march without that logic (CTA-uniform).
+    // (fused CG, mode 2: one path -- the split costs that kernel its register headroom, measured
+    // 1.32 -> 1.52 ms with spills, and gains nothing there)
+    const bool edge = MODE == 2 || (bc && (i0 <= 1 || i0 + TX - 1 >= g.nx || j0 <= 1 ||
+                                           j0 - 1 + 2 * TY >= g.ny || pfirst <= 0 || ke >= g.nz));
 
-    // loop state in two register sets (ping-pong: the z-march is unrolled by two, so nothing is
-    // moved at the back edge): faces of cells A, B at a node plane, carried top faces, the node
-    // values of rows nA, nB, and the material of the cell layer above the plane (x h/16)
-    Face fA[2][3], fB[2][3];
-    double cA[2][12], cB[2][12];
-    double xA[2][3], xB[2][3];
-    double LA[2], MA[2], LB[2], MB[2];
+    auto march = [&](auto mk) {
+      constexpr bool MK = decltype(mk)::value;
+      const bool mc0 = MK && bc && (ci == 0 || ci == g.nx), mc1 = MK && bc && (ci + 1 == 0 || ci + 1 == g.nx);
+      const bool mr0 = MK && bc && (cj == 0 || cj == g.ny), mr1 = MK && bc && (cj + 1 == 0 || cj + 1 == g.ny);
+      const bool mr2 = MK && bc && (cj + 2 == 0 || cj + 2 == g.ny);
+      const bool bnA_xy = MK && bc && (ci == 0 || ci == g.nx || nA == 0 || nA == g.ny);
+      const bool bnB_xy = MK && bc && (ci == 0 || ci == g.nx || nB == 0 || nB == g.ny);
+      const int qface0 = (MK && bc) ? (int)(0 - kb) : -1000000;
+      const int qface1 = (MK && bc) ? (int)(g.nz - kb) : -1000000;
+
+      // loop state in two register sets (ping-pong: the z-march is unrolled by two, so nothing is
+      // moved at the back edge): faces of cells A, B at a node plane, carried top faces, the node
+      // values of rows nA, nB, and the material of the cell layer above the plane (x h/16)
+      Face fA[2][3], fB[2][3];
+      double cA[2][12], cB[2][12];
+      double xA[2][3], xB[2][3];
+      double LA[2], MA[2], LB[2], MB[2];
 #pragma unroll
-    for (int t = 0; t < 12; ++t) { cA[0][t] = 0.0; cB[0][t] = 0.0; }
+      for (int t = 0; t < 12; ++t) { cA[0][t] = 0.0; cB[0][t] = 0.0; }
 
-    auto load_plane = [&](int t, Face* fA, Face* fB, double* xA, double* xB, double& LA, double& MA,
-                          double& LB, double& MB) {
-      const int slot = t & (S - 1);
-      ring.wait(slot, (uint32_t)((t / S) & 1));
-      if (PAIR) ring.set_pair_plane(pfirst + t);
-      const double2 lmA = ring.mat(slot, 2 * ty, tx), lmB = ring.mat(slot, 2 * ty + 1, tx);
-      const double* r0 = ring.row_ptr(slot, 2 * ty) + tx * 3;
-      const double* r1 = ring.row_ptr(slot, 2 * ty + 1) + tx * 3;
-      const double* r2 = ring.row_ptr(slot, 2 * ty + 2) + tx * 3;
-      const int64_t pl = pfirst + t;
-      const bool pface = TM && bc && (pl == 0 || pl == g.nz);
-      const bool m00 = pface || mc0 || mr0, m10 = pface || mc1 || mr0;
-      const bool m01 = pface || mc0 || mr1, m11 = pface || mc1 || mr1;
-      const bool m02 = pface || mc0 || mr2, m12 = pface || mc1 || mr2;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double a00 = r0[c], a10 = r0[3 + c], a01 = r1[c], a11 = r1[3 + c], a02 = r2[c], a12 = r2[3 + c];
-        if (mode == 2) {  // p = r + beta p_old (second box)
-          const double* q0 = r0 + Ring::UDBL;
-          const double* q1 = r1 + Ring::UDBL;
-          const double* q2 = r2 + Ring::UDBL;
-          a00 = fma(beta, q0[c], a00);
-          a10 = fma(beta, q0[3 + c], a10);
-          a01 = fma(beta, q1[c], a01);
-          a11 = fma(beta, q1[3 + c], a11);
-          a02 = fma(beta, q2[c], a02);
-          a12 = fma(beta, q2[3 + c], a12);
-        }
-        xA[c] = a01;  // node (ci, nA), unmasked
-        xB[c] = a02;  // node (ci, nB)
-        if (TM && bc && (m00 || m10 || m01 || m11 || m02 || m12)) {
-          a00 = m00 ? 0.0 : a00;
-          a10 = m10 ? 0.0 : a10;
-          a01 = m01 ? 0.0 : a01;
-          a11 = m11 ? 0.0 : a11;
-          a02 = m02 ? 0.0 : a02;
-          a12 = m12 ? 0.0 : a12;
-        }
-        // x butterflies per node row (the middle row is shared by the two faces)
-        const double s0 = a00 + a10, d0 = a10 - a00, s1 = a01 + a11, d1 = a11 - a01;
-        const double s2 = a02 + a12, d2 = a12 - a02;
-        fA[c] = Face{s0 + s1, s1 - s0, d0 + d1, d1 - d0};
-        fB[c] = Face{s1 + s2, s2 - s1, d1 + d2, d2 - d1};
-      }
-      ring.release(slot, tx);
-      if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
-        ring.wait_released(t);
-        if (tx == 0)
-          ring.issue_tm(t + S, pfirst + t + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0, &peer);
-      }
-      LA = lmA.x * hs;
-      MA = lmA.y * hs;
-      LB = lmB.x * hs;
-      MB = lmB.y * hs;
-    };
-    load_plane(0, fA[0], fB[0], xA[0], xB[0], LA[0], MA[0], LB[0], MB[0]);
-
-    // one step of the z-march: plane t arrives in set V; the cell layer between planes t-1 (set
-    // U) and t is applied; node plane t-2 is completed and written
-    auto step = [&](int t, auto uc) {
-      constexpr int U = decltype(uc)::value, V = 1 - U;
-      load_plane(t, fA[V], fB[V], xA[V], xB[V], LA[V], MA[V], LB[V], MB[V]);
-      // cell A's layer and corners first, then cell B's (A's face array is dead before B's is
-      // formed); per-node sums in the fixed order ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j))
-      double BA[3], TA[3], vA[3], TB[3];
-      {
-        double FA[12];
-        elastic_layer<GLL>(fA[U], fA[V], LA[U], MA[U], cA[U], cA[V], FA);
+      auto load_plane = [&](int t, Face* fA, Face* fB, double* xA, double* xB, double& LA, double& MA,
+                            double& LB, double& MB) {
+        const int slot = t & (S - 1);
+        ring.wait(slot, (uint32_t)((t / S) & 1));
+        if (PAIR) ring.set_pair_plane(pfirst + t);
+        const double2 lmA = ring.mat(slot, 2 * ty, tx), lmB = ring.mat(slot, 2 * ty + 1, tx);
+        const double* r0 = ring.row_ptr(slot, 2 * ty) + tx * 3;
+        const double* r1 = ring.row_ptr(slot, 2 * ty + 1) + tx * 3;
+        const double* r2 = ring.row_ptr(slot, 2 * ty + 2) + tx * 3;
+        const int64_t pl = pfirst + t;
+        const bool pface = MK && bc && (pl == 0 || pl == g.nz);
+        const bool m00 = pface || mc0 || mr0, m10 = pface || mc1 || mr0;
+        const bool m01 = pface || mc0 || mr1, m11 = pface || mc1 || mr1;
+        const bool m02 = pface || mc0 || mr2, m12 = pface || mc1 || mr2;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          double a00, a10, a01, a11;
-          face_corners(FA, c, a00, a10, a01, a11);
-          const double a10l = __shfl_up_sync(0xffffffffu, a10, 1);  // from cell i-1
-          const double a11l = __shfl_up_sync(0xffffffffu, a11, 1);
-          BA[c] = a10l + a00;  // node row cj (cells row cj): to warp ty-1
-          TA[c] = a11l + a01;  // node row nA, cells row cj
+          double a00 = r0[c], a10 = r0[3 + c], a01 = r1[c], a11 = r1[3 + c], a02 = r2[c], a12 = r2[3 + c];
+          if (mode == 2) {  // p = r + beta p_old (second box)
+            const double* q0 = r0 + Ring::UDBL;
+            const double* q1 = r1 + Ring::UDBL;
+            const double* q2 = r2 + Ring::UDBL;
+            a00 = fma(beta, q0[c], a00);
+            a10 = fma(beta, q0[3 + c], a10);
+            a01 = fma(beta, q1[c], a01);
+            a11 = fma(beta, q1[3 + c], a11);
+            a02 = fma(beta, q2[c], a02);
+            a12 = fma(beta, q2[3 + c], a12);
+          }
+          xA[c] = a01;  // node (ci, nA), unmasked
+          xB[c] = a02;  // node (ci, nB)
+          if (MK && bc && (m00 || m10 || m01 || m11 || m02 || m12)) {
+            a00 = m00 ? 0.0 : a00;
+            a10 = m10 ? 0.0 : a10;
+            a01 = m01 ? 0.0 : a01;
+            a11 = m11 ? 0.0 : a11;
+            a02 = m02 ? 0.0 : a02;
+            a12 = m12 ? 0.0 : a12;
+          }
+          // x butterflies per node row (the middle row is shared by the two faces)
+          const double s0 = a00 + a10, d0 = a10 - a00, s1 = a01 + a11, d1 = a11 - a01;
+          const double s2 = a02 + a12, d2 = a12 - a02;
+          fA[c] = Face{s0 + s1, s1 - s0, d0 + d1, d1 - d0};
+          fB[c] = Face{s1 + s2, s2 - s1, d1 + d2, d2 - d1};
         }
-      }
-      {
-        double FB[12];
-        elastic_layer<GLL>(fB[U], fB[V], LB[U], MB[U], cB[U], cB[V], FB);
+        ring.release(slot, tx);
+        if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
+          ring.wait_released(t);
+          if (tx == 0)
+            ring.issue_tm(t + S, pfirst + t + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0, &peer);
+        }
+        LA = lmA.x * hs;
+        MA = lmA.y * hs;
+        LB = lmB.x * hs;
+        MB = lmB.y * hs;
+      };
+      load_plane(0, fA[0], fB[0], xA[0], xB[0], LA[0], MA[0], LB[0], MB[0]);
+
+      // node output (identity rows on the Dirichlet box) + the fused CG epilogue terms
+      auto put = [&](double* yq, double* pq_new, const double* v, const double* xs, bool bnode) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          double b00, b10, b01, b11;
-          face_corners(FB, c, b00, b10, b01, b11);
-          const double b10l = __shfl_up_sync(0xffffffffu, b10, 1);
-          const double b11l = __shfl_up_sync(0xffffffffu, b11, 1);
-          vA[c] = TA[c] + (b10l + b00);  // node row nA: cells row cj, then row cj+1
-          TB[c] = b11l + b01;            // node row nB, cells row cj+1
+          double vv = v[c];
+          const double xv = xs[c];
+          if (MK && bnode) vv = xv;
+          yq[c] = vv;
+          if (mode == 2) pq_new[c] = xv;
+          if (mode >= 1) pq = fma(vv, xv, pq);
+          if (mode == 3) rr2 = fma(xv, xv, rr2);
         }
-      }
-      const double* xs_A = xA[U];  // node values at plane t-1 (= the output plane)
-      const double* xs_B = xB[U];
-      if (t >= 2) {  // node plane q = kb + t - 2 is complete
-        const int qo = t - 2;
-        const int b = qo & 3;
-        const uint32_t n = (uint32_t)(qo >> 2);
-        if (ty >= 1) {
-          if (n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
-          double* dst = tw0 + b * (TY * TX * 3);
-          dst[0] = BA[0]; dst[1] = BA[1]; dst[2] = BA[2];
-          __syncwarp();
-          if (tx == 0) mbar_arrive_a(tfw0 + 8u * TY * b);
-        }
-        const bool qf = qo == qface0 || qo == qface1;
-        if (ownA) {
-          const bool bnode = bnA_xy || qf;
+      };
+
+      // one step of the z-march: plane t arrives in set V; the cell layer between planes t-1 (set
+      // U) and t is applied; node plane t-1 of the ring (global kb + t - 2) is completed and written
+      auto step = [&](int t, auto uc) {
+        constexpr int U = decltype(uc)::value, V = 1 - U;
+        load_plane(t, fA[V], fB[V], xA[V], xB[V], LA[V], MA[V], LB[V], MB[V]);
+        const double* xs_A = xA[U];  // node values at plane t-1 (= the output plane)
+        const double* xs_B = xB[U];
+        // per-node order ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j)), independent of tiles and slabs
+        double BA[3], TA[3], vA[3], TB[3];
+        {
+          double FA[12];
+          elastic_layer<GLL>(fA[U], fA[V], LA[U], MA[U], cA[U], cA[V], FA);
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            double vv = vA[c], xv = xs_A[c];
-            if (bnode) {
-              vv = xv;
-            }
-            yp[c] = vv;
-            if (mode == 2) pnb[c] = xv;
-            if (mode >= 1) pq = fma(vv, xv, pq);
-            if (mode == 3) rr2 = fma(xv, xv, rr2);
+            double a00, a10, a01, a11;
+            face_corners(FA, c, a00, a10, a01, a11);
+            const double a10l = __shfl_up_sync(0xffffffffu, a10, 1);  // from cell i-1
+            const double a11l = __shfl_up_sync(0xffffffffu, a11, 1);
+            BA[c] = a10l + a00;  // node row cj (cells row cj): to warp ty-1
+            TA[c] = a11l + a01;  // node row nA, cells row cj
           }
         }
-        if (ty < TY - 1) {
-          mbar_wait_a(tfr0 + 8u * TY * b, n & 1);
-          const double* src = tr0 + b * (TY * TX * 3);
-          double v[3];
+        {
+          double FB[12];
+          elastic_layer<GLL>(fB[U], fB[V], LB[U], MB[U], cB[U], cB[V], FB);
 #pragma unroll
-          for (int c = 0; c < 3; ++c) v[c] = TB[c] + src[c];
-          __syncwarp();
-          if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
-          if (ownB) {
-            const bool bnode = bnB_xy || qf;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              double vv = v[c], xv = xs_B[c];
-              if (bnode) {
-                vv = xv;
-              }
-              yp[yo.rpitch + c] = vv;
-              if (mode == 2) pnb[x.rpitch + c] = xv;
-              if (mode >= 1) pq = fma(vv, xv, pq);
-              if (mode == 3) rr2 = fma(xv, xv, rr2);
-            }
+          for (int c = 0; c < 3; ++c) {
+            double b00, b10, b01, b11;
+            face_corners(FB, c, b00, b10, b01, b11);
+            const double b10l = __shfl_up_sync(0xffffffffu, b10, 1);
+            const double b11l = __shfl_up_sync(0xffffffffu, b11, 1);
+            vA[c] = TA[c] + (b10l + b00);  // node row nA: cells row cj, then row cj+1
+            TB[c] = b11l + b01;            // node row nB, cells row cj+1
           }
         }
-        if (mode == 2) pnb += x.ppitch;
-        yp += yo.ppitch;
+        if (t >= 2) {  // node plane q = kb + t - 2 is complete
+          const int qo = t - 2, b = qo & (HD - 1);
+          const uint32_t n = (uint32_t)qo / (uint32_t)HD;
+          if (ty >= 1) {
+            if (n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
+            double* dst = tw0 + b * (TY * TX * HW);
+            dst[0] = BA[0]; dst[1] = BA[1]; dst[2] = BA[2];
+            __syncwarp();
+            if (tx == 0) mbar_arrive_a(tfw0 + 8u * TY * b);
+          }
+          const bool qf = MK && (qo == qface0 || qo == qface1);
+          if (ownA) put(yp, pnb, vA, xs_A, bnA_xy || qf);
+          if (ty < TY - 1) {
+            mbar_wait_a(tfr0 + 8u * TY * b, n & 1);
+            const double* src = tr0 + b * (TY * TX * HW);
+            double v[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[c] = TB[c] + src[c];
+            __syncwarp();
+            if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
+            if (ownB) put(yp + yo.rpitch, pnb + x.rpitch, v, xs_B, bnB_xy || qf);
+          }
+          if (mode == 2) pnb += x.ppitch;
+          yp += yo.ppitch;
+        }
+      };
+      using I0 = std::integral_constant<int, 0>;
+      using I1 = std::integral_constant<int, 1>;
+#pragma unroll 1
+      for (int t = 1; t < nplane; t += 2) {
+        step(t, I0{});
+        if (t + 1 >= nplane) break;
+        step(t + 1, I1{});
       }
     };
-    using I0 = std::integral_constant<int, 0>;
-    using I1 = std::integral_constant<int, 1>;
-#pragma unroll 1
-    for (int t = 1; t < nplane; t += 2) {
-      step(t, I0{});
-      if (t + 1 >= nplane) break;
-      step(t + 1, I1{});
-    }
+    if constexpr (MODE == 2) march(std::true_type{});
+    else if (edge) march(std::true_type{});
+    else march(std::false_type{});
   }
   if (mode == 3) {
     const double bd = block_sum(pq, red_sh);
@@ -613,15 +614,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
       sc->rr_new = tg;
     }
   } else if (mode >= 1) {
-    double bsum = block_sum(pq, red_sh);
-    double total;
-    if (last_block_reduce(bsum, red, red_sh, &total)) {
-      sc->pq = total;
-      if (mode == 2) {
-        sc->rr = sc->rr_new;
-        sc->first = 0;
-      }
-    }
+    cg_apply_epilogue(pq, mode == 2, sc, red, red_sh);
   }
 }
 
@@ -631,8 +624,10 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   constexpr int TX = 32;
   using Ring1 = PlaneRing<TM, 2 * TY + 1, TX + 1, 3, S, kElMatRows, TX, 1, PAIR>;
   using Ring2 = PlaneRing<TM, 2 * TY + 1, TX + 1, 3, S, kElMatRows, TX, (TM ? 2 : 1)>;
-  const size_t ring_bytes = mode == 2 ? Ring2::BYTES + Ring2::META : Ring1::BYTES + Ring1::META;
-  const size_t smem = ring_bytes + 4 * TY * TX * 3 * sizeof(double) + 8 * TY * sizeof(uint64_t);
+  constexpr int HD1 = el2_handoff_depth<TY, Ring1::BYTES + Ring1::META>();
+  constexpr int HD2 = el2_handoff_depth<TY, Ring2::BYTES + Ring2::META>();
+  const size_t smem = mode == 2 ? Ring2::BYTES + Ring2::META + (size_t)HD2 * TY * (TX * kEl2HW * sizeof(double) + 2 * sizeof(uint64_t))
+                                : Ring1::BYTES + Ring1::META + (size_t)HD1 * TY * (TX * kEl2HW * sizeof(double) + 2 * sizeof(uint64_t));
   const bool gll = maps.quad == 1;
   if (mode == 3 && !TM) return cudaErrorInvalidValue;
   auto pick = [&](auto gl) {

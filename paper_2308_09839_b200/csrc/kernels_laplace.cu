@@ -248,15 +248,7 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
       sc->rr_new = tg;
     }
   } else if (mode >= 1) {
-    double bsum = block_sum(pq, red_sh);
-    double total;
-    if (last_block_reduce(bsum, red, red_sh, &total)) {
-      sc->pq = total;
-      if (mode == 2) {  // every block has read rr / rr_new / first: roll the recurrence
-        sc->rr = sc->rr_new;
-        sc->first = 0;
-      }
-    }
+    cg_apply_epilogue(pq, mode == 2, sc, red, red_sh);
   }
 }
 

@@ -298,6 +298,36 @@ def test_cg_r_norm_is_exit_residual(F, kind, variant):
     assert info["r_norm"] < info["r0_norm"]
 
 
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("dot_mode", [1, 2])
+def test_cg_dot_modes(F, oracle, kind, dot_mode):
+    """The dot ablation (option dot_mode): separate dot kernels (1) and atomic CTA
+    partials (2) give the fused CG of dot_mode 0 up to summation order: 3 iterations within
+    1e-12, the converged solution within 1e-10 of the oracle's CG."""
+    nx, ny, nz, h = 13, 11, 10, 1.0 / 13
+    g = I.rng(I.SEED_BASE + 41)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = I.interior_rhs(g, nx, ny, nz, I.ncomp(kind))
+    xs = {}
+    for dm in (0, dot_mode):
+        op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 1)
+        if kind == "elastic":
+            op.set_material(dev(lam), dev(mu))
+        op.set_option("dot_mode", dm)
+        assert op.get_option("dot_mode") == dm
+        x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+        info = op.cg_solve(dev(b), x, tol=0.0, maxit=3)
+        assert info["iterations"] == 3
+        xs[dm] = x.cpu().numpy()
+        xc = torch.zeros_like(x)
+        info = op.cg_solve(dev(b), xc, tol=1e-13, maxit=2000)
+        assert info["converged"]
+        ref = oracle.cg(kind, 1, nx, ny, nz, h, b, tol=1e-13, maxit=2000, lam=lam, mu=mu)
+        assert abs(info["iterations"] - ref.iterations) <= 3
+        assert np.abs(xc.cpu().numpy() - ref.x).max() <= 1e-10 * max(1.0, np.abs(ref.x).max())
+    assert np.abs(xs[dot_mode] - xs[0]).max() <= 1e-12 * np.abs(xs[0]).max()
+
+
 def test_cg_vector_host_pointers(F, oracle):
     nx, ny, nz, h = 10, 9, 8, 0.1
     g = I.rng(I.SEED_BASE + 2)

@@ -24,23 +24,27 @@ def main():
             m = re.match(r"\s+/\*([0-9a-f]{4,5})\*/\s+(.*?);", line)
             if m:
                 ins.append((int(m.group(1), 16), m.group(2)))
-        best = None
+        loops = []
         for a, s in ins:
             m = re.search(r"BRA(?:\.\w+)*\s+(?:!?U?P\d, )?0x([0-9a-f]+)", s)
             if m:
                 t = int(m.group(1), 16)
-                if t < a and (best is None or a - t > best[1] - best[0]):
-                    best = (t, a)
-        c = collections.Counter()
-        if best:
+                if t < a:
+                    loops.append((t, a))
+        # outermost backward branches spanning >= 200 instructions (the z-march bodies)
+        loops = [l for l in loops if (l[1] - l[0]) // 16 >= 200]
+        loops = [l for l in loops if not any(o != l and o[0] <= l[0] and l[1] <= o[1] for o in loops)]
+        print(f"{name[:90]}\n  total {len(ins)}")
+        for lo, hi in sorted(loops):
+            c = collections.Counter()
             for a, s in ins:
-                if best[0] <= a <= best[1]:
+                if lo <= a <= hi:
                     w = s.split()
                     op = w[1] if w[0].startswith("@") else w[0]
                     c[op.split(".")[0]] += 1
-        fp = c["DADD"] + c["DFMA"] + c["DMUL"]
-        print(f"{name[:90]}\n  total {len(ins)}  loop {sum(c.values())}  fp64 {fp}  "
-              + " ".join(f"{k}={v}" for k, v in c.most_common(14)))
+            fp = c["DADD"] + c["DFMA"] + c["DMUL"]
+            print(f"  loop [{lo:#x},{hi:#x}] {sum(c.values())}  fp64 {fp}  "
+                  + " ".join(f"{k}={v}" for k, v in c.most_common(16)))
 
 
 if __name__ == "__main__":
