@@ -213,7 +213,10 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * last-block pass over the CTA partials in block order (deterministic); 1 by separate dot
  * kernels after the apply and the update, re-reading p, q and r (+24 B/DOF, +2 launches per
  * iteration); 2 in the epilogue with the CTA partials added by FP64 atomics (summation order
- * varies from run to run); TMA path, cg_variant 0 only), "peer_halo" (1: collective over the slab ranks --
+ * varies from run to run); TMA path, cg_variant 0 only), "halo_overlap" (1, default: with an
+ * exchange step -- nranks > 1 without peer_halo -- the halo runs on a library stream while the
+ * interior node planes are applied, then the two boundary planes; 0: halo, then one apply),
+ * "peer_halo" (1: collective over the slab ranks --
  * every rank sets it -- exchanging CUDA IPC handles of the CG vectors with the neighbours over
  * NCCL; the apply kernels then load the ghost node planes straight from the neighbours' memory
  * over NVLink inside their TMA pipeline and the NCCL halo step disappears; the two CG allreduces

@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -190,6 +191,10 @@ struct fem_op_s {
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
   bool ev_capture = false;   // events are being captured as graph nodes
+  // halo overlap (apply_split): comm stream + fork / join events; option "halo_overlap"
+  int overlap = 1;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   struct MapEnt {
     const void* p = nullptr;
     unsigned long long id = 0;
@@ -590,6 +595,66 @@ static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* u
   return FEM_OK;
 }
 
+static int launch_maps(fem_op_s* op, const Grid& g, PlaneSrc x, OutVec y, const ApplyMaps& maps, int mode,
+                       Reduce red, cudaStream_t s) {
+  fem_mesh_s* m = op->mesh;
+  const cudaError_t e = op->kind == FEM_ELASTICITY
+                            ? launch_elastic(op->bc, g, x, y, maps, mode, op->sc, red, s, m->sm_count)
+                            : launch_laplace(op->comps, op->bc, g, x, y, maps, mode, op->sc, red, s, m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "apply launch failed: %s", cudaGetErrorString(e));
+  return FEM_OK;
+}
+
+static int ensure_comm_stream(fem_op_s* op) {
+  if (op->cstream) return FEM_OK;
+  CUDA_TRY(cudaStreamCreateWithFlags(&op->cstream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming));
+  return FEM_OK;
+}
+
+// Apply with an exchange step (NCCL or loopback halo, nranks > 1): the halo runs
+// on the operator's comm stream while the interior output planes [k0+1, k1-1) -- which read
+// owned planes only -- run on the caller's stream; after the join one launch covers the two
+// boundary planes k0 and k1-1 (two one-plane z-chunks, kchunk_force).  The dots of the two
+// launches add up (Reduce::acc); the fused-CG roll happens in the second.  Per node the sums
+// are those of a single launch, so the result stays bitwise slab invariant.  `halo(stream)`
+// posts the exchange; src / out / maps describe the whole owned range.
+static int apply_split(fem_op_s* op, cudaStream_t s, PlaneSrc src, OutVec out, ApplyMaps maps, int mode,
+                       Reduce red, const std::function<int(cudaStream_t)>& halo) {
+  const Grid& g = op->mesh->g;
+  const int64_t nl = g.k1 - g.k0;
+  if (!op->overlap || nl < 3) {
+    FEM_TRY(halo(s));
+    return launch_maps(op, g, src, out, maps, mode, red, s);
+  }
+  FEM_TRY(ensure_comm_stream(op));
+  CUDA_TRY(cudaEventRecord(op->ev_fork, s));
+  CUDA_TRY(cudaStreamWaitEvent(op->cstream, op->ev_fork, 0));
+  FEM_TRY(halo(op->cstream));
+  CUDA_TRY(cudaEventRecord(op->ev_join, op->cstream));
+  Grid gi = g;
+  gi.k0 = g.k0 + 1;
+  gi.k1 = g.k1 - 1;
+  const PlaneSrc si{src.main + src.ppitch, src.main, src.main + (nl - 1) * src.ppitch, src.rpitch, src.ppitch};
+  const OutVec oi{out.y + out.ppitch, out.rpitch, out.ppitch};
+  ApplyMaps mi = maps;
+  if (mi.pold) mi.pold += src.ppitch;  // (pold / pnew share the input's layout)
+  if (mi.pnew) mi.pnew += src.ppitch;
+  Reduce ri = red;
+  ri.acc = 0;
+  ri.roll = 0;
+  FEM_TRY(launch_maps(op, gi, si, oi, mi, mode, ri, s));
+  CUDA_TRY(cudaStreamWaitEvent(s, op->ev_join, 0));
+  ApplyMaps mb = maps;
+  mb.kchunk_force = nl - 1;
+  mb.zc_force = 2;
+  mb.kspan = 1;
+  Reduce rb = red;
+  rb.acc = 1;
+  return launch_maps(op, g, src, out, mb, mode, rb, s);
+}
+
 static PlaneSrc dense_src(fem_op_s* op, const double* x, const double* lo, const double* hi) {
   const Grid& g = op->mesh->g;
   return PlaneSrc{x, lo, hi, (g.nx + 1) * op->comps, g.plane * op->comps};
@@ -692,10 +757,13 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
     }
   }
   op->last_path = 0;
-  FEM_TRY(halo(op, x, op->ghost_lo, op->ghost_hi, s));
   PlaneSrc src = dense_src(op, x, op->mesh->rank > 0 ? op->ghost_lo : nullptr,
                            op->mesh->rank < op->mesh->nranks - 1 ? op->ghost_hi : nullptr);
-  return launch_apply(op, src, dense_out(op, y), nullptr, 0, s);
+  if (m->nranks == 1) return launch_apply(op, src, dense_out(op, y), nullptr, 0, s);
+  ApplyMaps maps{nullptr, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr,
+                 op->tm_interior ? 1 : 0, op->quad, nullptr, nullptr};
+  return apply_split(op, s, src, dense_out(op, y), maps, 0, op->red,
+                     [&](cudaStream_t hs) { return halo(op, x, op->ghost_lo, op->ghost_hi, hs); });
 }
 
 // q_pl = A_c v for a padded CG vector v (x_pl or p_pl): halo into its ghost planes, TMA path
@@ -703,9 +771,12 @@ static int apply_pl(fem_op_s* op, double* v, const CUtensorMap* map, int mode, c
   fem_mesh_s* m = op->mesh;
   if (m->hex) return apply_hex(op, pl_owned(op, v), pl_owned(op, op->q_pl), mode, s);
   if (m->nranks > 1 && !(op->peer_on && op->tm_ok)) {
-    double* own = pl_owned(op, v);
-    FEM_TRY(halo_pitch(op, own, v + op->pl_lead, v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp,
-                       op->pl_pp, s));
+    ApplyMaps maps{op->tm_ok ? map : nullptr, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
+                   nullptr, nullptr, nullptr, op->tm_interior ? 1 : 0, op->quad, nullptr, nullptr};
+    return apply_split(op, s, pl_src(op, v), pl_out(op, op->q_pl), maps, mode, op->red, [&](cudaStream_t hs) {
+      return halo_pitch(op, pl_owned(op, v), v + op->pl_lead, v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp,
+                        op->pl_pp, hs);
+    });
   }
   return launch_apply(op, pl_src(op, v), pl_out(op, op->q_pl), op->tm_ok ? map : nullptr, mode, s, v);
 }
@@ -987,6 +1058,9 @@ static void op_free(fem_op_s* op) {
   if (op->graph1) cudaGraphExecDestroy(op->graph1);
   if (op->graphN) cudaGraphExecDestroy(op->graphN);
   for (auto e : op->ev) cudaEventDestroy(e);
+  if (op->cstream) cudaStreamDestroy(op->cstream);
+  if (op->ev_fork) cudaEventDestroy(op->ev_fork);
+  if (op->ev_join) cudaEventDestroy(op->ev_join);
   if (op->peer_ipc)
     for (int v = 0; v < 4; ++v) {
       if (op->nb_lo[v]) cudaIpcCloseMemHandle(op->nb_lo[v]);
@@ -1453,11 +1527,6 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   double* pnew = parity ? op->p_pl : op->p2_pl;
   static thread_local PeerMaps pm;
   const bool peer = fill_peer(op, op->r_pl, pold, &pm);
-  if (m->nranks > 1 && !peer) {
-    for (double* v : {op->r_pl, pold})
-      FEM_TRY(halo_pitch(op, pl_owned(op, v), v + op->pl_lead,
-                         v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp, op->pl_pp, s));
-  }
   if (timed) FEM_TRY(apply_event(op, 0, s));
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
                  parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
@@ -1465,15 +1534,20 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   // the two dots per option "dot_mode" (Reduce::dot_mode; the paper's dot ablation)
   Reduce rd = op->red;
   rd.dot_mode = op->dot_mode;
-  cudaError_t e;
-  if (op->kind == FEM_ELASTICITY)
-    e = launch_elastic(op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc, rd, s,
-                       m->sm_count);
-  else
-    e = launch_laplace(op->comps, op->bc, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, op->sc,
-                       rd, s, m->sm_count);
-  if (e != cudaSuccess) return fail(FEM_ECUDA, "fused apply launch: %s", cudaGetErrorString(e));
+  if (m->nranks > 1 && !peer) {  // halo of r and p_old overlapped with the interior planes
+    auto halos = [&](cudaStream_t hs) -> int {
+      double* const vs[2] = {op->r_pl, pold};
+      for (double* v : vs)
+        FEM_TRY(halo_pitch(op, pl_owned(op, v), v + op->pl_lead, v + op->pl_lead + (op->nloc_planes + 1) * op->pl_pp,
+                           op->pl_pp, hs));
+      return FEM_OK;
+    };
+    FEM_TRY(apply_split(op, s, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, rd, halos));
+  } else {
+    FEM_TRY(launch_maps(op, m->g, pl_src(op, op->r_pl), pl_out(op, op->q_pl), maps, 2, rd, s));
+  }
   if (timed) FEM_TRY(apply_event(op, 1, s));
+  cudaError_t e;
   const int64_t n = pl_count(op);
   if (op->dot_mode == 1) {  // p.q by a separate kernel re-reading p and q
     e = launch_cg_dot(pl_owned(op, pnew), pl_owned(op, op->q_pl), n, 0, op->sc, op->red, s, m->sm_count);
@@ -1777,6 +1851,9 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (op->cg_active) return fail(FEM_ESTATE, "cg_variant cannot change during a CG solve");
     op->cg_variant = (int)value;
     drop_graphs(op);
+  } else if (!std::strcmp(key, "halo_overlap")) {
+    op->overlap = value != 0;
+    drop_graphs(op);
   } else if (!std::strcmp(key, "dot_mode")) {
     if (value < 0 || value > 2) return fail(FEM_EINVAL, "dot_mode must be 0 (fused epilogue), 1 (separate dot kernels) or 2 (atomic partials)");
     if (op->cg_active) return fail(FEM_ESTATE, "dot_mode cannot change during a CG solve");
@@ -1819,6 +1896,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "cg_variant")) *value = (op->tm_ok && op->cg_variant == 1) ? 1 : 0;
   else if (!std::strcmp(key, "peer_halo")) *value = op->peer_on ? 1 : 0;
   else if (!std::strcmp(key, "dot_mode")) *value = op->dot_mode;
+  else if (!std::strcmp(key, "halo_overlap")) *value = op->overlap;
   else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }

@@ -65,6 +65,10 @@ struct ApplyMaps {
   int quad;                // 0: 2x2x2 Gauss-Legendre (default), 1: 2x2x2 Gauss-Lobatto (BP5/BP6)
   const PeerMaps* peer;    // ghost planes from peer memory (nullptr / on = 0: local)
   const PairGeom* pair = nullptr;  // u is a row-pair view of a caller vector (kernels_common.cuh)
+  // halo overlap (fem_api.cu, launch_split): a fixed z-chunking instead of the launcher's --
+  // zc_force chunks starting kchunk_force planes apart, each kspan planes long (0: automatic)
+  int64_t kchunk_force = 0, kspan = 0;
+  int zc_force = 0;
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).
@@ -95,6 +99,9 @@ struct Reduce {
   // re-read the vectors; 2 in the epilogue, CTA partials added with FP64 atomics (run-order
   // dependent).  Kernels other than the fused apply / update always use 0.
   int dot_mode = 0;
+  // split applies (halo overlap): acc = 1 adds this launch's dots to the scalars instead of
+  // writing them; roll = 0 leaves the fused-CG recurrence roll (rr = rr_new) to a later launch
+  int acc = 0, roll = 1;
 };
 
 constexpr int kMaxCtas = 1 << 16;
@@ -323,7 +330,7 @@ __device__ __forceinline__ void cg_apply_epilogue(double pq, bool roll, CgScalar
   if (red.dot_mode == 2) {
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     if (tid == 0) atomicAdd(&sc->pq, bsum);  // zeroed by the previous update's last CTA
-    if (!roll) return;
+    if (!roll || !red.roll) return;
     double unused;
     if (last_block_reduce(0.0, red, sh, &unused)) {  // ticket only: the last CTA rolls
       sc->rr = sc->rr_new;
@@ -334,8 +341,8 @@ __device__ __forceinline__ void cg_apply_epilogue(double pq, bool roll, CgScalar
   }
   double total;
   if (last_block_reduce(bsum, red, sh, &total)) {
-    sc->pq = total;
-    if (roll) {  // every block has read rr / rr_new / first: roll the recurrence
+    sc->pq = red.acc ? sc->pq + total : total;
+    if (roll && red.roll) {  // every block has read rr / rr_new / first: roll the recurrence
       sc->rr = sc->rr_new;
       sc->first = 0;
     }

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
     elastic_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                    const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
-                   int bc, int64_t kchunk, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
+                   int bc, int64_t kchunk, int64_t kspan, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
                    int txa, int tya) {
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
   const int64_t i0 = (int64_t)blockIdx.x * txa;
   const int64_t j0 = (int64_t)blockIdx.y * tya;
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
-  const int64_t ke = min(g.k1, kb + kchunk);
+  const int64_t ke = min(g.k1, kb + kspan);
   const int64_t pfirst = kb - 1;  // planes kb-1 .. ke (cell layers kb-1 .. ke-1)
   if (tid < 4 * TY) {
     mbar_init(&tfull[tid], 1);
@@ -281,8 +281,8 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
     const double bg = block_sum(rr2, red_sh);
     double td, tg;
     if (last_block_reduce2(bd, bg, red, red_sh, &td, &tg)) {
-      sc->pq = td;
-      sc->rr_new = tg;
+      sc->pq = red.acc ? sc->pq + td : td;
+      sc->rr_new = red.acc ? sc->rr_new + tg : tg;
     }
   } else if (mode >= 1) {
     cg_apply_epilogue(pq, mode == 2, sc, red, red_sh);
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     elastic2_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                     TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                     const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
-                    int bc, int64_t kchunk, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
+                    int bc, int64_t kchunk, int64_t kspan, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
                     int txa, int tya, PairGeom pg) {
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   const int64_t i0 = (int64_t)blockIdx.x * txa;
   const int64_t j0 = (int64_t)blockIdx.y * tya;
   const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
-  const int64_t ke = min(g.k1, kb + kchunk);
+  const int64_t ke = min(g.k1, kb + kspan);
   const int64_t pfirst = kb - 1;
   if (tid < HD * TY) {
     mbar_init(&tfull[tid], 1);
@@ -610,8 +610,8 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     const double bg = block_sum(rr2, red_sh);
     double td, tg;
     if (last_block_reduce2(bd, bg, red, red_sh, &td, &tg)) {
-      sc->pq = td;
-      sc->rr_new = tg;
+      sc->pq = red.acc ? sc->pq + td : td;
+      sc->rr_new = red.acc ? sc->rr_new + tg : tg;
     }
   } else if (mode >= 1) {
     cg_apply_epilogue(pq, mode == 2, sc, red, red_sh);
@@ -660,6 +660,11 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
     zc = w.zc;
     kchunk = w.kchunk;
   }
+  if (maps.kchunk_force > 0) {  // halo overlap: the caller's plane selection
+    kchunk = maps.kchunk_force;
+    zc = maps.zc_force;
+  }
+  const int64_t kspan = maps.kspan > 0 ? maps.kspan : kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + ((TM && kEl2Self) ? 0 : 1));
   CUtensorMap um, um2;
@@ -669,7 +674,7 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   PeerMaps pm;
   if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
   kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
-                                 bc, kchunk, sc, red, pm, txa, tya, maps.pair ? *maps.pair : PairGeom{0, 0, 0});
+                                 bc, kchunk, kspan, sc, red, pm, txa, tya, maps.pair ? *maps.pair : PairGeom{0, 0, 0});
   add_launches(1);
   return cudaGetLastError();
 }
@@ -712,6 +717,11 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
     zc = w.zc;
     kchunk = w.kchunk;
   }
+  if (maps.kchunk_force > 0) {  // halo overlap: the caller's plane selection
+    kchunk = maps.kchunk_force;
+    zc = maps.zc_force;
+  }
+  const int64_t kspan = maps.kspan > 0 ? maps.kspan : kchunk;
   if (xt * yt * zc > kMaxCtas) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)xt, (unsigned)yt, (unsigned)zc), block(TX, TY + 1);
   CUtensorMap um, um2;
@@ -721,7 +731,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   PeerMaps pm;
   if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
   kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
-                                 bc, kchunk, sc, red, pm, txa, tya);
+                                 bc, kchunk, kspan, sc, red, pm, txa, tya);
   add_launches(1);
   return cudaGetLastError();
 }

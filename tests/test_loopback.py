@@ -122,7 +122,7 @@ def test_loopback_apply_and_dot(F, kind, P):
         assert abs(r[1] - d_ref) <= 1e-14 * abs(d_ref) + 1e-300
 
 
-def _cg_case(F, kind, P, variant, peer, iters, tol):
+def _cg_case(F, kind, P, variant, peer, iters, tol, overlap=1):
     nx, ny, nz = MESH
     h = 1.0 / nx
     c = I.ncomp(kind)
@@ -141,6 +141,7 @@ def _cg_case(F, kind, P, variant, peer, iters, tol):
         mesh, op = _slab_op(F, comms[r], kind, nx, ny, nz, h, lam, mu)
         if variant:
             op.set_option("cg_variant", 1)
+        op.set_option("halo_overlap", overlap)
         if peer:
             op.set_option("peer_halo", 1)
             assert op.get_option("peer_halo") == 1
@@ -162,9 +163,11 @@ def _cg_case(F, kind, P, variant, peer, iters, tol):
 
 @pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
 @pytest.mark.parametrize("P", [2, 3, 5])
-@pytest.mark.parametrize("variant,peer", [(0, False), (1, False), (0, True), (1, True)])
-def test_loopback_cg_three_iterations(F, kind, P, variant, peer):
-    x, xr, infos, ir, *_ = _cg_case(F, kind, P, variant, peer, 3, 0.0)
+@pytest.mark.parametrize("variant,peer,overlap", [(0, False, 1), (1, False, 1), (0, True, 1), (1, True, 1),
+                                                  (0, False, 0), (1, False, 0)])
+def test_loopback_cg_three_iterations(F, kind, P, variant, peer, overlap):
+    """overlap = 1: the halo runs on the comm stream beside the interior planes (apply_split)."""
+    x, xr, infos, ir, *_ = _cg_case(F, kind, P, variant, peer, 3, 0.0, overlap)
     assert np.abs(x - xr).max() <= 1e-12 * np.abs(xr).max()
     for info in infos:
         assert info["iterations"] == 3 and info["rc"] == 0
