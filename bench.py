@@ -262,8 +262,8 @@ def run_native(args, cfg):
     else:
         mesh = fem.Mesh(nx, ny, nz, h, comm)
     op = fem.Operator(mesh, kind, "dirichlet")
-    if hexmesh and args.pa:  # partial assembly: stored Gauss-point geometry (Table 3)
-        op.set_option("partial_assembly", 1)
+    if args.pa:  # partial assembly (Table 3): hex -- stored geometry; box elasticity --
+        op.set_option("partial_assembly", 1)  # 21 values per Gauss point, D_q = w det J C_e
     if args.gll:  # Gauss-Lobatto quadrature: the BP5 / BP6 operators (reading R1)
         op.set_option("quadrature", 1)
     if args.cgcg:  # Chronopoulos-Gear single-reduction CG (NEXT #1)
@@ -367,6 +367,8 @@ def run_native(args, cfg):
         fused = False
     # algorithmic bytes of one rank's apply launch: owned planes (+ its cell layers)
     alg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) * nloc_planes / (nz + 1)
+    if args.pa and not hexmesh:  # box PA: 21 x 8 stored doubles per cell (Table 3) + u read + y write
+        alg_bytes = 21 * 8 * 8 * nx * ny * nz + 16 * op.n_global
     achieved = alg_bytes / (apply_ms / 1e3) / 1e9
     if hexmesh:  # FP64-bound: flops of the per-cell body / apply time
         hex_flops = HEX_FLOPS_PER_CELL[kind] * nx * ny * nz
@@ -404,6 +406,8 @@ def run_native(args, cfg):
     extra["apply_only_ms"] = ams
     if not hexmesh:  # fem_apply on the caller's vectors: algorithmic bytes / time vs the HBM peak
         ab = algorithmic_apply_bytes(kind, nx, ny, nz) * nloc_planes / (nz + 1)
+        if args.pa:  # the stored 21 x 8 values per cell instead of lambda, mu
+            ab = 21 * 8 * 8 * nx * ny * nz + 16 * op.n_global
         extra["apply_only_gbs"] = ab / (ams / 1e3) / 1e9
         extra["apply_only_frac"] = extra["apply_only_gbs"] / hbm_peak
         extra["apply_only_path"] = ["bulk rows", "tensor map", "row-pair tensor map"][op.get_option("last_apply_path")]
@@ -482,7 +486,8 @@ def run_native(args, cfg):
                           "frac": achieved / hbm_peak, "traffic": traffic,
                           "kernel": (f"{kind} fused CG apply (p = r + beta p_old, q = A p, p.q)" if fused
                                      else (f"{kind} apply (single-reduction CG: w = A r, w.r, r.r)" if cgcg
-                                           else f"{kind} apply (CG mode, fused p.Ap)")),
+                                           else ("pa21_kernel (partial assembly, 21 values per Gauss point, "
+                                                 "CG mode)" if args.pa else f"{kind} apply (CG mode, fused p.Ap)"))),
                           "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                           "frac_of_8TBps_nominal": achieved / 8000.0} if not hexmesh else
                          {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -672,7 +677,7 @@ def main():
     if args.n:
         cfg["n"] = (args.n, args.n, args.n)
         cfg["name"] += f"_n{args.n}"
-    if args.pa and cfg.get("mesh") == "hex":
+    if args.pa:
         cfg["name"] += "_pa"
     if args.gll:
         cfg["name"] += "_gll"

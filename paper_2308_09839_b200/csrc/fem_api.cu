@@ -587,7 +587,9 @@ static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* u
   ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr,
                  op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr, pair};
   cudaError_t e;
-  if (op->kind == FEM_ELASTICITY)
+  if (op->use_pa)  // partial assembly on the box (21 stored values per Gauss point, bulk-row staging)
+    e = launch_pa21_apply(op->bc, op->quad, m->g, x, y, op->pa, mode, op->sc, op->red, s, m->sm_count);
+  else if (op->kind == FEM_ELASTICITY)
     e = launch_elastic(op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
   else
     e = launch_laplace(op->comps, op->bc, m->g, x, y, maps, mode, op->sc, op->red, s, m->sm_count);
@@ -718,7 +720,7 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
   // is described by a tensor map directly (full box, like the CG vectors), so the apply stages ONE
   // TMA box per plane instead of one bulk copy per row.  Single rank: the ghost planes of a slab
   // are not adjacent to the caller's memory.
-  if (op->direct_tm && m->nranks == 1 && op->tm_ok && !op->tm_interior && (rp & 1) == 0 &&
+  if (op->direct_tm && !op->use_pa && m->nranks == 1 && op->tm_ok && !op->tm_interior && (rp & 1) == 0 &&
       ((uintptr_t)x & 15) == 0) {
     const CUtensorMap* map = cached_map(op, x, xi.id, 1);
     if (!map) {
@@ -737,7 +739,7 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
   // strides) -- so the apply still stages two TMA boxes per plane.  Boxes read up to one row and
   // two box widths past the vector's end (last plane): taken only when the caller's allocation
   // extends that far (cuMemGetAddressRange), else the bulk-row path.
-  if (op->direct_tm && m->nranks == 1 && op->tm_ok && !op->tm_interior && op->bc && (rp & 1) &&
+  if (op->direct_tm && !op->use_pa && m->nranks == 1 && op->tm_ok && !op->tm_interior && op->bc && (rp & 1) &&
       (op->kind != FEM_ELASTICITY || kElCY == 2) && ((uintptr_t)x & 15) == 0) {
     unsigned bw, bh;
     u_box(op->kind, &bw, &bh);
@@ -780,6 +782,31 @@ static int apply_pl(fem_op_s* op, double* v, const CUtensorMap* map, int mode, c
   }
   return launch_apply(op, pl_src(op, v), pl_out(op, op->q_pl), op->tm_ok ? map : nullptr, mode, s, v);
 }
+
+// (re)compute the stored Gauss-point geometry when partial assembly is on and the rule changed
+static int pa_setup(fem_op_s* op, bool force = false) {
+  if (!op->use_pa) return FEM_OK;
+  if (!op->mesh->hex) {  // box: D_q = w_q det J_q C_e from the material (quadrature independent)
+    if (!op->has_mat) return FEM_OK;  // computed by fem_set_material
+    if (op->pa_quad >= 0 && !force) return FEM_OK;
+    const int64_t ncells = op->mesh->g.nx * op->mesh->g.ny * op->mesh->g.nz;
+    if (!op->pa) FEM_TRY(dalloc(&op->pa, pa21_doubles(ncells)));
+    cudaError_t e = launch_pa21_setup(op->lm, ncells, op->mesh->g.h, op->pa, 0, op->mesh->sm_count);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return fail(FEM_ECUDA, "partial-assembly setup: %s", cudaGetErrorString(e));
+    op->pa_quad = 0;
+    return FEM_OK;
+  }
+  if (op->pa_quad == op->quad) return FEM_OK;
+  if (!op->pa) FEM_TRY(dalloc(&op->pa, hex_pa_doubles(op->kind, op->mesh->hx_ncells)));
+  cudaError_t e = launch_hex_pa_setup(op->kind, op->quad, op->mesh->hx_cells, op->mesh->hx_xyz, op->pa,
+                                      op->mesh->hx_ncells, 0, op->mesh->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "partial-assembly setup: %s", cudaGetErrorString(e));
+  CUDA_TRY(cudaDeviceSynchronize());
+  op->pa_quad = op->quad;
+  return FEM_OK;
+}
+
 
 static int pack(fem_op_s* op, const double* dense, double* v, int to_padded, cudaStream_t s) {
   if (op->mesh->hex) {  // CG vectors are dense on general meshes
@@ -1264,6 +1291,7 @@ int fem_set_material(fem_op_t op, const double* lam, const double* mu, int64_t l
   FEM_TRY(make_mat_map(op));
   op->has_mat = true;
   op->cg_active = false;
+  if (op->use_pa) FEM_TRY(pa_setup(op, true));  // D_q folds the material in
   return FEM_OK;
 }
 
@@ -1583,6 +1611,7 @@ static int cg_cgcg_body(fem_op_s* op, cudaStream_t s, bool timed) {
 }
 
 static int iteration(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
+  if (op->use_pa) return cg_iteration_body(op, s, timed);  // partial assembly: unfused iteration
   if (op->tm_ok && op->cg_variant == 1) return cg_cgcg_body(op, s, timed);
   return op->tm_ok ? cg_fused_body(op, parity, s, timed) : cg_iteration_body(op, s, timed);
 }
@@ -1646,7 +1675,7 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
 
 static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
   const int per_iter_launches =
-      op->tm_ok ? ((op->cg_variant == 0 && op->dot_mode == 1) ? 4 : 2)
+      (op->tm_ok && !op->use_pa) ? ((op->cg_variant == 0 && op->dot_mode == 1) ? 4 : 2)
                 : (op->mesh->hex ? 3 + ((op->bc && op->mesh->hx_nb) ? 1 : 0) : 3);
   // loopback ranks rendezvous on the host inside every collective: not capturable, run eagerly
   const bool loop = op->mesh->comm && op->mesh->comm->loop && op->mesh->nranks > 1;
@@ -1810,17 +1839,6 @@ static void drop_graphs(fem_op_s* op) {
   op->graphT.clear();
 }
 
-// (re)compute the stored Gauss-point geometry when partial assembly is on and the rule changed
-static int pa_setup(fem_op_s* op) {
-  if (!op->use_pa || op->pa_quad == op->quad) return FEM_OK;
-  if (!op->pa) FEM_TRY(dalloc(&op->pa, hex_pa_doubles(op->kind, op->mesh->hx_ncells)));
-  cudaError_t e = launch_hex_pa_setup(op->kind, op->quad, op->mesh->hx_cells, op->mesh->hx_xyz, op->pa,
-                                      op->mesh->hx_ncells, 0, op->mesh->sm_count);
-  if (e != cudaSuccess) return fail(FEM_ECUDA, "partial-assembly setup: %s", cudaGetErrorString(e));
-  CUDA_TRY(cudaDeviceSynchronize());
-  op->pa_quad = op->quad;
-  return FEM_OK;
-}
 
 int fem_set_option(fem_op_t op, const char* key, int64_t value) {
   if (!op || !key) return fail(FEM_EINVAL, "op/key is NULL");
@@ -1831,9 +1849,16 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
   } else if (!std::strcmp(key, "time_apply")) op->time_apply = value != 0;
   else if (!std::strcmp(key, "direct_tma")) op->direct_tm = value != 0;
   else if (!std::strcmp(key, "partial_assembly")) {
-    if (!op->mesh->hex) return fail(FEM_EUNSUPPORTED, "partial_assembly is an option of general hex meshes");
+    if (!op->mesh->hex && (op->kind != FEM_ELASTICITY || op->mesh->nranks != 1))
+      return fail(FEM_EUNSUPPORTED, "partial_assembly: general hex meshes, or the single-rank elasticity box operator");
+    if (op->cg_active) return fail(FEM_ESTATE, "partial_assembly cannot change during a CG solve");
     FEM_TRY(set_device(op->mesh->device));
     op->use_pa = value != 0;
+    if (!op->use_pa && !op->mesh->hex && op->pa) {  // release the 1,344 B/cell
+      cudaFree(op->pa);
+      op->pa = nullptr;
+      op->pa_quad = -1;
+    }
     FEM_TRY(pa_setup(op));
     // captured CG graphs hold the other kernel
     drop_graphs(op);
@@ -1885,7 +1910,8 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
 
 int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   if (!op || !key || !value) return fail(FEM_EINVAL, "op/key/value is NULL");
-  if (!std::strcmp(key, "fused_cg") || !std::strcmp(key, "tma")) *value = op->tm_ok ? 1 : 0;
+  if (!std::strcmp(key, "fused_cg")) *value = (op->tm_ok && !op->use_pa) ? 1 : 0;
+  else if (!std::strcmp(key, "tma")) *value = op->tm_ok ? 1 : 0;
   else if (!std::strcmp(key, "use_graph")) *value = op->use_graph;
   else if (!std::strcmp(key, "check_every")) *value = op->check_every;
   else if (!std::strcmp(key, "time_apply")) *value = op->time_apply;
@@ -1893,7 +1919,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "last_apply_path")) *value = op->last_path;
   else if (!std::strcmp(key, "partial_assembly")) *value = op->use_pa;
   else if (!std::strcmp(key, "quadrature")) *value = op->quad;
-  else if (!std::strcmp(key, "cg_variant")) *value = (op->tm_ok && op->cg_variant == 1) ? 1 : 0;
+  else if (!std::strcmp(key, "cg_variant")) *value = (op->tm_ok && !op->use_pa && op->cg_variant == 1) ? 1 : 0;
   else if (!std::strcmp(key, "peer_halo")) *value = op->peer_on ? 1 : 0;
   else if (!std::strcmp(key, "dot_mode")) *value = op->dot_mode;
   else if (!std::strcmp(key, "halo_overlap")) *value = op->overlap;

@@ -216,6 +216,12 @@ cudaError_t launch_hex_pa_setup(int kind, int quad, const int4* cells, const dou
 cudaError_t launch_hex_pa_apply(int kind, int bc, int quad, const int4* cells, const double* pa, const double2* lm,
                                 const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
                                 Reduce red, cudaStream_t s, int sm_count);
+// partial assembly on the box (kernels_pa.cu): 21 values per Gauss point and cell,
+// D_q = w_q det J_q C_e (Voigt, upper triangle), SoA [q][k][cell]
+int64_t pa21_doubles(int64_t ncells);
+cudaError_t launch_pa21_setup(const double2* lm, int64_t ncells, double h, double* D, cudaStream_t s, int sm_count);
+cudaError_t launch_pa21_apply(int bc, int quad, const Grid& g, PlaneSrc x, OutVec y, const double* D, int mode,
+                              CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
 // y = x on the constrained nodes; mode 1: sc->pq += sum x_b^2
 cudaError_t launch_hex_dirichlet(const int32_t* nodes, int64_t nb, int comps, const double* x, double* y,
                                  int mode, CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);

@@ -206,7 +206,59 @@ def test_hex_partial_assembly_cg(F, oracle, kind):
 
 
 def test_partial_assembly_box_unsupported(F):
+    """Box partial assembly is the 21-value elasticity operator (Table 3); Laplace kinds and
+    multi-rank operators are not supported."""
     op = F.Operator(F.Mesh(4, 4, 4, 0.25), "scalar", 1)
     with pytest.raises(F.FemError) as e:
         op.set_option("partial_assembly", 1)
     assert e.value.status == F.FEM_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("quad", [0, 1])
+@pytest.mark.parametrize("dims", [(1, 1, 1), (5, 7, 9), (33, 17, 12), (40, 9, 13)])
+def test_box_partial_assembly_21(F, oracle, bc, quad, dims):
+    """Elasticity partial assembly on the box (Table 3: 21 values per Gauss point,
+    D_q = w_q det J_q C_e): the oracle's operator (Gauss rule; the Lobatto rule against the
+    oracle run with that rule) and the matrix-free kernel, within 1e-12."""
+    nx, ny, nz = dims
+    h = 1.0 / max(dims)
+    g = I.rng(I.SEED_BASE + 700 + nx)
+    x = I.uniform_vector(g, nx, ny, nz, 3)
+    lam, mu = I.materials(g, nx, ny, nz)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), "elastic", bc)
+    op.set_option("quadrature", quad)
+    op.set_option("partial_assembly", 1)  # before the material: D is formed by fem_set_material
+    op.set_material(dev(lam), dev(mu))
+    assert op.get_option("partial_assembly") == 1 and op.get_option("fused_cg") == 0
+    y_pa = op.apply(dev(x)).cpu().numpy()
+    with oracle.quadrature("gll" if quad else "gauss"):
+        ref = oracle.apply("elastic", bc, nx, ny, nz, h, x, lam=lam, mu=mu)
+    assert relerr(y_pa, ref) <= APPLY_TOL
+    y_pa_host = op.apply(x)  # host vectors: staged copies, same kernel
+    assert np.array_equal(y_pa_host, y_pa)
+    op.set_option("partial_assembly", 0)
+    y_mf = op.apply(dev(x)).cpu().numpy()
+    assert relerr(y_pa, y_mf) <= APPLY_TOL
+    # material changed after enabling: D is recomputed
+    op.set_option("partial_assembly", 1)
+    op.set_material(dev(2.0 * lam), dev(mu))
+    with oracle.quadrature("gll" if quad else "gauss"):
+        ref2 = oracle.apply("elastic", bc, nx, ny, nz, h, x, lam=2.0 * lam, mu=mu)
+    assert relerr(op.apply(dev(x)).cpu().numpy(), ref2) <= APPLY_TOL
+
+
+def test_box_partial_assembly_cg(F, oracle):
+    nx, ny, nz = 9, 8, 7
+    h = 1.0 / 9
+    g = I.rng(I.SEED_BASE + 710)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = I.interior_rhs(g, nx, ny, nz, 3)
+    ref = oracle.cg("elastic", 1, nx, ny, nz, h, b, tol=1e-14, maxit=3000, lam=lam, mu=mu)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), "elastic", 1)
+    op.set_material(dev(lam), dev(mu))
+    op.set_option("partial_assembly", 1)
+    x = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+    info = op.cg_solve(dev(b), x, tol=1e-14, maxit=3000)
+    assert info["converged"] and abs(info["iterations"] - ref.iterations) <= 3
+    assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10 * max(1.0, np.abs(ref.x).max())
