@@ -197,9 +197,12 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
 /* Options: "use_graph" (default 1), "check_every" (default 16 iterations between host
  * convergence polls in fem_cg_solve), "time_apply" (1: record CUDA events around every apply
  * launched by fem_cg_iterate; read back with fem_apply_time), "partial_assembly" (general hex
- * meshes only, else FEM_EUNSUPPORTED; 1: store the Gauss-point geometry once -- 6 values per
- * point for the Laplace kinds, 9 for elasticity -- and apply from it, the paper's comparison
- * method P:308-309 / Table 3; 0: matrix-free recomputation, the default), "quadrature" (0: the
+ * meshes, and the single-rank elasticity box operator; else FEM_EUNSUPPORTED; 1: store per Gauss
+ * point what the matrix-free kernel recomputes and apply from it, the paper's comparison method
+ * P:308-309 / Table 3 -- general hexes: the geometry, 6 values per point for the Laplace kinds,
+ * 9 for elasticity; elasticity box: Table 3's 21 values per point, D_q = w_q det J_q C_e (the
+ * symmetric 6x6 Voigt stiffness with the cell's lambda, mu folded in), 1,344 B per cell;
+ * 0: matrix-free recomputation, the default), "quadrature" (0: the
  * 2x2x2 Gauss-Legendre rule, default; 1: the 2x2x2 Gauss-Lobatto rule collocated with the nodes,
  * the quadrature of the CEED benchmark problems BP5 / BP6 the paper names, P:581, P:638,
  * a different operator (the 7-point stencil for Laplace on the box); applies to
@@ -216,6 +219,12 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * varies from run to run); TMA path, cg_variant 0 only), "halo_overlap" (1, default: with an
  * exchange step -- nranks > 1 without peer_halo -- the halo runs on a library stream while the
  * interior node planes are applied, then the two boundary planes; 0: halo, then one apply),
+ * "trace" (1: CUDA timing events around the halo, the interior and the boundary launches of
+ * every eager exchange apply; read back, blocking on the last traced apply, as the read-only
+ * "trace_halo_ns", "trace_interior_ns", "trace_boundary_ns", "trace_total_ns" -- the
+ * halo / interior overlap timeline; FEM_ESTATE before the first traced apply; host-side NVTX
+ * ranges fem:apply, fem:halo, fem:allreduce, fem:interior, fem:boundary, fem:cg_* are always
+ * emitted and cost nothing without a tool attached),
  * "peer_halo" (1: collective over the slab ranks --
  * every rank sets it -- exchanging CUDA IPC handles of the CG vectors with the neighbours over
  * NCCL; the apply kernels then load the ghost node planes straight from the neighbours' memory

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool attached
 
 #include <algorithm>
 #include <atomic>
@@ -23,6 +24,16 @@
 #include "fem_internal.cuh"
 
 namespace fem {
+
+// NVTX range over a host-side scope (SURVEY §5 "Tracing"): fem:apply, fem:halo, fem:allreduce,
+// fem:interior / fem:boundary of the overlapped apply, fem:cg_iterate ...  Visible to nsys / ncu
+// --nvtx when a tool is attached; a no-op otherwise.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 cudaError_t upload_unit_matrices(const double* K, const double* Kl, const double* Km);
 static std::atomic<int64_t> g_launches{0};
 void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -195,6 +206,12 @@ struct fem_op_s {
   int overlap = 1;
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // option "trace": timing events of the last exchange apply (apply_split) -- [0] start on the
+  // caller's stream, [1] halo done (comm stream), [2] interior planes done, [3] boundary planes
+  // done; read back as trace_{halo,interior,boundary,total}_ns (the overlap timeline)
+  int trace = 0;
+  cudaEvent_t tr_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool tr_valid = false;
   struct MapEnt {
     const void* p = nullptr;
     unsigned long long id = 0;
@@ -432,6 +449,7 @@ static int halo_pitch(fem_op_s* op, const double* owned, double* lo, double* hi,
                       cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
   if (m->nranks == 1) return FEM_OK;
+  NvtxRange nv("fem:halo");
   if (m->comm->loop) return loop_halo(m, owned, lo, hi, pitch, s);
   const size_t cnt = (size_t)pitch;
   const int64_t np = m->g.k1 - m->g.k0;
@@ -455,6 +473,7 @@ static int halo(fem_op_s* op, const double* owned, double* lo, double* hi, cudaS
 static int allreduce1(fem_op_s* op, double* dev_scalar, cudaStream_t s, int count = 1) {
   fem_mesh_s* m = op->mesh;
   if (m->nranks == 1) return FEM_OK;
+  NvtxRange nv("fem:allreduce");
   if (m->comm->loop) return loop_allreduce(m, dev_scalar, count, s);
   NCCL_TRY(ncclAllReduce(dev_scalar, dev_scalar, count, ncclDouble, ncclSum, m->comm->nccl, s));
   return FEM_OK;
@@ -626,14 +645,35 @@ static int apply_split(fem_op_s* op, cudaStream_t s, PlaneSrc src, OutVec out, A
                        Reduce red, const std::function<int(cudaStream_t)>& halo) {
   const Grid& g = op->mesh->g;
   const int64_t nl = g.k1 - g.k0;
+  // trace events are plain records on the eager path (inside a graph capture they would be
+  // nodes recorded at replay; the trace is a diagnostic of eager applies)
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(s, &cst));
+  const bool tr = op->trace && cst == cudaStreamCaptureStatusNone;
+  if (tr) {
+    for (auto& e : op->tr_ev)
+      if (!e) CUDA_TRY(cudaEventCreate(&e));
+    CUDA_TRY(cudaEventRecord(op->tr_ev[0], s));
+    op->tr_valid = true;
+  }
   if (!op->overlap || nl < 3) {
     FEM_TRY(halo(s));
-    return launch_maps(op, g, src, out, maps, mode, red, s);
+    if (tr) CUDA_TRY(cudaEventRecord(op->tr_ev[1], s));
+    {
+      NvtxRange nv("fem:apply_planes");
+      FEM_TRY(launch_maps(op, g, src, out, maps, mode, red, s));
+    }
+    if (tr) {
+      CUDA_TRY(cudaEventRecord(op->tr_ev[2], s));
+      CUDA_TRY(cudaEventRecord(op->tr_ev[3], s));
+    }
+    return FEM_OK;
   }
   FEM_TRY(ensure_comm_stream(op));
   CUDA_TRY(cudaEventRecord(op->ev_fork, s));
   CUDA_TRY(cudaStreamWaitEvent(op->cstream, op->ev_fork, 0));
   FEM_TRY(halo(op->cstream));
+  if (tr) CUDA_TRY(cudaEventRecord(op->tr_ev[1], op->cstream));
   CUDA_TRY(cudaEventRecord(op->ev_join, op->cstream));
   Grid gi = g;
   gi.k0 = g.k0 + 1;
@@ -646,7 +686,11 @@ static int apply_split(fem_op_s* op, cudaStream_t s, PlaneSrc src, OutVec out, A
   Reduce ri = red;
   ri.acc = 0;
   ri.roll = 0;
-  FEM_TRY(launch_maps(op, gi, si, oi, mi, mode, ri, s));
+  {
+    NvtxRange nv("fem:interior");
+    FEM_TRY(launch_maps(op, gi, si, oi, mi, mode, ri, s));
+  }
+  if (tr) CUDA_TRY(cudaEventRecord(op->tr_ev[2], s));
   CUDA_TRY(cudaStreamWaitEvent(s, op->ev_join, 0));
   ApplyMaps mb = maps;
   mb.kchunk_force = nl - 1;
@@ -654,7 +698,12 @@ static int apply_split(fem_op_s* op, cudaStream_t s, PlaneSrc src, OutVec out, A
   mb.kspan = 1;
   Reduce rb = red;
   rb.acc = 1;
-  return launch_maps(op, g, src, out, mb, mode, rb, s);
+  {
+    NvtxRange nv("fem:boundary");
+    FEM_TRY(launch_maps(op, g, src, out, mb, mode, rb, s));
+  }
+  if (tr) CUDA_TRY(cudaEventRecord(op->tr_ev[3], s));
+  return FEM_OK;
 }
 
 static PlaneSrc dense_src(fem_op_s* op, const double* x, const double* lo, const double* hi) {
@@ -1088,6 +1137,8 @@ static void op_free(fem_op_s* op) {
   if (op->cstream) cudaStreamDestroy(op->cstream);
   if (op->ev_fork) cudaEventDestroy(op->ev_fork);
   if (op->ev_join) cudaEventDestroy(op->ev_join);
+  for (auto e : op->tr_ev)
+    if (e) cudaEventDestroy(e);
   if (op->peer_ipc)
     for (int v = 0; v < 4; ++v) {
       if (op->nb_lo[v]) cudaIpcCloseMemHandle(op->nb_lo[v]);
@@ -1465,6 +1516,7 @@ static int peer_halo_ipc(fem_op_s* op) {
 }
 
 int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
+  NvtxRange nv("fem:apply");
   if (!op) return fail(FEM_EINVAL, "op is NULL");
   FEM_TRY(need_comm(op));
   FEM_TRY(check_vec(x, "x"));
@@ -1493,6 +1545,7 @@ int fem_apply(fem_op_t op, const double* x, double* y, void* stream) {
 }
 
 int fem_dot(fem_op_t op, const double* a, const double* b, double* result, void* stream) {
+  NvtxRange nv("fem:dot");
   if (!op) return fail(FEM_EINVAL, "op is NULL");
   FEM_TRY(need_comm(op));
   FEM_TRY(check_vec(a, "a"));
@@ -1757,6 +1810,7 @@ static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
 }
 
 int fem_cg_begin(fem_op_t op, const double* b, double* x, double tol, int32_t maxit, void* stream) {
+  NvtxRange nv("fem:cg_begin");
   if (!op) return fail(FEM_EINVAL, "op is NULL");
   FEM_TRY(need_comm(op));
   FEM_TRY(check_vec(b, "b"));
@@ -1771,6 +1825,7 @@ int fem_cg_begin(fem_op_t op, const double* b, double* x, double tol, int32_t ma
 }
 
 int fem_cg_iterate(fem_op_t op, int32_t iters, void* stream) {
+  NvtxRange nv("fem:cg_iterate");
   if (!op) return fail(FEM_EINVAL, "op is NULL");
   if (!op->cg_active) return fail(FEM_ESTATE, "fem_cg_begin not called");
   if (iters < 0) return fail(FEM_EINVAL, "iters < 0");
@@ -1779,6 +1834,7 @@ int fem_cg_iterate(fem_op_t op, int32_t iters, void* stream) {
 }
 
 int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream) {
+  NvtxRange nv("fem:cg_end");
   if (!op) return fail(FEM_EINVAL, "op is NULL");
   if (!op->cg_active) return fail(FEM_ESTATE, "fem_cg_begin not called");
   FEM_TRY(set_device(op->mesh->device));
@@ -1876,6 +1932,8 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (op->cg_active) return fail(FEM_ESTATE, "cg_variant cannot change during a CG solve");
     op->cg_variant = (int)value;
     drop_graphs(op);
+  } else if (!std::strcmp(key, "trace")) {
+    op->trace = value != 0;
   } else if (!std::strcmp(key, "halo_overlap")) {
     op->overlap = value != 0;
     drop_graphs(op);
@@ -1923,6 +1981,24 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "peer_halo")) *value = op->peer_on ? 1 : 0;
   else if (!std::strcmp(key, "dot_mode")) *value = op->dot_mode;
   else if (!std::strcmp(key, "halo_overlap")) *value = op->overlap;
+  else if (!std::strcmp(key, "trace")) *value = op->trace;
+  else if (!std::strncmp(key, "trace_", 6)) {
+    // trace_{halo,interior,boundary,total}_ns of the last traced exchange apply (blocks on it)
+    static const char* names[4] = {"trace_halo_ns", "trace_interior_ns", "trace_boundary_ns", "trace_total_ns"};
+    static const int from[4] = {0, 0, 0, 0}, to[4] = {1, 2, 3, 3};
+    int k = -1;
+    for (int t = 0; t < 4; ++t)
+      if (!std::strcmp(key, names[t])) k = t;
+    if (k < 0) return fail(FEM_EINVAL, "unknown option '%s'", key);
+    if (!op->tr_valid) return fail(FEM_ESTATE, "%s: no traced exchange apply yet (option trace, nranks > 1)", key);
+    FEM_TRY(set_device(op->mesh->device));
+    CUDA_TRY(cudaEventSynchronize(op->tr_ev[3]));
+    CUDA_TRY(cudaEventSynchronize(op->tr_ev[1]));
+    float ms = 0.f;
+    if (k == 2) CUDA_TRY(cudaEventElapsedTime(&ms, op->tr_ev[2], op->tr_ev[3]));  // boundary: after interior
+    else CUDA_TRY(cudaEventElapsedTime(&ms, op->tr_ev[from[k]], op->tr_ev[to[k]]));
+    *value = (int64_t)(ms * 1e6);
+  }
   else return fail(FEM_EINVAL, "unknown option '%s'", key);
   return FEM_OK;
 }

@@ -91,6 +91,9 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t addr, uint32_t parity) {
       "r"(parity), "r"(1000000)
       : "memory");
 }
+#ifndef FEM_RING_FENCE
+#define FEM_RING_FENCE 0
+#endif
 __device__ __forceinline__ void mbar_arrive_a(uint32_t addr) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(addr) : "memory");
 }
@@ -356,7 +359,10 @@ struct PlaneRing {
       if (t >= S) mbar_wait_a(empty_a + 8u * s, (uint32_t)(((t / S) - 1) & 1));
       double* slot = buf + (size_t)s * SLOT;
       if (TM) {
-        if (lane == 0) issue_tm(t, p, ux, uy, mx, my, uorg, umap, umap2, mmap, mlayer0, peer);
+        if (lane == 0) {
+          fence_proxy_async();  // the consumers' generic reads of the slot before the TMA write
+          issue_tm(t, p, ux, uy, mx, my, uorg, umap, umap2, mmap, mlayer0, peer);
+        }
         continue;
       }
       fence_proxy_async();
@@ -413,8 +419,16 @@ struct PlaneRing {
     return __shfl_sync(0xffffffffu, last, 0) != 0u;
   }
 
-  // consumer warp: release slot s after its last read
+  // consumer warp: release slot s after its last read.  (The thread that refills the slot issues
+  // fence.proxy.async between observing the release and the TMA: the generic-proxy reads of the
+  // slot must be ordered before the async-proxy write.  Without that fence the vector Laplace
+  // fused CG at 256^3 sporadically corrupted part of one warp row of one plane -- the TMA refill
+  // landed before queued LDS of the releasing warp.  FEM_RING_FENCE=1 adds a consumer-side fence
+  // as well: not needed, and 3-5 % slower.)
   __device__ __forceinline__ void release(int s, int lane) {
+#if FEM_RING_FENCE
+    fence_proxy_async();
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive_a(empty_a + 8u * s);
   }

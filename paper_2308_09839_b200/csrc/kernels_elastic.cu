@@ -507,8 +507,10 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
         ring.release(slot, tx);
         if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
           ring.wait_released(t);
-          if (tx == 0)
+          if (tx == 0) {
+            fence_proxy_async();  // every warp's generic reads of the slot before the TMA write
             ring.issue_tm(t + S, pfirst + t + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0, &peer);
+          }
         }
         LA = lmA.x * hs;
         MA = lmA.y * hs;

@@ -17,6 +17,10 @@
 
 #include "kernels_common.cuh"
 
+#ifndef FEM_LAP_FORCE_EDGE
+#define FEM_LAP_FORCE_EDGE 0  // 1: every CTA takes the Dirichlet-aware march (experiments)
+#endif
+
 namespace fem {
 
 // GLL: 2-point Gauss-Lobatto quadrature (BP5/BP6, reading R1): the 1-D mass is
@@ -77,7 +81,11 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
     const double h36 = g.h * (1.0 / 36.0);
     // CTAs whose tile (with its one-node halo) and z-chunk stay away from the box faces run the
     // march with constant 1-D multiplicities (m = 2) and without Dirichlet / identity-row logic
+#if FEM_LAP_FORCE_EDGE
+    const bool edge = true;
+#else
     const bool edge = i0 <= 1 || i0 + TX >= g.nx || j0 <= 1 || j0 + TY * R >= g.ny || pfirst <= 0 || ke >= g.nz;
+#endif
     auto march = [&](auto mkc) {
       constexpr bool MK = decltype(mkc)::value;
       // per-node 1-D multiplicities m = (#1-D elements touching the node) in x, y

@@ -179,6 +179,36 @@ def test_fused_cg_deterministic(F, kind):
     assert torch.equal(xs[0], xs[1]) and torch.equal(xs[0], xs[2])
 
 
+@pytest.mark.parametrize("kind,n", [("scalar", 192), ("vector", 160), ("elastic", 128)])
+def test_fused_cg_ring_refill_race(F, kind, n):
+    """Regression: at sizes with thousands of CTAs the producer-warp vector kernel sporadically
+    read part of a warp row from a ring slot the TMA refill had already overwritten (the refill
+    lacked fence.proxy.async after observing the release; kernels_common.cuh PlaneRing::produce).
+    One fused CG iteration (x = alpha r) against textbook CG around fem_apply, repeated on the
+    captured graph and eagerly: every repeat bitwise identical and within 1e-13."""
+    g = I.rng(I.SEED_BASE + 204)
+    c = I.ncomp(kind)
+    op = F.Operator(F.Mesh(n, n, n, 1.0 / n), kind, 1)
+    if kind == "elastic":
+        lam, mu = I.materials(g, n, n, n)
+        op.set_material(dev(lam), dev(mu))
+    b = dev(I.interior_rhs(g, n, n, n, c))
+    q = op.apply(b)
+    xr = (torch.dot(b, b) / torch.dot(b, q)) * b
+    for use_graph in (1, 0):
+        op.set_option("use_graph", use_graph)
+        xs = []
+        for _ in range(6):
+            x = torch.zeros_like(b)
+            op.cg_begin(b, x, tol=0.0, maxit=1)
+            op.cg_iterate(1)
+            op.cg_end()
+            xs.append(x)
+        for x in xs:
+            assert torch.equal(x, xs[0])
+        assert float((xs[0] - xr).abs().max() / xr.abs().max()) <= 1e-13
+
+
 @pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
 def test_null_space_and_symmetry_gpu(F, kind):
     """Properties that hold at any size, checked on the GPU alone (no oracle)."""

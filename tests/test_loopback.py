@@ -204,3 +204,38 @@ def test_loopback_missing_rank_fails(F):
     with pytest.raises(F.FemError) as e:
         op.apply(x)
     assert e.value.status == F.FEM_ESTATE
+
+
+@pytest.mark.parametrize("overlap", [1, 0])
+def test_loopback_trace_timeline(F, overlap):
+    """option "trace": device timeline of an exchange apply -- halo on the comm stream, interior
+    planes on the caller's stream, then the boundary planes (SURVEY §5 tracing)."""
+    nx, ny, nz = 40, 36, 30
+    kind = "vector"
+    c = I.ncomp(kind)
+    g = I.rng(I.SEED_BASE + 620)
+    x = I.uniform_vector(g, nx, ny, nz, c)
+    comms = F.Comm.loopback(2)
+    plane = (nx + 1) * (ny + 1) * c
+
+    def rank(r, st):
+        mesh, op = _slab_op(F, comms[r], kind, nx, ny, nz, 1.0 / nx, None, None)
+        op.set_option("halo_overlap", overlap)
+        with pytest.raises(F.FemError):
+            op.get_option("trace_total_ns")  # nothing traced yet
+        op.set_option("trace", 1)
+        k0, k1 = mesh.plane_begin, mesh.plane_end
+        xl = torch.from_numpy(x[k0 * plane:k1 * plane].copy()).cuda()
+        op.apply(xl, stream=st)
+        t = {k: op.get_option("trace_%s_ns" % k) for k in ("halo", "interior", "boundary", "total")}
+        op.close(); mesh.close()
+        return t
+
+    res = _run_ranks(2, rank)
+    for cm in comms:
+        cm.close()
+    for t in res:
+        assert all(v >= 0 for v in t.values())
+        assert t["total"] > 0
+        assert t["interior"] <= t["total"] and t["halo"] <= t["total"]
+        assert t["boundary"] <= t["total"]
