@@ -211,6 +211,9 @@ struct fem_op_s {
   // done; read back as trace_{halo,interior,boundary,total}_ns (the overlap timeline)
   int trace = 0;
   cudaEvent_t tr_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // elasticity fused apply: second stream for the edge grid beside the interior grid
+  cudaStream_t astream = nullptr;
+  cudaEvent_t ev_a0 = nullptr, ev_a1 = nullptr;
   bool tr_valid = false;
   struct MapEnt {
     const void* p = nullptr;
@@ -623,6 +626,14 @@ static int launch_maps(fem_op_s* op, const Grid& g, PlaneSrc x, OutVec y, const 
                             ? launch_elastic(op->bc, g, x, y, maps, mode, op->sc, red, s, m->sm_count)
                             : launch_laplace(op->comps, op->bc, g, x, y, maps, mode, op->sc, red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "apply launch failed: %s", cudaGetErrorString(e));
+  return FEM_OK;
+}
+
+static int ensure_aux_stream(fem_op_s* op) {
+  if (op->astream) return FEM_OK;
+  CUDA_TRY(cudaStreamCreateWithFlags(&op->astream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&op->ev_a0, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&op->ev_a1, cudaEventDisableTiming));
   return FEM_OK;
 }
 
@@ -1139,6 +1150,9 @@ static void op_free(fem_op_s* op) {
   if (op->ev_join) cudaEventDestroy(op->ev_join);
   for (auto e : op->tr_ev)
     if (e) cudaEventDestroy(e);
+  if (op->astream) cudaStreamDestroy(op->astream);
+  if (op->ev_a0) cudaEventDestroy(op->ev_a0);
+  if (op->ev_a1) cudaEventDestroy(op->ev_a1);
   if (op->peer_ipc)
     for (int v = 0; v < 4; ++v) {
       if (op->nb_lo[v]) cudaIpcCloseMemHandle(op->nb_lo[v]);
@@ -1612,6 +1626,12 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
                  parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
                  op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr};
+  if (op->kind == FEM_ELASTICITY) {  // interior / edge grids of the fused apply side by side
+    FEM_TRY(ensure_aux_stream(op));
+    maps.aux = op->astream;
+    maps.ev_fork = op->ev_a0;
+    maps.ev_join = op->ev_a1;
+  }
   // the two dots per option "dot_mode" (Reduce::dot_mode; the paper's dot ablation)
   Reduce rd = op->red;
   rd.dot_mode = op->dot_mode;

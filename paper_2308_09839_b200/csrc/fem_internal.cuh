@@ -69,6 +69,10 @@ struct ApplyMaps {
   // zc_force chunks starting kchunk_force planes apart, each kspan planes long (0: automatic)
   int64_t kchunk_force = 0, kspan = 0;
   int zc_force = 0;
+  // elasticity fused apply: interior / edge CTAs as two grids (fem_api.cu passes a second stream
+  // and two events to run them concurrently; nullptr: one after the other on the same stream)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).
@@ -102,6 +106,10 @@ struct Reduce {
   // split applies (halo overlap): acc = 1 adds this launch's dots to the scalars instead of
   // writing them; roll = 0 leaves the fused-CG recurrence roll (rr = rr_new) to a later launch
   int acc = 0, roll = 1;
+  // two grids sharing one reduction (the elasticity fused apply's interior / edge grids): this
+  // grid's CTAs take partial slots boff .. boff + grid - 1 and the ticket counts btot CTAs in all
+  // (0: this grid alone)
+  int boff = 0, btot = 0;
 };
 
 constexpr int kMaxCtas = 1 << 16;
@@ -304,8 +312,8 @@ __device__ __forceinline__ bool last_block_reduce(double partial, Reduce red, do
                                                   double* total) {
   const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
   const int nthr = blockDim.x * blockDim.y * blockDim.z;
-  const unsigned int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  const unsigned int nblk = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned int bid = red.boff + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned int nblk = red.btot ? (unsigned)red.btot : gridDim.x * gridDim.y * gridDim.z;
   __shared__ unsigned int s_is_last;
   if (tid == 0) {
     red.partials[bid] = partial;
@@ -360,8 +368,8 @@ __device__ __forceinline__ bool last_block_reduce2(double a, double b, Reduce re
                                                    double* ta, double* tb) {
   const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
   const int nthr = blockDim.x * blockDim.y * blockDim.z;
-  const unsigned int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  const unsigned int nblk = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned int bid = red.boff + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned int nblk = red.btot ? (unsigned)red.btot : gridDim.x * gridDim.y * gridDim.z;
   __shared__ unsigned int s_is_last2;
   if (tid == 0) {
     red.partials[bid] = a;

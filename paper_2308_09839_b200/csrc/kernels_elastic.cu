@@ -21,6 +21,10 @@
 
 #include "kernels_common.cuh"
 
+#ifndef FEM_EL2_TWOGRID
+#define FEM_EL2_TWOGRID 1  // fused CG apply: interior (mask-free) and edge CTAs as two kernels
+#endif
+
 namespace fem {
 
 namespace {
@@ -355,13 +359,55 @@ __device__ __forceinline__ void face_corners(const double* F, int c, double& c00
 // bottom corners handed down by warp ty+1.  Per cell: 9 instead of 12 staged node values, one
 // y hand-off per two cells, the x butterflies of the shared node row computed once.  Per node the
 // summation order is the one of elastic_kernel: ((i-1,j-1)+(i,j-1)) + ((i-1,j)+(i,j)).
-template <bool TM, int MODE, int TY, int S, bool GLL, bool PAIR = false>
+// Which CTAs a launch covers (GM template parameter of elastic2_kernel): 0 the whole xt x yt x zc
+// grid (blockIdx = tile, tile, z-chunk); 1 the "interior" box [xa,xb] x [ya,yb] x [za,zb] of it
+// -- CTAs whose staged region touches no Dirichlet face, run without any mask / identity-row
+// logic; 2 its complement (the "shell"), 1-D grid, every CTA Dirichlet-aware.  1 and 2 are two
+// separately register-allocated kernels (one kernel holding both marches spills), launched
+// side by side on two streams and sharing one reduction (Reduce::boff / btot).
+struct TileMap {
+  int X, Y, Z;                    // tiles in x, y; z-chunks
+  int xa, xb, ya, yb, za, zb;     // interior box (inclusive)
+};
+__device__ __forceinline__ void tile_of_block(int GM, const TileMap& m, int& bx, int& by, int& bz) {
+  if (GM == 0) { bx = blockIdx.x; by = blockIdx.y; bz = blockIdx.z; return; }
+  if (GM == 1) { bx = m.xa + blockIdx.x; by = m.ya + blockIdx.y; bz = m.za + blockIdx.z; return; }
+  const int nxi = m.xb - m.xa + 1, nyi = m.yb - m.ya + 1, nzi = m.zb - m.za + 1;
+  const int XY = m.X * m.Y;
+  int L = blockIdx.x;
+  const int nfull = (m.Z - nzi) * XY;  // z-chunks outside [za, zb]: whole xy layers
+  if (L < nfull) {
+    const int zz = L / XY, r = L - zz * XY;
+    bz = zz < m.za ? zz : zz + nzi;
+    by = r / m.X;
+    bx = r - by * m.X;
+    return;
+  }
+  L -= nfull;
+  const int R = XY - nxi * nyi;  // ring of one z-chunk inside [za, zb]
+  bz = m.za + L / R;
+  int r = L % R;
+  const int nrow = (m.Y - nyi) * m.X;  // tile rows outside [ya, yb]: whole rows
+  if (r < nrow) {
+    const int yy = r / m.X;
+    by = yy < m.ya ? yy : yy + nyi;
+    bx = r - yy * m.X;
+    return;
+  }
+  r -= nrow;
+  const int w = m.X - nxi;
+  by = m.ya + r / w;
+  const int xx = r % w;
+  bx = xx < m.xa ? xx : xx + nxi;
+}
+
+template <bool TM, int MODE, int TY, int S, bool GLL, bool PAIR = false, int GM = 0>
 __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     elastic2_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                     TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                     const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
                     int bc, int64_t kchunk, int64_t kspan, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
-                    int txa, int tya, PairGeom pg) {
+                    int txa, int tya, PairGeom pg, TileMap tmap) {
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   constexpr int TX = 32;
@@ -392,10 +438,12 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
+  int bx, by, bz;
+  tile_of_block(GM, tmap, bx, by, bz);
   // output tile: nodes i0 .. i0+txa-1 (txa <= TX-1), j0 .. j0+tya-1 (tya <= 2TY-1)
-  const int64_t i0 = (int64_t)blockIdx.x * txa;
-  const int64_t j0 = (int64_t)blockIdx.y * tya;
-  const int64_t kb = g.k0 + (int64_t)blockIdx.z * kchunk;
+  const int64_t i0 = (int64_t)bx * txa;
+  const int64_t j0 = (int64_t)by * tya;
+  const int64_t kb = g.k0 + (int64_t)bz * kchunk;
   const int64_t ke = min(g.k1, kb + kspan);
   const int64_t pfirst = kb - 1;
   if (tid < HD * TY) {
@@ -603,7 +651,8 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
         step(t + 1, I1{});
       }
     };
-    if constexpr (MODE == 2) march(std::true_type{});
+    if constexpr (GM == 1) march(std::false_type{});
+    else if constexpr (GM == 2 || MODE == 2) march(std::true_type{});
     else if (edge) march(std::true_type{});
     else march(std::false_type{});
   }
@@ -649,6 +698,7 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   int txa, tya;
   const int64_t xt = balanced_tiles(g.nx + 1, TX - 1, &txa);
   const int64_t yt = balanced_tiles(g.ny + 1, 2 * TY - 1, &tya);
+  const TileMap tm0{(int)xt, (int)yt, 1, 0, 0, 0, 0, 0, 0};
   const int64_t nplanes = g.k1 - g.k0;
   // resident CTAs per SM at ~255 registers per thread: 65536 / (32 (TY [+1]) 255)
   constexpr int kRes = (TY + ((TM && kEl2Self) ? 0 : 1)) <= 4 ? 2 : 1;
@@ -675,8 +725,75 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   TmaOrigin org{maps.t_i0, maps.t_j0, maps.t_k0};
   PeerMaps pm;
   if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
+  const PairGeom pgeo = maps.pair ? *maps.pair : PairGeom{0, 0, 0};
+  if constexpr (TM && !PAIR) {
+    if (FEM_EL2_TWOGRID && mode == 2 && maps.kchunk_force == 0) {
+      // interior / edge grids (TileMap): per axis, the tiles whose staged region touches no
+      // Dirichlet face (the kernel's own `edge` predicate, separable per axis)
+      auto range = [](int64_t n, auto is_edge, int& lo, int& hi) {
+        lo = 0;
+        while (lo < n && is_edge(lo)) ++lo;
+        hi = (int)n - 1;
+        while (hi >= lo && is_edge(hi)) --hi;
+      };
+      int xa, xb, ya, yb, za, zb;
+      range(xt, [&](int64_t b) { const int64_t i0 = b * txa; return bc && (i0 <= 1 || i0 + TX - 1 >= g.nx); }, xa, xb);
+      range(yt, [&](int64_t b) { const int64_t j0 = b * tya; return bc && (j0 <= 1 || j0 - 1 + 2 * TY >= g.ny); }, ya, yb);
+      range(zc, [&](int64_t b) {
+        const int64_t kb = g.k0 + b * kchunk, ke = std::min(g.k1, kb + kspan);
+        return bc && (kb - 1 <= 0 || ke >= g.nz);
+      }, za, zb);
+      if (xa <= xb && ya <= yb && za <= zb) {
+        const TileMap tm{(int)xt, (int)yt, (int)zc, xa, xb, ya, yb, za, zb};
+        const int64_t n_in = (int64_t)(xb - xa + 1) * (yb - ya + 1) * (zb - za + 1);
+        const int64_t n_all = xt * yt * zc, n_edge = n_all - n_in;
+        auto pick2 = [&](auto gl, auto gm) {
+          constexpr bool G = decltype(gl)::value;
+          constexpr int M = decltype(gm)::value;
+          return elastic2_kernel<TM, 2, TY, S, G, false, M>;
+        };
+        using GI = std::integral_constant<int, 1>;
+        using GE = std::integral_constant<int, 2>;
+        auto kin = gll ? pick2(std::true_type{}, GI{}) : pick2(std::false_type{}, GI{});
+        auto ked = gll ? pick2(std::true_type{}, GE{}) : pick2(std::false_type{}, GE{});
+        for (auto k : {kin, ked}) {
+          const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(k), (int)smem);
+          if (e != cudaSuccess) return e;
+        }
+        Reduce ri = red, re = red;
+        ri.boff = 0;
+        ri.btot = (int)n_all;
+        re.boff = (int)n_in;
+        re.btot = (int)n_all;
+        const bool two = maps.aux && maps.ev_fork && maps.ev_join && n_edge > 0;
+        cudaStream_t se = two ? maps.aux : s;
+        if (two) {
+          cudaError_t e = cudaEventRecord(maps.ev_fork, s);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(maps.aux, maps.ev_fork, 0);
+          if (e != cudaSuccess) return e;
+        }
+        if (n_edge > 0) {  // the slower, Dirichlet-aware CTAs first
+          ked<<<dim3((unsigned)n_edge), block, smem, se>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold,
+                                                           maps.pnew, bc, kchunk, kspan, sc, re, pm, txa, tya, pgeo, tm);
+          add_launches(1);
+          const cudaError_t e = cudaGetLastError();
+          if (e != cudaSuccess) return e;
+        }
+        kin<<<dim3((unsigned)(xb - xa + 1), (unsigned)(yb - ya + 1), (unsigned)(zb - za + 1)), block, smem, s>>>(
+            g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew, bc, kchunk, kspan, sc, ri, pm,
+            txa, tya, pgeo, tm);
+        add_launches(1);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess && two) {
+          e = cudaEventRecord(maps.ev_join, maps.aux);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(s, maps.ev_join, 0);
+        }
+        return e;
+      }
+    }
+  }
   kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
-                                 bc, kchunk, kspan, sc, red, pm, txa, tya, maps.pair ? *maps.pair : PairGeom{0, 0, 0});
+                                 bc, kchunk, kspan, sc, red, pm, txa, tya, pgeo, tm0);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -41,7 +41,10 @@ def main():
                 if lo <= a <= hi:
                     w = s.split()
                     op = w[1] if w[0].startswith("@") else w[0]
-                    c[op.split(".")[0]] += 1
+                    k = op.split(".")[0]
+                    if k == "IMAD" and ".MOV" in op:
+                        k = "IMAD.MOV"
+                    c[k] += 1
             fp = c["DADD"] + c["DFMA"] + c["DMUL"]
             print(f"  loop [{lo:#x},{hi:#x}] {sum(c.values())}  fp64 {fp}  "
                   + " ".join(f"{k}={v}" for k, v in c.most_common(16)))
