@@ -146,6 +146,10 @@ struct fem_mesh_s {
   double4* hx_xyz = nullptr;
   int4* hx_cells = nullptr;
   int32_t* hx_bnodes = nullptr;  // constrained nodes (identity rows)
+  // deterministic scatter (option "deterministic"): node -> (cell, corner) entry CSR, ascending
+  // entries per node, built on first use
+  int32_t* hx_n2e_off = nullptr;  // [hx_nodes + 1]
+  int32_t* hx_n2e = nullptr;      // [8 hx_ncells]: cell * 8 + corner
 };
 
 struct fem_op_s {
@@ -191,6 +195,9 @@ struct fem_op_s {
   int quad = 0;      // 0: 2x2x2 Gauss-Legendre, 1: 2x2x2 Gauss-Lobatto (BP5/BP6; reading R1)
   int cg_variant = 0;  // 0: fused Hestenes-Stiefel (Table 4), 1: Chronopoulos-Gear single reduction
   int dot_mode = 0;    // fused Hestenes-Stiefel dots: 0 epilogue, 1 separate kernels, 2 atomics
+  // general hexes: deterministic scatter (element outputs + per-node gather) instead of FP64 atomics
+  int det = 0;
+  double* hx_E = nullptr;  // [ncells][8][C]
   // peer halo: the neighbour ranks' padded vectors x, p, r, p2 (CUDA IPC or, for single-process
   // tests, the other operator's buffers) and tensor maps over their ghost-plane sources
   bool peer_on = false, peer_ipc = false;
@@ -601,6 +608,25 @@ static bool fill_peer(const fem_op_s* op, const double* v, const double* v2, Pee
   return true;
 }
 
+static int ensure_aux_stream(fem_op_s* op) {
+  if (op->astream) return FEM_OK;
+  CUDA_TRY(cudaStreamCreateWithFlags(&op->astream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&op->ev_a0, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&op->ev_a1, cudaEventDisableTiming));
+  return FEM_OK;
+}
+
+// elasticity applies run as an interior and an edge grid side by side (kernels_elastic.cu,
+// TileMap): hand the launcher the operator's second stream and fork / join events
+static int with_aux(fem_op_s* op, ApplyMaps* maps) {
+  if (op->kind != FEM_ELASTICITY) return FEM_OK;
+  FEM_TRY(ensure_aux_stream(op));
+  maps->aux = op->astream;
+  maps->ev_fork = op->ev_a0;
+  maps->ev_join = op->ev_a1;
+  return FEM_OK;
+}
+
 static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* umap, int mode,
                         cudaStream_t s, const double* vsrc = nullptr, const PairGeom* pair = nullptr) {
   fem_mesh_s* m = op->mesh;
@@ -608,6 +634,7 @@ static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* u
   const bool peer = umap && vsrc && fill_peer(op, vsrc, nullptr, &pm);
   ApplyMaps maps{umap, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr,
                  op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr, pair};
+  FEM_TRY(with_aux(op, &maps));
   cudaError_t e;
   if (op->use_pa)  // partial assembly on the box (21 stored values per Gauss point, bulk-row staging)
     e = launch_pa21_apply(op->bc, op->quad, m->g, x, y, op->pa, mode, op->sc, op->red, s, m->sm_count);
@@ -622,18 +649,12 @@ static int launch_apply(fem_op_s* op, PlaneSrc x, OutVec y, const CUtensorMap* u
 static int launch_maps(fem_op_s* op, const Grid& g, PlaneSrc x, OutVec y, const ApplyMaps& maps, int mode,
                        Reduce red, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
+  ApplyMaps mm = maps;
+  FEM_TRY(with_aux(op, &mm));
   const cudaError_t e = op->kind == FEM_ELASTICITY
-                            ? launch_elastic(op->bc, g, x, y, maps, mode, op->sc, red, s, m->sm_count)
+                            ? launch_elastic(op->bc, g, x, y, mm, mode, op->sc, red, s, m->sm_count)
                             : launch_laplace(op->comps, op->bc, g, x, y, maps, mode, op->sc, red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "apply launch failed: %s", cudaGetErrorString(e));
-  return FEM_OK;
-}
-
-static int ensure_aux_stream(fem_op_s* op) {
-  if (op->astream) return FEM_OK;
-  CUDA_TRY(cudaStreamCreateWithFlags(&op->astream, cudaStreamNonBlocking));
-  CUDA_TRY(cudaEventCreateWithFlags(&op->ev_a0, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventCreateWithFlags(&op->ev_a1, cudaEventDisableTiming));
   return FEM_OK;
 }
 
@@ -735,16 +756,22 @@ static PlaneSrc pl_src(fem_op_s* op, double* v) {
 static OutVec pl_out(fem_op_s* op, double* v) { return OutVec{pl_owned(op, v), op->pl_rp, op->pl_pp}; }
 static int64_t pl_count(fem_op_s* op) { return op->nloc_planes * op->pl_pp; }  // owned range
 
-// general hex mesh: y = A_c x (zero y, element kernel with red.add scatter, identity rows)
+// general hex mesh: y = A_c x (zero y, element kernel with red.add scatter, identity rows); with
+// option "deterministic": element outputs to hx_E, then the per-node gather writes every y entry
 static int apply_hex(fem_op_s* op, const double* x, double* y, int mode, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
-  CUDA_TRY(cudaMemsetAsync(y, 0, op->n_local * sizeof(double), s));
+  double* E = op->det ? op->hx_E : nullptr;
+  if (!E) CUDA_TRY(cudaMemsetAsync(y, 0, op->n_local * sizeof(double), s));
   cudaError_t e = op->use_pa
-                      ? launch_hex_pa_apply(op->kind, op->bc, op->quad, m->hx_cells, op->pa, op->lm, x, y,
+                      ? launch_hex_pa_apply(op->kind, op->bc, op->quad, m->hx_cells, op->pa, op->lm, x, y, E,
                                             m->hx_ncells, mode, op->sc, op->red, s, m->sm_count)
-                      : launch_hex_apply(op->kind, op->bc, op->quad, m->hx_cells, m->hx_xyz, op->lm, x, y,
+                      : launch_hex_apply(op->kind, op->bc, op->quad, m->hx_cells, m->hx_xyz, op->lm, x, y, E,
                                          m->hx_ncells, mode, op->sc, op->red, s, m->sm_count);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "hex apply launch: %s", cudaGetErrorString(e));
+  if (E) {
+    e = launch_hex_gather(op->comps, m->hx_n2e_off, m->hx_n2e, E, y, m->hx_nodes, s, m->sm_count);
+    if (e != cudaSuccess) return fail(FEM_ECUDA, "hex gather launch: %s", cudaGetErrorString(e));
+  }
   if (op->bc && m->hx_nb) {
     e = launch_hex_dirichlet(m->hx_bnodes, m->hx_nb, op->comps, x, y, mode, op->sc, op->red, s, m->sm_count);
     if (e != cudaSuccess) return fail(FEM_ECUDA, "hex identity-row launch: %s", cudaGetErrorString(e));
@@ -1135,6 +1162,8 @@ void fem_mesh_destroy(fem_mesh_t m) {
     cudaFree(m->hx_xyz);
     cudaFree(m->hx_cells);
     cudaFree(m->hx_bnodes);
+    cudaFree(m->hx_n2e_off);
+    cudaFree(m->hx_n2e);
   }
   delete m;
 }
@@ -1160,6 +1189,7 @@ static void op_free(fem_op_s* op) {
     }
   cudaFree(op->lm);
   cudaFree(op->pa);
+  cudaFree(op->hx_E);
   cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
   if (op->graph1b) cudaGraphExecDestroy(op->graph1b);
   for (const auto& t : op->graphT) cudaGraphExecDestroy(t.exec);
@@ -1626,12 +1656,6 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
                  parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
                  op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr};
-  if (op->kind == FEM_ELASTICITY) {  // interior / edge grids of the fused apply side by side
-    FEM_TRY(ensure_aux_stream(op));
-    maps.aux = op->astream;
-    maps.ev_fork = op->ev_a0;
-    maps.ev_join = op->ev_a1;
-  }
   // the two dots per option "dot_mode" (Reduce::dot_mode; the paper's dot ablation)
   Reduce rd = op->red;
   rd.dot_mode = op->dot_mode;
@@ -1749,7 +1773,7 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
 static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
   const int per_iter_launches =
       (op->tm_ok && !op->use_pa) ? ((op->cg_variant == 0 && op->dot_mode == 1) ? 4 : 2)
-                : (op->mesh->hex ? 3 + ((op->bc && op->mesh->hx_nb) ? 1 : 0) : 3);
+                : (op->mesh->hex ? 3 + ((op->bc && op->mesh->hx_nb) ? 1 : 0) + (op->det ? 1 : 0) : 3);
   // loopback ranks rendezvous on the host inside every collective: not capturable, run eagerly
   const bool loop = op->mesh->comm && op->mesh->comm->loop && op->mesh->nranks > 1;
   if (op->time_apply && op->use_graph && !loop && iters > 0) {
@@ -1954,6 +1978,29 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     drop_graphs(op);
   } else if (!std::strcmp(key, "trace")) {
     op->trace = value != 0;
+  } else if (!std::strcmp(key, "deterministic")) {
+    if (!op->mesh->hex) return fail(FEM_EUNSUPPORTED, "deterministic: general hex meshes (the box kernels are atomic-free)");
+    if (op->cg_active) return fail(FEM_ESTATE, "deterministic cannot change during a CG solve");
+    FEM_TRY(set_device(op->mesh->device));
+    fem_mesh_s* m = op->mesh;
+    if (value && !m->hx_n2e) {
+      FEM_TRY(dalloc(&m->hx_n2e_off, m->hx_nodes + 1));
+      FEM_TRY(dalloc(&m->hx_n2e, 8 * m->hx_ncells));
+      const cudaError_t e = launch_hex_node_csr(m->hx_cells, m->hx_ncells, m->hx_nodes, m->hx_n2e_off, m->hx_n2e,
+                                                m->sm_count);
+      if (e != cudaSuccess) {
+        cudaFree(m->hx_n2e_off); cudaFree(m->hx_n2e);
+        m->hx_n2e_off = nullptr; m->hx_n2e = nullptr;
+        return fail(FEM_ECUDA, "node-to-cell map: %s", cudaGetErrorString(e));
+      }
+    }
+    if (value && !op->hx_E) FEM_TRY(dalloc(&op->hx_E, 8 * op->comps * m->hx_ncells));
+    if (!value && op->hx_E) {
+      cudaFree(op->hx_E);
+      op->hx_E = nullptr;
+    }
+    op->det = value != 0;
+    drop_graphs(op);
   } else if (!std::strcmp(key, "halo_overlap")) {
     op->overlap = value != 0;
     drop_graphs(op);
@@ -2002,6 +2049,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "dot_mode")) *value = op->dot_mode;
   else if (!std::strcmp(key, "halo_overlap")) *value = op->overlap;
   else if (!std::strcmp(key, "trace")) *value = op->trace;
+  else if (!std::strcmp(key, "deterministic")) *value = op->mesh->hex ? op->det : 1;
   else if (!std::strncmp(key, "trace_", 6)) {
     // trace_{halo,interior,boundary,total}_ns of the last traced exchange apply (blocks on it)
     static const char* names[4] = {"trace_halo_ns", "trace_interior_ns", "trace_boundary_ns", "trace_total_ns"};

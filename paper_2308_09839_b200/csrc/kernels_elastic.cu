@@ -726,8 +726,8 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   PeerMaps pm;
   if (maps.peer && maps.peer->on) pm = *maps.peer; else { std::memset(&pm, 0, sizeof(pm)); pm.klo = pm.khi = -(int64_t(1) << 62); }
   const PairGeom pgeo = maps.pair ? *maps.pair : PairGeom{0, 0, 0};
-  if constexpr (TM && !PAIR) {
-    if (FEM_EL2_TWOGRID && mode == 2 && maps.kchunk_force == 0) {
+  if constexpr (TM) {
+    if (FEM_EL2_TWOGRID && maps.kchunk_force == 0) {
       // interior / edge grids (TileMap): per axis, the tiles whose staged region touches no
       // Dirichlet face (the kernel's own `edge` predicate, separable per axis)
       auto range = [](int64_t n, auto is_edge, int& lo, int& hi) {
@@ -750,7 +750,12 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
         auto pick2 = [&](auto gl, auto gm) {
           constexpr bool G = decltype(gl)::value;
           constexpr int M = decltype(gm)::value;
-          return elastic2_kernel<TM, 2, TY, S, G, false, M>;
+          if constexpr (PAIR) return elastic2_kernel<TM, 0, TY, S, G, true, M>;
+          else
+            return mode == 3 ? elastic2_kernel<TM, 3, TY, S, G, false, M>
+                 : mode == 2 ? elastic2_kernel<TM, 2, TY, S, G, false, M>
+                 : mode == 1 ? elastic2_kernel<TM, 1, TY, S, G, false, M>
+                             : elastic2_kernel<TM, 0, TY, S, G, false, M>;
         };
         using GI = std::integral_constant<int, 1>;
         using GE = std::integral_constant<int, 2>;
