@@ -264,6 +264,8 @@ def run_native(args, cfg):
     op = fem.Operator(mesh, kind, "dirichlet")
     if args.pa:  # partial assembly (Table 3): hex -- stored geometry; box elasticity --
         op.set_option("partial_assembly", 1)  # 21 values per Gauss point, D_q = w det J C_e
+    if args.det and hexmesh:  # general hexes: no FP64 atomics, bitwise reproducible
+        op.set_option("deterministic", 1)
     if args.gll:  # Gauss-Lobatto quadrature: the BP5 / BP6 operators (reading R1)
         op.set_option("quadrature", 1)
     if args.cgcg:  # Chronopoulos-Gear single-reduction CG (NEXT #1)
@@ -668,6 +670,8 @@ def main():
                     help="how the fused CG forms p.Ap and r.r (option dot_mode; P:714-728 ablation)")
     ap.add_argument("--gll", action="store_true",
                     help="2x2x2 Gauss-Lobatto quadrature (the CEED BP5/BP6 operators) instead of Gauss")
+    ap.add_argument("--det", action="store_true",
+                    help="general-hex configs (6/7): deterministic scatter (element outputs + node gather)")
     ap.add_argument("--pa", action="store_true",
                     help="general-hex configs (6/7): partial assembly instead of matrix-free")
     args = ap.parse_args()
@@ -679,6 +683,8 @@ def main():
         cfg["name"] += f"_n{args.n}"
     if args.pa:
         cfg["name"] += "_pa"
+    if args.det:
+        cfg["name"] += "_det"
     if args.gll:
         cfg["name"] += "_gll"
     if args.cgcg:

@@ -219,7 +219,12 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * varies from run to run); TMA path, cg_variant 0 only), "halo_overlap" (1, default: with an
  * exchange step -- nranks > 1 without peer_halo -- the halo runs on a library stream while the
  * interior node planes are applied, then the two boundary planes; 0: halo, then one apply),
- * "trace" (1: CUDA timing events around the halo, the interior and the boundary launches of
+ * "deterministic" (general hex meshes: 1 replaces
+ * the FP64 atomic scatter by element outputs E[cell][8][C] and a per-node gather over the node's
+ * (cell, corner) entries in ascending order -- bitwise reproducible results run after run, at
+ * 24 C extra bytes of traffic per cell each way; the node map is built on the first switch-on;
+ * box operators read back 1, their kernels are atomic-free, and reject the setting with
+ * FEM_EUNSUPPORTED), "trace" (1: CUDA timing events around the halo, the interior and the boundary launches of
  * every eager exchange apply; read back, blocking on the last traced apply, as the read-only
  * "trace_halo_ns", "trace_interior_ns", "trace_boundary_ns", "trace_total_ns" -- the
  * halo / interior overlap timeline; FEM_ESTATE before the first traced apply; host-side NVTX

@@ -213,16 +213,22 @@ cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const 
 // order, bit 31 = Dirichlet node), xyz = node coordinates (w unused), lm = (lambda, mu) per cell.
 // mode 0: y += A (P x) at unconstrained nodes (y zeroed by the caller); mode 1: + sc->pq = the
 // sum of the element energies (P x)^T A (P x).
+// E != nullptr: deterministic scatter -- element outputs E[cell][8][C] instead of FP64 atomics
+// into y, then launch_hex_gather sums them per node (node -> entry CSR of launch_hex_node_csr)
 cudaError_t launch_hex_apply(int kind, int bc, int quad, const int4* cells, const double4* xyz, const double2* lm,
-                             const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
+                             const double* x, double* y, double* E, int64_t ncells, int mode, CgScalars* sc,
                              Reduce red, cudaStream_t s, int sm_count);
+cudaError_t launch_hex_node_csr(const int4* cells, int64_t ncells, int64_t nnodes, int32_t* off, int32_t* list,
+                                int sm_count);
+cudaError_t launch_hex_gather(int comps, const int32_t* off, const int32_t* list, const double* E, double* y,
+                              int64_t nnodes, cudaStream_t s, int sm_count);
 // partial assembly on general hex meshes: per-Gauss-point geometry stored once (setup), then
 // applied without recomputing J (Laplace kinds share the 6-value D'; elasticity 9-value B)
 int64_t hex_pa_doubles(int kind, int64_t ncells);
 cudaError_t launch_hex_pa_setup(int kind, int quad, const int4* cells, const double4* xyz, double* pa,
                                 int64_t ncells, cudaStream_t s, int sm_count);
 cudaError_t launch_hex_pa_apply(int kind, int bc, int quad, const int4* cells, const double* pa, const double2* lm,
-                                const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
+                                const double* x, double* y, double* E, int64_t ncells, int mode, CgScalars* sc,
                                 Reduce red, cudaStream_t s, int sm_count);
 // partial assembly on the box (kernels_pa.cu): 21 values per Gauss point and cell,
 // D_q = w_q det J_q C_e (Voigt, upper triangle), SoA [q][k][cell]

@@ -21,6 +21,8 @@
 // grad^ phi_a carries 1/8: v_a = (1/512) sum_q sum_e (sigma cof J')_{ce} s_ae prod(1 + ..g).
 #include <algorithm>
 
+#include <cub/cub.cuh>
+
 #include "fem_internal.cuh"
 
 namespace fem {
@@ -159,7 +161,8 @@ template <int KIND, int MODE, bool GLL>
 __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
     hex_apply_kernel(const int4* __restrict__ cells, const double4* __restrict__ xyz,
                      const double2* __restrict__ lm, const double* __restrict__ u,
-                     double* __restrict__ y, int64_t ncells, int bc, CgScalars* sc, Reduce red) {
+                     double* __restrict__ y, double* __restrict__ E, int64_t ncells, int bc, CgScalars* sc,
+                     Reduce red) {
   constexpr int C = (KIND == 0) ? 1 : 3;
   __shared__ double red_sh[32];
   if (MODE >= 1 && sc->done) return;
@@ -222,9 +225,14 @@ __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
       m.xy *= g * kInv512; m.xz *= g * kInv512; m.yz *= g * kInv512; m.xyz *= g2 * kInv512;
       double v[8];
       inverse(m, v);
+      if (E) {  // deterministic scatter: element outputs, summed per node by hex_gather_kernel
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
-        if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+        for (int a = 0; a < 8; ++a) E[((int64_t)e * 8 + a) * C + c] = fix[a] ? 0.0 : v[a];
+      } else {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+      }
     }
   }
   if (MODE >= 1) {  // p.Ap of the masked operator part: sum of the element energies
@@ -259,7 +267,8 @@ template <int KIND, int MODE, bool GLL>
 __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
     hex_apply_pf_kernel(const int4* __restrict__ cells, const double4* __restrict__ xyz,
                         const double2* __restrict__ lm, const double* __restrict__ u,
-                        double* __restrict__ y, int64_t ncells, int bc, CgScalars* sc, Reduce red) {
+                        double* __restrict__ y, double* __restrict__ E, int64_t ncells, int bc, CgScalars* sc,
+                        Reduce red) {
   constexpr int C = (KIND == 0) ? 1 : 3;
   constexpr int T = kHexThreads;
   __shared__ double red_sh[32];
@@ -358,9 +367,14 @@ __global__ void __launch_bounds__(kHexThreads, (KIND == 0) ? 3 : 2)
       m.xy *= g * kInv512; m.xz *= g * kInv512; m.yz *= g * kInv512; m.xyz *= g2 * kInv512;
       double v[8];
       inverse(m, v);
+      if (E) {  // deterministic scatter: element outputs, summed per node by hex_gather_kernel
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
-        if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+        for (int a = 0; a < 8; ++a) E[((int64_t)e * 8 + a) * C + c] = fix[a] ? 0.0 : v[a];
+      } else {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+      }
     }
   }
   hex_wait_all();
@@ -574,7 +588,8 @@ template <int KIND, int MODE, bool GLL>
 __global__ void __launch_bounds__(128, (KIND == 0) ? 4 : 2)
     hex_pa_apply_kernel(const int4* __restrict__ cells, const double* __restrict__ pa,
                         const double2* __restrict__ lm, const double* __restrict__ u,
-                        double* __restrict__ y, int64_t ncells, int bc, CgScalars* sc, Reduce red) {
+                        double* __restrict__ y, double* __restrict__ E, int64_t ncells, int bc, CgScalars* sc,
+                        Reduce red) {
   constexpr int C = (KIND == 0) ? 1 : 3;
   constexpr int K = (KIND == 2) ? 9 : 6;
   __shared__ double red_sh[32];
@@ -626,9 +641,14 @@ __global__ void __launch_bounds__(128, (KIND == 0) ? 4 : 2)
       m.xy *= g * kInv512; m.xz *= g * kInv512; m.yz *= g * kInv512; m.xyz *= g2 * kInv512;
       double v[8];
       inverse(m, v);
+      if (E) {  // deterministic scatter: element outputs, summed per node by hex_gather_kernel
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
-        if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+        for (int a = 0; a < 8; ++a) E[((int64_t)e * 8 + a) * C + c] = fix[a] ? 0.0 : v[a];
+      } else {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          if (!fix[a]) atomicAdd(y + (int64_t)C * id[a] + c, v[a]);
+      }
     }
   }
   if (MODE >= 1) {
@@ -645,7 +665,7 @@ int grid_for(int64_t n, int threads, int sm_count, int per_sm) {
 }  // namespace
 
 cudaError_t launch_hex_apply(int kind, int bc, int quad, const int4* cells, const double4* xyz, const double2* lm,
-                             const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
+                             const double* x, double* y, double* E, int64_t ncells, int mode, CgScalars* sc,
                              Reduce red, cudaStream_t s, int sm_count) {
   if (ncells <= 0) return cudaSuccess;
   // measured: the pipelined kernel wins for the elasticity CG apply (2.87 ->
@@ -663,7 +683,7 @@ cudaError_t launch_hex_apply(int kind, int bc, int quad, const int4* cells, cons
                                              (int)sm);                                                    \
       if (e != cudaSuccess) return e;                                                                     \
     }                                                                                                     \
-    hex_apply_pf_kernel<K, M, G><<<grid, kHexThreads, sm, s>>>(cells, xyz, lm, x, y, ncells, bc, sc, red); \
+    hex_apply_pf_kernel<K, M, G><<<grid, kHexThreads, sm, s>>>(cells, xyz, lm, x, y, E, ncells, bc, sc, red); \
   }
 #define PF_LAUNCH2(K, M) { if (quad == 1) PF_LAUNCH(K, M, true) else PF_LAUNCH(K, M, false) }
     if (kind == 0) { if (mode) PF_LAUNCH2(0, 1) else PF_LAUNCH2(0, 0) }
@@ -676,7 +696,7 @@ cudaError_t launch_hex_apply(int kind, int bc, int quad, const int4* cells, cons
   }
   const int grid = grid_for(ncells, kHexThreads, sm_count, 8);
   if (mode >= 1 && grid > red.capacity) return cudaErrorInvalidConfiguration;
-#define HEX_LAUNCH(K, M, G) hex_apply_kernel<K, M, G><<<grid, kHexThreads, 0, s>>>(cells, xyz, lm, x, y, ncells, bc, sc, red)
+#define HEX_LAUNCH(K, M, G) hex_apply_kernel<K, M, G><<<grid, kHexThreads, 0, s>>>(cells, xyz, lm, x, y, E, ncells, bc, sc, red)
 #define HEX_LAUNCH2(K, M) { if (quad == 1) HEX_LAUNCH(K, M, true); else HEX_LAUNCH(K, M, false); }
   if (kind == 0) { if (mode) HEX_LAUNCH2(0, 1) else HEX_LAUNCH2(0, 0) }
   else if (kind == 1) { if (mode) HEX_LAUNCH2(1, 1) else HEX_LAUNCH2(1, 0) }
@@ -704,12 +724,12 @@ cudaError_t launch_hex_pa_setup(int kind, int quad, const int4* cells, const dou
 }
 
 cudaError_t launch_hex_pa_apply(int kind, int bc, int quad, const int4* cells, const double* pa, const double2* lm,
-                                const double* x, double* y, int64_t ncells, int mode, CgScalars* sc,
+                                const double* x, double* y, double* E, int64_t ncells, int mode, CgScalars* sc,
                                 Reduce red, cudaStream_t s, int sm_count) {
   if (ncells <= 0) return cudaSuccess;
   const int grid = grid_for(ncells, 128, sm_count, 8);
   if (mode >= 1 && grid > red.capacity) return cudaErrorInvalidConfiguration;
-#define PA_LAUNCH(K, M, G) hex_pa_apply_kernel<K, M, G><<<grid, 128, 0, s>>>(cells, pa, lm, x, y, ncells, bc, sc, red)
+#define PA_LAUNCH(K, M, G) hex_pa_apply_kernel<K, M, G><<<grid, 128, 0, s>>>(cells, pa, lm, x, y, E, ncells, bc, sc, red)
 #define PA_LAUNCH2(K, M) { if (quad == 1) PA_LAUNCH(K, M, true); else PA_LAUNCH(K, M, false); }
   if (kind == 0) { if (mode) PA_LAUNCH2(0, 1) else PA_LAUNCH2(0, 0) }
   else if (kind == 1) { if (mode) PA_LAUNCH2(1, 1) else PA_LAUNCH2(1, 0) }
@@ -740,6 +760,95 @@ cudaError_t launch_hex_check(const int4* cells, const double4* xyz, int64_t ncel
 cudaError_t launch_hex_pack_cells(const int32_t* vtk, const uint8_t* dir, int64_t ncells, int64_t nnodes,
                                   int* out, unsigned long long* bad, cudaStream_t s, int sm_count) {
   hex_pack_cells_kernel<<<grid_for(ncells * 8, 256, sm_count, 8), 256, 0, s>>>(vtk, dir, ncells, nnodes, out, bad);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+// ---- deterministic scatter (option "deterministic") ---------------------------
+// The apply kernels write every cell's 8 x C element outputs to E[cell][corner][comp]; one thread
+// per node then sums the entries of its incident (cell, corner) pairs in ascending entry order
+// (node -> entry CSR built once per mesh by a stable radix sort), so the result is independent of
+// the launch configuration and of the run: no floating-point atomics.
+template <int C>
+__global__ void __launch_bounds__(256) hex_gather_kernel(const int32_t* __restrict__ off,
+                                                         const int32_t* __restrict__ list,
+                                                         const double* __restrict__ E, double* __restrict__ y,
+                                                         int64_t nnodes) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nnodes; n += stride) {
+    double acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0.0;
+    const int32_t b = off[n], e = off[n + 1];
+    for (int32_t k = b; k < e; ++k) {
+      const double* src = E + (int64_t)list[k] * C;
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] += src[c];
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) y[n * C + c] = acc[c];
+  }
+}
+
+__global__ void hex_entry_keys_kernel(const int4* __restrict__ cells, int64_t ncells, int32_t* __restrict__ key,
+                                      int32_t* __restrict__ val) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncells * 8; i += stride) {
+    const int* c = reinterpret_cast<const int*>(cells);
+    key[i] = c[i] & 0x7fffffff;  // node of (cell i / 8, corner i % 8)
+    val[i] = (int32_t)i;
+  }
+}
+
+// off[n] = first sorted entry of node n (keys sorted ascending), off[nnodes] = n_entries; nodes
+// without entries get an empty range
+__global__ void hex_entry_offsets_kernel(const int32_t* __restrict__ key, int64_t n_entries, int64_t nnodes,
+                                         int32_t* __restrict__ off) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n_entries; i += stride) {
+    const int64_t prev = (i == 0) ? -1 : key[i - 1];
+    const int64_t cur = (i == n_entries) ? nnodes : key[i];
+    for (int64_t n = prev + 1; n <= cur; ++n) off[n] = (int32_t)i;
+  }
+}
+
+cudaError_t launch_hex_node_csr(const int4* cells, int64_t ncells, int64_t nnodes, int32_t* off, int32_t* list,
+                                int sm_count) {
+  const int64_t n = ncells * 8;
+  if (n > 0x7fffffffLL) return cudaErrorInvalidValue;
+  int32_t *k0 = nullptr, *k1 = nullptr, *v0 = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e = cudaMalloc(&k0, n * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&k1, n * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&v0, n * sizeof(int32_t));
+  if (e == cudaSuccess) {
+    hex_entry_keys_kernel<<<grid_for(n, 256, sm_count, 8), 256>>>(cells, ncells, k0, v0);
+    add_launches(1);
+    e = cudaGetLastError();
+  }
+  int end_bit = 1;
+  while (end_bit < 31 && (int64_t(1) << end_bit) < nnodes) ++end_bit;
+  if (e == cudaSuccess)  // stable LSD radix sort: equal nodes keep ascending entry order
+    e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, v0, list, (int)n, 0, end_bit);
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes);
+  if (e == cudaSuccess) e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, list, (int)n, 0, end_bit);
+  if (e == cudaSuccess) {
+    hex_entry_offsets_kernel<<<grid_for(n + 1, 256, sm_count, 8), 256>>>(k1, n, nnodes, off);
+    add_launches(1);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(k0); cudaFree(k1); cudaFree(v0); cudaFree(tmp);
+  return e;
+}
+
+cudaError_t launch_hex_gather(int comps, const int32_t* off, const int32_t* list, const double* E, double* y,
+                              int64_t nnodes, cudaStream_t s, int sm_count) {
+  if (nnodes <= 0) return cudaSuccess;
+  const int grid = grid_for(nnodes, 256, sm_count, 8);
+  if (comps == 1) hex_gather_kernel<1><<<grid, 256, 0, s>>>(off, list, E, y, nnodes);
+  else hex_gather_kernel<3><<<grid, 256, 0, s>>>(off, list, E, y, nnodes);
   add_launches(1);
   return cudaGetLastError();
 }

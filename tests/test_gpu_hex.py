@@ -262,3 +262,48 @@ def test_box_partial_assembly_cg(F, oracle):
     info = op.cg_solve(dev(b), x, tol=1e-14, maxit=3000)
     assert info["converged"] and abs(info["iterations"] - ref.iterations) <= 3
     assert np.abs(x.cpu().numpy() - ref.x).max() <= 1e-10 * max(1.0, np.abs(ref.x).max())
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("pa", [0, 1])
+def test_hex_deterministic_scatter(F, oracle, kind, bc, pa):
+    """option "deterministic": element outputs + per-node gather in ascending (cell, corner) order
+    instead of FP64 atomics -- oracle parity as before, and bitwise identical applies and CG
+    iterates run after run (the atomic scatter's summation order varies)."""
+    coords, cells, bnd, lam, mu = make((17, 9, 6), 0.2, True, 3)
+    c = I.ncomp(kind)
+    x = np.random.default_rng(31).uniform(-1, 1, coords.shape[0] * c)
+    ref = oracle.apply_hex(kind, coords, cells, x, bnd if bc else None, lam, mu)
+    op = F.Operator(F.HexMesh(dev(coords), dev(cells), dev(bnd)), kind, bc)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    if pa:
+        op.set_option("partial_assembly", 1)
+    assert op.get_option("deterministic") == 0
+    y_atomic = op.apply(dev(x))
+    op.set_option("deterministic", 1)
+    assert op.get_option("deterministic") == 1
+    ys = [op.apply(dev(x)) for _ in range(3)]
+    for y in ys[1:]:
+        assert torch.equal(y, ys[0])
+    assert relerr(ys[0].cpu().numpy(), ref) <= APPLY_TOL
+    assert float((ys[0] - y_atomic).abs().max() / y_atomic.abs().max()) <= 1e-14
+    if bc:
+        b = np.random.default_rng(32).uniform(-1, 1, coords.shape[0] * c)
+        b[np.repeat(bnd == 1, c)] = 0.0
+        xs = []
+        for _ in range(2):
+            xg = torch.zeros(b.size, dtype=torch.float64, device="cuda")
+            op.cg_solve(dev(b), xg, tol=0.0, maxit=40)
+            xs.append(xg)
+        assert torch.equal(xs[0], xs[1])
+    op.set_option("deterministic", 0)
+    assert op.get_option("deterministic") == 0
+
+
+def test_hex_deterministic_box_only_option(F):
+    op = F.Operator(F.Mesh(4, 4, 4, 0.25), "scalar", 1)
+    assert op.get_option("deterministic") == 1  # the box kernels are atomic-free
+    with pytest.raises(F.FemError):
+        op.set_option("deterministic", 1)
