@@ -21,6 +21,9 @@
 
 #include "kernels_common.cuh"
 
+#ifndef FEM_EL2_REFILL2
+#define FEM_EL2_REFILL2 1  // elastic2_kernel: warp 0 refills two ring slots every other plane
+#endif
 #ifndef FEM_EL2_TWOGRID
 #define FEM_EL2_TWOGRID 1  // fused CG apply: interior (mask-free) and edge CTAs as two kernels
 #endif
@@ -553,7 +556,21 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
           fB[c] = Face{s1 + s2, s2 - s1, d1 + d2, d2 - d1};
         }
         ring.release(slot, tx);
-        if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
+        if (FEM_EL2_REFILL2) {
+          // refill two slots every other plane (odd t: planes t-1+S and t+S) -- warp 0, the last
+          // warp through every plane and hence the one pacing the CTA, pays the refill block
+          // (wait, fence, expect-tx, 2-3 TMA issues) half as often
+          if (SELF && ty == 0 && (t & 1) && t - 1 + S < nplane) {
+            ring.wait_released(t);  // (warp 0 releases in order: plane t-1 is released too)
+            if (tx == 0) {
+              fence_proxy_async();  // every warp's generic reads of the slots before the TMA writes
+              ring.issue_tm(t - 1 + S, pfirst + t - 1 + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0,
+                            &peer);
+              if (t + S < nplane)
+                ring.issue_tm(t + S, pfirst + t + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0, &peer);
+            }
+          }
+        } else if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
           ring.wait_released(t);
           if (tx == 0) {
             fence_proxy_async();  // every warp's generic reads of the slot before the TMA write
