@@ -237,6 +237,7 @@ struct fem_op_s {
     int iters = 0, parity = 0;
   };
   std::vector<TimedGraph> graphT;  // up to 4 (iteration count, parity) shapes
+  std::vector<TimedGraph> graphK;  // plain graphs of exactly k iterations (k <= 64), up to 6 shapes
 };
 
 struct fem_csr_s {
@@ -1193,6 +1194,7 @@ static void op_free(fem_op_s* op) {
   cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
   if (op->graph1b) cudaGraphExecDestroy(op->graph1b);
   for (const auto& t : op->graphT) cudaGraphExecDestroy(t.exec);
+  for (const auto& t : op->graphK) cudaGraphExecDestroy(t.exec);
   cudaFree(op->ghost_lo); cudaFree(op->ghost_hi);
   cudaFree(op->stage_a); cudaFree(op->stage_b);
   cudaFree(op->sc); cudaFree(op->dot_dev); cudaFree(op->bad);
@@ -1803,22 +1805,32 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
     }
     return FEM_OK;
   }
-  const int N = 8;  // even: a graph of N iterations starts and ends on parity 0
-  if (!op->graph1) FEM_TRY(capture(op, 1, 0, s, &op->graph1));
-  if (!op->graph1b) FEM_TRY(capture(op, 1, 1, s, &op->graph1b));
-  if (iters >= N && !op->graphN) FEM_TRY(capture(op, N, 0, s, &op->graphN));
+  // plain graphs of exactly k iterations (k <= 64; longer runs replay the 64-iteration graph),
+  // cached per (k, parity): a K-step call is one or a few graph launches, so small problems pay
+  // one launch latency per call instead of one per 8 iterations
+  constexpr int KMAX = 64;
+  auto launch_k = [&](int k) -> int {
+    cudaGraphExec_t ge = nullptr;
+    for (const auto& t : op->graphK)
+      if (t.iters == k && t.parity == op->cg_parity) ge = t.exec;
+    if (!ge) {
+      if (op->graphK.size() >= 6) {
+        cudaGraphExecDestroy(op->graphK.front().exec);
+        op->graphK.erase(op->graphK.begin());
+      }
+      FEM_TRY(capture(op, k, op->cg_parity, s, &ge));
+      op->graphK.push_back({ge, k, op->cg_parity});
+    }
+    CUDA_TRY(cudaGraphLaunch(ge, s));
+    add_launches((int64_t)k * per_iter_launches);
+    op->cg_parity ^= (k & 1);
+    return FEM_OK;
+  };
   int left = iters;
   while (left > 0) {
-    if (op->cg_parity == 0 && left >= N) {
-      CUDA_TRY(cudaGraphLaunch(op->graphN, s));
-      add_launches(N * per_iter_launches);
-      left -= N;
-    } else {
-      CUDA_TRY(cudaGraphLaunch(op->cg_parity ? op->graph1b : op->graph1, s));
-      add_launches(per_iter_launches);
-      op->cg_parity ^= 1;
-      --left;
-    }
+    const int k = std::min(left, KMAX);
+    FEM_TRY(launch_k(k));
+    left -= k;
   }
   return FEM_OK;
 }
@@ -1937,6 +1949,8 @@ static void drop_graphs(fem_op_s* op) {
     }
   for (const auto& t : op->graphT) cudaGraphExecDestroy(t.exec);
   op->graphT.clear();
+  for (const auto& t : op->graphK) cudaGraphExecDestroy(t.exec);
+  op->graphK.clear();
 }
 
 

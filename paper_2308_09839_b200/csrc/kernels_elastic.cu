@@ -24,6 +24,9 @@
 #ifndef FEM_EL2_REFILL2
 #define FEM_EL2_REFILL2 1  // elastic2_kernel: warp 0 refills two ring slots every other plane
 #endif
+#ifndef FEM_EL2_ZFACE
+#define FEM_EL2_ZFACE 1  // interior grid: z-face chunks with interior x/y tiles, mask-free except the face plane
+#endif
 #ifndef FEM_EL2_TWOGRID
 #define FEM_EL2_TWOGRID 1  // fused CG apply: interior (mask-free) and edge CTAs as two kernels
 #endif
@@ -498,8 +501,13 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
       const bool mr2 = MK && bc && (cj + 2 == 0 || cj + 2 == g.ny);
       const bool bnA_xy = MK && bc && (ci == 0 || ci == g.nx || nA == 0 || nA == g.ny);
       const bool bnB_xy = MK && bc && (ci == 0 || ci == g.nx || nB == 0 || nB == g.ny);
-      const int qface0 = (MK && bc) ? (int)(0 - kb) : -1000000;
-      const int qface1 = (MK && bc) ? (int)(g.nz - kb) : -1000000;
+      // ZF: the mask-free march of the interior grid also covers CTAs whose z-chunk touches a
+      // z face (their x/y tiles are interior): per plane a uniform check zeroes a face plane's
+      // staged values and makes the face plane's outputs identity rows
+      constexpr bool ZF = !MK && GM == 1 && FEM_EL2_ZFACE;
+      constexpr bool MZ = MK || ZF;
+      const int qface0 = (MZ && bc) ? (int)(0 - kb) : -1000000;
+      const int qface1 = (MZ && bc) ? (int)(g.nz - kb) : -1000000;
 
       // loop state in two register sets (ping-pong: the z-march is unrolled by two, so nothing is
       // moved at the back edge): faces of cells A, B at a node plane, carried top faces, the node
@@ -541,6 +549,9 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
           }
           xA[c] = a01;  // node (ci, nA), unmasked
           xB[c] = a02;  // node (ci, nB)
+          if (ZF && bc && (pl == 0 || pl == g.nz)) {  // a z-face plane: all its nodes are masked
+            a00 = 0.0; a10 = 0.0; a01 = 0.0; a11 = 0.0; a02 = 0.0; a12 = 0.0;
+          }
           if (MK && bc && (m00 || m10 || m01 || m11 || m02 || m12)) {
             a00 = m00 ? 0.0 : a00;
             a10 = m10 ? 0.0 : a10;
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
         for (int c = 0; c < 3; ++c) {
           double vv = v[c];
           const double xv = xs[c];
-          if (MK && bnode) vv = xv;
+          if (MZ && bnode) vv = xv;
           yq[c] = vv;
           if (mode == 2) pq_new[c] = xv;
           if (mode >= 1) pq = fma(vv, xv, pq);
@@ -643,7 +654,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
             __syncwarp();
             if (tx == 0) mbar_arrive_a(tfw0 + 8u * TY * b);
           }
-          const bool qf = MK && (qo == qface0 || qo == qface1);
+          const bool qf = MZ && (qo == qface0 || qo == qface1);
           if (ownA) put(yp, pnb, vA, xs_A, bnA_xy || qf);
           if (ty < TY - 1) {
             mbar_wait_a(tfr0 + 8u * TY * b, n & 1);
@@ -756,9 +767,9 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
       int xa, xb, ya, yb, za, zb;
       range(xt, [&](int64_t b) { const int64_t i0 = b * txa; return bc && (i0 <= 1 || i0 + TX - 1 >= g.nx); }, xa, xb);
       range(yt, [&](int64_t b) { const int64_t j0 = b * tya; return bc && (j0 <= 1 || j0 - 1 + 2 * TY >= g.ny); }, ya, yb);
-      range(zc, [&](int64_t b) {
+      range(zc, [&](int64_t b) {  // (FEM_EL2_ZFACE: the interior kernel handles the z faces)
         const int64_t kb = g.k0 + b * kchunk, ke = std::min(g.k1, kb + kspan);
-        return bc && (kb - 1 <= 0 || ke >= g.nz);
+        return !FEM_EL2_ZFACE && bc && (kb - 1 <= 0 || ke >= g.nz);
       }, za, zb);
       if (xa <= xb && ya <= yb && za <= zb) {
         const TileMap tm{(int)xt, (int)yt, (int)zc, xa, xb, ya, yb, za, zb};

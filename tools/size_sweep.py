@@ -1,9 +1,10 @@
 #!/usr/bin/env python
 """Size sweep (SURVEY §8(d) "locates where peak is reached").
 
-For each kind and cube size: operator-only GDOF/s (fem_apply on caller vectors, dense layout)
-and CG-iteration GDOF/s (fused CG, CUDA graphs), CUDA events on the launching stream, one JSON
-line per point.  Working sets below 2x L2 are flagged "l2_resident" (not an HBM number).
+For each kind and cube size: operator-only GDOF/s (fem_apply on caller vectors, dense layout;
+issued from the host per call, and replayed from one captured CUDA graph -- the GPU-side time
+without the per-call host cost) and CG-iteration GDOF/s (fused CG, CUDA graphs), CUDA events on
+the launching stream, one JSON line per point.  Working sets below 2x L2 are flagged "l2_resident" (not an HBM number).
 
     python tools/size_sweep.py [--kinds scalar,vector,elastic] [--out FILE]
 """
@@ -62,6 +63,18 @@ def main():
                 op.apply(x, y)
             reps = max(5, min(200, int(2e9 / max(ndof, 1) / 8)))
             t_apply = events(lambda: op.apply(x, y), reps)
+            # the same applies replayed from one captured CUDA graph: GPU time per apply without
+            # the host's per-call cost (ctypes, argument checks, pointer query, launch)
+            gs = torch.cuda.Stream()
+            gs.wait_stream(s)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=gs):
+                for _ in range(20):
+                    op.apply(x, y, stream=gs)
+            torch.cuda.synchronize()
+            graph.replay()
+            t_graph = events(lambda: graph.replay(), max(2, reps // 20)) / 20
+            del graph
             b = torch.from_numpy(I.interior_rhs(g, n, n, n, I.ncomp(kind))).cuda()
             xs = torch.zeros_like(b)
             op.cg_begin(b, xs, tol=0.0, maxit=1 << 30)
@@ -70,7 +83,7 @@ def main():
             t_cg = events(lambda: op.cg_iterate(its), 1) / its
             op.cg_end()
             ws_bytes = 5 * ndof * 8 + (16 * n ** 3 if kind == "elastic" else 0)
-            line = {"kind": kind, "cells": n, "ndof": ndof, "apply_ms": t_apply,
+            line = {"kind": kind, "cells": n, "ndof": ndof, "apply_ms": t_apply, "apply_graph_ms": t_graph,
                     "apply_gdofs": ndof / t_apply / 1e6, "cg_iter_ms": t_cg,
                     "cg_gdofs": ndof / t_cg / 1e6, "fused_cg": op.get_option("fused_cg"),
                     "l2_resident": ws_bytes < 2 * l2}
