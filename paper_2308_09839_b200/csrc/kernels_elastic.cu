@@ -24,6 +24,9 @@
 #ifndef FEM_EL2_REFILL2
 #define FEM_EL2_REFILL2 1  // elastic2_kernel: warp 0 refills two ring slots every other plane
 #endif
+#ifndef FEM_EL2_HD
+#define FEM_EL2_HD 4  // y hand-off ring depth of elastic2_kernel when shared memory allows (4 or 8)
+#endif
 #ifndef FEM_EL2_ZFACE
 #define FEM_EL2_ZFACE 1  // interior grid: z-face chunks with interior x/y tiles, mask-free except the face plane
 #endif
@@ -349,7 +352,9 @@ __device__ __forceinline__ void elastic_layer(const Face* fb, const Face* ft, do
 // plane ring (227 KB per CTA), else 2 (the 8-stage row-pair ring of fem_apply)
 template <int TY, size_t RING>
 constexpr int el2_handoff_depth() {
-  return RING + 4ull * TY * (32 * kEl2HW * sizeof(double) + 2 * sizeof(uint64_t)) + 1024 <= 232448 ? 4 : 2;
+  constexpr size_t per = (size_t)TY * (32 * kEl2HW * sizeof(double) + 2 * sizeof(uint64_t));
+  return (FEM_EL2_HD >= 8 && RING + 8 * per + 1024 <= 232448) ? 8
+       : (RING + 4 * per + 1024 <= 232448) ? 4 : 2;
 }
 
 // corner values of a complete face F (4 modes x 3 comps): c00, c10, c01, c11 per component

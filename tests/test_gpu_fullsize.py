@@ -216,3 +216,92 @@ def test_fullsize_hex_cg(F, idx):
         rr = rr_new
     d = float((x - xr).abs().max() / xr.abs().max())
     assert d <= 1e-11, (cfg["name"], d)
+
+
+# ---- the whole operator at full size, against the separable (Kronecker) form -----------------
+# SURVEY §8(c) "Large configs": on the uniform box the assembled operator is a sum of tensor
+# products of 1-D FE matrices (App. A.3 / A.5; pinned against the oracle's explicit quadrature
+# in tests/test_oracle_pins.py::test_*_kronecker).  Evaluated here with plain torch FP64 ops on
+# the (z, y, x) node grid -- one 1-D banded operator per axis, no FE kernel involved -- it checks
+# EVERY entry of fem_apply at the bench sizes (elasticity with constant lambda, mu, where the
+# Kronecker form is exact).
+def _op1d(v, axis, kind, h):
+    """1-D assembled K, M, D or D^T applied along `axis` of v."""
+    n = v.shape[axis]
+    lo = torch.zeros_like(v.narrow(axis, 0, 1))
+    prev = torch.cat([lo, v.narrow(axis, 0, n - 1)], axis)  # v_{i-1}, 0 before the first node
+    nxt = torch.cat([v.narrow(axis, 1, n - 1), lo], axis)   # v_{i+1}, 0 after the last node
+    m = torch.full((n,), 2.0, dtype=v.dtype, device=v.device)
+    m[0] = m[-1] = 1.0  # elements touching the node
+    shape = [1] * v.dim()
+    shape[axis] = n
+    m = m.view(shape)
+    if kind == "M":
+        return (h / 6.0) * (2.0 * m * v + prev + nxt)
+    if kind == "K":
+        return (m * v - prev - nxt) / h
+    end = torch.zeros((n,), dtype=v.dtype, device=v.device)
+    end[0], end[-1] = -0.5, 0.5
+    end = end.view(shape) * v
+    if kind == "D":  # D_ij = int phi_i phi_j'
+        return 0.5 * (nxt - prev) + end
+    return 0.5 * (prev - nxt) + end  # D^T
+
+
+def _term(v, ops, h):  # ops per dim (x, y, z) -> tensor axes (2, 1, 0)
+    for d, k in enumerate(ops):
+        v = _op1d(v, 2 - d, k, h)
+    return v
+
+
+def _kron_apply(kind, nx, ny, nz, h, x, lam=None, mu=None):
+    c = I.ncomp(kind)
+    X = x.view(nz + 1, ny + 1, nx + 1, c)
+    bnd = torch.zeros((nz + 1, ny + 1, nx + 1), dtype=torch.bool, device=x.device)
+    bnd[0] = bnd[-1] = True
+    bnd[:, 0] = bnd[:, -1] = True
+    bnd[:, :, 0] = bnd[:, :, -1] = True
+    Xm = X.masked_fill(bnd[..., None], 0.0)  # P x (S:314)
+    Y = torch.empty_like(X)
+    if kind != "elastic":
+        for k in range(c):
+            v = Xm[..., k]
+            Y[..., k] = (_term(v, "MMK", h) + _term(v, "MKM", h) + _term(v, "KMM", h))
+    else:
+        for k in range(3):
+            acc = (lam + 2 * mu) * _term(Xm[..., k], ["K" if d == k else "M" for d in range(3)], h)
+            for j in range(3):
+                if j != k:
+                    acc += mu * _term(Xm[..., k], ["K" if d == j else "M" for d in range(3)], h)
+            for l in range(3):
+                if l == k:
+                    continue
+                def pick(dk, dl):
+                    return ["DT" if d == dk else ("D" if d == dl else "M") for d in range(3)]
+                acc += lam * _term(Xm[..., l], pick(k, l), h) + mu * _term(Xm[..., l], pick(l, k), h)
+            Y[..., k] = acc
+    Y = torch.where(bnd[..., None], X, Y)  # identity rows
+    return Y.reshape(-1)
+
+
+@pytest.mark.parametrize("idx", CASES)
+def test_fullsize_kron_identity(F, idx):
+    cfg = I.CONFIGS[idx]
+    kind = cfg["kind"]
+    nx, ny, nz = I.config_cells(cfg)
+    h = 1.0 / nx
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, "dirichlet")
+    lam, mu = 1.7, 0.6
+    if kind == "elastic":  # constant material: the Kronecker form is exact
+        ncell = nx * ny * nz
+        op.set_material(torch.full((ncell,), lam, dtype=torch.float64, device="cuda"),
+                        torch.full((ncell,), mu, dtype=torch.float64, device="cuda"))
+    c = I.ncomp(kind)
+    gen = torch.Generator(device="cuda").manual_seed(700 + idx)
+    x = torch.rand(I.n_nodes(nx, ny, nz) * c, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    y = op.apply(x)
+    ref = _kron_apply(kind, nx, ny, nz, h, x, lam, mu)
+    err = float((y - ref).abs().max() / ref.abs().max())
+    assert err <= APPLY_TOL, (cfg["name"], err)
+    del x, y, ref
+    torch.cuda.empty_cache()

@@ -56,11 +56,79 @@ def main():
             x = dev(np.random.default_rng(0).uniform(-1, 1, coords.shape[0] * I.ncomp(kind)))
             for pa in (0, 1):
                 op.set_option("partial_assembly", pa)
-                op.apply(x)
-                b = torch.zeros_like(x); b.uniform_(-1, 1)
-                xs = torch.zeros_like(b)
-                op.cg_solve(b, xs, tol=1e-10, maxit=8)
+                for det in (0, 1):  # atomic scatter / element outputs + ordered node gather
+                    op.set_option("deterministic", det)
+                    op.apply(x)
+                    b = torch.zeros_like(x); b.uniform_(-1, 1)
+                    xs = torch.zeros_like(b)
+                    op.cg_solve(b, xs, tol=1e-10, maxit=8)
+                op.set_option("deterministic", 0)
             op.close()
+    # round 2: meshes with interior CTAs (Laplace interior march, elasticity interior / edge
+    # grids side by side), the dot-implementation modes, box partial assembly (21 values), and
+    # P = 2 slab ranks through the loopback communicator (halo overlap, peer halo)
+    n = 72
+    g = I.rng(I.SEED_BASE + 177)
+    lam, mu = I.materials(g, n, n, n)
+    for kind in ("scalar", "vector", "elastic"):
+        c = I.ncomp(kind)
+        op = fem.Operator(fem.Mesh(n, n, n, 1.0 / n), kind, 1)
+        if kind == "elastic":
+            op.set_material(dev(lam), dev(mu))
+        x = dev(I.uniform_vector(g, n, n, n, c))
+        op.apply(x)
+        b = dev(I.interior_rhs(g, n, n, n, c))
+        for dm in (0, 1, 2):
+            op.set_option("dot_mode", dm)
+            xs = torch.zeros_like(b)
+            op.cg_solve(b, xs, tol=0.0, maxit=4)
+        op.set_option("dot_mode", 0)
+        if kind == "elastic":
+            op.set_option("partial_assembly", 1)
+            op.apply(x)
+            xs = torch.zeros_like(b)
+            op.cg_solve(b, xs, tol=0.0, maxit=3)
+        op.close()
+    import threading
+    nx, ny, nz = 40, 36, 30
+    x = I.uniform_vector(g, nx, ny, nz, 3)
+    lam, mu = I.materials(g, nx, ny, nz)
+    for peer in (False, True):
+        comms = fem.Comm.loopback(2)
+        errs = []
+
+        def rank(r):
+            try:
+                torch.cuda.set_device(0)
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st):
+                    mesh = fem.Mesh(nx, ny, nz, 1.0 / nx, comms[r])
+                    op = fem.Operator(mesh, "elastic", 1)
+                    k0, k1 = mesh.plane_begin, mesh.plane_end
+                    lb, le = max(k0 - 1, 0), min(k1, nz)
+                    op.set_material(np.ascontiguousarray(lam[lb * nx * ny:le * nx * ny]),
+                                    np.ascontiguousarray(mu[lb * nx * ny:le * nx * ny]), lb, le - lb)
+                    if peer:
+                        op.set_option("peer_halo", 1)
+                    plane = (nx + 1) * (ny + 1) * 3
+                    xl = dev(x[k0 * plane:k1 * plane])
+                    op.apply(xl, stream=st)
+                    xs = torch.zeros_like(xl)
+                    op.cg_solve(xl, xs, tol=0.0, maxit=3, stream=st)
+                    st.synchronize()
+                    op.close(); mesh.close()
+            except BaseException as ex:
+                errs.append(ex)
+
+        ts = [threading.Thread(target=rank, args=(r,)) for r in range(2)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for cm in comms:
+            cm.close()
+        if errs:
+            raise errs[0]
     torch.cuda.synchronize()
     print("sanitize workload done")
 
