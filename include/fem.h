@@ -219,7 +219,11 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * varies from run to run); TMA path, cg_variant 0 only), "halo_overlap" (1, default: with an
  * exchange step -- nranks > 1 without peer_halo -- the halo runs on a library stream while the
  * interior node planes are applied, then the two boundary planes; 0: halo, then one apply),
- * "deterministic" (general hex meshes: 1 replaces
+ * "delay_x" (elasticity box, fused CG with the
+ * epilogue dots: 1 makes the fused apply also perform the previous iteration's x += alpha p_old at
+ * its owned nodes -- staged one plane ahead by cp.async -- so the update kernel streams only r and
+ * q, 72 instead of 80 B/DOF per iteration; cg_end adds the last pending update; default 0, measured
+ * slower on one B200), "deterministic" (general hex meshes: 1 replaces
  * the FP64 atomic scatter by element outputs E[cell][8][C] and a per-node gather over the node's
  * (cell, corner) entries in ascending order -- bitwise reproducible results run after run, at
  * 24 C extra bytes of traffic per cell each way; the node map is built on the first switch-on;

@@ -198,6 +198,8 @@ struct fem_op_s {
   // general hexes: deterministic scatter (element outputs + per-node gather) instead of FP64 atomics
   int det = 0;
   double* hx_E = nullptr;  // [ncells][8][C]
+  // elasticity fused CG: delayed x update (the apply does x += alpha p_old; option "delay_x")
+  int delay_x = 0;  // measured slower: kept as an option
   // peer halo: the neighbour ranks' padded vectors x, p, r, p2 (CUDA IPC or, for single-process
   // tests, the other operator's buffers) and tensor maps over their ghost-plane sources
   bool peer_on = false, peer_ipc = false;
@@ -235,6 +237,7 @@ struct fem_op_s {
   struct TimedGraph {
     cudaGraphExec_t exec = nullptr;
     int iters = 0, parity = 0;
+    int64_t launches = 0;  // kernel launches the graph replays (counted during its capture)
   };
   std::vector<TimedGraph> graphT;  // up to 4 (iteration count, parity) shapes
   std::vector<TimedGraph> graphK;  // plain graphs of exactly k iterations (k <= 64), up to 6 shapes
@@ -1216,7 +1219,8 @@ static int op_common_alloc(fem_op_s* op) {
     return fail(FEM_ENOMEM, "pinned host allocation failed");
   }
   if (cudaMemset(op->red.ticket, 0, sizeof(unsigned int)) != cudaSuccess ||
-      cudaMemset(op->sc, 0, sizeof(CgScalars)) != cudaSuccess)
+      cudaMemset(op->sc, 0, sizeof(CgScalars)) != cudaSuccess ||
+      cudaMemset(op->dot_dev, 0, sizeof(double)) != cudaSuccess)  // (also the peer-halo sync allreduce)
     return fail(FEM_ECUDA, "cudaMemset failed");
   return FEM_OK;
 }
@@ -1303,6 +1307,7 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   }
   if (cudaMemset(op->red.ticket, 0, sizeof(unsigned int)) != cudaSuccess ||
       cudaMemset(op->sc, 0, sizeof(CgScalars)) != cudaSuccess ||
+      cudaMemset(op->dot_dev, 0, sizeof(double)) != cudaSuccess ||  // (also the peer-halo sync allreduce)
       cudaMemset(op->x_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
       cudaMemset(op->r_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
       cudaMemset(op->p_pl, 0, sizeof(double) * op->pl_n) != cudaSuccess ||
@@ -1648,6 +1653,13 @@ static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
 
 // fused CG iteration (TMA path): p = r + beta p_old formed inside the apply (NEXT #1 of the
 // survey, 88 -> 80 B/DOF for Laplace); parity selects the p ping-pong buffers.
+// delayed x update (option "delay_x"): elasticity, fused Hestenes-Stiefel CG with the epilogue
+// dots, TMA path
+static bool delay_x_active(const fem_op_s* op) {
+  return op->delay_x && op->kind == FEM_ELASTICITY && op->tm_ok && !op->use_pa && op->cg_variant == 0 &&
+         op->dot_mode == 0 && !op->mesh->hex;
+}
+
 static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
   double* pold = parity ? op->p2_pl : op->p_pl;
@@ -1661,6 +1673,12 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   // the two dots per option "dot_mode" (Reduce::dot_mode; the paper's dot ablation)
   Reduce rd = op->red;
   rd.dot_mode = op->dot_mode;
+  const bool dx = delay_x_active(op);
+  if (dx) {  // x += alpha p_old at the apply's owned output nodes; the update streams r, q only
+    maps.delay_x = true;
+    maps.dx = pl_owned(op, op->x_pl) - pl_owned(op, pnew);
+    maps.dpo = pl_owned(op, pold) - pl_owned(op, pnew);
+  }
   if (m->nranks > 1 && !peer) {  // halo of r and p_old overlapped with the interior planes
     auto halos = [&](cudaStream_t hs) -> int {
       double* const vs[2] = {op->r_pl, pold};
@@ -1682,7 +1700,7 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   }
   FEM_TRY(allreduce1(op, &op->sc->pq, s));
   e = launch_cg_update_fused(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, pnew),
-                             pl_owned(op, op->q_pl), n, op->sc, rd, s, m->sm_count);
+                             pl_owned(op, op->q_pl), n, op->sc, rd, s, m->sm_count, dx);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
   if (op->dot_mode == 1) {  // r.r by a separate kernel re-reading r
     e = launch_cg_dot(pl_owned(op, op->r_pl), pl_owned(op, op->r_pl), n, 1, op->sc, op->red, s, m->sm_count);
@@ -1716,7 +1734,7 @@ static int iteration(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
 }
 
 static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGraphExec_t* out,
-                   bool timed = false) {
+                   bool timed = false, int64_t* launches = nullptr) {
   // capture on a private stream (legacy stream 0 cannot be captured)
   if (timed) {
     op->ev_used = 0;
@@ -1731,6 +1749,7 @@ static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGrap
   for (int t = 0; t < iters && st == FEM_OK; ++t) st = iteration(op, (parity + t) & 1, cs, timed);
   op->ev_capture = false;
   if (timed) op->ev_used = 0;  // set at each replay
+  if (launches) *launches = g_launches.load() - before;
   g_launches.store(before);  // captured launches are counted at replay
   cudaGraph_t graph;
   cudaError_t e = cudaStreamEndCapture(cs, &graph);
@@ -1773,9 +1792,6 @@ static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, in
 }
 
 static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
-  const int per_iter_launches =
-      (op->tm_ok && !op->use_pa) ? ((op->cg_variant == 0 && op->dot_mode == 1) ? 4 : 2)
-                : (op->mesh->hex ? 3 + ((op->bc && op->mesh->hx_nb) ? 1 : 0) + (op->det ? 1 : 0) : 3);
   // loopback ranks rendezvous on the host inside every collective: not capturable, run eagerly
   const bool loop = op->mesh->comm && op->mesh->comm->loop && op->mesh->nranks > 1;
   if (op->time_apply && op->use_graph && !loop && iters > 0) {
@@ -1789,11 +1805,13 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
         cudaGraphExecDestroy(op->graphT.front().exec);
         op->graphT.erase(op->graphT.begin());
       }
-      FEM_TRY(capture(op, iters, op->cg_parity, s, &ge, true));
-      op->graphT.push_back({ge, iters, op->cg_parity});
+      int64_t nl = 0;
+      FEM_TRY(capture(op, iters, op->cg_parity, s, &ge, true, &nl));
+      op->graphT.push_back({ge, iters, op->cg_parity, nl});
     }
+    for (const auto& t : op->graphT)
+      if (t.exec == ge) add_launches(t.launches);
     CUDA_TRY(cudaGraphLaunch(ge, s));
-    add_launches((int64_t)iters * per_iter_launches);
     op->ev_used = 2 * (size_t)iters;
     op->cg_parity ^= (iters & 1);
     return FEM_OK;
@@ -1818,11 +1836,13 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
         cudaGraphExecDestroy(op->graphK.front().exec);
         op->graphK.erase(op->graphK.begin());
       }
-      FEM_TRY(capture(op, k, op->cg_parity, s, &ge));
-      op->graphK.push_back({ge, k, op->cg_parity});
+      int64_t nl = 0;
+      FEM_TRY(capture(op, k, op->cg_parity, s, &ge, false, &nl));
+      op->graphK.push_back({ge, k, op->cg_parity, nl});
     }
+    for (const auto& t : op->graphK)
+      if (t.exec == ge) add_launches(t.launches);
     CUDA_TRY(cudaGraphLaunch(ge, s));
-    add_launches((int64_t)k * per_iter_launches);
     op->cg_parity ^= (k & 1);
     return FEM_OK;
   };
@@ -1836,6 +1856,12 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
 }
 
 static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
+  if (delay_x_active(op)) {  // the last iteration's x += alpha p (if an update ran after the last apply)
+    double* plast = op->cg_parity ? op->p2_pl : op->p_pl;  // the last fused apply's p
+    const cudaError_t e = launch_cg_xpend(pl_owned(op, op->x_pl), pl_owned(op, plast), pl_count(op), op->sc, s,
+                                          op->mesh->sm_count);
+    if (e != cudaSuccess) return fail(FEM_ECUDA, "x update launch: %s", cudaGetErrorString(e));
+  }
   FEM_TRY(pack(op, op->cg_x, op->x_pl, 0, s));  // x = x_pl (caller layout)
   CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -1992,6 +2018,10 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     drop_graphs(op);
   } else if (!std::strcmp(key, "trace")) {
     op->trace = value != 0;
+  } else if (!std::strcmp(key, "delay_x")) {
+    if (op->cg_active) return fail(FEM_ESTATE, "delay_x cannot change during a CG solve");
+    op->delay_x = value != 0;
+    drop_graphs(op);
   } else if (!std::strcmp(key, "deterministic")) {
     if (!op->mesh->hex) return fail(FEM_EUNSUPPORTED, "deterministic: general hex meshes (the box kernels are atomic-free)");
     if (op->cg_active) return fail(FEM_ESTATE, "deterministic cannot change during a CG solve");
@@ -2064,6 +2094,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "halo_overlap")) *value = op->overlap;
   else if (!std::strcmp(key, "trace")) *value = op->trace;
   else if (!std::strcmp(key, "deterministic")) *value = op->mesh->hex ? op->det : 1;
+  else if (!std::strcmp(key, "delay_x")) *value = delay_x_active(op) ? 1 : 0;
   else if (!std::strncmp(key, "trace_", 6)) {
     // trace_{halo,interior,boundary,total}_ns of the last traced exchange apply (blocks on it)
     static const char* names[4] = {"trace_halo_ns", "trace_interior_ns", "trace_boundary_ns", "trace_total_ns"};

@@ -49,6 +49,8 @@ __global__ void cg_finish_init_kernel(CgScalars* sc, double tol, int maxit) {
   sc->stop_rr = tol * tol * rr;
   sc->pq = 0.0;
   sc->rr_acc = 0.0;
+  sc->alpha_x = 0.0;
+  sc->xpend = 0;
   sc->it = 0;
   sc->maxit = maxit;
   sc->breakdown_iter = -1;
@@ -89,6 +91,9 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 // fused CG (mode-2 apply has formed p = r + beta p_old and q = A p):
 //   alpha = rr / pq; x += alpha p; r -= alpha q; rr_new = r.r; it++; convergence -> done.
 // The next mode-2 apply reads beta = rr_new / rr and rolls rr = rr_new in its last block.
+// DX (delayed x update, elasticity fused CG): x and p are not touched here -- the next fused
+// apply performs x += alpha p_old at its owned nodes (alpha_x, xpend), cg_end the last one.
+template <bool DX>
 __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __restrict__ x,
                                                                       double* __restrict__ r,
                                                                       const double* __restrict__ p,
@@ -113,6 +118,10 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __
     return;
   }
   const double alpha = sc->rr / pq;
+  if (DX && blockIdx.x == 0 && threadIdx.x == 0) {  // the next fused apply adds alpha p to x
+    sc->alpha_x = alpha;
+    sc->xpend = 1;
+  }
   double acc = 0.0;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -120,7 +129,7 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __
   // unaligned element and a trailing odd element are handled by thread 0 / the last thread
   const int64_t head = (reinterpret_cast<uintptr_t>(r) & 15) ? 1 : 0;
   auto one = [&](int64_t i) {
-    x[i] = fma(alpha, p[i], x[i]);
+    if (!DX) x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
     acc = fma(ri, ri, acc);
@@ -133,10 +142,12 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __
   const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q + head);
   int64_t i = gtid;
   for (; i + stride < n2; i += 2 * stride) {  // two independent 16-B groups in flight per thread
-    const double2 pa = p2[i], pb = p2[i + stride], xa = x2[i], xb = x2[i + stride];
     const double2 qa = q2[i], qb = q2[i + stride], ra = r2[i], rb = r2[i + stride];
-    x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
-    x2[i + stride] = make_double2(fma(alpha, pb.x, xb.x), fma(alpha, pb.y, xb.y));
+    if (!DX) {
+      const double2 pa = p2[i], pb = p2[i + stride], xa = x2[i], xb = x2[i + stride];
+      x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
+      x2[i + stride] = make_double2(fma(alpha, pb.x, xb.x), fma(alpha, pb.y, xb.y));
+    }
     const double2 na = make_double2(fma(-alpha, qa.x, ra.x), fma(-alpha, qa.y, ra.y));
     const double2 nb = make_double2(fma(-alpha, qb.x, rb.x), fma(-alpha, qb.y, rb.y));
     r2[i] = na;
@@ -145,8 +156,11 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __
     acc = fma(nb.x, nb.x, acc); acc = fma(nb.y, nb.y, acc);
   }
   for (; i < n2; i += stride) {
-    const double2 pa = p2[i], xa = x2[i], qa = q2[i], ra = r2[i];
-    x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
+    const double2 qa = q2[i], ra = r2[i];
+    if (!DX) {
+      const double2 pa = p2[i], xa = x2[i];
+      x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
+    }
     const double2 na = make_double2(fma(-alpha, qa.x, ra.x), fma(-alpha, qa.y, ra.y));
     r2[i] = na;
     acc = fma(na.x, na.x, acc); acc = fma(na.y, na.y, acc);
@@ -370,8 +384,24 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
   return cudaGetLastError();
 }
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
-                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
-  cg_update_fused_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
+                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, bool delay_x) {
+  if (delay_x) cg_update_fused_kernel<true><<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
+  else cg_update_fused_kernel<false><<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+// delayed x update, end of a solve: the update of the last iteration (x += alpha_x p) if pending
+__global__ void __launch_bounds__(kVecThreads) cg_xpend_kernel(double* __restrict__ x, const double* __restrict__ p,
+                                                               int64_t n, const CgScalars* __restrict__ sc) {
+  if (!sc->xpend) return;
+  const double a = sc->alpha_x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) x[i] = fma(a, p[i], x[i]);
+}
+cudaError_t launch_cg_xpend(double* x, const double* p, int64_t n, const CgScalars* sc, cudaStream_t s,
+                            int sm_count) {
+  cg_xpend_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, p, n, sc);
   add_launches(1);
   return cudaGetLastError();
 }
