@@ -91,6 +91,9 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t addr, uint32_t parity) {
       "r"(parity), "r"(1000000)
       : "memory");
 }
+#ifndef FEM_REFILL_FENCE
+#define FEM_REFILL_FENCE 1  // fence.proxy.async before every TMA refill of a released ring slot
+#endif
 #ifndef FEM_RING_FENCE
 #define FEM_RING_FENCE 0
 #endif
@@ -362,7 +365,7 @@ struct PlaneRing {
       double* slot = buf + (size_t)s * SLOT;
       if (TM) {
         if (lane == 0) {
-          fence_proxy_async();  // the consumers' generic reads of the slot before the TMA write
+          if (FEM_REFILL_FENCE) fence_proxy_async();  // the consumers' generic reads of the slot before the TMA write
           issue_tm(t, p, ux, uy, mx, my, uorg, umap, umap2, mmap, mlayer0, peer);
         }
         continue;

@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
             ring.wait_released(t - 1);
             ring.wait_released(t);
             if (tx == 0) {
-              fence_proxy_async();  // every warp's generic reads of the slots before the TMA writes
+              if (FEM_REFILL_FENCE) fence_proxy_async();  // every warp's generic reads of the slots before the TMA writes
               ring.issue_tm(t - 1 + S, pfirst + t - 1 + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0,
                             &peer);
               if (t + S < nplane)
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
         } else if (SELF && ty == 0 && t + S < nplane) {  // refill this slot with plane t+S
           ring.wait_released(t);
           if (tx == 0) {
-            fence_proxy_async();  // every warp's generic reads of the slot before the TMA write
+            if (FEM_REFILL_FENCE) fence_proxy_async();  // every warp's generic reads of the slot before the TMA write
             ring.issue_tm(t + S, pfirst + t + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0, &peer);
           }
         }

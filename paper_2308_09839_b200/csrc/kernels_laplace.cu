@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
         else xfilter(std::false_type{});
         if (SELF) {
           if (ring.release_last(slot, tx, TY) && t + S < nplane && tx == 0) {  // refill: plane t+S
-            fence_proxy_async();
+            if (FEM_REFILL_FENCE) fence_proxy_async();
             ring.issue_tm(t + S, p + S, tux, tuy, 0, 0, uorg, &umap, &umap2, nullptr, 0, &peer);
           }
         } else {
