@@ -207,6 +207,10 @@ struct fem_op_s {
   double* nb_hi[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t nb_lo_nloc = 0;
   CUtensorMap pm_lo[4]{}, pm_hi[4]{};
+  // fem_apply on caller vectors at P > 1: tensor maps over the ghost-plane buffers (direct view,
+  // row-pair view), built on first use
+  CUtensorMap gm_dir[2]{}, gm_pair[2]{};
+  bool gm_dir_ok = false, gm_pair_ok = false;
   int64_t pm_klo = -(int64_t(1) << 62), pm_khi = -(int64_t(1) << 62);
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
@@ -849,6 +853,61 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
       return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), map, 0, s, nullptr, &pg);
     }
   }
+  // P > 1: the same two TMA views over the rank's owned planes [k0, k1) (tensor origin k0), the
+  // ghost planes k0 - 1 / k1 from the library's ghost buffers -- filled by the halo, overlapped
+  // with the interior planes (apply_split) -- through the PeerMaps plane substitution
+  if (op->direct_tm && !op->use_pa && m->nranks > 1 && op->tm_ok && !op->tm_interior && ((uintptr_t)x & 15) == 0 &&
+      ((rp & 1) == 0 || (op->bc && (op->kind != FEM_ELASTICITY || kElCY == 2)))) {
+    unsigned bw, bh;
+    u_box(op->kind, &bw, &bh);
+    const int64_t lp = g.plane * op->comps;
+    const int64_t nloc = g.k1 - g.k0;
+    const bool pair = (rp & 1) != 0;
+    const size_t need = (size_t)(op->n_local + rp + 2 * (int64_t)bw) * sizeof(double);
+    if (!pair || (xi.id && (uintptr_t)x + need <= xi.base + xi.size)) {
+      const int path = pair ? 4 : 3;
+      const CUtensorMap* map = cached_map(op, x, xi.id, path);
+      if (!map) {
+        CUtensorMap* slot = new_map_slot(op, x, xi.id, path);
+        if (pair)
+          FEM_TRY(make_map3d(slot, x, (uint64_t)(lp + 2 * rp), (uint64_t)((g.ny + 2) / 2), (uint64_t)((nloc + 1) / 2),
+                             (uint64_t)(2 * rp) * 8, (uint64_t)(2 * lp) * 8, bw, (bh + 1) / 2));
+        else
+          FEM_TRY(make_map3d(slot, x, (uint64_t)rp, (uint64_t)(g.ny + 1), (uint64_t)nloc, (uint64_t)rp * 8,
+                             (uint64_t)lp * 8, bw, bh));
+        map = slot;
+      }
+      CUtensorMap* gm = pair ? op->gm_pair : op->gm_dir;
+      bool& gm_ok = pair ? op->gm_pair_ok : op->gm_dir_ok;
+      if (!gm_ok) {
+        double* gb[2] = {op->ghost_lo, op->ghost_hi};
+        for (int k = 0; k < 2; ++k) {
+          if (pair)
+            FEM_TRY(make_map3d(&gm[k], gb[k], (uint64_t)(lp + 2 * rp), (uint64_t)((g.ny + 2) / 2), 1,
+                               (uint64_t)(2 * rp) * 8, (uint64_t)(2 * lp) * 8, bw, (bh + 1) / 2));
+          else
+            FEM_TRY(make_map3d(&gm[k], gb[k], (uint64_t)rp, (uint64_t)(g.ny + 1), 1, (uint64_t)rp * 8,
+                               (uint64_t)lp * 8, bw, bh));
+        }
+        gm_ok = true;
+      }
+      static thread_local PeerMaps pm;
+      constexpr int64_t kNone = -(int64_t(1) << 62);
+      pm.lo = gm[0];
+      pm.hi = gm[1];
+      pm.lo2 = gm[0];
+      pm.hi2 = gm[1];
+      pm.klo = m->rank > 0 ? g.k0 - 1 : kNone;
+      pm.khi = m->rank < m->nranks - 1 ? g.k1 : kNone;
+      pm.on = 1;
+      const PairGeom pg{rp, lp, g.k1 - 1, g.k0};
+      ApplyMaps maps{map, 0, 0, g.k0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr, 0, op->quad, &pm,
+                     pair ? &pg : nullptr};
+      op->last_path = pair ? 2 : 1;
+      return apply_split(op, s, dense_src(op, x, op->ghost_lo, op->ghost_hi), dense_out(op, y), maps, 0, op->red,
+                         [&](cudaStream_t hs) { return halo(op, x, op->ghost_lo, op->ghost_hi, hs); });
+    }
+  }
   op->last_path = 0;
   PlaneSrc src = dense_src(op, x, op->mesh->rank > 0 ? op->ghost_lo : nullptr,
                            op->mesh->rank < op->mesh->nranks - 1 ? op->ghost_hi : nullptr);
@@ -1291,8 +1350,9 @@ int fem_op_create(fem_mesh_t mesh, int32_t kind, int32_t bc, fem_op_t* out) {
   OP_TRY(dalloc(&op->p_pl, op->pl_n));
   OP_TRY(dalloc(&op->q_pl, op->pl_n));
   OP_TRY(dalloc(&op->p2_pl, op->pl_n));
-  OP_TRY(dalloc(&op->ghost_lo, op->plane_dofs));
-  OP_TRY(dalloc(&op->ghost_hi, op->plane_dofs));
+  // (+ one row and two box widths: the row-pair tensor view of a ghost plane reads that far)
+  OP_TRY(dalloc(&op->ghost_lo, op->plane_dofs + (g.nx + 1) * op->comps + 2 * 128));
+  OP_TRY(dalloc(&op->ghost_hi, op->plane_dofs + (g.nx + 1) * op->comps + 2 * 128));
   OP_TRY(dalloc(&op->sc, 1));
   OP_TRY(dalloc(&op->dot_dev, 1));
   OP_TRY(dalloc(&op->bad, 1));

@@ -47,7 +47,9 @@ struct __align__(64) PeerMaps {
 // Row-pair view of a dense caller vector with odd rows (PlaneRing PAIR, kernels_common.cuh)
 struct PairGeom {
   int64_t lr, lp;  // row / plane length of the caller vector in elements
-  int64_t nz;      // last node plane
+  int64_t nz;      // last node plane of the view (global index)
+  int64_t k0 = 0;  // first node plane of the view (a slab's owned planes start at k0; plane pairs
+                   // and parities count from there; other planes come from PeerMaps or read as 0)
 };
 
 // TMA tensor maps of one apply launch (u plane: padded layout; material: interleaved lambda/mu)

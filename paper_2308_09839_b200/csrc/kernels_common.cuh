@@ -286,14 +286,22 @@ struct PlaneRing {
     const int s = t & (S - 1);
     double* slot = buf + (size_t)s * SLOT;
     mbar_arrive_expect_tx(&full[s], NU * UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
-    if (PAIR) {  // two half boxes (row parities); planes outside [0, nz] read as zeros
-      const bool in = p >= 0 && p <= pg.nz;
-      const int z = in ? (int)(p >> 1) : -1;
+    if (PAIR) {  // two half boxes (row parities); planes outside [k0, nz] read as zeros, except
+                 // the ghost planes of a slab (PeerMaps: a row-pair view of a one-plane buffer)
+      const CUtensorMap* m = umap;
+      int64_t rel = p - pg.k0;
+      bool in = p >= pg.k0 && p <= pg.nz;
+      if (peer && peer->on && (p == peer->klo || p == peer->khi)) {
+        m = (p == peer->klo) ? &peer->lo : &peer->hi;
+        rel = 0;
+        in = true;
+      }
+      const int z = in ? (int)(rel >> 1) : -1;
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         const int64_t j = pjlo + b;
-        const int64_t d0 = pilo * C + (j & 1) * pg.lr + (p & 1) * pg.lp;
-        tma_load_3d(slot + b * HALF, umap, (int)(d0 & ~(int64_t)1), (int)(j >> 1), z, &full[s]);
+        const int64_t d0 = pilo * C + (j & 1) * pg.lr + (rel & 1) * pg.lp;
+        tma_load_3d(slot + b * HALF, m, (int)(d0 & ~(int64_t)1), (int)(j >> 1), z, &full[s]);
       }
       if (MROWS > 0) tma_load_3d(slot + UDBL, mmap, mx, my, (int)(p - mlayer0), &full[s]);
       return;
@@ -443,9 +451,11 @@ struct PlaneRing {
   __device__ __forceinline__ void set_pair_tile(int64_t ilo, int64_t jlo, const PairGeom& g) {
     pilo = ilo; pjlo = jlo; pg = g;
   }
+  // (ghost planes of a slab, p = k0 - 1 or nz + 1, are served at parity 0 -- PeerMaps)
   __device__ __forceinline__ void set_pair_plane(int64_t p) {
-    psh0 = (int)((pilo * C + (pjlo & 1) * pg.lr + (p & 1) * pg.lp) & 1);
-    psh1 = (int)((pilo * C + ((pjlo + 1) & 1) * pg.lr + (p & 1) * pg.lp) & 1);
+    const int64_t rel = (p >= pg.k0 && p <= pg.nz) ? p - pg.k0 : 0;
+    psh0 = (int)((pilo * C + (pjlo & 1) * pg.lr + (rel & 1) * pg.lp) & 1);
+    psh1 = (int)((pilo * C + ((pjlo + 1) & 1) * pg.lr + (rel & 1) * pg.lp) & 1);
   }
   __device__ __forceinline__ const double* row_ptr(int s, int r) const {
     if (PAIR) return buf + (size_t)s * SLOT + (r & 1) * HALF + (r >> 1) * BOXW + ((r & 1) ? psh1 : psh0);

@@ -82,10 +82,14 @@ def _ref_op(F, kind, nx, ny, nz, h, lam, mu):
 MESH = (13, 11, 14)  # ragged against every tile width; 15 node planes: 2-3 per rank at P = 5
 
 
+@pytest.mark.parametrize("mesh", [MESH, (12, 11, 14), (40, 30, 24)])
 @pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
 @pytest.mark.parametrize("P", [2, 3, 5])
-def test_loopback_apply_and_dot(F, kind, P):
-    nx, ny, nz = MESH
+def test_loopback_apply_and_dot(F, kind, P, mesh):
+    """fem_apply on caller vectors at P > 1 goes through the TMA views of the owned planes (even
+    rows: direct tensor map; odd rows: row-pair view) with the ghost planes substituted from the
+    halo buffers -- bitwise equal to P = 1 either way."""
+    nx, ny, nz = mesh
     h = 1.0 / nx
     c = I.ncomp(kind)
     g = I.rng(I.SEED_BASE + 600)
@@ -103,17 +107,21 @@ def test_loopback_apply_and_dot(F, kind, P):
         k0, k1 = mesh.plane_begin, mesh.plane_end
         xl = torch.from_numpy(x[k0 * plane:k1 * plane].copy()).cuda()
         zl = torch.from_numpy(z[k0 * plane:k1 * plane].copy()).cuda()
-        y = op.apply(xl, stream=st)  # caller vectors: halo through the loopback, bulk-row kernel
+        y = op.apply(xl, stream=st)  # caller vectors: halo through the loopback, TMA views
+        path = op.get_option("last_apply_path")
         d = op.dot(xl, zl, stream=st)
         yh = op.apply(x[k0 * plane:k1 * plane].copy())  # host vectors (staged)
         st.synchronize()
-        res = (y.cpu().numpy(), d, yh)
+        res = (y.cpu().numpy(), d, yh, path)
         op.close(); mesh.close()
         return res
 
     res = _run_ranks(P, rank)
     for cm in comms:
         cm.close()
+    for r in res:  # 1: direct tensor map (even rows); 2: row-pair view (odd rows, when the
+        # allocation has the slack the view reads), else 0: bulk rows
+        assert r[3] == 1 if ((nx + 1) * c) % 2 == 0 else r[3] in (0, 2)
     y = np.concatenate([r[0] for r in res])
     assert np.array_equal(y, y_ref)
     assert np.array_equal(np.concatenate([r[2] for r in res]), y_ref)
