@@ -211,6 +211,9 @@ struct fem_op_s {
   // row-pair view), built on first use
   CUtensorMap gm_dir[2]{}, gm_pair[2]{};
   bool gm_dir_ok = false, gm_pair_ok = false;
+  // P = 1 row-pair view without slack after the caller's vector: the last plane from a copy
+  double* last_plane = nullptr;
+  CUtensorMap gm_last{};
   int64_t pm_klo = -(int64_t(1) << 62), pm_khi = -(int64_t(1) << 62);
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
@@ -852,6 +855,34 @@ static int apply_device(fem_op_s* op, const double* x, double* y, cudaStream_t s
       op->last_path = 2;
       return launch_apply(op, dense_src(op, x, nullptr, nullptr), dense_out(op, y), map, 0, s, nullptr, &pg);
     }
+    if (g.nz >= 1 && xi.id) {
+      // No slack after the vector (e.g. an exact-size cudaMalloc): the view covers planes
+      // [0, nz - 1] only -- its boxes then stay inside the vector -- and the last plane is served
+      // from a one-plane copy with slack (3.6 MB at C4) through the PeerMaps plane substitution
+      if (!op->last_plane) {
+        FEM_TRY(dalloc(&op->last_plane, lp + rp + 2 * 128));
+        CUDA_TRY(cudaMemset(op->last_plane, 0, (lp + rp + 2 * 128) * sizeof(double)));
+        FEM_TRY(make_map3d(&op->gm_last, op->last_plane, (uint64_t)(lp + 2 * rp), (uint64_t)((g.ny + 2) / 2), 1,
+                           (uint64_t)(2 * rp) * 8, (uint64_t)(2 * lp) * 8, bw, (bh + 1) / 2));
+      }
+      CUDA_TRY(cudaMemcpyAsync(op->last_plane, x + g.nz * lp, lp * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      const CUtensorMap* map = cached_map(op, x, xi.id, 5);
+      if (!map) {
+        CUtensorMap* slot = new_map_slot(op, x, xi.id, 5);
+        FEM_TRY(make_map3d(slot, x, (uint64_t)(lp + 2 * rp), (uint64_t)((g.ny + 2) / 2), (uint64_t)((g.nz + 1) / 2),
+                           (uint64_t)(2 * rp) * 8, (uint64_t)(2 * lp) * 8, bw, (bh + 1) / 2));
+        map = slot;
+      }
+      static thread_local PeerMaps pm;
+      pm.lo = pm.hi = pm.lo2 = pm.hi2 = op->gm_last;
+      pm.klo = -(int64_t(1) << 62);
+      pm.khi = g.nz;
+      pm.on = 1;
+      const PairGeom pg{rp, lp, g.nz - 1, 0};
+      ApplyMaps maps{map, 0, 0, 0, &op->tm_mat, op->mat_layer0, nullptr, nullptr, nullptr, 0, op->quad, &pm, &pg};
+      op->last_path = 2;
+      return launch_maps(op, g, dense_src(op, x, nullptr, nullptr), dense_out(op, y), maps, 0, op->red, s);
+    }
   }
   // P > 1: the same two TMA views over the rank's owned planes [k0, k1) (tensor origin k0), the
   // ghost planes k0 - 1 / k1 from the library's ghost buffers -- filled by the halo, overlapped
@@ -1253,6 +1284,7 @@ static void op_free(fem_op_s* op) {
   cudaFree(op->lm);
   cudaFree(op->pa);
   cudaFree(op->hx_E);
+  cudaFree(op->last_plane);
   cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
   if (op->graph1b) cudaGraphExecDestroy(op->graph1b);
   for (const auto& t : op->graphT) cudaGraphExecDestroy(t.exec);
@@ -2101,6 +2133,7 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     if (value && !op->hx_E) FEM_TRY(dalloc(&op->hx_E, 8 * op->comps * m->hx_ncells));
     if (!value && op->hx_E) {
       cudaFree(op->hx_E);
+  cudaFree(op->last_plane);
       op->hx_E = nullptr;
     }
     op->det = value != 0;

@@ -43,6 +43,52 @@ MESHES = [(1, 1, 1), (2, 2, 2), (5, 7, 9), (33, 17, 12), (40, 31, 20), (64, 3, 5
 # caller vectors with 16-B rows ((nx+1) c even): fem_apply stages them through a tensor map over
 # the caller's memory ("direct_tma"); same operator as the bulk-row path, bit for bit
 @pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
+@pytest.mark.parametrize("dims", [(32, 17, 12), (64, 40, 21), (30, 45, 4)])
+def test_apply_row_pairs_exact_allocation(F, oracle, kind, dims):
+    """Odd rows in a buffer that ends exactly where the vector ends (cudaMalloc of the exact size,
+    no slack for the row-pair view's last boxes): the view then covers planes 0 .. nz-1 and the
+    last plane comes from a one-plane copy -- still the row-pair path, equal to the slack case."""
+    import ctypes
+    from cuda.bindings import runtime as rt
+    nx, ny, nz = dims
+    h = 1.0 / max(dims)
+    g = I.rng(I.SEED_BASE + 410 + nx + 7 * ny + 31 * nz)
+    c = I.ncomp(kind)
+    x = I.uniform_vector(g, nx, ny, nz, c)
+    lam, mu = I.materials(g, nx, ny, nz)
+    op = F.Operator(F.Mesh(nx, ny, nz, h), kind, 1)
+    if kind == "elastic":
+        op.set_material(dev(lam), dev(mu))
+    roomy = torch.empty(x.size + 4096, dtype=torch.float64, device="cuda")[:x.size]
+    roomy.copy_(torch.from_numpy(x))
+    y_ref = op.apply(roomy)
+    assert op.get_option("last_apply_path") == 2
+    nbytes = x.size * 8
+    err, xp = rt.cudaMalloc(nbytes)
+    assert err == rt.cudaError_t.cudaSuccess
+    err, yp = rt.cudaMalloc(nbytes)
+    assert err == rt.cudaError_t.cudaSuccess
+    try:
+        (err,) = rt.cudaMemcpy(xp, roomy.data_ptr(), nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+        assert err == rt.cudaError_t.cudaSuccess
+        torch.cuda.synchronize()
+        lib = F.load()
+        rc = lib.fem_apply(op.h, ctypes.c_void_p(int(xp)), ctypes.c_void_p(int(yp)), None)
+        assert rc == 0, lib.fem_last_error()
+        assert op.get_option("last_apply_path") == 2
+        y = torch.empty_like(y_ref)
+        (err,) = rt.cudaMemcpy(y.data_ptr(), yp, nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+        assert err == rt.cudaError_t.cudaSuccess
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref)
+    finally:
+        rt.cudaFree(xp)
+        rt.cudaFree(yp)
+    ref = oracle.apply(kind, 1, nx, ny, nz, h, x, lam=lam, mu=mu)
+    assert relerr(y.cpu().numpy(), ref) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("kind", ["scalar", "vector", "elastic"])
 @pytest.mark.parametrize("bc", [0, 1])
 @pytest.mark.parametrize("quad", [0, 1])
 @pytest.mark.parametrize("dims", [(5, 7, 9), (33, 17, 12), (63, 40, 21), (1, 1, 1)])
