@@ -1,7 +1,7 @@
 #!/bin/bash
 # GPU-box session: bench lines for every config, ncu launch list + one full capture of the
 # dominant kernels.  Usage (from repo root, under gpurun): bash tools/run_bench_suite.sh TAG
-TAG=${1:-r01}
+TAG=${1:-r02f}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
@@ -27,3 +27,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:lapl
 timeout 600 ncu --set full --clock-control none -k regex:csr_spmv -s 2 -c 1 \
   -o $OUT/prof_spmv python bench.py --config 1 --steps 3 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_spmv.log 2>&1
 echo suite done
+timeout 300 python bench.py --config 6 --det --no-cpu --no-e2e > $OUT/bench_x6det.json 2> $OUT/bench_x6det.err
+timeout 300 python bench.py --config 7 --det --no-cpu --no-e2e > $OUT/bench_x7det.json 2> $OUT/bench_x7det.err
+timeout 600 python tools/size_sweep.py --out $OUT/size_sweep.jsonl > $OUT/size_sweep.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:elastic2_kernel -s 40 -c 1 \
+  -o $OUT/prof_elastic_apply python bench.py --steps 3 --warmup 3 --no-e2e --no-csr --no-cpu > $OUT/ncu_apply.log 2>&1
+echo suite2 done
