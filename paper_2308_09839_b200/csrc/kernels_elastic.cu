@@ -25,7 +25,10 @@
 #define FEM_EL2_REFILL2 1  // elastic2_kernel: warp 0 refills two ring slots every other plane
 #endif
 #ifndef FEM_EL2_HD
-#define FEM_EL2_HD 4  // y hand-off ring depth of elastic2_kernel when shared memory allows (4 or 8)
+#define FEM_EL2_HD 8  // y hand-off ring depth of elastic2_kernel when shared memory allows (4 or 8)
+#endif
+#ifndef FEM_EL2_NOEMPTY
+#define FEM_EL2_NOEMPTY 0  // 1: drop the hand-off "consumed" barriers (redundant when HD >= S + 2; measured: no gain)
 #endif
 #ifndef FEM_EL2_ZFACE
 #define FEM_EL2_ZFACE 1  // interior grid: z-face chunks with interior x/y tiles, mask-free except the face plane
@@ -435,6 +438,12 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   constexpr int HW = kEl2HW;        // doubles per thread and y hand-off (3 corner sums)
   using Ring = PlaneRing<TM, ROWS, COLS, 3, S, kElMatRows, TX, NU, PAIR>;
   constexpr int HD = el2_handoff_depth<TY, Ring::BYTES + Ring::META>();  // y hand-off ring depth
+  // The hand-off slot written for output plane q is rewritten for plane q + HD at the writer's
+  // step q + HD + 2, which needs ring plane q + HD + 2, whose refill needs every warp to have
+  // released plane q + HD + 2 - S (q + HD + 3 - S with the paired refills), i.e. the reader to
+  // have finished its step q + HD + 1 - S >= q + 2 -- its read of plane q -- whenever
+  // HD >= S + 1.  With HD >= S + 2 the "slot consumed" barriers are therefore redundant.
+  constexpr bool NOEMPTY = SELF && FEM_EL2_NOEMPTY && HD >= S + 2;
   constexpr int TPART = HD * TY * TX * HW;
   static_assert(kElMatRows >= 2 * TY, "material box covers the tile's cell rows");
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -688,7 +697,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
           const int qo = t - 2, b = qo & (HD - 1);
           const uint32_t n = (uint32_t)qo / (uint32_t)HD;
           if (ty >= 1) {
-            if (n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
+            if (!NOEMPTY && n >= 1) mbar_wait_a(tew0 + 8u * TY * b, (n - 1) & 1);
             double* dst = tw0 + b * (TY * TX * HW);
             dst[0] = BA[0]; dst[1] = BA[1]; dst[2] = BA[2];
             __syncwarp();
@@ -702,8 +711,10 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
             double v[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) v[c] = TB[c] + src[c];
-            __syncwarp();
-            if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
+            if (!NOEMPTY) {
+              __syncwarp();
+              if (tx == 0) mbar_arrive_a(ter0 + 8u * TY * b);
+            }
             if (ownB) put(yp + yo.rpitch, pnb + x.rpitch, v, xs_B, bnB_xy || qf);
           }
           if (DX && mode == 2 && dox) {  // x += alpha p_old at plane qo (staged at step t - 1)
