@@ -27,6 +27,9 @@
 #ifndef FEM_EL2_HD
 #define FEM_EL2_HD 8  // y hand-off ring depth of elastic2_kernel when shared memory allows (4 or 8)
 #endif
+#ifndef FEM_EL2_S0
+#define FEM_EL2_S0 FEM_EL2_S  // ring stages outside fused CG (one input box); 4 + an 8-deep hand-off beat 8 + 4 (C5b fem_apply 0.73 -> 0.69 ms)
+#endif
 #ifndef FEM_EL2_NOEMPTY
 #define FEM_EL2_NOEMPTY 0  // 1: drop the hand-off "consumed" barriers (redundant when HD >= S + 2; measured: no gain)
 #endif
@@ -964,11 +967,11 @@ cudaError_t launch_elastic(int bc, const Grid& g, PlaneSrc x, OutVec y, ApplyMap
   // per ring row): one cell row per thread, 16 rows per copy batch (measured faster there)
   if (maps.pair) {  // caller vector with odd rows through a row-pair tensor (fem_apply)
     if (mode != 0 || !bc) return cudaErrorInvalidValue;
-    return launch_cfg2<true, kEl2TY, 2 * kEl2S, true>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    return launch_cfg2<true, kEl2TY, FEM_EL2_S0, true>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
   }
   if (kElCY == 2 && maps.u) {
     if (mode == 2) return launch_cfg2<true, kEl2TY, kEl2S>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
-    return launch_cfg2<true, kEl2TY, 2 * kEl2S>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    return launch_cfg2<true, kEl2TY, FEM_EL2_S0>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
   }
   if (maps.u) {
     if (mode == 2) return launch_cfg<true, kElTY, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
