@@ -359,7 +359,8 @@ __device__ __forceinline__ void elastic_layer(const Face* fb, const Face* ft, do
 template <int TY, size_t RING>
 constexpr int el2_handoff_depth() {
   constexpr size_t per = (size_t)TY * (32 * kEl2HW * sizeof(double) + 2 * sizeof(uint64_t));
-  return (FEM_EL2_HD >= 8 && RING + 8 * per + 1024 <= 232448) ? 8
+  return (FEM_EL2_HD >= 16 && RING + 16 * per + 1024 <= 232448) ? 16
+       : (FEM_EL2_HD >= 8 && RING + 8 * per + 1024 <= 232448) ? 8
        : (RING + 4 * per + 1024 <= 232448) ? 4 : 2;
 }
 

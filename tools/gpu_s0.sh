@@ -1,8 +1,8 @@
 #!/bin/bash
-for fl in "" "-DFEM_EL2_S0=4"; do
+for fl in "" "-DFEM_EL2_HD=16"; do
   FEM_NVCC_FLAGS="$fl" python -c "from paper_2308_09839_b200 import build as B; B.build(force=True)" || exit 1
   echo "=== $fl"
-  [ -n "$fl" ] && timeout 900 python -m pytest -q -x -m gpu tests/test_gpu_parity.py -k "elastic and (row_pairs or apply)" 2>&1 | tail -1
+  [ -n "$fl" ] && timeout 900 python -m pytest -q -x -m gpu tests/test_gpu_parity.py -k "elastic" 2>&1 | tail -1
   for i in 1 2; do
   timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-csr --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); x=d['extra']; print(d['config']['workload'], 'CG %.2f' % d['value'], 'frac %.3f' % d['roofline']['frac'], 'aonly %.4f ms %.3f' % (x['apply_only_ms'], x['apply_only_frac']))"
   timeout 300 python bench.py --config 5 --steps 20 --warmup 5 --no-e2e --no-csr --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); x=d['extra']; print(d['config']['workload'], 'CG %.2f' % d['value'], 'frac %.3f' % d['roofline']['frac'], 'aonly %.4f ms %.3f' % (x['apply_only_ms'], x['apply_only_frac']))"
