@@ -226,7 +226,7 @@ struct PlaneRing {
   static_assert(!PAIR || (TM && NU == 1), "row-pair staging: tensor path, one input box");
   static constexpr uint32_t MBOX_BYTES = MROWS * MPITCH * 8;
   static_assert(TM || ROWS <= 32, "one producer lane per row (row path)");
-  static_assert((S & (S - 1)) == 0, "S must be a power of two");
+  static_assert(S >= 2, "at least two ring stages");
   static_assert(ROWS <= 256 && BOXW <= 256 && MPITCH <= 256, "TMA box dims <= 256");
 
   double* buf;      // NSLOT * SLOT doubles, 128-B aligned
@@ -283,7 +283,7 @@ struct PlaneRing {
   __device__ __forceinline__ void issue_tm(int t, int64_t p, int ux, int uy, int mx, int my, TmaOrigin uorg,
                                            const CUtensorMap* umap, const CUtensorMap* umap2,
                                            const CUtensorMap* mmap, int64_t mlayer0, const PeerMaps* peer) {
-    const int s = t & (S - 1);
+    const int s = t % S;
     double* slot = buf + (size_t)s * SLOT;
     mbar_arrive_expect_tx(&full[s], NU * UBOX_BYTES + (MROWS > 0 ? MBOX_BYTES : 0u));
     if (PAIR) {  // two half boxes (row parities); planes outside [k0, nz] read as zeros, except
@@ -318,7 +318,7 @@ struct PlaneRing {
   }
   // TM: wait until every consumer warp released ring position t (slot t % S)
   __device__ __forceinline__ void wait_released(int t) {
-    mbar_wait_a(empty_a + 8u * (t & (S - 1)), (uint32_t)((t / S) & 1));
+    mbar_wait_a(empty_a + 8u * (t % S), (uint32_t)((t / S) & 1));
   }
 
   // producer warp: stream planes pfirst .. plast (and material layers) through the ring.
@@ -368,7 +368,7 @@ struct PlaneRing {
 #pragma unroll 1
     for (int64_t p = pfirst; p <= plast; ++p) {
       const int t = tbase + (int)(p - pfirst);
-      const int s = t & (S - 1);
+      const int s = t % S;
       if (t >= S) mbar_wait_a(empty_a + 8u * s, (uint32_t)(((t / S) - 1) & 1));
       double* slot = buf + (size_t)s * SLOT;
       if (TM) {

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
     double Ln, Mn;  // material of the cell layer above the bottom plane (x h/16)
 
     auto load_plane = [&](int t, Face* ft, double* xn, double& L, double& M) {
-      const int slot = t & (S - 1);
+      const int slot = t % S;
       ring.wait(slot, (uint32_t)((t / S) & 1));
       const double2 lmn = ring.mat(slot, ty, tx);  // material layer of this plane
       const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
 
       auto load_plane = [&](int t, Face* fA, Face* fB, double* xA, double* xB, double& LA, double& MA,
                             double& LB, double& MB) {
-        const int slot = t & (S - 1);
+        const int slot = t % S;
         ring.wait(slot, (uint32_t)((t / S) & 1));
         if (PAIR) ring.set_pair_plane(pfirst + t);
         const double2 lmA = ring.mat(slot, 2 * ty, tx), lmB = ring.mat(slot, 2 * ty + 1, tx);

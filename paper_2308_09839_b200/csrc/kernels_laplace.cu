@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
       auto plane = [&](int64_t p, auto kc) {
         constexpr int W0 = decltype(kc)::value % 3, W1 = (W0 + 1) % 3, W2 = (W0 + 2) % 3;
         const int t = (int)(p - pfirst);
-        const int slot = t & (S - 1);
+        const int slot = t % S;
         ring.wait(slot, (uint32_t)((t / S) & 1));
         if (PAIR) ring.set_pair_plane(p);
         // x-direction filters for the R+2 rows this thread needs

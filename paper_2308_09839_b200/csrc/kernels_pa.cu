@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(32 * (TY + 1), 1)
     for (int t = 0; t < 12; ++t) cb[t] = 0.0;
 
     auto load_plane = [&](int t, FaceP* ft, double* xn) {
-      const int slot = t & (S - 1);
+      const int slot = t % S;
       ring.wait(slot, (uint32_t)((t / S) & 1));
       const double* r0 = ring.row_ptr(slot, ty) + tx * 3;
       const double* r1 = ring.row_ptr(slot, ty + 1) + tx * 3;
