@@ -17,6 +17,9 @@
 
 #include "kernels_common.cuh"
 
+#ifndef FEM_LAP_S3
+#define FEM_LAP_S3 4  // ring stages of the vector fused CG apply
+#endif
 #ifndef FEM_LAP_FORCE_EDGE
 #define FEM_LAP_FORCE_EDGE 0  // 1: every CTA takes the Dirichlet-aware march (experiments)
 #endif
@@ -345,7 +348,7 @@ cudaError_t launch_laplace(int comps, int bc, const Grid& g, PlaneSrc x, OutVec 
   if (maps.u) {
     if (comps == 1 && mode == 2) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, kLapS1>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     if (comps == 1) return launch_cfg<true, 1, kLapTX, kLapTY1, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
-    if (mode == 2) return launch_cfg<true, 3, kLapTX, kLapTY3, kLapR3, 4>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
+    if (mode == 2) return launch_cfg<true, 3, kLapTX, kLapTY3, kLapR3, FEM_LAP_S3>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
     return launch_cfg<true, 3, kLapTX, kLapTY3, kLapR3, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
   }
   if (comps == 1) return launch_cfg<false, 1, kLapTX, kLapTY, kLapR1, 8>(g, x, y, maps, bc, mode, sc, red, s, sm_count);
