@@ -93,8 +93,11 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 // The next mode-2 apply reads beta = rr_new / rr and rolls rr = rr_new in its last block.
 // DX (delayed x update, elasticity fused CG): x and p are not touched here -- the next fused
 // apply performs x += alpha p_old at its owned nodes (alpha_x, xpend), cg_end the last one.
+#ifndef FEM_UPD_MINB
+#define FEM_UPD_MINB 1  // resident blocks per SM the fused update kernel is compiled for
+#endif
 template <bool DX>
-__global__ void __launch_bounds__(kVecThreads) cg_update_fused_kernel(double* __restrict__ x,
+__global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
                                                                       double* __restrict__ r,
                                                                       const double* __restrict__ p,
                                                                       const double* __restrict__ q,
