@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 // DX (delayed x update, elasticity fused CG): x and p are not touched here -- the next fused
 // apply performs x += alpha p_old at its owned nodes (alpha_x, xpend), cg_end the last one.
 #ifndef FEM_UPD_MINB
-#define FEM_UPD_MINB 1  // resident blocks per SM the fused update kernel is compiled for
+#define FEM_UPD_MINB 3  // resident blocks per SM the fused update kernel is compiled for (80 registers)
 #endif
 template <bool DX>
 __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
 //   beta = gamma / gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev)  (first: beta = 0,
 //   alpha = gamma / delta); p = r + beta p; s = w + beta s; x += alpha p; r -= alpha s.
 // gamma is the residual of the iterate before this update, so convergence is decided here.
-__global__ void __launch_bounds__(kVecThreads) cg_cgcg_update_kernel(double* __restrict__ x, double* __restrict__ r,
+__global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_cgcg_update_kernel(double* __restrict__ x, double* __restrict__ r,
                                                                      double* __restrict__ p, double* __restrict__ s,
                                                                      const double* __restrict__ w, int64_t n,
                                                                      CgScalars* sc, Reduce red) {

@@ -1,5 +1,5 @@
 #!/bin/bash
-for fl in "-DFEM_UPD_MINB=4" "-DFEM_UPD_MINB=3" ""; do
+for fl in "" "-DFEM_UPD_MINB=3" "-DFEM_UPD_MINB=4"; do
   FEM_NVCC_FLAGS="$fl" python -c "from paper_2308_09839_b200 import build as B; B.build(force=True)" || exit 1
   echo "=== $fl"
   for c in 3 1; do for i in 1 2; do
