@@ -58,12 +58,11 @@ def algorithmic_apply_bytes(kind, nx, ny, nz):
     return b
 
 
-def cg_apply_bytes(kind, nx, ny, nz, fused, delay_x=False):
+def cg_apply_bytes(kind, nx, ny, nz, fused):
     """Algorithmic bytes of the apply launched inside one CG iteration.  Fused:
-    read r and p_old, write p and q (32 B/DOF) + lambda, mu (16 B/cell); unfused: 16 B/DOF.
-    Delayed x update (option delay_x): + read and write x (48 B/DOF)."""
+    read r and p_old, write p and q (32 B/DOF) + lambda, mu (16 B/cell); unfused: 16 B/DOF."""
     ndof = I.n_nodes(nx, ny, nz) * I.ncomp(kind)
-    b = (32 if fused else 16) * ndof + (16 * ndof if delay_x else 0)
+    b = (32 if fused else 16) * ndof
     if kind == "elastic":
         b += 16 * nx * ny * nz
     return b
@@ -76,11 +75,12 @@ HEX_FLOPS_PER_CELL = {"elastic": 635 + 337 + 2 * 609, "vector": 594 + 345 + 2 * 
 FP64_PEAK_TFLOPS = 2 * 17.08  # own DFMA microbenchmark, profiles/r01_microbench_fp64_hbm.txt
 
 
-def cg_vector_bytes(ndof, fused, delay_x=False):
+def cg_vector_bytes(ndof, fused, x_pairs=False):
     # update: read x,p,r,q write x,r (48 B/DOF); unfused p-update: read r,p write p (24 B/DOF);
-    # delayed x update: the update reads r, q and writes r (24 B/DOF)
-    if delay_x:
-        return 24 * ndof
+    # paired x update: r, q -> r every iteration, x, p_old, p -> x every other
+    # one (24 + 32 / 2 = 40 B/DOF)
+    if x_pairs:
+        return 40 * ndof
     return (48 if fused else 72) * ndof
 
 
@@ -268,8 +268,8 @@ def run_native(args, cfg):
     op = fem.Operator(mesh, kind, "dirichlet")
     if args.pa:  # partial assembly (Table 3): hex -- stored geometry; box elasticity --
         op.set_option("partial_assembly", 1)  # 21 values per Gauss point, D_q = w det J C_e
-    if args.delay_x >= 0:  # option delay_x (elasticity fused CG)
-        op.set_option("delay_x", args.delay_x)
+    if args.x_pairs >= 0:  # option x_pairs (fused CG: x advanced every other iteration)
+        op.set_option("x_pairs", args.x_pairs)
     if args.det and hexmesh:  # general hexes: no FP64 atomics, bitwise reproducible
         op.set_option("deterministic", 1)
     if args.gll:  # Gauss-Lobatto quadrature: the BP5 / BP6 operators (reading R1)
@@ -396,8 +396,8 @@ def run_native(args, cfg):
     if cgcg:  # apply reads r, writes w (16 B/DOF); update reads r,w,p,s,x writes p,s,x,r (72 B/DOF)
         fused = False
     # algorithmic bytes of one rank's apply launch: owned planes (+ its cell layers)
-    delay_x = bool(op.get_option("delay_x"))
-    alg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused, delay_x) * nloc_planes / (nz + 1)
+    x_pairs = bool(op.get_option("x_pairs"))
+    alg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) * nloc_planes / (nz + 1)
     if args.pa and not hexmesh:  # box PA: 21 x 8 stored doubles per cell (Table 3) + u read + y write
         alg_bytes = 21 * 8 * 8 * nx * ny * nz + 16 * op.n_global
     achieved = alg_bytes / (apply_ms / 1e3) / 1e9
@@ -447,13 +447,13 @@ def run_native(args, cfg):
     extra["cg_iteration_ms_event_graph"] = ms_event_graph / args.steps  # the time_apply pass
     extra["apply_share_of_step"] = share
     extra["cg_iteration_ms"] = ms / args.steps
-    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused, delay_x) + cg_vector_bytes(ndof_global, fused, delay_x)
+    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused, x_pairs)
     extra["cg_bytes_per_dof_alg"] = cg_bytes / ndof_global
     extra["cg_iteration_gbs"] = cg_bytes / (ms / args.steps / 1e3) / 1e9
     extra["fused_cg"] = fused
     extra["cg_variant"] = "chronopoulos-gear" if cgcg else "hestenes-stiefel"
     extra["dot_mode"] = "single reduction (CG-CG)" if cgcg else args.dot
-    extra["delay_x"] = delay_x
+    extra["x_pairs"] = x_pairs
     del xx, yy
 
     # ---- e2e: the public call a user makes, with pinned HOST buffers ----
@@ -516,8 +516,7 @@ def run_native(args, cfg):
                        "l2": l2_label},
             "roofline": ({"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": traffic,
-                          "kernel": (f"{kind} fused CG apply (p = r + beta p_old, q = A p, p.q"
-                                     + (", delayed x += alpha p_old)" if delay_x else ")") if fused
+                          "kernel": (f"{kind} fused CG apply (p = r + beta p_old, q = A p, p.q)" if fused
                                      else (f"{kind} apply (single-reduction CG: w = A r, w.r, r.r)" if cgcg
                                            else ("pa21_kernel (partial assembly, 21 values per Gauss point, "
                                                  "CG mode)" if args.pa else f"{kind} apply (CG mode, fused p.Ap)"))),
@@ -701,8 +700,8 @@ def main():
                     help="how the fused CG forms p.Ap and r.r (option dot_mode; P:714-728 ablation)")
     ap.add_argument("--gll", action="store_true",
                     help="2x2x2 Gauss-Lobatto quadrature (the CEED BP5/BP6 operators) instead of Gauss")
-    ap.add_argument("--delay-x", type=int, default=-1, choices=[-1, 0, 1],
-                    help="elasticity fused CG: 1 the apply performs the delayed x += alpha p, 0 the update kernel does (default)")
+    ap.add_argument("--x-pairs", type=int, default=-1, choices=[-1, 0, 1],
+                    help="fused CG: 1 x advanced every other iteration from both p buffers (library default), 0 every iteration")
     ap.add_argument("--det", action="store_true",
                     help="general-hex configs (6/7): deterministic scatter (element outputs + node gather)")
     ap.add_argument("--pa", action="store_true",

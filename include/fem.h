@@ -219,11 +219,12 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * varies from run to run); TMA path, cg_variant 0 only), "halo_overlap" (1, default: with an
  * exchange step -- nranks > 1 without peer_halo -- the halo runs on a library stream while the
  * interior node planes are applied, then the two boundary planes; 0: halo, then one apply),
- * "delay_x" (elasticity box, fused CG with the
- * epilogue dots: 1 makes the fused apply also perform the previous iteration's x += alpha p_old at
- * its owned nodes -- staged one plane ahead by cp.async -- so the update kernel streams only r and
- * q, 72 instead of 80 B/DOF per iteration; cg_end adds the last pending update; default 0, measured
- * slower on one B200), "deterministic" (general hex meshes: 1 replaces
+ * "x_pairs" (fused Hestenes-Stiefel CG on the box, default 1: x is advanced
+ * every other iteration, x = (x + alpha_{k-1} p_{k-1}) + alpha_k p_k from the two p ping-pong
+ * buffers, so the update of the first iteration of a pair streams r and q only -- 80 instead of 96
+ * B/DOF of update traffic per two iterations, x bitwise equal to the per-iteration update
+ * (Table 4's axpy rows); cg_end adds a pending first half; 0: x += alpha p every
+ * iteration; reads back 0 where it does not apply), "deterministic" (general hex meshes: 1 replaces
  * the FP64 atomic scatter by element outputs E[cell][8][C] and a per-node gather over the node's
  * (cell, corner) entries in ascending order -- bitwise reproducible results run after run, at
  * 24 C extra bytes of traffic per cell each way; the node map is built on the first switch-on;

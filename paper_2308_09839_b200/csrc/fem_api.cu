@@ -198,8 +198,9 @@ struct fem_op_s {
   // general hexes: deterministic scatter (element outputs + per-node gather) instead of FP64 atomics
   int det = 0;
   double* hx_E = nullptr;  // [ncells][8][C]
-  // elasticity fused CG: delayed x update (the apply does x += alpha p_old; option "delay_x")
-  int delay_x = 0;  // measured slower: kept as an option
+  // fused CG: paired x update (x advanced every other iteration from both p buffers, 80 instead
+  // of 96 B/DOF of update traffic per two iterations; option "x_pairs")
+  int x_pairs = 1;
   // peer halo: the neighbour ranks' padded vectors x, p, r, p2 (CUDA IPC or, for single-process
   // tests, the other operator's buffers) and tensor maps over their ghost-plane sources
   bool peer_on = false, peer_ipc = false;
@@ -1745,11 +1746,9 @@ static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
 
 // fused CG iteration (TMA path): p = r + beta p_old formed inside the apply (NEXT #1 of the
 // survey, 88 -> 80 B/DOF for Laplace); parity selects the p ping-pong buffers.
-// delayed x update (option "delay_x"): elasticity, fused Hestenes-Stiefel CG with the epilogue
-// dots, TMA path
-static bool delay_x_active(const fem_op_s* op) {
-  return op->delay_x && op->kind == FEM_ELASTICITY && op->tm_ok && !op->use_pa && op->cg_variant == 0 &&
-         op->dot_mode == 0 && !op->mesh->hex;
+// paired x update (option "x_pairs"): fused Hestenes-Stiefel CG on the box
+static bool x_pairs_active(const fem_op_s* op) {
+  return op->x_pairs && op->tm_ok && !op->use_pa && op->cg_variant == 0 && !op->mesh->hex;
 }
 
 static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
@@ -1765,12 +1764,6 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   // the two dots per option "dot_mode" (Reduce::dot_mode; the paper's dot ablation)
   Reduce rd = op->red;
   rd.dot_mode = op->dot_mode;
-  const bool dx = delay_x_active(op);
-  if (dx) {  // x += alpha p_old at the apply's owned output nodes; the update streams r, q only
-    maps.delay_x = true;
-    maps.dx = pl_owned(op, op->x_pl) - pl_owned(op, pnew);
-    maps.dpo = pl_owned(op, pold) - pl_owned(op, pnew);
-  }
   if (m->nranks > 1 && !peer) {  // halo of r and p_old overlapped with the interior planes
     auto halos = [&](cudaStream_t hs) -> int {
       double* const vs[2] = {op->r_pl, pold};
@@ -1791,8 +1784,11 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
     if (e != cudaSuccess) return fail(FEM_ECUDA, "dot launch: %s", cudaGetErrorString(e));
   }
   FEM_TRY(allreduce1(op, &op->sc->pq, s));
+  // paired x update: iteration parity 0 leaves alpha p pending (p in p2_pl, the p_old of the
+  // parity-1 iteration that follows), parity 1 adds both halves of the pair
+  const int xpair = x_pairs_active(op) ? (parity ? 2 : 1) : 0;
   e = launch_cg_update_fused(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, pnew),
-                             pl_owned(op, op->q_pl), n, op->sc, rd, s, m->sm_count, dx);
+                             pl_owned(op, op->q_pl), n, op->sc, rd, s, m->sm_count, xpair, pl_owned(op, pold));
   if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
   if (op->dot_mode == 1) {  // r.r by a separate kernel re-reading r
     e = launch_cg_dot(pl_owned(op, op->r_pl), pl_owned(op, op->r_pl), n, 1, op->sc, op->red, s, m->sm_count);
@@ -1948,12 +1944,14 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
 }
 
 static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
-  if (delay_x_active(op)) {  // the last iteration's x += alpha p (if an update ran after the last apply)
-    double* plast = op->cg_parity ? op->p2_pl : op->p_pl;  // the last fused apply's p
-    const cudaError_t e = launch_cg_xpend(pl_owned(op, op->x_pl), pl_owned(op, plast), pl_count(op), op->sc, s,
-                                          op->mesh->sm_count);
+  if (x_pairs_active(op)) {  // the first half of a pair, if the solve ended after it
+    const cudaError_t e = launch_cg_xpair_flush(pl_owned(op, op->x_pl), pl_owned(op, op->p2_pl), pl_count(op),
+                                                op->sc, s, op->mesh->sm_count);
     if (e != cudaSuccess) return fail(FEM_ECUDA, "x update launch: %s", cudaGetErrorString(e));
   }
+  // peer halo: the true-residual apply below reads the neighbours' x -- wait for their last x update
+  if (op->peer_on && op->mesh->nranks > 1 && x_pairs_active(op))
+    FEM_TRY(allreduce1(op, op->dot_dev, s));
   FEM_TRY(pack(op, op->cg_x, op->x_pl, 0, s));  // x = x_pl (caller layout)
   CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -2110,9 +2108,9 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     drop_graphs(op);
   } else if (!std::strcmp(key, "trace")) {
     op->trace = value != 0;
-  } else if (!std::strcmp(key, "delay_x")) {
-    if (op->cg_active) return fail(FEM_ESTATE, "delay_x cannot change during a CG solve");
-    op->delay_x = value != 0;
+  } else if (!std::strcmp(key, "x_pairs")) {
+    if (op->cg_active) return fail(FEM_ESTATE, "x_pairs cannot change during a CG solve");
+    op->x_pairs = value != 0;
     drop_graphs(op);
   } else if (!std::strcmp(key, "deterministic")) {
     if (!op->mesh->hex) return fail(FEM_EUNSUPPORTED, "deterministic: general hex meshes (the box kernels are atomic-free)");
@@ -2187,7 +2185,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "halo_overlap")) *value = op->overlap;
   else if (!std::strcmp(key, "trace")) *value = op->trace;
   else if (!std::strcmp(key, "deterministic")) *value = op->mesh->hex ? op->det : 1;
-  else if (!std::strcmp(key, "delay_x")) *value = delay_x_active(op) ? 1 : 0;
+  else if (!std::strcmp(key, "x_pairs")) *value = x_pairs_active(op) ? 1 : 0;
   else if (!std::strncmp(key, "trace_", 6)) {
     // trace_{halo,interior,boundary,total}_ns of the last traced exchange apply (blocks on it)
     static const char* names[4] = {"trace_halo_ns", "trace_interior_ns", "trace_boundary_ns", "trace_total_ns"};

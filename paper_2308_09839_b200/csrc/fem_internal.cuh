@@ -75,10 +75,6 @@ struct ApplyMaps {
   // and two events to run them concurrently; nullptr: one after the other on the same stream)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  // elasticity fused CG apply (mode 2): delayed x update -- the apply also performs the previous
-  // iteration's x += alpha p_old at its owned nodes (x = pnew + dx, p_old = pnew + dpo elements)
-  bool delay_x = false;
-  int64_t dx = 0, dpo = 0;
 };
 
 // Device scalars of one CG solve (rank-global after the allreduce steps).
@@ -90,13 +86,13 @@ struct CgScalars {
   double stop_rr;   // tol^2 * rr0
   double alpha;     // Chronopoulos-Gear CG: alpha of the last update
   double rr_acc;    // dot_mode 2: atomic accumulator of the update's r.r
-  double alpha_x;   // delayed x update: alpha of the last update (x += alpha_x p pending)
+  double alpha_p;   // paired x update: alpha of the pending first iteration of a pair
   int32_t done;     // 0 running, 1 converged, 2 breakdown, 3 maxit reached
   int32_t it;       // iterations completed
   int32_t maxit;
   int32_t breakdown_iter;
   int32_t first;    // fused CG: 1 before the first apply (beta = 0, p = r)
-  int32_t xpend;    // delayed x update: 1 if x += alpha_x p (p = the last fused apply's p) pending
+  int32_t xp;       // paired x update: 1 if x += alpha_p p (p = the pair's first p, buffer p2) pending
 };
 
 // Last-block reduction workspace: per-CTA partials + ticket counter.
@@ -215,9 +211,10 @@ cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* 
                               cudaStream_t s, int sm_count);
 // fused CG: x += alpha p; r -= alpha q; rr_new = r.r; iteration bookkeeping (p update is in the apply)
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
-                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, bool delay_x = false);
-cudaError_t launch_cg_xpend(double* x, const double* p, int64_t n, const CgScalars* sc, cudaStream_t s,
-                            int sm_count);
+                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int xpair = 0, const double* pold = nullptr);
+// paired x update: x += alpha_p p if the first half of a pair is pending (end of a solve)
+cudaError_t launch_cg_xpair_flush(double* x, const double* p, int64_t n, const CgScalars* sc, cudaStream_t s,
+                                  int sm_count);
 // general hexahedral meshes (kernels_hex.cu): cells = 2 int4 per cell (node ids in corner-bit
 // order, bit 31 = Dirichlet node), xyz = node coordinates (w unused), lm = (lambda, mu) per cell.
 // mode 0: y += A (P x) at unconstrained nodes (y zeroed by the caller); mode 1: + sc->pq = the
@@ -364,7 +361,6 @@ __device__ __forceinline__ void cg_apply_epilogue(double pq, bool roll, CgScalar
     if (last_block_reduce(0.0, red, sh, &unused)) {  // ticket only: the last CTA rolls
       sc->rr = sc->rr_new;
       sc->first = 0;
-      sc->xpend = 0;     // (delayed x update: consumed by this apply)
       sc->rr_acc = 0.0;  // the update's atomic target
     }
     return;
@@ -375,7 +371,6 @@ __device__ __forceinline__ void cg_apply_epilogue(double pq, bool roll, CgScalar
     if (roll && red.roll) {  // every block has read rr / rr_new / first: roll the recurrence
       sc->rr = sc->rr_new;
       sc->first = 0;
-      sc->xpend = 0;  // (delayed x update: consumed by this apply)
     }
   }
 }

@@ -49,8 +49,8 @@ __global__ void cg_finish_init_kernel(CgScalars* sc, double tol, int maxit) {
   sc->stop_rr = tol * tol * rr;
   sc->pq = 0.0;
   sc->rr_acc = 0.0;
-  sc->alpha_x = 0.0;
-  sc->xpend = 0;
+  sc->alpha_p = 0.0;
+  sc->xp = 0;
   sc->it = 0;
   sc->maxit = maxit;
   sc->breakdown_iter = -1;
@@ -91,15 +91,21 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 // fused CG (mode-2 apply has formed p = r + beta p_old and q = A p):
 //   alpha = rr / pq; x += alpha p; r -= alpha q; rr_new = r.r; it++; convergence -> done.
 // The next mode-2 apply reads beta = rr_new / rr and rolls rr = rr_new in its last block.
-// DX (delayed x update, elasticity fused CG): x and p are not touched here -- the next fused
-// apply performs x += alpha p_old at its owned nodes (alpha_x, xpend), cg_end the last one.
+// XM, how x is advanced (DESIGN.md §5.3 "paired x update"):
+//   0  x += alpha p                                                  (48 B/DOF)
+//   1  x untouched: the first iteration of a pair (alpha and p stay pending: p lives in the p
+//      ping-pong buffer the next apply reads as p_old and does not overwrite)   (24 B/DOF)
+//   2  second iteration of a pair: x = (x + alpha_p p_old) + alpha p, the two updates in their
+//      sequential order (bitwise the same x as XM = 0 twice)         (56 B/DOF)
+// so a pair of iterations moves 80 instead of 96 B/DOF of update traffic.
 #ifndef FEM_UPD_MINB
 #define FEM_UPD_MINB 3  // resident blocks per SM the fused update kernel is compiled for (80 registers)
 #endif
-template <bool DX>
+template <int XM>
 __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
                                                                       double* __restrict__ r,
                                                                       const double* __restrict__ p,
+                                                                      const double* __restrict__ pold,
                                                                       const double* __restrict__ q,
                                                                       int64_t n, CgScalars* sc,
                                                                       Reduce red) {
@@ -121,18 +127,23 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
     return;
   }
   const double alpha = sc->rr / pq;
-  if (DX && blockIdx.x == 0 && threadIdx.x == 0) {  // the next fused apply adds alpha p to x
-    sc->alpha_x = alpha;
-    sc->xpend = 1;
+  // (alpha_p / xp are read by later kernels only: block 0 may write them) the next update adds
+  // alpha p (its p_old) before its own alpha p
+  if (XM == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->alpha_p = alpha;
+    sc->xp = 1;
   }
+  const double ap = (XM == 2) ? sc->alpha_p : 0.0;
+  if (XM == 2 && blockIdx.x == 0 && threadIdx.x == 0) sc->xp = 0;
   double acc = 0.0;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // 16-B vector accesses (the four vectors share one layout, hence one alignment); a leading
+  // 16-B vector accesses (the five vectors share one layout, hence one alignment); a leading
   // unaligned element and a trailing odd element are handled by thread 0 / the last thread
   const int64_t head = (reinterpret_cast<uintptr_t>(r) & 15) ? 1 : 0;
   auto one = [&](int64_t i) {
-    if (!DX) x[i] = fma(alpha, p[i], x[i]);
+    if (XM == 0) x[i] = fma(alpha, p[i], x[i]);
+    if (XM == 2) x[i] = fma(alpha, p[i], fma(ap, pold[i], x[i]));
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
     acc = fma(ri, ri, acc);
@@ -142,15 +153,22 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
   double2* __restrict__ x2 = reinterpret_cast<double2*>(x + head);
   double2* __restrict__ r2 = reinterpret_cast<double2*>(r + head);
   const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p + head);
+  const double2* __restrict__ o2 = reinterpret_cast<const double2*>((XM == 2 ? pold : p) + head);
   const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q + head);
+  auto xupd = [&](int64_t j) {
+    if (XM == 0) {
+      const double2 pa = p2[j], xa = x2[j];
+      x2[j] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
+    } else if (XM == 2) {
+      const double2 pa = p2[j], oa = o2[j], xa = x2[j];
+      x2[j] = make_double2(fma(alpha, pa.x, fma(ap, oa.x, xa.x)), fma(alpha, pa.y, fma(ap, oa.y, xa.y)));
+    }
+  };
   int64_t i = gtid;
   for (; i + stride < n2; i += 2 * stride) {  // two independent 16-B groups in flight per thread
     const double2 qa = q2[i], qb = q2[i + stride], ra = r2[i], rb = r2[i + stride];
-    if (!DX) {
-      const double2 pa = p2[i], pb = p2[i + stride], xa = x2[i], xb = x2[i + stride];
-      x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
-      x2[i + stride] = make_double2(fma(alpha, pb.x, xb.x), fma(alpha, pb.y, xb.y));
-    }
+    xupd(i);
+    xupd(i + stride);
     const double2 na = make_double2(fma(-alpha, qa.x, ra.x), fma(-alpha, qa.y, ra.y));
     const double2 nb = make_double2(fma(-alpha, qb.x, rb.x), fma(-alpha, qb.y, rb.y));
     r2[i] = na;
@@ -160,10 +178,7 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
   }
   for (; i < n2; i += stride) {
     const double2 qa = q2[i], ra = r2[i];
-    if (!DX) {
-      const double2 pa = p2[i], xa = x2[i];
-      x2[i] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
-    }
+    xupd(i);
     const double2 na = make_double2(fma(-alpha, qa.x, ra.x), fma(-alpha, qa.y, ra.y));
     r2[i] = na;
     acc = fma(na.x, na.x, acc); acc = fma(na.y, na.y, acc);
@@ -387,27 +402,31 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
   return cudaGetLastError();
 }
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
-                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, bool delay_x) {
-  if (delay_x) cg_update_fused_kernel<true><<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
-  else cg_update_fused_kernel<false><<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
+                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count,
+                                   int xpair, const double* pold) {
+  const unsigned nb = vec_blocks(n, sm_count);
+  if (xpair == 1) cg_update_fused_kernel<1><<<nb, kVecThreads, 0, s>>>(x, r, p, p, q, n, sc, red);
+  else if (xpair == 2) cg_update_fused_kernel<2><<<nb, kVecThreads, 0, s>>>(x, r, p, pold, q, n, sc, red);
+  else cg_update_fused_kernel<0><<<nb, kVecThreads, 0, s>>>(x, r, p, p, q, n, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }
 
-// delayed x update, end of a solve: the update of the last iteration (x += alpha_x p) if pending
-__global__ void __launch_bounds__(kVecThreads) cg_xpend_kernel(double* __restrict__ x, const double* __restrict__ p,
-                                                               int64_t n, const CgScalars* __restrict__ sc) {
-  if (!sc->xpend) return;
-  const double a = sc->alpha_x;
+// paired x update, end of a solve: the pending first half of a pair (x += alpha_p p) if any
+__global__ void __launch_bounds__(kVecThreads) cg_xpair_flush_kernel(double* __restrict__ x, const double* __restrict__ p,
+                                                                     int64_t n, const CgScalars* sc) {
+  if (!sc->xp) return;
+  const double a = sc->alpha_p;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) x[i] = fma(a, p[i], x[i]);
 }
-cudaError_t launch_cg_xpend(double* x, const double* p, int64_t n, const CgScalars* sc, cudaStream_t s,
-                            int sm_count) {
-  cg_xpend_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, p, n, sc);
+cudaError_t launch_cg_xpair_flush(double* x, const double* p, int64_t n, const CgScalars* sc, cudaStream_t s,
+                                  int sm_count) {
+  cg_xpair_flush_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, p, n, sc);
   add_launches(1);
   return cudaGetLastError();
 }
+
 cudaError_t launch_cg_cgcg_update(double* x, double* r, double* p, double* s, const double* w, int64_t n,
                                   CgScalars* sc, Reduce red, cudaStream_t st, int sm_count) {
   cg_cgcg_update_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, st>>>(x, r, p, s, w, n, sc, red);

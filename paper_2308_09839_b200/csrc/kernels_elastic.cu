@@ -419,16 +419,13 @@ __device__ __forceinline__ void tile_of_block(int GM, const TileMap& m, int& bx,
   bx = xx < m.xa ? xx : xx + nxi;
 }
 
-// DX (fused CG, mode 2): delayed x update -- at every owned output node the apply also performs the
-// previous iteration's x += alpha_x p_old (x at pnew + dxo, p_old at pnew + dpo), staged one plane
-// ahead by per-thread cp.async into shared memory; the update kernel then streams only r and q.
-template <bool TM, int MODE, int TY, int S, bool GLL, bool PAIR = false, int GM = 0, bool DX = false>
+template <bool TM, int MODE, int TY, int S, bool GLL, bool PAIR = false, int GM = 0>
 __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     elastic2_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                     TmaOrigin uorg, const __grid_constant__ CUtensorMap mmap, int64_t mat_layer0,
                     const __grid_constant__ CUtensorMap umap2, const double* pold, double* pnew,
                     int bc, int64_t kchunk, int64_t kspan, CgScalars* sc, Reduce red, const __grid_constant__ PeerMaps peer,
-                    int txa, int tya, PairGeom pg, TileMap tmap, int64_t dxo, int64_t dpo) {
+                    int txa, int tya, PairGeom pg, TileMap tmap) {
   constexpr int mode = MODE;
   constexpr int NU = (MODE == 2) ? 2 : 1;
   constexpr int TX = 32;
@@ -462,16 +459,9 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   if (mode >= 1 && sc->done) return;
   // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
   const double beta = (mode == 2) ? (sc->first ? 0.0 : sc->rr_new / sc->rr) : 0.0;
-  // DX: the pending x += alpha p_old of the previous iteration (none before the first update)
-  const bool dox = DX && sc->xpend != 0;
-  const double ax = DX ? sc->alpha_x : 0.0;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
-  // DX staging: [2 planes][12 doubles: x, p_old of rows A and B][NT threads] after the meta
-  constexpr size_t kXsOff = (Ring::BYTES + (size_t)TPART * sizeof(double) + 2 * HD * TY * sizeof(uint64_t) +
-                             Ring::META + 15) & ~size_t(15);
-  double* const xst = reinterpret_cast<double*>(smem_raw + kXsOff) + tid;
   int bx, by, bz;
   tile_of_block(GM, tmap, bx, by, bz);
   // output tile: nodes i0 .. i0+txa-1 (txa <= TX-1), j0 .. j0+tya-1 (tya <= 2TY-1)
@@ -619,28 +609,6 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
             ring.issue_tm(t + S, pfirst + t + S, tux, tuy, tmx, tmy, uorg, &umap, &umap2, &mmap, mat_layer0, &peer);
           }
         }
-        if (DX && mode == 2 && dox && t >= 1) {
-          // x and p_old of this thread's output nodes at plane t (written at step t + 1); every
-          // step commits a group (empty on the last) so wait_group 1 always covers plane t - 1
-          double* base = pnb + (t >= 2 ? x.ppitch : 0);
-          double* st = xst + (t & 1) * (12 * NT);
-          const bool stage = t <= nplane - 2;
-          if (stage && ownA) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              cp_async8(st + c * NT, base + dxo + c);
-              cp_async8(st + (3 + c) * NT, base + dpo + c);
-            }
-          }
-          if (stage && ownB) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              cp_async8(st + (6 + c) * NT, base + x.rpitch + dxo + c);
-              cp_async8(st + (9 + c) * NT, base + x.rpitch + dpo + c);
-            }
-          }
-          cp_async_commit();
-        }
         LA = lmA.x * hs;
         MA = lmA.y * hs;
         LB = lmB.x * hs;
@@ -721,18 +689,6 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
             }
             if (ownB) put(yp + yo.rpitch, pnb + x.rpitch, v, xs_B, bnB_xy || qf);
           }
-          if (DX && mode == 2 && dox) {  // x += alpha p_old at plane qo (staged at step t - 1)
-            cp_async_wait_1();
-            const double* st = xst + ((t - 1) & 1) * (12 * NT);
-            if (ownA) {
-#pragma unroll
-              for (int c = 0; c < 3; ++c) pnb[dxo + c] = fma(ax, st[(3 + c) * NT], st[c * NT]);
-            }
-            if (ownB) {
-#pragma unroll
-              for (int c = 0; c < 3; ++c) pnb[x.rpitch + dxo + c] = fma(ax, st[(9 + c) * NT], st[(6 + c) * NT]);
-            }
-          }
           if (mode == 2) pnb += x.ppitch;
           yp += yo.ppitch;
         }
@@ -772,9 +728,7 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
   using Ring2 = PlaneRing<TM, 2 * TY + 1, TX + 1, 3, S, kElMatRows, TX, (TM ? 2 : 1)>;
   constexpr int HD1 = el2_handoff_depth<TY, Ring1::BYTES + Ring1::META>();
   constexpr int HD2 = el2_handoff_depth<TY, Ring2::BYTES + Ring2::META>();
-  const bool dx = TM && !PAIR && mode == 2 && maps.delay_x;
   const size_t smem = mode == 2 ? Ring2::BYTES + Ring2::META + (size_t)HD2 * TY * (TX * kEl2HW * sizeof(double) + 2 * sizeof(uint64_t))
-                                       + (dx ? 2 * 12 * sizeof(double) * TX * TY + 16 : 0)
                                 : Ring1::BYTES + Ring1::META + (size_t)HD1 * TY * (TX * kEl2HW * sizeof(double) + 2 * sizeof(uint64_t));
   const bool gll = maps.quad == 1;
   if (mode == 3 && !TM) return cudaErrorInvalidValue;
@@ -783,7 +737,6 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
     if constexpr (PAIR) return elastic2_kernel<TM, 0, TY, S, G, true>;  // fem_apply only
     else
       return mode == 3 ? elastic2_kernel<TM, (TM ? 3 : 1), TY, S, G>
-           : (mode == 2 && dx) ? elastic2_kernel<TM, (TM ? 2 : 1), TY, S, G, false, 0, true>
            : mode == 2 ? elastic2_kernel<TM, (TM ? 2 : 1), TY, S, G>
            : mode == 1 ? elastic2_kernel<TM, 1, TY, S, G>
                        : elastic2_kernel<TM, 0, TY, S, G>;
@@ -851,7 +804,6 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
           if constexpr (PAIR) return elastic2_kernel<TM, 0, TY, S, G, true, M>;
           else
             return mode == 3 ? elastic2_kernel<TM, 3, TY, S, G, false, M>
-                 : (mode == 2 && dx) ? elastic2_kernel<TM, 2, TY, S, G, false, M, true>
                  : mode == 2 ? elastic2_kernel<TM, 2, TY, S, G, false, M>
                  : mode == 1 ? elastic2_kernel<TM, 1, TY, S, G, false, M>
                              : elastic2_kernel<TM, 0, TY, S, G, false, M>;
@@ -878,15 +830,14 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
         }
         if (n_edge > 0) {  // the slower, Dirichlet-aware CTAs first
           ked<<<dim3((unsigned)n_edge), block, smem, se>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold,
-                                                           maps.pnew, bc, kchunk, kspan, sc, re, pm, txa, tya, pgeo, tm,
-                                                           maps.dx, maps.dpo);
+                                                           maps.pnew, bc, kchunk, kspan, sc, re, pm, txa, tya, pgeo, tm);
           add_launches(1);
           const cudaError_t e = cudaGetLastError();
           if (e != cudaSuccess) return e;
         }
         kin<<<dim3((unsigned)(xb - xa + 1), (unsigned)(yb - ya + 1), (unsigned)(zb - za + 1)), block, smem, s>>>(
             g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew, bc, kchunk, kspan, sc, ri, pm,
-            txa, tya, pgeo, tm, maps.dx, maps.dpo);
+            txa, tya, pgeo, tm);
         add_launches(1);
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess && two) {
@@ -898,7 +849,7 @@ static cudaError_t launch_cfg2(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps ma
     }
   }
   kern<<<grid, block, smem, s>>>(g, x, y, um, org, *maps.mat, maps.mat_layer0, um2, maps.pold, maps.pnew,
-                                 bc, kchunk, kspan, sc, red, pm, txa, tya, pgeo, tm0, maps.dx, maps.dpo);
+                                 bc, kchunk, kspan, sc, red, pm, txa, tya, pgeo, tm0);
   add_launches(1);
   return cudaGetLastError();
 }
