@@ -432,6 +432,22 @@ struct PlaneRing {
     return __shfl_sync(0xffffffffu, last, 0) != 0u;
   }
 
+  // release_last split in two (FEM_LAP_LATE_REFILL): the warp's arrive on the slot counter is
+  // issued right after its last read of the slot, the "was it the last" test -- which waits for
+  // the atomic's return -- only after the plane's arithmetic, so the atomic latency overlaps it
+  __device__ __forceinline__ unsigned release_begin(int s, int lane) {
+    __syncwarp();
+    unsigned old = 0;
+    if (lane == 0)
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n"
+                   : "=r"(old) : "r"(smem_u32(cnt + s)) : "memory");
+    return old;
+  }
+  __device__ __forceinline__ bool release_end(unsigned old, int lane, int nwarps) const {
+    const unsigned last = (lane == 0) ? (unsigned)(((old + 1) % (unsigned)nwarps) == 0u) : 0u;
+    return __shfl_sync(0xffffffffu, last, 0) != 0u;
+  }
+
   // consumer warp: release slot s after its last read.  (The thread that refills the slot issues
   // fence.proxy.async between observing the release and the TMA: the generic-proxy reads of the
   // slot must be ordered before the async-proxy write.  Without that fence the vector Laplace

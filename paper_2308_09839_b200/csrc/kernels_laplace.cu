@@ -20,6 +20,9 @@
 #ifndef FEM_LAP_S3
 #define FEM_LAP_S3 4  // ring stages of the vector fused CG apply
 #endif
+#ifndef FEM_LAP_LATE_REFILL
+#define FEM_LAP_LATE_REFILL 1  // self-refilling scalar ring: the last-release test after the plane's arithmetic
+#endif
 #ifndef FEM_LAP_FORCE_EDGE
 #define FEM_LAP_FORCE_EDGE 0  // 1: every CTA takes the Dirichlet-aware march (experiments)
 #endif
@@ -173,8 +176,11 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
         };
         if (MK && rmask && (wedge || p == 0 || p == g.nz)) xfilter(std::true_type{});
         else xfilter(std::false_type{});
+        unsigned rel = 0;
         if (SELF) {
-          if (ring.release_last(slot, tx, TY) && t + S < nplane && tx == 0) {  // refill: plane t+S
+          if (FEM_LAP_LATE_REFILL) {
+            rel = ring.release_begin(slot, tx);  // the refill test follows the plane's arithmetic
+          } else if (ring.release_last(slot, tx, TY) && t + S < nplane && tx == 0) {  // refill: plane t+S
             if (FEM_REFILL_FENCE) fence_proxy_async();
             ring.issue_tm(t + S, p + S, tux, tuy, 0, 0, uorg, &umap, &umap2, nullptr, 0, &peer);
           }
@@ -232,6 +238,10 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
             if (MK && !rmask) pq_old += x.ppitch;
             pq_new += x.ppitch;
           }
+        }
+        if (SELF && FEM_LAP_LATE_REFILL && ring.release_end(rel, tx, TY) && t + S < nplane && tx == 0) {
+          if (FEM_REFILL_FENCE) fence_proxy_async();  // refill: plane t+S
+          ring.issue_tm(t + S, p + S, tux, tuy, 0, 0, uorg, &umap, &umap2, nullptr, 0, &peer);
         }
       };
       using K0 = std::integral_constant<int, 0>;
