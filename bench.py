@@ -75,12 +75,12 @@ HEX_FLOPS_PER_CELL = {"elastic": 635 + 337 + 2 * 609, "vector": 594 + 345 + 2 * 
 FP64_PEAK_TFLOPS = 2 * 17.08  # own DFMA microbenchmark, profiles/r01_microbench_fp64_hbm.txt
 
 
-def cg_vector_bytes(ndof, fused, x_pairs=False):
+def cg_vector_bytes(ndof, fused, x_defer=1):
     # update: read x,p,r,q write x,r (48 B/DOF); unfused p-update: read r,p write p (24 B/DOF);
-    # paired x update: r, q -> r every iteration, x, p_old, p -> x every other
-    # one (24 + 32 / 2 = 40 B/DOF)
-    if x_pairs:
-        return 40 * ndof
+    # deferred x update over m iterations: r, q -> r every iteration, x and the
+    # group's m p vectors -> x once per group: 24 + (16 + 8 m) / m = 32 + 16 / m B/DOF
+    if fused and x_defer > 1:
+        return (32 + 16 / x_defer) * ndof
     return (48 if fused else 72) * ndof
 
 
@@ -268,8 +268,8 @@ def run_native(args, cfg):
     op = fem.Operator(mesh, kind, "dirichlet")
     if args.pa:  # partial assembly (Table 3): hex -- stored geometry; box elasticity --
         op.set_option("partial_assembly", 1)  # 21 values per Gauss point, D_q = w det J C_e
-    if args.x_pairs >= 0:  # option x_pairs (fused CG: x advanced every other iteration)
-        op.set_option("x_pairs", args.x_pairs)
+    if args.x_defer > 0:  # option x_defer (fused CG: x advanced every m-th iteration)
+        op.set_option("x_defer", args.x_defer)
     if args.det and hexmesh:  # general hexes: no FP64 atomics, bitwise reproducible
         op.set_option("deterministic", 1)
     if args.gll:  # Gauss-Lobatto quadrature: the BP5 / BP6 operators (reading R1)
@@ -328,9 +328,9 @@ def run_native(args, cfg):
         op.cg_iterate(k)
         its[0] += k
 
-    def even():
-        if its[0] % 2:
-            iterate(1)
+    def even():  # every K-step pass starts at phase 0 of the p-buffer ring (4 buffers with x_defer 4)
+        if its[0] % 4:
+            iterate(4 - its[0] % 4)
 
     iterate(args.warmup)
     even()
@@ -396,7 +396,7 @@ def run_native(args, cfg):
     if cgcg:  # apply reads r, writes w (16 B/DOF); update reads r,w,p,s,x writes p,s,x,r (72 B/DOF)
         fused = False
     # algorithmic bytes of one rank's apply launch: owned planes (+ its cell layers)
-    x_pairs = bool(op.get_option("x_pairs"))
+    x_defer = op.get_option("x_defer")
     alg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) * nloc_planes / (nz + 1)
     if args.pa and not hexmesh:  # box PA: 21 x 8 stored doubles per cell (Table 3) + u read + y write
         alg_bytes = 21 * 8 * 8 * nx * ny * nz + 16 * op.n_global
@@ -447,13 +447,13 @@ def run_native(args, cfg):
     extra["cg_iteration_ms_event_graph"] = ms_event_graph / args.steps  # the time_apply pass
     extra["apply_share_of_step"] = share
     extra["cg_iteration_ms"] = ms / args.steps
-    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused, x_pairs)
+    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused, x_defer)
     extra["cg_bytes_per_dof_alg"] = cg_bytes / ndof_global
     extra["cg_iteration_gbs"] = cg_bytes / (ms / args.steps / 1e3) / 1e9
     extra["fused_cg"] = fused
     extra["cg_variant"] = "chronopoulos-gear" if cgcg else "hestenes-stiefel"
     extra["dot_mode"] = "single reduction (CG-CG)" if cgcg else args.dot
-    extra["x_pairs"] = x_pairs
+    extra["x_defer"] = x_defer
     del xx, yy
 
     # ---- e2e: the public call a user makes, with pinned HOST buffers ----
@@ -700,8 +700,8 @@ def main():
                     help="how the fused CG forms p.Ap and r.r (option dot_mode; P:714-728 ablation)")
     ap.add_argument("--gll", action="store_true",
                     help="2x2x2 Gauss-Lobatto quadrature (the CEED BP5/BP6 operators) instead of Gauss")
-    ap.add_argument("--x-pairs", type=int, default=-1, choices=[-1, 0, 1],
-                    help="fused CG: 1 x advanced every other iteration from both p buffers (library default), 0 every iteration")
+    ap.add_argument("--x-defer", type=int, default=0, choices=[0, 1, 2, 4],
+                    help="fused CG: x updated every m-th iteration from the group's p buffers (0: library default)")
     ap.add_argument("--det", action="store_true",
                     help="general-hex configs (6/7): deterministic scatter (element outputs + node gather)")
     ap.add_argument("--pa", action="store_true",

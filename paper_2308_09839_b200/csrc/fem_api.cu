@@ -23,6 +23,10 @@
 #include "../../include/fem.h"
 #include "fem_internal.cuh"
 
+#ifndef FEM_X_DEFER
+#define FEM_X_DEFER 4  // fused CG: x updated every FEM_X_DEFER-th iteration (1, 2 or 4; option x_defer)
+#endif
+
 namespace fem {
 
 // NVTX range over a host-side scope (SURVEY §5 "Tracing"): fem:apply, fem:halo, fem:allreduce,
@@ -168,8 +172,9 @@ struct fem_op_s {
   int64_t pl_lead = 0, pl_rp = 0, pl_pp = 0, pl_n = 0;
   int64_t pl_off = 0;  // offset of the owned range (pl_lead + pl_pp; 0 on general hex meshes)
   double *x_pl = nullptr, *r_pl = nullptr, *p_pl = nullptr, *q_pl = nullptr, *p2_pl = nullptr;
-  CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{};
-  int cg_parity = 0;  // fused CG: iteration parity (p_pl / p2_pl ping-pong)
+  double *p3_pl = nullptr, *p4_pl = nullptr;  // deferred x update over 4 iterations (allocated on use)
+  CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{}, tm_p3{}, tm_p4{};
+  int cg_parity = 0;  // fused CG: iteration phase mod 4 (selects the p buffers)
   bool tm_ok = false;
   bool tm_interior = false;  // u tensor spans the interior only (Laplace + Dirichlet)
   int64_t tm_i0 = 0, tm_j0 = 0, tm_k0 = 0;
@@ -198,9 +203,9 @@ struct fem_op_s {
   // general hexes: deterministic scatter (element outputs + per-node gather) instead of FP64 atomics
   int det = 0;
   double* hx_E = nullptr;  // [ncells][8][C]
-  // fused CG: paired x update (x advanced every other iteration from both p buffers, 80 instead
-  // of 96 B/DOF of update traffic per two iterations; option "x_pairs")
-  int x_pairs = 1;
+  // fused CG: deferred x update (x advanced every x_defer-th iteration from the p buffers of the
+  // group: 1, 2 or 4; option "x_defer")
+  int x_defer = FEM_X_DEFER;
   // peer halo: the neighbour ranks' padded vectors x, p, r, p2 (CUDA IPC or, for single-process
   // tests, the other operator's buffers) and tensor maps over their ghost-plane sources
   bool peer_on = false, peer_ipc = false;
@@ -554,9 +559,10 @@ static int make_pl_maps(fem_op_s* op) {
   op->tm_j0 = lo;
   op->tm_k0 = k0;
   const int64_t off = op->pl_lead + (k0 - (g.k0 - 1)) * op->pl_pp + lo * op->pl_rp + lo * C;
-  double* vecs[4] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl};
-  CUtensorMap* maps[4] = {&op->tm_x, &op->tm_p, &op->tm_r, &op->tm_p2};
-  for (int v = 0; v < 4; ++v) {
+  double* vecs[6] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl, op->p3_pl, op->p4_pl};
+  CUtensorMap* maps[6] = {&op->tm_x, &op->tm_p, &op->tm_r, &op->tm_p2, &op->tm_p3, &op->tm_p4};
+  for (int v = 0; v < 6; ++v) {
+    if (!vecs[v]) continue;  // (p3, p4: allocated for x_defer = 4 only)
     FEM_TRY(make_map3d(maps[v], vecs[v] + off, (uint64_t)((i1 - lo + 1) * C), (uint64_t)(j1 - lo + 1),
                        (uint64_t)(k1 - k0 + 1), op->pl_rp * 8, op->pl_pp * 8, bw, bh));
   }
@@ -1287,6 +1293,7 @@ static void op_free(fem_op_s* op) {
   cudaFree(op->hx_E);
   cudaFree(op->last_plane);
   cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
+  cudaFree(op->p3_pl); cudaFree(op->p4_pl);
   if (op->graph1b) cudaGraphExecDestroy(op->graph1b);
   for (const auto& t : op->graphT) cudaGraphExecDestroy(t.exec);
   for (const auto& t : op->graphK) cudaGraphExecDestroy(t.exec);
@@ -1746,20 +1753,52 @@ static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
 
 // fused CG iteration (TMA path): p = r + beta p_old formed inside the apply (NEXT #1 of the
 // survey, 88 -> 80 B/DOF for Laplace); parity selects the p ping-pong buffers.
-// paired x update (option "x_pairs"): fused Hestenes-Stiefel CG on the box
-static bool x_pairs_active(const fem_op_s* op) {
-  return op->x_pairs && op->tm_ok && !op->use_pa && op->cg_variant == 0 && !op->mesh->hex;
+static void drop_graphs(fem_op_s* op);
+// deferred x update (option "x_defer"): fused Hestenes-Stiefel CG on the box.  Returns the group
+// length m (1: x += alpha p every iteration).  The peer halo maps the neighbours' p and p2 only,
+// so with it m is at most 2.
+static int x_defer_m(const fem_op_s* op) {
+  if (op->x_defer <= 1 || !op->tm_ok || op->use_pa || op->cg_variant != 0 || op->mesh->hex) return 1;
+  return (op->x_defer >= 4 && !op->peer_on) ? 4 : 2;
+}
+// the p buffers of the deferral group: iteration phase j writes p into buf[j % m] and reads p_old
+// from buf[(j - 1) % m]; buf[m - 1] is p_pl, the buffer cg_begin initialises (so the first
+// iteration's p_old, multiplied by beta = 0, is finite)
+static void p_ring(fem_op_s* op, int m, double** buf, const CUtensorMap** maps) {
+  if (m == 4) {
+    double* b[4] = {op->p2_pl, op->p3_pl, op->p4_pl, op->p_pl};
+    const CUtensorMap* t[4] = {&op->tm_p2, &op->tm_p3, &op->tm_p4, &op->tm_p};
+    for (int i = 0; i < 4; ++i) { buf[i] = b[i]; maps[i] = t[i]; }
+  } else {
+    buf[0] = op->p2_pl; buf[1] = op->p_pl;
+    maps[0] = &op->tm_p2; maps[1] = &op->tm_p;
+  }
+}
+static int ensure_p_ring(fem_op_s* op) {
+  if (x_defer_m(op) < 4 || op->p3_pl) return FEM_OK;
+  CUDA_TRY(cudaMalloc(&op->p3_pl, sizeof(double) * op->pl_n));
+  CUDA_TRY(cudaMalloc(&op->p4_pl, sizeof(double) * op->pl_n));
+  CUDA_TRY(cudaMemset(op->p3_pl, 0, sizeof(double) * op->pl_n));
+  CUDA_TRY(cudaMemset(op->p4_pl, 0, sizeof(double) * op->pl_n));
+  drop_graphs(op);
+  return make_pl_maps(op);
 }
 
-static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
+static int cg_fused_body(fem_op_s* op, int phase, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
-  double* pold = parity ? op->p2_pl : op->p_pl;
-  double* pnew = parity ? op->p_pl : op->p2_pl;
+  const int xm = x_defer_m(op);
+  double* pb[4];
+  const CUtensorMap* pmap[4];
+  p_ring(op, xm, pb, pmap);
+  const int gm = xm == 4 ? 4 : 2;  // ring length (m = 1 keeps the ping-pong pair)
+  const int jn = phase % gm, jo = (phase + gm - 1) % gm;
+  double* pold = pb[jo];
+  double* pnew = pb[jn];
   static thread_local PeerMaps pm;
   const bool peer = fill_peer(op, op->r_pl, pold, &pm);
   if (timed) FEM_TRY(apply_event(op, 0, s));
   ApplyMaps maps{&op->tm_r, op->tm_i0, op->tm_j0, op->tm_k0, &op->tm_mat, op->mat_layer0,
-                 parity ? &op->tm_p2 : &op->tm_p, pl_owned(op, pold), pl_owned(op, pnew),
+                 pmap[jo], pl_owned(op, pold), pl_owned(op, pnew),
                  op->tm_interior ? 1 : 0, op->quad, peer ? &pm : nullptr};
   // the two dots per option "dot_mode" (Reduce::dot_mode; the paper's dot ablation)
   Reduce rd = op->red;
@@ -1784,11 +1823,21 @@ static int cg_fused_body(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
     if (e != cudaSuccess) return fail(FEM_ECUDA, "dot launch: %s", cudaGetErrorString(e));
   }
   FEM_TRY(allreduce1(op, &op->sc->pq, s));
-  // paired x update: iteration parity 0 leaves alpha p pending (p in p2_pl, the p_old of the
-  // parity-1 iteration that follows), parity 1 adds both halves of the pair
-  const int xpair = x_pairs_active(op) ? (parity ? 2 : 1) : 0;
+  // deferred x update: phases 0 .. m-2 of a group leave alpha p pending (p stays in its ring
+  // buffer until the group's last phase), phase m-1 adds the group's m updates in order
+  const double* po[3] = {nullptr, nullptr, nullptr};
+  int nold = 0;
+  if (xm > 1) {
+    const int j = phase % xm;
+    if (j < xm - 1) {
+      nold = -1;
+    } else {
+      nold = xm - 1;
+      for (int k = 0; k < nold; ++k) po[k] = pl_owned(op, pb[k]);
+    }
+  }
   e = launch_cg_update_fused(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, pnew),
-                             pl_owned(op, op->q_pl), n, op->sc, rd, s, m->sm_count, xpair, pl_owned(op, pold));
+                             pl_owned(op, op->q_pl), n, op->sc, rd, s, m->sm_count, nold, po, phase % xm);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
   if (op->dot_mode == 1) {  // r.r by a separate kernel re-reading r
     e = launch_cg_dot(pl_owned(op, op->r_pl), pl_owned(op, op->r_pl), n, 1, op->sc, op->red, s, m->sm_count);
@@ -1834,7 +1883,7 @@ static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGrap
   const int64_t before = g_launches.load();
   int st = FEM_OK;
   op->ev_capture = timed;
-  for (int t = 0; t < iters && st == FEM_OK; ++t) st = iteration(op, (parity + t) & 1, cs, timed);
+  for (int t = 0; t < iters && st == FEM_OK; ++t) st = iteration(op, (parity + t) & 3, cs, timed);
   op->ev_capture = false;
   if (timed) op->ev_used = 0;  // set at each replay
   if (launches) *launches = g_launches.load() - before;
@@ -1861,6 +1910,7 @@ static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGrap
 // CG on the padded copies: x_pl = x0; r = b - A x0; p = r (the caller's x is written at the end)
 static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, int maxit, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
+  FEM_TRY(ensure_p_ring(op));  // (x_defer = 4: two more p buffers on first use)
   FEM_TRY(pack(op, x, op->x_pl, 1, s));
   // peer halo: the neighbours must have packed their x0 before this rank's apply reads it
   if (op->peer_on && m->nranks > 1) FEM_TRY(allreduce1(op, op->dot_dev, s));
@@ -1901,13 +1951,13 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
       if (t.exec == ge) add_launches(t.launches);
     CUDA_TRY(cudaGraphLaunch(ge, s));
     op->ev_used = 2 * (size_t)iters;
-    op->cg_parity ^= (iters & 1);
+    op->cg_parity = (op->cg_parity + iters) & 3;
     return FEM_OK;
   }
   if (op->time_apply || !op->use_graph || loop) {
     for (int t = 0; t < iters; ++t) {
       FEM_TRY(iteration(op, op->cg_parity, s, op->time_apply != 0));
-      op->cg_parity ^= 1;
+      op->cg_parity = (op->cg_parity + 1) & 3;
     }
     return FEM_OK;
   }
@@ -1931,7 +1981,7 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
     for (const auto& t : op->graphK)
       if (t.exec == ge) add_launches(t.launches);
     CUDA_TRY(cudaGraphLaunch(ge, s));
-    op->cg_parity ^= (k & 1);
+    op->cg_parity = (op->cg_parity + k) & 3;
     return FEM_OK;
   };
   int left = iters;
@@ -1944,13 +1994,18 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
 }
 
 static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
-  if (x_pairs_active(op)) {  // the first half of a pair, if the solve ended after it
-    const cudaError_t e = launch_cg_xpair_flush(pl_owned(op, op->x_pl), pl_owned(op, op->p2_pl), pl_count(op),
-                                                op->sc, s, op->mesh->sm_count);
+  const int xm = x_defer_m(op);
+  if (xm > 1) {  // the pending updates of an unfinished group, if the solve ended inside one
+    double* pb[4];
+    const CUtensorMap* pmap[4];
+    p_ring(op, xm, pb, pmap);
+    const double* pend[3] = {pl_owned(op, pb[0]), pl_owned(op, pb[xm == 4 ? 1 : 0]), pl_owned(op, pb[xm == 4 ? 2 : 0])};
+    const cudaError_t e = launch_cg_xdefer_flush(pl_owned(op, op->x_pl), pend, pl_count(op), op->sc, s,
+                                                 op->mesh->sm_count);
     if (e != cudaSuccess) return fail(FEM_ECUDA, "x update launch: %s", cudaGetErrorString(e));
   }
   // peer halo: the true-residual apply below reads the neighbours' x -- wait for their last x update
-  if (op->peer_on && op->mesh->nranks > 1 && x_pairs_active(op))
+  if (op->peer_on && op->mesh->nranks > 1 && xm > 1)
     FEM_TRY(allreduce1(op, op->dot_dev, s));
   FEM_TRY(pack(op, op->cg_x, op->x_pl, 0, s));  // x = x_pl (caller layout)
   CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
@@ -2108,9 +2163,10 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
     drop_graphs(op);
   } else if (!std::strcmp(key, "trace")) {
     op->trace = value != 0;
-  } else if (!std::strcmp(key, "x_pairs")) {
-    if (op->cg_active) return fail(FEM_ESTATE, "x_pairs cannot change during a CG solve");
-    op->x_pairs = value != 0;
+  } else if (!std::strcmp(key, "x_defer")) {
+    if (value != 1 && value != 2 && value != 4) return fail(FEM_EINVAL, "x_defer must be 1, 2 or 4");
+    if (op->cg_active) return fail(FEM_ESTATE, "x_defer cannot change during a CG solve");
+    op->x_defer = (int)value;
     drop_graphs(op);
   } else if (!std::strcmp(key, "deterministic")) {
     if (!op->mesh->hex) return fail(FEM_EUNSUPPORTED, "deterministic: general hex meshes (the box kernels are atomic-free)");
@@ -2185,7 +2241,7 @@ int fem_get_option(fem_op_t op, const char* key, int64_t* value) {
   else if (!std::strcmp(key, "halo_overlap")) *value = op->overlap;
   else if (!std::strcmp(key, "trace")) *value = op->trace;
   else if (!std::strcmp(key, "deterministic")) *value = op->mesh->hex ? op->det : 1;
-  else if (!std::strcmp(key, "x_pairs")) *value = x_pairs_active(op) ? 1 : 0;
+  else if (!std::strcmp(key, "x_defer")) *value = x_defer_m(op);
   else if (!std::strncmp(key, "trace_", 6)) {
     // trace_{halo,interior,boundary,total}_ns of the last traced exchange apply (blocks on it)
     static const char* names[4] = {"trace_halo_ns", "trace_interior_ns", "trace_boundary_ns", "trace_total_ns"};

@@ -86,13 +86,13 @@ struct CgScalars {
   double stop_rr;   // tol^2 * rr0
   double alpha;     // Chronopoulos-Gear CG: alpha of the last update
   double rr_acc;    // dot_mode 2: atomic accumulator of the update's r.r
-  double alpha_p;   // paired x update: alpha of the pending first iteration of a pair
+  double alpha_h[3];  // deferred x update: alphas of the pending iterations of the group
   int32_t done;     // 0 running, 1 converged, 2 breakdown, 3 maxit reached
   int32_t it;       // iterations completed
   int32_t maxit;
   int32_t breakdown_iter;
   int32_t first;    // fused CG: 1 before the first apply (beta = 0, p = r)
-  int32_t xp;       // paired x update: 1 if x += alpha_p p (p = the pair's first p, buffer p2) pending
+  int32_t xp;       // deferred x update: number of pending x += alpha_h[j] P_j (P_j in p buffer j)
 };
 
 // Last-block reduction workspace: per-CTA partials + ticket counter.
@@ -211,10 +211,11 @@ cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* 
                               cudaStream_t s, int sm_count);
 // fused CG: x += alpha p; r -= alpha q; rr_new = r.r; iteration bookkeeping (p update is in the apply)
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
-                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int xpair = 0, const double* pold = nullptr);
-// paired x update: x += alpha_p p if the first half of a pair is pending (end of a solve)
-cudaError_t launch_cg_xpair_flush(double* x, const double* p, int64_t n, const CgScalars* sc, cudaStream_t s,
-                                  int sm_count);
+                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold = 0,
+                                   const double* const* pold = nullptr, int jpend = 0);
+// deferred x update: x += alpha_h[j] P_j for the sc->xp pending iterations (end of a solve)
+cudaError_t launch_cg_xdefer_flush(double* x, const double* const* pend, int64_t n, const CgScalars* sc,
+                                   cudaStream_t s, int sm_count);
 // general hexahedral meshes (kernels_hex.cu): cells = 2 int4 per cell (node ids in corner-bit
 // order, bit 31 = Dirichlet node), xyz = node coordinates (w unused), lm = (lambda, mu) per cell.
 // mode 0: y += A (P x) at unconstrained nodes (y zeroed by the caller); mode 1: + sc->pq = the

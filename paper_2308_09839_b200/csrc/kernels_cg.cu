@@ -49,7 +49,7 @@ __global__ void cg_finish_init_kernel(CgScalars* sc, double tol, int maxit) {
   sc->stop_rr = tol * tol * rr;
   sc->pq = 0.0;
   sc->rr_acc = 0.0;
-  sc->alpha_p = 0.0;
+  sc->alpha_h[0] = sc->alpha_h[1] = sc->alpha_h[2] = 0.0;
   sc->xp = 0;
   sc->it = 0;
   sc->maxit = maxit;
@@ -91,24 +91,27 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 // fused CG (mode-2 apply has formed p = r + beta p_old and q = A p):
 //   alpha = rr / pq; x += alpha p; r -= alpha q; rr_new = r.r; it++; convergence -> done.
 // The next mode-2 apply reads beta = rr_new / rr and rolls rr = rr_new in its last block.
-// XM, how x is advanced (DESIGN.md §5.3 "paired x update"):
-//   0  x += alpha p                                                  (48 B/DOF)
-//   1  x untouched: the first iteration of a pair (alpha and p stay pending: p lives in the p
-//      ping-pong buffer the next apply reads as p_old and does not overwrite)   (24 B/DOF)
-//   2  second iteration of a pair: x = (x + alpha_p p_old) + alpha p, the two updates in their
-//      sequential order (bitwise the same x as XM = 0 twice)         (56 B/DOF)
-// so a pair of iterations moves 80 instead of 96 B/DOF of update traffic.
+// Deferred x update (option x_defer = m): the fused CG keeps the p of m
+// consecutive iterations in m buffers (the apply writes p_k into buffer k mod m and reads p_{k-1}
+// as p_old), so x needs updating only every m-th iteration.  NOLD selects the update's x work:
+//   -1  x untouched: alpha is left pending (sc->alpha_h[j], sc->xp = j + 1)        (24 B/DOF)
+//   k   x = (((x + alpha_0 P_0) + ...) + alpha_{k-1} P_{k-1}) + alpha p: the k pending updates,
+//       then this one, in their sequential order -- bitwise the x of k + 1 per-iteration updates
+//       (k = 0: the plain x += alpha p, 48 B/DOF; k = 1: 56; k = 3: 72)
+// so m = 2 moves 80 instead of 96 B/DOF of update traffic per two iterations, m = 4 144 / 192.
 #ifndef FEM_UPD_MINB
 #define FEM_UPD_MINB 3  // resident blocks per SM the fused update kernel is compiled for (80 registers)
 #endif
-template <int XM>
+struct OldP {
+  const double* p[3];  // the pending p vectors P_0 .. P_{NOLD-1}
+};
+template <int NOLD>
 __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
                                                                       double* __restrict__ r,
                                                                       const double* __restrict__ p,
-                                                                      const double* __restrict__ pold,
                                                                       const double* __restrict__ q,
                                                                       int64_t n, CgScalars* sc,
-                                                                      Reduce red) {
+                                                                      Reduce red, OldP po, int jpend) {
   __shared__ double sh[32];
   if (sc->done) return;
   // convergence of the current iterate: rr_new is the allreduced (rank-global) r.r of the
@@ -127,23 +130,28 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
     return;
   }
   const double alpha = sc->rr / pq;
-  // (alpha_p / xp are read by later kernels only: block 0 may write them) the next update adds
-  // alpha p (its p_old) before its own alpha p
-  if (XM == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
-    sc->alpha_p = alpha;
-    sc->xp = 1;
+  // (alpha_h / xp are read by later kernels only: block 0 may write them)
+  if (NOLD < 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->alpha_h[jpend] = alpha;
+    sc->xp = jpend + 1;
   }
-  const double ap = (XM == 2) ? sc->alpha_p : 0.0;
-  if (XM == 2 && blockIdx.x == 0 && threadIdx.x == 0) sc->xp = 0;
+  double ah[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) ah[k] = sc->alpha_h[k];
+  if (NOLD > 0 && blockIdx.x == 0 && threadIdx.x == 0) sc->xp = 0;
   double acc = 0.0;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // 16-B vector accesses (the five vectors share one layout, hence one alignment); a leading
+  // 16-B vector accesses (the vectors share one layout, hence one alignment); a leading
   // unaligned element and a trailing odd element are handled by thread 0 / the last thread
   const int64_t head = (reinterpret_cast<uintptr_t>(r) & 15) ? 1 : 0;
   auto one = [&](int64_t i) {
-    if (XM == 0) x[i] = fma(alpha, p[i], x[i]);
-    if (XM == 2) x[i] = fma(alpha, p[i], fma(ap, pold[i], x[i]));
+    if (NOLD >= 0) {
+      double xv = x[i];
+#pragma unroll
+      for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) xv = fma(ah[k], po.p[k][i], xv);
+      x[i] = fma(alpha, p[i], xv);
+    }
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
     acc = fma(ri, ri, acc);
@@ -153,28 +161,34 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
   double2* __restrict__ x2 = reinterpret_cast<double2*>(x + head);
   double2* __restrict__ r2 = reinterpret_cast<double2*>(r + head);
   const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p + head);
-  const double2* __restrict__ o2 = reinterpret_cast<const double2*>((XM == 2 ? pold : p) + head);
   const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q + head);
   auto xupd = [&](int64_t j) {
-    if (XM == 0) {
-      const double2 pa = p2[j], xa = x2[j];
-      x2[j] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
-    } else if (XM == 2) {
-      const double2 pa = p2[j], oa = o2[j], xa = x2[j];
-      x2[j] = make_double2(fma(alpha, pa.x, fma(ap, oa.x, xa.x)), fma(alpha, pa.y, fma(ap, oa.y, xa.y)));
+    if (NOLD < 0) return;
+    double2 xa = x2[j];
+    double2 o[3];
+#pragma unroll
+    for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) o[k] = reinterpret_cast<const double2*>(po.p[k] + head)[j];
+    const double2 pa = p2[j];
+#pragma unroll
+    for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) {
+      xa.x = fma(ah[k], o[k].x, xa.x);
+      xa.y = fma(ah[k], o[k].y, xa.y);
     }
+    x2[j] = make_double2(fma(alpha, pa.x, xa.x), fma(alpha, pa.y, xa.y));
   };
   int64_t i = gtid;
-  for (; i + stride < n2; i += 2 * stride) {  // two independent 16-B groups in flight per thread
-    const double2 qa = q2[i], qb = q2[i + stride], ra = r2[i], rb = r2[i + stride];
-    xupd(i);
-    xupd(i + stride);
-    const double2 na = make_double2(fma(-alpha, qa.x, ra.x), fma(-alpha, qa.y, ra.y));
-    const double2 nb = make_double2(fma(-alpha, qb.x, rb.x), fma(-alpha, qb.y, rb.y));
-    r2[i] = na;
-    r2[i + stride] = nb;
-    acc = fma(na.x, na.x, acc); acc = fma(na.y, na.y, acc);
-    acc = fma(nb.x, nb.x, acc); acc = fma(nb.y, nb.y, acc);
+  if (NOLD <= 1) {
+    for (; i + stride < n2; i += 2 * stride) {  // two independent 16-B groups in flight per thread
+      const double2 qa = q2[i], qb = q2[i + stride], ra = r2[i], rb = r2[i + stride];
+      xupd(i);
+      xupd(i + stride);
+      const double2 na = make_double2(fma(-alpha, qa.x, ra.x), fma(-alpha, qa.y, ra.y));
+      const double2 nb = make_double2(fma(-alpha, qb.x, rb.x), fma(-alpha, qb.y, rb.y));
+      r2[i] = na;
+      r2[i + stride] = nb;
+      acc = fma(na.x, na.x, acc); acc = fma(na.y, na.y, acc);
+      acc = fma(nb.x, nb.x, acc); acc = fma(nb.y, nb.y, acc);
+    }
   }
   for (; i < n2; i += stride) {
     const double2 qa = q2[i], ra = r2[i];
@@ -402,27 +416,41 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
   return cudaGetLastError();
 }
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
-                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count,
-                                   int xpair, const double* pold) {
+                                   CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
+                                   const double* const* pold, int jpend) {
   const unsigned nb = vec_blocks(n, sm_count);
-  if (xpair == 1) cg_update_fused_kernel<1><<<nb, kVecThreads, 0, s>>>(x, r, p, p, q, n, sc, red);
-  else if (xpair == 2) cg_update_fused_kernel<2><<<nb, kVecThreads, 0, s>>>(x, r, p, pold, q, n, sc, red);
-  else cg_update_fused_kernel<0><<<nb, kVecThreads, 0, s>>>(x, r, p, p, q, n, sc, red);
+  OldP po{{p, p, p}};
+  for (int k = 0; k < nold && k < 3; ++k) po.p[k] = pold[k];
+  switch (nold) {
+    case -1: cg_update_fused_kernel<-1><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, jpend); break;
+    case 0: cg_update_fused_kernel<0><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
+    case 1: cg_update_fused_kernel<1><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
+    case 3: cg_update_fused_kernel<3><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
+    default: return cudaErrorInvalidValue;
+  }
   add_launches(1);
   return cudaGetLastError();
 }
 
-// paired x update, end of a solve: the pending first half of a pair (x += alpha_p p) if any
-__global__ void __launch_bounds__(kVecThreads) cg_xpair_flush_kernel(double* __restrict__ x, const double* __restrict__ p,
-                                                                     int64_t n, const CgScalars* sc) {
-  if (!sc->xp) return;
-  const double a = sc->alpha_p;
+// deferred x update, end of a solve: the xp pending updates x += alpha_j P_j, in order
+__global__ void __launch_bounds__(kVecThreads) cg_xdefer_flush_kernel(double* __restrict__ x, OldP po, int64_t n,
+                                                                      const CgScalars* sc) {
+  const int np = sc->xp;
+  if (np <= 0) return;
+  double ah[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) ah[k] = k < np ? sc->alpha_h[k] : 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) x[i] = fma(a, p[i], x[i]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double xv = x[i];
+    for (int k = 0; k < np && k < 3; ++k) xv = fma(ah[k], po.p[k][i], xv);
+    x[i] = xv;
+  }
 }
-cudaError_t launch_cg_xpair_flush(double* x, const double* p, int64_t n, const CgScalars* sc, cudaStream_t s,
-                                  int sm_count) {
-  cg_xpair_flush_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, p, n, sc);
+cudaError_t launch_cg_xdefer_flush(double* x, const double* const* pend, int64_t n, const CgScalars* sc,
+                                   cudaStream_t s, int sm_count) {
+  OldP po{{pend[0], pend[1], pend[2]}};
+  cg_xdefer_flush_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, po, n, sc);
   add_launches(1);
   return cudaGetLastError();
 }
