@@ -328,9 +328,9 @@ def run_native(args, cfg):
         op.cg_iterate(k)
         its[0] += k
 
-    def even():  # every K-step pass starts at phase 0 of the p-buffer ring (4 buffers with x_defer 4)
-        if its[0] % 4:
-            iterate(4 - its[0] % 4)
+    def even():  # every K-step pass starts at phase 0 of the p-buffer ring (m buffers, x_defer m <= 8)
+        if its[0] % 8:
+            iterate(8 - its[0] % 8)
 
     iterate(args.warmup)
     even()
@@ -700,7 +700,7 @@ def main():
                     help="how the fused CG forms p.Ap and r.r (option dot_mode; P:714-728 ablation)")
     ap.add_argument("--gll", action="store_true",
                     help="2x2x2 Gauss-Lobatto quadrature (the CEED BP5/BP6 operators) instead of Gauss")
-    ap.add_argument("--x-defer", type=int, default=0, choices=[0, 1, 2, 4],
+    ap.add_argument("--x-defer", type=int, default=0, choices=[0, 1, 2, 4, 8],
                     help="fused CG: x updated every m-th iteration from the group's p buffers (0: library default)")
     ap.add_argument("--det", action="store_true",
                     help="general-hex configs (6/7): deterministic scatter (element outputs + node gather)")

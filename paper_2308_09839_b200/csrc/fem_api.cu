@@ -24,7 +24,7 @@
 #include "fem_internal.cuh"
 
 #ifndef FEM_X_DEFER
-#define FEM_X_DEFER 4  // fused CG: x updated every FEM_X_DEFER-th iteration (1, 2 or 4; option x_defer)
+#define FEM_X_DEFER 8  // fused CG: x updated every FEM_X_DEFER-th iteration (1, 2, 4 or 8; option x_defer)
 #endif
 
 namespace fem {
@@ -172,9 +172,10 @@ struct fem_op_s {
   int64_t pl_lead = 0, pl_rp = 0, pl_pp = 0, pl_n = 0;
   int64_t pl_off = 0;  // offset of the owned range (pl_lead + pl_pp; 0 on general hex meshes)
   double *x_pl = nullptr, *r_pl = nullptr, *p_pl = nullptr, *q_pl = nullptr, *p2_pl = nullptr;
-  double *p3_pl = nullptr, *p4_pl = nullptr;  // deferred x update over 4 iterations (allocated on use)
-  CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{}, tm_p3{}, tm_p4{};
-  int cg_parity = 0;  // fused CG: iteration phase mod 4 (selects the p buffers)
+  // deferred x update over m = 4 / 8 iterations: m - 2 more p buffers (allocated on use)
+  double* pex[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{}, tm_pex[6]{};
+  int cg_parity = 0;  // fused CG: iteration phase mod 8 (selects the p buffers)
   bool tm_ok = false;
   bool tm_interior = false;  // u tensor spans the interior only (Laplace + Dirichlet)
   int64_t tm_i0 = 0, tm_j0 = 0, tm_k0 = 0;
@@ -559,10 +560,11 @@ static int make_pl_maps(fem_op_s* op) {
   op->tm_j0 = lo;
   op->tm_k0 = k0;
   const int64_t off = op->pl_lead + (k0 - (g.k0 - 1)) * op->pl_pp + lo * op->pl_rp + lo * C;
-  double* vecs[6] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl, op->p3_pl, op->p4_pl};
-  CUtensorMap* maps[6] = {&op->tm_x, &op->tm_p, &op->tm_r, &op->tm_p2, &op->tm_p3, &op->tm_p4};
-  for (int v = 0; v < 6; ++v) {
-    if (!vecs[v]) continue;  // (p3, p4: allocated for x_defer = 4 only)
+  double* vecs[10] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl};
+  CUtensorMap* maps[10] = {&op->tm_x, &op->tm_p, &op->tm_r, &op->tm_p2};
+  for (int e = 0; e < 6; ++e) { vecs[4 + e] = op->pex[e]; maps[4 + e] = &op->tm_pex[e]; }
+  for (int v = 0; v < 10; ++v) {
+    if (!vecs[v]) continue;  // (pex: allocated for x_defer >= 4 only)
     FEM_TRY(make_map3d(maps[v], vecs[v] + off, (uint64_t)((i1 - lo + 1) * C), (uint64_t)(j1 - lo + 1),
                        (uint64_t)(k1 - k0 + 1), op->pl_rp * 8, op->pl_pp * 8, bw, bh));
   }
@@ -1293,7 +1295,7 @@ static void op_free(fem_op_s* op) {
   cudaFree(op->hx_E);
   cudaFree(op->last_plane);
   cudaFree(op->x_pl); cudaFree(op->r_pl); cudaFree(op->p_pl); cudaFree(op->q_pl); cudaFree(op->p2_pl);
-  cudaFree(op->p3_pl); cudaFree(op->p4_pl);
+  for (double* e : op->pex) cudaFree(e);
   if (op->graph1b) cudaGraphExecDestroy(op->graph1b);
   for (const auto& t : op->graphT) cudaGraphExecDestroy(t.exec);
   for (const auto& t : op->graphK) cudaGraphExecDestroy(t.exec);
@@ -1759,27 +1761,27 @@ static void drop_graphs(fem_op_s* op);
 // so with it m is at most 2.
 static int x_defer_m(const fem_op_s* op) {
   if (op->x_defer <= 1 || !op->tm_ok || op->use_pa || op->cg_variant != 0 || op->mesh->hex) return 1;
-  return (op->x_defer >= 4 && !op->peer_on) ? 4 : 2;
+  return op->peer_on ? 2 : op->x_defer;
 }
 // the p buffers of the deferral group: iteration phase j writes p into buf[j % m] and reads p_old
 // from buf[(j - 1) % m]; buf[m - 1] is p_pl, the buffer cg_begin initialises (so the first
 // iteration's p_old, multiplied by beta = 0, is finite)
 static void p_ring(fem_op_s* op, int m, double** buf, const CUtensorMap** maps) {
-  if (m == 4) {
-    double* b[4] = {op->p2_pl, op->p3_pl, op->p4_pl, op->p_pl};
-    const CUtensorMap* t[4] = {&op->tm_p2, &op->tm_p3, &op->tm_p4, &op->tm_p};
-    for (int i = 0; i < 4; ++i) { buf[i] = b[i]; maps[i] = t[i]; }
-  } else {
-    buf[0] = op->p2_pl; buf[1] = op->p_pl;
-    maps[0] = &op->tm_p2; maps[1] = &op->tm_p;
-  }
+  const int g = m < 2 ? 2 : m;  // (m = 1 keeps the ping-pong pair)
+  buf[0] = op->p2_pl; maps[0] = &op->tm_p2;
+  for (int i = 1; i < g - 1; ++i) { buf[i] = op->pex[i - 1]; maps[i] = &op->tm_pex[i - 1]; }
+  buf[g - 1] = op->p_pl; maps[g - 1] = &op->tm_p;
 }
 static int ensure_p_ring(fem_op_s* op) {
-  if (x_defer_m(op) < 4 || op->p3_pl) return FEM_OK;
-  CUDA_TRY(cudaMalloc(&op->p3_pl, sizeof(double) * op->pl_n));
-  CUDA_TRY(cudaMalloc(&op->p4_pl, sizeof(double) * op->pl_n));
-  CUDA_TRY(cudaMemset(op->p3_pl, 0, sizeof(double) * op->pl_n));
-  CUDA_TRY(cudaMemset(op->p4_pl, 0, sizeof(double) * op->pl_n));
+  const int m = x_defer_m(op);
+  bool grew = false;
+  for (int e = 0; e < m - 2; ++e) {
+    if (op->pex[e]) continue;
+    CUDA_TRY(cudaMalloc(&op->pex[e], sizeof(double) * op->pl_n));
+    CUDA_TRY(cudaMemset(op->pex[e], 0, sizeof(double) * op->pl_n));
+    grew = true;
+  }
+  if (!grew) return FEM_OK;
   drop_graphs(op);
   return make_pl_maps(op);
 }
@@ -1787,10 +1789,10 @@ static int ensure_p_ring(fem_op_s* op) {
 static int cg_fused_body(fem_op_s* op, int phase, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
   const int xm = x_defer_m(op);
-  double* pb[4];
-  const CUtensorMap* pmap[4];
+  double* pb[8];
+  const CUtensorMap* pmap[8];
   p_ring(op, xm, pb, pmap);
-  const int gm = xm == 4 ? 4 : 2;  // ring length (m = 1 keeps the ping-pong pair)
+  const int gm = xm < 2 ? 2 : xm;  // ring length (m = 1 keeps the ping-pong pair)
   const int jn = phase % gm, jo = (phase + gm - 1) % gm;
   double* pold = pb[jo];
   double* pnew = pb[jn];
@@ -1825,7 +1827,7 @@ static int cg_fused_body(fem_op_s* op, int phase, cudaStream_t s, bool timed) {
   FEM_TRY(allreduce1(op, &op->sc->pq, s));
   // deferred x update: phases 0 .. m-2 of a group leave alpha p pending (p stays in its ring
   // buffer until the group's last phase), phase m-1 adds the group's m updates in order
-  const double* po[3] = {nullptr, nullptr, nullptr};
+  const double* po[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int nold = 0;
   if (xm > 1) {
     const int j = phase % xm;
@@ -1883,7 +1885,7 @@ static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGrap
   const int64_t before = g_launches.load();
   int st = FEM_OK;
   op->ev_capture = timed;
-  for (int t = 0; t < iters && st == FEM_OK; ++t) st = iteration(op, (parity + t) & 3, cs, timed);
+  for (int t = 0; t < iters && st == FEM_OK; ++t) st = iteration(op, (parity + t) & 7, cs, timed);
   op->ev_capture = false;
   if (timed) op->ev_used = 0;  // set at each replay
   if (launches) *launches = g_launches.load() - before;
@@ -1910,7 +1912,7 @@ static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGrap
 // CG on the padded copies: x_pl = x0; r = b - A x0; p = r (the caller's x is written at the end)
 static int cg_begin_dev(fem_op_s* op, const double* b, double* x, double tol, int maxit, cudaStream_t s) {
   fem_mesh_s* m = op->mesh;
-  FEM_TRY(ensure_p_ring(op));  // (x_defer = 4: two more p buffers on first use)
+  FEM_TRY(ensure_p_ring(op));  // (x_defer = m >= 4: m - 2 more p buffers on first use)
   FEM_TRY(pack(op, x, op->x_pl, 1, s));
   // peer halo: the neighbours must have packed their x0 before this rank's apply reads it
   if (op->peer_on && m->nranks > 1) FEM_TRY(allreduce1(op, op->dot_dev, s));
@@ -1951,13 +1953,13 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
       if (t.exec == ge) add_launches(t.launches);
     CUDA_TRY(cudaGraphLaunch(ge, s));
     op->ev_used = 2 * (size_t)iters;
-    op->cg_parity = (op->cg_parity + iters) & 3;
+    op->cg_parity = (op->cg_parity + iters) & 7;
     return FEM_OK;
   }
   if (op->time_apply || !op->use_graph || loop) {
     for (int t = 0; t < iters; ++t) {
       FEM_TRY(iteration(op, op->cg_parity, s, op->time_apply != 0));
-      op->cg_parity = (op->cg_parity + 1) & 3;
+      op->cg_parity = (op->cg_parity + 1) & 7;
     }
     return FEM_OK;
   }
@@ -1981,7 +1983,7 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
     for (const auto& t : op->graphK)
       if (t.exec == ge) add_launches(t.launches);
     CUDA_TRY(cudaGraphLaunch(ge, s));
-    op->cg_parity = (op->cg_parity + k) & 3;
+    op->cg_parity = (op->cg_parity + k) & 7;
     return FEM_OK;
   };
   int left = iters;
@@ -1996,10 +1998,11 @@ static int cg_iterate_dev(fem_op_s* op, int iters, cudaStream_t s) {
 static int cg_end_dev(fem_op_s* op, fem_cg_info* info, cudaStream_t s) {
   const int xm = x_defer_m(op);
   if (xm > 1) {  // the pending updates of an unfinished group, if the solve ended inside one
-    double* pb[4];
-    const CUtensorMap* pmap[4];
+    double* pb[8];
+    const CUtensorMap* pmap[8];
     p_ring(op, xm, pb, pmap);
-    const double* pend[3] = {pl_owned(op, pb[0]), pl_owned(op, pb[xm == 4 ? 1 : 0]), pl_owned(op, pb[xm == 4 ? 2 : 0])};
+    const double* pend[7];
+    for (int k = 0; k < 7; ++k) pend[k] = pl_owned(op, pb[k < xm - 1 ? k : 0]);
     const cudaError_t e = launch_cg_xdefer_flush(pl_owned(op, op->x_pl), pend, pl_count(op), op->sc, s,
                                                  op->mesh->sm_count);
     if (e != cudaSuccess) return fail(FEM_ECUDA, "x update launch: %s", cudaGetErrorString(e));
@@ -2164,7 +2167,7 @@ int fem_set_option(fem_op_t op, const char* key, int64_t value) {
   } else if (!std::strcmp(key, "trace")) {
     op->trace = value != 0;
   } else if (!std::strcmp(key, "x_defer")) {
-    if (value != 1 && value != 2 && value != 4) return fail(FEM_EINVAL, "x_defer must be 1, 2 or 4");
+    if (value != 1 && value != 2 && value != 4 && value != 8) return fail(FEM_EINVAL, "x_defer must be 1, 2, 4 or 8");
     if (op->cg_active) return fail(FEM_ESTATE, "x_defer cannot change during a CG solve");
     op->x_defer = (int)value;
     drop_graphs(op);

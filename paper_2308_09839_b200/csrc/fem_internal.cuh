@@ -86,7 +86,7 @@ struct CgScalars {
   double stop_rr;   // tol^2 * rr0
   double alpha;     // Chronopoulos-Gear CG: alpha of the last update
   double rr_acc;    // dot_mode 2: atomic accumulator of the update's r.r
-  double alpha_h[3];  // deferred x update: alphas of the pending iterations of the group
+  double alpha_h[7];  // deferred x update: alphas of the pending iterations of the group
   int32_t done;     // 0 running, 1 converged, 2 breakdown, 3 maxit reached
   int32_t it;       // iterations completed
   int32_t maxit;

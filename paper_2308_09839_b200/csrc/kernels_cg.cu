@@ -49,7 +49,7 @@ __global__ void cg_finish_init_kernel(CgScalars* sc, double tol, int maxit) {
   sc->stop_rr = tol * tol * rr;
   sc->pq = 0.0;
   sc->rr_acc = 0.0;
-  sc->alpha_h[0] = sc->alpha_h[1] = sc->alpha_h[2] = 0.0;
+  for (int k = 0; k < 7; ++k) sc->alpha_h[k] = 0.0;
   sc->xp = 0;
   sc->it = 0;
   sc->maxit = maxit;
@@ -97,13 +97,13 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 //   -1  x untouched: alpha is left pending (sc->alpha_h[j], sc->xp = j + 1)        (24 B/DOF)
 //   k   x = (((x + alpha_0 P_0) + ...) + alpha_{k-1} P_{k-1}) + alpha p: the k pending updates,
 //       then this one, in their sequential order -- bitwise the x of k + 1 per-iteration updates
-//       (k = 0: the plain x += alpha p, 48 B/DOF; k = 1: 56; k = 3: 72)
-// so m = 2 moves 80 instead of 96 B/DOF of update traffic per two iterations, m = 4 144 / 192.
+//       (k = 0: the plain x += alpha p, 48 B/DOF; k = 1: 56; k = 3: 72; k = 7: 104)
+// so a group of m iterations moves 32 m + 16 instead of 48 m B/DOF of update traffic.
 #ifndef FEM_UPD_MINB
 #define FEM_UPD_MINB 3  // resident blocks per SM the fused update kernel is compiled for (80 registers)
 #endif
 struct OldP {
-  const double* p[3];  // the pending p vectors P_0 .. P_{NOLD-1}
+  const double* p[7];  // the pending p vectors P_0 .. P_{NOLD-1}
 };
 template <int NOLD>
 __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
     sc->alpha_h[jpend] = alpha;
     sc->xp = jpend + 1;
   }
-  double ah[3] = {0.0, 0.0, 0.0};
+  double ah[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) ah[k] = sc->alpha_h[k];
   if (NOLD > 0 && blockIdx.x == 0 && threadIdx.x == 0) sc->xp = 0;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
   auto xupd = [&](int64_t j) {
     if (NOLD < 0) return;
     double2 xa = x2[j];
-    double2 o[3];
+    double2 o[7];
 #pragma unroll
     for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) o[k] = reinterpret_cast<const double2*>(po.p[k] + head)[j];
     const double2 pa = p2[j];
@@ -419,13 +419,14 @@ cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const 
                                    CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
                                    const double* const* pold, int jpend) {
   const unsigned nb = vec_blocks(n, sm_count);
-  OldP po{{p, p, p}};
-  for (int k = 0; k < nold && k < 3; ++k) po.p[k] = pold[k];
+  OldP po{{p, p, p, p, p, p, p}};
+  for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
     case -1: cg_update_fused_kernel<-1><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, jpend); break;
     case 0: cg_update_fused_kernel<0><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
     case 1: cg_update_fused_kernel<1><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
     case 3: cg_update_fused_kernel<3><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
+    case 7: cg_update_fused_kernel<7><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
     default: return cudaErrorInvalidValue;
   }
   add_launches(1);
@@ -437,19 +438,19 @@ __global__ void __launch_bounds__(kVecThreads) cg_xdefer_flush_kernel(double* __
                                                                       const CgScalars* sc) {
   const int np = sc->xp;
   if (np <= 0) return;
-  double ah[3];
+  double ah[7];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) ah[k] = k < np ? sc->alpha_h[k] : 0.0;
+  for (int k = 0; k < 7; ++k) ah[k] = k < np ? sc->alpha_h[k] : 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     double xv = x[i];
-    for (int k = 0; k < np && k < 3; ++k) xv = fma(ah[k], po.p[k][i], xv);
+    for (int k = 0; k < np && k < 7; ++k) xv = fma(ah[k], po.p[k][i], xv);
     x[i] = xv;
   }
 }
 cudaError_t launch_cg_xdefer_flush(double* x, const double* const* pend, int64_t n, const CgScalars* sc,
                                    cudaStream_t s, int sm_count) {
-  OldP po{{pend[0], pend[1], pend[2]}};
+  OldP po{{pend[0], pend[1], pend[2], pend[3], pend[4], pend[5], pend[6]}};
   cg_xdefer_flush_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, po, n, sc);
   add_launches(1);
   return cudaGetLastError();

@@ -4,7 +4,7 @@ TAG=${1:-xp}; OUT=gpurun_out/$TAG; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { cat $OUT/build.log; exit 1; }
 timeout 900 python -m pytest -m gpu -q -x tests/test_gpu_xdefer.py tests/test_loopback.py tests/test_gpu_parity.py > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest.log
 tail -5 $OUT/pytest.log
-for c in 3 1 2; do for xp in 1 2 4; do
+for c in 3 1 2; do for xp in 1 4 8; do
   timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu --no-csr --no-e2e --x-defer $xp > $OUT/b_c${c}_xp$xp.json 2> $OUT/b_c${c}_xp$xp.err
   python - $OUT/b_c${c}_xp$xp.json <<'P'
 import json,sys
