@@ -75,11 +75,14 @@ HEX_FLOPS_PER_CELL = {"elastic": 635 + 337 + 2 * 609, "vector": 594 + 345 + 2 * 
 FP64_PEAK_TFLOPS = 2 * 17.08  # own DFMA microbenchmark, profiles/r01_microbench_fp64_hbm.txt
 
 
-def cg_vector_bytes(ndof, fused, x_defer=1):
+def cg_vector_bytes(ndof, fused, x_defer=1, steps=None):
     # update: read x,p,r,q write x,r (48 B/DOF); unfused p-update: read r,p write p (24 B/DOF);
     # deferred x update over m iterations: r, q -> r every iteration, x and the
-    # group's m p vectors -> x once per group: 24 + (16 + 8 m) / m = 32 + 16 / m B/DOF
+    # group's m p vectors -> x once per group: 24 + (16 + 8 m) / m = 32 + 16 / m B/DOF in the
+    # steady state; a timed pass of K steps ending on a group boundary holds ceil(K / m) x updates
     if fused and x_defer > 1:
+        if steps:
+            return (24 + -(-steps // x_defer) * (16 + 8 * x_defer) / steps) * ndof
         return (32 + 16 / x_defer) * ndof
     return (48 if fused else 72) * ndof
 
@@ -318,19 +321,24 @@ def run_native(args, cfg):
 
     # ---- warm-up (W CG steps) ----
     # The timed region replays the library's plain CUDA graph of K iterations (fem_cg_iterate
-    # captures graphs of exactly k <= 64 iterations per ping-pong parity), as fem_cg_solve runs
+    # captures graphs of exactly k <= 64 iterations per p-ring phase), as fem_cg_solve runs
     # them; the warm-up runs W iterations and then K more, so the graph is captured beforehand.
     op.set_option("time_apply", 0)
     op.cg_begin(b, x, tol=0.0, maxit=1 << 30)
-    its = [0]  # iterations run so far: every K-step pass starts on an even ping-pong parity, so
+    its = [0]  # iterations run so far: every K-step pass starts at the same ring phase, so
 
     def iterate(k):  # the graphs the timed passes replay are the ones captured before them
         op.cg_iterate(k)
         its[0] += k
 
-    def even():  # every K-step pass starts at phase 0 of the p-buffer ring (m buffers, x_defer m <= 8)
-        if its[0] % 8:
-            iterate(8 - its[0] % 8)
+    def even():
+        # every K-step pass starts at the same phase of the p-buffer ring (m <= 8 buffers, option
+        # x_defer), chosen so that the pass ENDS on a group boundary: its last iteration performs
+        # the x update of its group, so a pass of K iterations contains ceil(K / m) x updates --
+        # never fewer than the steady-state K / m (the bytes below count exactly these)
+        want = (-args.steps) % 8
+        if its[0] % 8 != want:
+            iterate((want - its[0]) % 8)
 
     iterate(args.warmup)
     even()
@@ -447,7 +455,7 @@ def run_native(args, cfg):
     extra["cg_iteration_ms_event_graph"] = ms_event_graph / args.steps  # the time_apply pass
     extra["apply_share_of_step"] = share
     extra["cg_iteration_ms"] = ms / args.steps
-    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused, x_defer)
+    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused, x_defer, args.steps)
     extra["cg_bytes_per_dof_alg"] = cg_bytes / ndof_global
     extra["cg_iteration_gbs"] = cg_bytes / (ms / args.steps / 1e3) / 1e9
     extra["fused_cg"] = fused
