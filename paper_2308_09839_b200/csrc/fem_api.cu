@@ -207,6 +207,7 @@ struct fem_op_s {
   // fused CG: deferred x update (x advanced every x_defer-th iteration from the p buffers of the
   // group: 1, 2 or 4; option "x_defer")
   int x_defer = FEM_X_DEFER;
+  int x_defer_cap = 8;  // lowered when the p ring does not fit in device memory
   // peer halo: the neighbour ranks' padded vectors x, p, r, p2 (CUDA IPC or, for single-process
   // tests, the other operator's buffers) and tensor maps over their ghost-plane sources
   bool peer_on = false, peer_ipc = false;
@@ -1761,7 +1762,7 @@ static void drop_graphs(fem_op_s* op);
 // so with it m is at most 2.
 static int x_defer_m(const fem_op_s* op) {
   if (op->x_defer <= 1 || !op->tm_ok || op->use_pa || op->cg_variant != 0 || op->mesh->hex) return 1;
-  return op->peer_on ? 2 : op->x_defer;
+  return std::min(op->peer_on ? 2 : op->x_defer, op->x_defer_cap);
 }
 // the p buffers of the deferral group: iteration phase j writes p into buf[j % m] and reads p_old
 // from buf[(j - 1) % m]; buf[m - 1] is p_pl, the buffer cg_begin initialises (so the first
@@ -1772,12 +1773,19 @@ static void p_ring(fem_op_s* op, int m, double** buf, const CUtensorMap** maps) 
   for (int i = 1; i < g - 1; ++i) { buf[i] = op->pex[i - 1]; maps[i] = &op->tm_pex[i - 1]; }
   buf[g - 1] = op->p_pl; maps[g - 1] = &op->tm_p;
 }
+// (out of device memory for m - 2 more p vectors: the group length drops to what fits -- 4, then
+// 2, which needs none -- and stays capped for the operator's lifetime)
 static int ensure_p_ring(fem_op_s* op) {
-  const int m = x_defer_m(op);
   bool grew = false;
-  for (int e = 0; e < m - 2; ++e) {
+  for (int e = 0; e < x_defer_m(op) - 2; ++e) {
     if (op->pex[e]) continue;
-    CUDA_TRY(cudaMalloc(&op->pex[e], sizeof(double) * op->pl_n));
+    if (cudaMalloc(&op->pex[e], sizeof(double) * op->pl_n) != cudaSuccess) {
+      cudaGetLastError();
+      op->pex[e] = nullptr;
+      op->x_defer_cap = e >= 2 ? 4 : 2;  // extra buffers 0 .. e-1 exist: a ring of e + 2 >= m fits
+      e = -1;  // re-check with the cap
+      continue;
+    }
     CUDA_TRY(cudaMemset(op->pex[e], 0, sizeof(double) * op->pl_n));
     grew = true;
   }
