@@ -127,6 +127,31 @@ def test_fullsize_fused_cg(F, idx):
 
 
 @pytest.mark.parametrize("idx", CASES)
+def test_fullsize_x_defer_bitwise(F, idx):
+    """The deferred x update at the bench's sizes and launch configuration: 11 iterations = one
+    complete group of 8 (the 11-stream group update) + 3 pending added by cg_end, bitwise equal to
+    x += alpha p every iteration."""
+    cfg, kind, (nx, ny, nz, h), lam, mu, op = _setup(F, idx)
+    c = I.ncomp(kind)
+    gb = I.rng(I.SEED_BASE + idx + 1000)
+    b = torch.from_numpy(I.interior_rhs(gb, nx, ny, nz, c)).cuda()
+    xs = []
+    for m in (8, 1):
+        op.set_option("x_defer", m)
+        assert op.get_option("x_defer") == m
+        x = torch.zeros_like(b)
+        op.cg_begin(b, x, tol=0.0, maxit=11)
+        op.cg_iterate(11)
+        info = op.cg_end()
+        assert info["iterations"] == 11
+        xs.append(x)
+    assert torch.equal(xs[0], xs[1]), cfg["name"]
+    op.set_option("x_defer", 8)
+    del xs, b
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("idx", CASES)
 def test_fullsize_symmetry(F, idx):
     """x^T (A y) = y^T (A x) with A = A_c (symmetric elimination) at full size."""
     cfg, kind, (nx, ny, nz, h), lam, mu, op = _setup(F, idx)
