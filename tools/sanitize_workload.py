@@ -83,6 +83,11 @@ def main():
             xs = torch.zeros_like(b)
             op.cg_solve(b, xs, tol=0.0, maxit=4)
         op.set_option("dot_mode", 0)
+        for m in (1, 2, 4, 8):  # deferred x update: complete groups + pending updates at cg_end
+            op.set_option("x_defer", m)
+            xs = torch.zeros_like(b)
+            op.cg_solve(b, xs, tol=0.0, maxit=11)
+        op.set_option("x_defer", 8)
         if kind == "elastic":
             op.set_option("partial_assembly", 1)
             op.apply(x)
@@ -114,7 +119,7 @@ def main():
                     xl = dev(x[k0 * plane:k1 * plane])
                     op.apply(xl, stream=st)
                     xs = torch.zeros_like(xl)
-                    op.cg_solve(xl, xs, tol=0.0, maxit=3, stream=st)
+                    op.cg_solve(xl, xs, tol=0.0, maxit=11, stream=st)
                     st.synchronize()
                     op.close(); mesh.close()
             except BaseException as ex:
