@@ -75,11 +75,19 @@ HEX_FLOPS_PER_CELL = {"elastic": 635 + 337 + 2 * 609, "vector": 594 + 345 + 2 * 
 FP64_PEAK_TFLOPS = 2 * 17.08  # own DFMA microbenchmark, profiles/r01_microbench_fp64_hbm.txt
 
 
-def cg_vector_bytes(ndof, fused, x_defer=1, steps=None):
+def cg_vector_bytes(ndof, fused, x_defer=1, steps=None, cgcg=False):
     # update: read x,p,r,q write x,r (48 B/DOF); unfused p-update: read r,p write p (24 B/DOF);
     # deferred x update over m iterations: r, q -> r every iteration, x and the
     # group's m p vectors -> x once per group: 24 + (16 + 8 m) / m = 32 + 16 / m B/DOF in the
     # steady state; a timed pass of K steps ending on a group boundary holds ceil(K / m) x updates
+    if cgcg:  # single reduction: r, w, p_old, s -> p, s, r (56 B/DOF) + x += alpha p (16 B/DOF every
+        # iteration, or x and the group's m - 1 older p vectors once per group of m)
+        if x_defer <= 1:
+            return 72 * ndof
+        per_group = 16 + 8 * (x_defer - 1)
+        if steps:
+            return (56 + -(-steps // x_defer) * per_group / steps) * ndof
+        return (56 + per_group / x_defer) * ndof
     if fused and x_defer > 1:
         if steps:
             return (24 + -(-steps // x_defer) * (16 + 8 * x_defer) / steps) * ndof
@@ -401,7 +409,7 @@ def run_native(args, cfg):
     nloc_planes = k1 - k0
     fused = bool(op.get_option("fused_cg"))
     cgcg = bool(op.get_option("cg_variant"))
-    if cgcg:  # apply reads r, writes w (16 B/DOF); update reads r,w,p,s,x writes p,s,x,r (72 B/DOF)
+    if cgcg:  # apply reads r, writes w (16 B/DOF); update: cg_vector_bytes
         fused = False
     # algorithmic bytes of one rank's apply launch: owned planes (+ its cell layers)
     x_defer = op.get_option("x_defer")
@@ -455,7 +463,7 @@ def run_native(args, cfg):
     extra["cg_iteration_ms_event_graph"] = ms_event_graph / args.steps  # the time_apply pass
     extra["apply_share_of_step"] = share
     extra["cg_iteration_ms"] = ms / args.steps
-    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused, x_defer, args.steps)
+    cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused, x_defer, args.steps, cgcg)
     extra["cg_bytes_per_dof_alg"] = cg_bytes / ndof_global
     extra["cg_iteration_gbs"] = cg_bytes / (ms / args.steps / 1e3) / 1e9
     extra["fused_cg"] = fused

@@ -173,8 +173,8 @@ struct fem_op_s {
   int64_t pl_off = 0;  // offset of the owned range (pl_lead + pl_pp; 0 on general hex meshes)
   double *x_pl = nullptr, *r_pl = nullptr, *p_pl = nullptr, *q_pl = nullptr, *p2_pl = nullptr;
   // deferred x update over m = 4 / 8 iterations: m - 2 more p buffers (allocated on use)
-  double* pex[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{}, tm_pex[6]{};
+  double* pex[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  CUtensorMap tm_x{}, tm_p{}, tm_mat{}, tm_r{}, tm_p2{}, tm_pex[7]{};
   int cg_parity = 0;  // fused CG: iteration phase mod 8 (selects the p buffers)
   bool tm_ok = false;
   bool tm_interior = false;  // u tensor spans the interior only (Laplace + Dirichlet)
@@ -561,10 +561,10 @@ static int make_pl_maps(fem_op_s* op) {
   op->tm_j0 = lo;
   op->tm_k0 = k0;
   const int64_t off = op->pl_lead + (k0 - (g.k0 - 1)) * op->pl_pp + lo * op->pl_rp + lo * C;
-  double* vecs[10] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl};
-  CUtensorMap* maps[10] = {&op->tm_x, &op->tm_p, &op->tm_r, &op->tm_p2};
-  for (int e = 0; e < 6; ++e) { vecs[4 + e] = op->pex[e]; maps[4 + e] = &op->tm_pex[e]; }
-  for (int v = 0; v < 10; ++v) {
+  double* vecs[11] = {op->x_pl, op->p_pl, op->r_pl, op->p2_pl};
+  CUtensorMap* maps[11] = {&op->tm_x, &op->tm_p, &op->tm_r, &op->tm_p2};
+  for (int e = 0; e < 7; ++e) { vecs[4 + e] = op->pex[e]; maps[4 + e] = &op->tm_pex[e]; }
+  for (int v = 0; v < 11; ++v) {
     if (!vecs[v]) continue;  // (pex: allocated for x_defer >= 4 only)
     FEM_TRY(make_map3d(maps[v], vecs[v] + off, (uint64_t)((i1 - lo + 1) * C), (uint64_t)(j1 - lo + 1),
                        (uint64_t)(k1 - k0 + 1), op->pl_rp * 8, op->pl_pp * 8, bw, bh));
@@ -1761,13 +1761,20 @@ static void drop_graphs(fem_op_s* op);
 // length m (1: x += alpha p every iteration).  The peer halo maps the neighbours' p and p2 only,
 // so with it m is at most 2.
 static int x_defer_m(const fem_op_s* op) {
-  if (op->x_defer <= 1 || !op->tm_ok || op->use_pa || op->cg_variant != 0 || op->mesh->hex) return 1;
-  return std::min(op->peer_on ? 2 : op->x_defer, op->x_defer_cap);
+  if (op->x_defer <= 1 || !op->tm_ok || op->use_pa || op->mesh->hex) return 1;
+  // (single-reduction CG: its apply reads r only, so the peer halo does not limit its p ring)
+  return std::min((op->peer_on && op->cg_variant == 0) ? 2 : op->x_defer, op->x_defer_cap);
 }
 // the p buffers of the deferral group: iteration phase j writes p into buf[j % m] and reads p_old
 // from buf[(j - 1) % m]; buf[m - 1] is p_pl, the buffer cg_begin initialises (so the first
 // iteration's p_old, multiplied by beta = 0, is finite)
+// Single-reduction CG: p2_pl holds s, so its ring is pex[0 .. m-2] + p_pl (m = 1: p_pl alone).
 static void p_ring(fem_op_s* op, int m, double** buf, const CUtensorMap** maps) {
+  if (op->cg_variant == 1) {
+    for (int i = 0; i < m - 1; ++i) { buf[i] = op->pex[i]; maps[i] = &op->tm_pex[i]; }
+    buf[m - 1] = op->p_pl; maps[m - 1] = &op->tm_p;
+    return;
+  }
   const int g = m < 2 ? 2 : m;  // (m = 1 keeps the ping-pong pair)
   buf[0] = op->p2_pl; maps[0] = &op->tm_p2;
   for (int i = 1; i < g - 1; ++i) { buf[i] = op->pex[i - 1]; maps[i] = &op->tm_pex[i - 1]; }
@@ -1777,12 +1784,14 @@ static void p_ring(fem_op_s* op, int m, double** buf, const CUtensorMap** maps) 
 // 2, which needs none -- and stays capped for the operator's lifetime)
 static int ensure_p_ring(fem_op_s* op) {
   bool grew = false;
-  for (int e = 0; e < x_defer_m(op) - 2; ++e) {
+  for (int e = 0; e < x_defer_m(op) - (op->cg_variant == 1 ? 1 : 2); ++e) {
     if (op->pex[e]) continue;
     if (cudaMalloc(&op->pex[e], sizeof(double) * op->pl_n) != cudaSuccess) {
       cudaGetLastError();
       op->pex[e] = nullptr;
-      op->x_defer_cap = e >= 2 ? 4 : 2;  // extra buffers 0 .. e-1 exist: a ring of e + 2 >= m fits
+      // extra buffers 0 .. e-1 exist: a ring of e + 2 (single-reduction CG: e + 1) >= m fits
+      const int fit = e + (op->cg_variant == 1 ? 1 : 2);
+      op->x_defer_cap = fit >= 4 ? 4 : (fit >= 2 ? 2 : 1);
       e = -1;  // re-check with the cap
       continue;
     }
@@ -1859,15 +1868,32 @@ static int cg_fused_body(fem_op_s* op, int phase, cudaStream_t s, bool timed) {
 
 // Chronopoulos-Gear iteration (option "cg_variant" = 1; TMA path): w = A r with delta = w.r and
 // gamma = r.r reduced together (one allreduce of 2 values), then one update kernel
-static int cg_cgcg_body(fem_op_s* op, cudaStream_t s, bool timed) {
+static int cg_cgcg_body(fem_op_s* op, int phase, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
   if (timed) FEM_TRY(apply_event(op, 0, s));
   FEM_TRY(apply_pl(op, op->r_pl, &op->tm_r, 3, s));  // w (q_pl) = A r; pq = w.r, rr_new = r.r
   if (timed) FEM_TRY(apply_event(op, 1, s));
   FEM_TRY(allreduce1(op, &op->sc->pq, s, 2));  // pq and rr_new are adjacent in CgScalars
-  cudaError_t e = launch_cg_cgcg_update(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, op->p_pl),
+  // deferred x update (§5.3a): p_k into ring buffer k mod m, x once per group of m iterations
+  const int xm = x_defer_m(op);
+  double* pb[8];
+  const CUtensorMap* pmap[8];
+  p_ring(op, xm, pb, pmap);
+  const int j = phase % xm;
+  const double* po[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int nold = 0;
+  if (xm > 1) {
+    if (j < xm - 1) {
+      nold = -1;
+    } else {
+      nold = xm - 1;
+      for (int k = 0; k < nold; ++k) po[k] = pl_owned(op, pb[k]);
+    }
+  }
+  cudaError_t e = launch_cg_cgcg_update(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl),
+                                        pl_owned(op, pb[(j + xm - 1) % xm]), pl_owned(op, pb[j]),
                                         pl_owned(op, op->p2_pl), pl_owned(op, op->q_pl), pl_count(op), op->sc,
-                                        op->red, s, m->sm_count);
+                                        op->red, s, m->sm_count, nold, po, j);
   if (e != cudaSuccess) return fail(FEM_ECUDA, "cgcg update launch: %s", cudaGetErrorString(e));
   // peer halo: the next apply reads the neighbours' r -- wait for their updates
   if (op->peer_on && m->nranks > 1) FEM_TRY(allreduce1(op, op->dot_dev, s));
@@ -1876,7 +1902,7 @@ static int cg_cgcg_body(fem_op_s* op, cudaStream_t s, bool timed) {
 
 static int iteration(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
   if (op->use_pa) return cg_iteration_body(op, s, timed);  // partial assembly: unfused iteration
-  if (op->tm_ok && op->cg_variant == 1) return cg_cgcg_body(op, s, timed);
+  if (op->tm_ok && op->cg_variant == 1) return cg_cgcg_body(op, parity, s, timed);
   return op->tm_ok ? cg_fused_body(op, parity, s, timed) : cg_iteration_body(op, s, timed);
 }
 

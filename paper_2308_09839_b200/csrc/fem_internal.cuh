@@ -256,8 +256,9 @@ cudaError_t launch_hex_pack_cells(const int32_t* vtk, const uint8_t* dir, int64_
 // Chronopoulos-Gear CG (single reduction, NEXT #1): with gamma = r.r and delta = w.r from the
 // apply (mode 3): beta = gamma / gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev);
 // p = r + beta p, s = w + beta s, x += alpha p, r -= alpha s (first step: p = r, s = w)
-cudaError_t launch_cg_cgcg_update(double* x, double* r, double* p, double* s, const double* w, int64_t n,
-                                  CgScalars* sc, Reduce red, cudaStream_t st, int sm_count);
+cudaError_t launch_cg_cgcg_update(double* x, double* r, const double* pr, double* pw, double* s, const double* w,
+                                  int64_t n, CgScalars* sc, Reduce red, cudaStream_t st, int sm_count, int nold = 0,
+                                  const double* const* pold = nullptr, int jpend = 0);
 // loopback allreduce: out[i] = sum over ranks q = 0..P-1 (in order) of stage[q * stride + i]
 cudaError_t launch_loop_sum(const double* stage, int P, int stride, int count, double* out, cudaStream_t s);
 // dot_mode 1 of the fused CG: which = 0: sc->pq = a.b, then roll rr = rr_new, first = 0;

@@ -228,10 +228,15 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_ker
 //   beta = gamma / gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev)  (first: beta = 0,
 //   alpha = gamma / delta); p = r + beta p; s = w + beta s; x += alpha p; r -= alpha s.
 // gamma is the residual of the iterate before this update, so convergence is decided here.
+// Deferred x update in the single-reduction CG (option x_defer): p_k is written
+// into ring buffer k mod m (pw) from p_{k-1} (pr), s stays in place; NOLD as in
+// cg_update_fused_kernel (-1: alpha pending, k: the k pending updates, then this one).
+template <int NOLD>
 __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_cgcg_update_kernel(double* __restrict__ x, double* __restrict__ r,
-                                                                     double* __restrict__ p, double* __restrict__ s,
+                                                                     const double* pr, double* pw,  // (alias when m = 1)
+                                                                     double* __restrict__ s,
                                                                      const double* __restrict__ w, int64_t n,
-                                                                     CgScalars* sc, Reduce red) {
+                                                                     CgScalars* sc, Reduce red, OldP po, int jpend) {
   __shared__ double sh[32];
   if (sc->done) return;
   const double gam = sc->rr_new, delta = sc->pq;
@@ -252,37 +257,61 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_cgcg_update_kern
     }
     return;
   }
+  // (alpha_h / xp are read by later kernels only: block 0 may write them)
+  if (NOLD < 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->alpha_h[jpend] = alpha;
+    sc->xp = jpend + 1;
+  }
+  double ah[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) ah[k] = sc->alpha_h[k];
+  if (NOLD > 0 && blockIdx.x == 0 && threadIdx.x == 0) sc->xp = 0;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   auto one = [&](int64_t i) {
     const double ri = r[i], wi = w[i];
-    const double pi = first ? ri : fma(beta, p[i], ri);
+    const double pi = first ? ri : fma(beta, pr[i], ri);
     const double si = first ? wi : fma(beta, s[i], wi);
-    p[i] = pi;
+    pw[i] = pi;
     s[i] = si;
-    x[i] = fma(alpha, pi, x[i]);
+    if (NOLD >= 0) {
+      double xv = x[i];
+#pragma unroll
+      for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) xv = fma(ah[k], po.p[k][i], xv);
+      x[i] = fma(alpha, pi, xv);
+    }
     r[i] = fma(-alpha, si, ri);
   };
-  // 16-B accesses (the five vectors share one layout), head / tail elements scalar
+  // 16-B accesses (the vectors share one layout), head / tail elements scalar
   const int64_t head = (reinterpret_cast<uintptr_t>(r) & 15) ? 1 : 0;
   if (head && gtid == 0 && n > 0) one(0);
   const int64_t n2 = (n - head) / 2;
   double2* __restrict__ x2 = reinterpret_cast<double2*>(x + head);
   double2* __restrict__ r2 = reinterpret_cast<double2*>(r + head);
-  double2* __restrict__ p2 = reinterpret_cast<double2*>(p + head);
+  const double2* pr2 = reinterpret_cast<const double2*>(pr + head);
+  double2* pw2 = reinterpret_cast<double2*>(pw + head);
   double2* __restrict__ s2 = reinterpret_cast<double2*>(s + head);
   const double2* __restrict__ w2 = reinterpret_cast<const double2*>(w + head);
   for (int64_t i = gtid; i < n2; i += stride) {
-    const double2 rv = r2[i], wv = w2[i], xv = x2[i];
+    const double2 rv = r2[i], wv = w2[i];
     double2 pv = rv, sv = wv;
     if (!first) {
-      const double2 po = p2[i], so = s2[i];
-      pv = make_double2(fma(beta, po.x, rv.x), fma(beta, po.y, rv.y));
-      sv = make_double2(fma(beta, so.x, wv.x), fma(beta, so.y, wv.y));
+      const double2 pov = pr2[i], sov = s2[i];
+      pv = make_double2(fma(beta, pov.x, rv.x), fma(beta, pov.y, rv.y));
+      sv = make_double2(fma(beta, sov.x, wv.x), fma(beta, sov.y, wv.y));
     }
-    p2[i] = pv;
+    pw2[i] = pv;
     s2[i] = sv;
-    x2[i] = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+    if (NOLD >= 0) {
+      double2 xv = x2[i];
+#pragma unroll
+      for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) {
+        const double2 o = reinterpret_cast<const double2*>(po.p[k] + head)[i];
+        xv.x = fma(ah[k], o.x, xv.x);
+        xv.y = fma(ah[k], o.y, xv.y);
+      }
+      x2[i] = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+    }
     r2[i] = make_double2(fma(-alpha, sv.x, rv.x), fma(-alpha, sv.y, rv.y));
   }
   if (((n - head) & 1) && gtid == stride - 1) one(n - 1);
@@ -456,9 +485,20 @@ cudaError_t launch_cg_xdefer_flush(double* x, const double* const* pend, int64_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_cgcg_update(double* x, double* r, double* p, double* s, const double* w, int64_t n,
-                                  CgScalars* sc, Reduce red, cudaStream_t st, int sm_count) {
-  cg_cgcg_update_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, st>>>(x, r, p, s, w, n, sc, red);
+cudaError_t launch_cg_cgcg_update(double* x, double* r, const double* pr, double* pw, double* s, const double* w,
+                                  int64_t n, CgScalars* sc, Reduce red, cudaStream_t st, int sm_count, int nold,
+                                  const double* const* pold, int jpend) {
+  const unsigned nb = vec_blocks(n, sm_count);
+  OldP po{{pr, pr, pr, pr, pr, pr, pr}};
+  for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
+  switch (nold) {
+    case -1: cg_cgcg_update_kernel<-1><<<nb, kVecThreads, 0, st>>>(x, r, pr, pw, s, w, n, sc, red, po, jpend); break;
+    case 0: cg_cgcg_update_kernel<0><<<nb, kVecThreads, 0, st>>>(x, r, pr, pw, s, w, n, sc, red, po, 0); break;
+    case 1: cg_cgcg_update_kernel<1><<<nb, kVecThreads, 0, st>>>(x, r, pr, pw, s, w, n, sc, red, po, 0); break;
+    case 3: cg_cgcg_update_kernel<3><<<nb, kVecThreads, 0, st>>>(x, r, pr, pw, s, w, n, sc, red, po, 0); break;
+    case 7: cg_cgcg_update_kernel<7><<<nb, kVecThreads, 0, st>>>(x, r, pr, pw, s, w, n, sc, red, po, 0); break;
+    default: return cudaErrorInvalidValue;
+  }
   add_launches(1);
   return cudaGetLastError();
 }

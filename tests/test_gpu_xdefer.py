@@ -100,13 +100,13 @@ def test_x_defer_dot_modes(F, dot_mode):
 
 
 def test_x_defer_applicability(F):
-    """x_defer acts on the fused Hestenes-Stiefel iteration only: it reads back 1 under the
-    single-reduction variant (whose update carries its own p / s recurrences), takes 1, 2, 4 or 8
-    only, and can not change during a solve."""
+    """x_defer acts on the fused iterations (Hestenes-Stiefel and single-reduction): it reads back
+    1 on the unfused partial-assembly iteration, takes 1, 2, 4 or 8 only, and can not change
+    during a solve."""
     op, b = make(F, "elastic", (20, 20, 20), 613)
-    op.set_option("cg_variant", 1)
+    op.set_option("partial_assembly", 1)  # unfused iteration: no p ring
     assert op.get_option("x_defer") == 1
-    op.set_option("cg_variant", 0)
+    op.set_option("partial_assembly", 0)
     assert op.get_option("x_defer") == 8
     for bad in (0, 3, 5, 16):
         with pytest.raises(F.FemError):
@@ -117,3 +117,28 @@ def test_x_defer_applicability(F):
         op.set_option("x_defer", 2)
     op.cg_iterate(4)
     op.cg_end()
+
+
+@pytest.mark.parametrize("kind", ["scalar", "elastic"])
+def test_x_defer_single_reduction(F, kind):
+    """Chronopoulos-Gear CG (cg_variant 1): its update writes p into the ring and
+    defers x the same way -- bitwise equal to m = 1 (x += alpha p every iteration, p in place)."""
+    op, b = make(F, kind, (33, 21, 17), 614)
+    op.set_option("cg_variant", 1)
+    for use_graph in (1, 0):
+        op.set_option("use_graph", use_graph)
+        for chunks in ([1], [7], [8], [9], [3, 6], [17]):
+            xs = []
+            for m in (1, 2, 4, 8):
+                op.set_option("x_defer", m)
+                assert op.get_option("x_defer") == m
+                xs.append(run(op, b, chunks)[0])
+            for x in xs[1:]:
+                assert torch.equal(xs[0], x), (use_graph, chunks)
+    for tol in (1e-4, 1e-9):
+        res = []
+        for m in (1, 8):
+            op.set_option("x_defer", m)
+            res.append(run(op, b, [300], tol=tol))
+        assert res[0][1]["iterations"] == res[1][1]["iterations"] < 300
+        assert torch.equal(res[0][0], res[1][0])
