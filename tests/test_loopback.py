@@ -247,3 +247,47 @@ def test_loopback_trace_timeline(F, overlap):
         assert t["total"] > 0
         assert t["interior"] <= t["total"] and t["halo"] <= t["total"]
         assert t["boundary"] <= t["total"]
+
+
+@pytest.mark.parametrize("kind", ["scalar", "elastic"])
+@pytest.mark.parametrize("variant,peer", [(0, False), (0, True), (1, False), (1, True)])
+def test_loopback_x_defer_bitwise(F, kind, variant, peer):
+    """Deferred x update at P = 3: for the same slab split the iterates of
+    x_defer = 8 (Hestenes-Stiefel with the peer halo: capped at 2) are bitwise those of
+    x_defer = 1 after 11 iterations -- a complete group plus pending updates added by cg_end,
+    with the halo / allreduce call sites of the multi-rank drivers in between."""
+    P = 3
+    nx, ny, nz = MESH
+    h = 1.0 / nx
+    c = I.ncomp(kind)
+    g = I.rng(I.SEED_BASE + 615)
+    lam, mu = I.materials(g, nx, ny, nz)
+    b = I.interior_rhs(g, nx, ny, nz, c)
+    plane = (nx + 1) * (ny + 1) * c
+    res = {}
+    for m in (1, 8):
+        comms = F.Comm.loopback(P)
+
+        def rank(r, st):
+            mesh, op = _slab_op(F, comms[r], kind, nx, ny, nz, h, lam, mu)
+            op.set_option("cg_variant", variant)
+            if peer:
+                op.set_option("peer_halo", 1)
+            op.set_option("x_defer", m)
+            want = m if (variant == 1 or not peer) else min(m, 2)
+            assert op.get_option("x_defer") == want
+            k0, k1 = mesh.plane_begin, mesh.plane_end
+            bl = torch.from_numpy(b[k0 * plane:k1 * plane].copy()).cuda()
+            xl = torch.zeros_like(bl)
+            info = op.cg_solve(bl, xl, tol=0.0, maxit=11, stream=st)
+            st.synchronize()
+            out = (xl.cpu().numpy(), info["true_r_norm"])
+            op.close(); mesh.close()
+            return out
+
+        res[m] = _run_ranks(P, rank)
+        for cm in comms:
+            cm.close()
+    for a, bb in zip(res[1], res[8]):
+        assert np.array_equal(a[0], bb[0])
+        assert a[1] == bb[1]
