@@ -1738,39 +1738,35 @@ static int apply_event(fem_op_s* op, int end, cudaStream_t s) {
   return FEM_OK;
 }
 
-static int cg_iteration_body(fem_op_s* op, cudaStream_t s, bool timed) {
-  fem_mesh_s* m = op->mesh;
-  const int64_t n = pl_count(op);
-  if (timed) FEM_TRY(apply_event(op, 0, s));
-  FEM_TRY(apply_pl(op, op->p_pl, &op->tm_p, 1, s));  // q = A p, pq (halo inside when P > 1)
-  if (timed) FEM_TRY(apply_event(op, 1, s));
-  FEM_TRY(allreduce1(op, &op->sc->pq, s));
-  cudaError_t e = launch_cg_update(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, op->p_pl),
-                                   pl_owned(op, op->q_pl), n, op->sc, op->red, s, m->sm_count);
-  if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
-  FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
-  e = launch_cg_pupdate(pl_owned(op, op->r_pl), pl_owned(op, op->p_pl), n, op->sc, op->red, s, m->sm_count);
-  if (e != cudaSuccess) return fail(FEM_ECUDA, "pupdate launch: %s", cudaGetErrorString(e));
-  return FEM_OK;
-}
-
-// fused CG iteration (TMA path): p = r + beta p_old formed inside the apply (NEXT #1 of the
-// survey, 88 -> 80 B/DOF for Laplace); parity selects the p ping-pong buffers.
 static void drop_graphs(fem_op_s* op);
 // deferred x update (option "x_defer"): fused Hestenes-Stiefel CG on the box.  Returns the group
 // length m (1: x += alpha p every iteration).  The peer halo maps the neighbours' p and p2 only,
 // so with it m is at most 2.
+// which CG iteration runs (iteration()): the fused Hestenes-Stiefel one, the single-reduction
+// one, or the unfused one (partial assembly, general hexes, degenerate boxes)
+static int iter_kind(const fem_op_s* op) {
+  if (op->use_pa || !op->tm_ok) return 2;
+  return op->cg_variant == 1 ? 1 : 0;
+}
 static int x_defer_m(const fem_op_s* op) {
-  if (op->x_defer <= 1 || !op->tm_ok || op->use_pa || op->mesh->hex) return 1;
-  // (single-reduction CG: its apply reads r only, so the peer halo does not limit its p ring)
-  return std::min((op->peer_on && op->cg_variant == 0) ? 2 : op->x_defer, op->x_defer_cap);
+  if (op->x_defer <= 1) return 1;
+  // (the fused Hestenes-Stiefel apply reads p_old through the peer halo, which maps the
+  // neighbours' p and p2 only; the other iterations' applies do not read old p vectors)
+  return std::min((op->peer_on && iter_kind(op) == 0) ? 2 : op->x_defer, op->x_defer_cap);
 }
 // the p buffers of the deferral group: iteration phase j writes p into buf[j % m] and reads p_old
 // from buf[(j - 1) % m]; buf[m - 1] is p_pl, the buffer cg_begin initialises (so the first
 // iteration's p_old, multiplied by beta = 0, is finite)
 // Single-reduction CG: p2_pl holds s, so its ring is pex[0 .. m-2] + p_pl (m = 1: p_pl alone).
+// Unfused iteration: p_pl (cg_begin's p0), p2_pl, pex[0 .. m-3] (m = 1: p_pl alone, in place).
 static void p_ring(fem_op_s* op, int m, double** buf, const CUtensorMap** maps) {
-  if (op->cg_variant == 1) {
+  if (iter_kind(op) == 2) {
+    buf[0] = op->p_pl; maps[0] = &op->tm_p;
+    if (m >= 2) { buf[1] = op->p2_pl; maps[1] = &op->tm_p2; }
+    for (int i = 2; i < m; ++i) { buf[i] = op->pex[i - 2]; maps[i] = &op->tm_pex[i - 2]; }
+    return;
+  }
+  if (iter_kind(op) == 1) {
     for (int i = 0; i < m - 1; ++i) { buf[i] = op->pex[i]; maps[i] = &op->tm_pex[i]; }
     buf[m - 1] = op->p_pl; maps[m - 1] = &op->tm_p;
     return;
@@ -1784,13 +1780,23 @@ static void p_ring(fem_op_s* op, int m, double** buf, const CUtensorMap** maps) 
 // 2, which needs none -- and stays capped for the operator's lifetime)
 static int ensure_p_ring(fem_op_s* op) {
   bool grew = false;
-  for (int e = 0; e < x_defer_m(op) - (op->cg_variant == 1 ? 1 : 2); ++e) {
+  if (iter_kind(op) == 2 && x_defer_m(op) >= 2 && !op->p2_pl) {  // (general hexes do not allocate it)
+    if (cudaMalloc(&op->p2_pl, sizeof(double) * op->pl_n) != cudaSuccess) {
+      cudaGetLastError();
+      op->p2_pl = nullptr;
+      op->x_defer_cap = 1;
+      return FEM_OK;
+    }
+    CUDA_TRY(cudaMemset(op->p2_pl, 0, sizeof(double) * op->pl_n));
+    grew = true;
+  }
+  for (int e = 0; e < x_defer_m(op) - (iter_kind(op) == 1 ? 1 : 2); ++e) {
     if (op->pex[e]) continue;
     if (cudaMalloc(&op->pex[e], sizeof(double) * op->pl_n) != cudaSuccess) {
       cudaGetLastError();
       op->pex[e] = nullptr;
       // extra buffers 0 .. e-1 exist: a ring of e + 2 (single-reduction CG: e + 1) >= m fits
-      const int fit = e + (op->cg_variant == 1 ? 1 : 2);
+      const int fit = e + (iter_kind(op) == 1 ? 1 : 2);
       op->x_defer_cap = fit >= 4 ? 4 : (fit >= 2 ? 2 : 1);
       e = -1;  // re-check with the cap
       continue;
@@ -1800,8 +1806,46 @@ static int ensure_p_ring(fem_op_s* op) {
   }
   if (!grew) return FEM_OK;
   drop_graphs(op);
-  return make_pl_maps(op);
+  return op->mesh->hex ? FEM_OK : make_pl_maps(op);
 }
+
+static int cg_iteration_body(fem_op_s* op, int phase, cudaStream_t s, bool timed) {
+  fem_mesh_s* m = op->mesh;
+  const int64_t n = pl_count(op);
+  // deferred x update (§5.3): p_k in ring buffer k mod m, p_{k+1} written to the next one
+  const int xm = x_defer_m(op);
+  double* pb[8];
+  const CUtensorMap* pmap[8];
+  p_ring(op, xm, pb, pmap);
+  const int j = phase % xm;
+  double* pc = pb[j];
+  double* pn = pb[(j + 1) % xm];
+  if (timed) FEM_TRY(apply_event(op, 0, s));
+  FEM_TRY(apply_pl(op, pc, pmap[j], 1, s));  // q = A p, pq (halo inside when P > 1)
+  if (timed) FEM_TRY(apply_event(op, 1, s));
+  FEM_TRY(allreduce1(op, &op->sc->pq, s));
+  const double* po[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int nold = 0;
+  if (xm > 1) {
+    if (j < xm - 1) {
+      nold = -1;
+    } else {
+      nold = xm - 1;
+      for (int k = 0; k < nold; ++k) po[k] = pl_owned(op, pb[k]);
+    }
+  }
+  cudaError_t e = launch_cg_update(pl_owned(op, op->x_pl), pl_owned(op, op->r_pl), pl_owned(op, pc),
+                                   pl_owned(op, op->q_pl), n, op->sc, op->red, s, m->sm_count, nold, po, j);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "update launch: %s", cudaGetErrorString(e));
+  FEM_TRY(allreduce1(op, &op->sc->rr_new, s));
+  e = launch_cg_pupdate(pl_owned(op, op->r_pl), pl_owned(op, pc), pl_owned(op, pn), n, op->sc, op->red, s,
+                        m->sm_count);
+  if (e != cudaSuccess) return fail(FEM_ECUDA, "pupdate launch: %s", cudaGetErrorString(e));
+  return FEM_OK;
+}
+
+// fused CG iteration (TMA path): p = r + beta p_old formed inside the apply (NEXT #1 of the
+// survey, 88 -> 80 B/DOF for Laplace); parity selects the p ping-pong buffers.
 
 static int cg_fused_body(fem_op_s* op, int phase, cudaStream_t s, bool timed) {
   fem_mesh_s* m = op->mesh;
@@ -1901,9 +1945,11 @@ static int cg_cgcg_body(fem_op_s* op, int phase, cudaStream_t s, bool timed) {
 }
 
 static int iteration(fem_op_s* op, int parity, cudaStream_t s, bool timed) {
-  if (op->use_pa) return cg_iteration_body(op, s, timed);  // partial assembly: unfused iteration
-  if (op->tm_ok && op->cg_variant == 1) return cg_cgcg_body(op, parity, s, timed);
-  return op->tm_ok ? cg_fused_body(op, parity, s, timed) : cg_iteration_body(op, s, timed);
+  switch (iter_kind(op)) {
+    case 0: return cg_fused_body(op, parity, s, timed);
+    case 1: return cg_cgcg_body(op, parity, s, timed);
+    default: return cg_iteration_body(op, parity, s, timed);  // partial assembly, hexes, degenerate
+  }
 }
 
 static int capture(fem_op_s* op, int iters, int parity, cudaStream_t s, cudaGraphExec_t* out,

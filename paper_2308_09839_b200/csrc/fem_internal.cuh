@@ -206,8 +206,9 @@ cudaError_t launch_cg_init(const double* b, const double* ax, double* r, double*
                            CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
 cudaError_t launch_cg_finish_init(CgScalars* sc, double tol, int maxit, cudaStream_t s);
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* q, int64_t n,
-                             CgScalars* sc, Reduce red, cudaStream_t s, int sm_count);
-cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* sc, Reduce red,
+                             CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold = 0,
+                             const double* const* pold = nullptr, int jpend = 0);
+cudaError_t launch_cg_pupdate(const double* r, const double* pr, double* pw, int64_t n, CgScalars* sc, Reduce red,
                               cudaStream_t s, int sm_count);
 // fused CG: x += alpha p; r -= alpha q; rr_new = r.r; iteration bookkeeping (p update is in the apply)
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,

@@ -58,12 +58,20 @@ __global__ void cg_finish_init_kernel(CgScalars* sc, double tol, int maxit) {
   sc->done = (rr == 0.0 || rr <= sc->stop_rr) ? 1 : (maxit <= 0 ? 3 : 0);
 }
 
+struct OldP {
+  const double* p[7];  // the pending p vectors P_0 .. P_{NOLD-1} (deferred x update)
+};
+
+// unfused iteration (general hexes, partial assembly, degenerate boxes): x += alpha p; r -= alpha
+// q; rr_new = r.r.  NOLD: the deferred x update as in cg_update_fused_kernel below (-1: alpha
+// pending in sc->alpha_h[jpend]; k: the k pending updates, then this one).
+template <int NOLD>
 __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restrict__ x,
                                                                 double* __restrict__ r,
                                                                 const double* __restrict__ p,
                                                                 const double* __restrict__ q,
                                                                 int64_t n, CgScalars* sc,
-                                                                Reduce red) {
+                                                                Reduce red, OldP po, int jpend) {
   __shared__ double sh[32];
   if (sc->done) return;
   const double pq = sc->pq;
@@ -75,10 +83,23 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
     return;
   }
   const double alpha = sc->rr / pq;
+  if (NOLD < 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->alpha_h[jpend] = alpha;
+    sc->xp = jpend + 1;
+  }
+  double ah[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) ah[k] = sc->alpha_h[k];
+  if (NOLD > 0 && blockIdx.x == 0 && threadIdx.x == 0) sc->xp = 0;
   double acc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    x[i] = fma(alpha, p[i], x[i]);
+    if (NOLD >= 0) {
+      double xv = x[i];
+#pragma unroll
+      for (int k = 0; k < (NOLD > 0 ? NOLD : 0); ++k) xv = fma(ah[k], po.p[k][i], xv);
+      x[i] = fma(alpha, p[i], xv);
+    }
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
     acc = fma(ri, ri, acc);
@@ -102,9 +123,6 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 #ifndef FEM_UPD_MINB
 #define FEM_UPD_MINB 3  // resident blocks per SM the fused update kernel is compiled for (80 registers)
 #endif
-struct OldP {
-  const double* p[7];  // the pending p vectors P_0 .. P_{NOLD-1}
-};
 template <int NOLD>
 __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
                                                                       double* __restrict__ r,
@@ -326,8 +344,9 @@ __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_cgcg_update_kern
   }
 }
 
+// p_next = r + beta p (pw = pr: in place; a ring buffer of the deferred x update otherwise)
 __global__ void __launch_bounds__(kVecThreads) cg_pupdate_kernel(const double* __restrict__ r,
-                                                                 double* __restrict__ p, int64_t n,
+                                                                 const double* pr, double* pw, int64_t n,
                                                                  CgScalars* sc, Reduce red) {
   __shared__ double sh[32];
   if (sc->done) return;
@@ -335,7 +354,7 @@ __global__ void __launch_bounds__(kVecThreads) cg_pupdate_kernel(const double* _
   const double beta = rr_new / sc->rr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    p[i] = fma(beta, p[i], r[i]);
+    pw[i] = fma(beta, pr[i], r[i]);
   double tot;
   if (last_block_reduce(0.0, red, sh, &tot)) {
     // all blocks have read rr / rr_new: advance the recurrence
@@ -439,8 +458,19 @@ cudaError_t launch_cg_finish_init(CgScalars* sc, double tol, int maxit, cudaStre
   return cudaGetLastError();
 }
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* q, int64_t n,
-                             CgScalars* sc, Reduce red, cudaStream_t s, int sm_count) {
-  cg_update_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(x, r, p, q, n, sc, red);
+                             CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
+                             const double* const* pold, int jpend) {
+  const unsigned nb = vec_blocks(n, sm_count);
+  OldP po{{p, p, p, p, p, p, p}};
+  for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
+  switch (nold) {
+    case -1: cg_update_kernel<-1><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, jpend); break;
+    case 0: cg_update_kernel<0><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
+    case 1: cg_update_kernel<1><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
+    case 3: cg_update_kernel<3><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
+    case 7: cg_update_kernel<7><<<nb, kVecThreads, 0, s>>>(x, r, p, q, n, sc, red, po, 0); break;
+    default: return cudaErrorInvalidValue;
+  }
   add_launches(1);
   return cudaGetLastError();
 }
@@ -502,9 +532,9 @@ cudaError_t launch_cg_cgcg_update(double* x, double* r, const double* pr, double
   add_launches(1);
   return cudaGetLastError();
 }
-cudaError_t launch_cg_pupdate(const double* r, double* p, int64_t n, CgScalars* sc, Reduce red,
+cudaError_t launch_cg_pupdate(const double* r, const double* pr, double* pw, int64_t n, CgScalars* sc, Reduce red,
                               cudaStream_t s, int sm_count) {
-  cg_pupdate_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(r, p, n, sc, red);
+  cg_pupdate_kernel<<<vec_blocks(n, sm_count), kVecThreads, 0, s>>>(r, pr, pw, n, sc, red);
   add_launches(1);
   return cudaGetLastError();
 }

@@ -100,13 +100,8 @@ def test_x_defer_dot_modes(F, dot_mode):
 
 
 def test_x_defer_applicability(F):
-    """x_defer acts on the fused iterations (Hestenes-Stiefel and single-reduction): it reads back
-    1 on the unfused partial-assembly iteration, takes 1, 2, 4 or 8 only, and can not change
-    during a solve."""
+    """x_defer takes 1, 2, 4 or 8 only and can not change during a solve."""
     op, b = make(F, "elastic", (20, 20, 20), 613)
-    op.set_option("partial_assembly", 1)  # unfused iteration: no p ring
-    assert op.get_option("x_defer") == 1
-    op.set_option("partial_assembly", 0)
     assert op.get_option("x_defer") == 8
     for bad in (0, 3, 5, 16):
         with pytest.raises(F.FemError):
@@ -142,3 +137,46 @@ def test_x_defer_single_reduction(F, kind):
             res.append(run(op, b, [300], tol=tol))
         assert res[0][1]["iterations"] == res[1][1]["iterations"] < 300
         assert torch.equal(res[0][0], res[1][0])
+
+
+def _unfused_ops(F):
+    """Operators on the unfused CG iteration (apply, update, p-update): general hexes (matrix-free
+    and partial assembly, with the deterministic scatter -- the FP64-atomic one is not bitwise
+    reproducible run to run), partial assembly on the box, and a degenerate box (one cell thick:
+    no interior nodes in z, so no TMA path)."""
+    g = I.rng(I.SEED_BASE + 616)
+    out = []
+    for kind in ("scalar", "elastic"):
+        c = I.ncomp(kind)
+        coords, cells, bnd = I.hex_box_mesh(9, 7, 6, h=1.0 / 9, g=g, jitter=0.15, permute=True)
+        b = torch.zeros(coords.shape[0] * c, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+        hl, hm = I.materials(g, cells.shape[0], 1, 1)
+        for pa in (0, 1):
+            op = F.Operator(F.HexMesh(dev(coords), dev(cells), dev(bnd)), kind, 1)
+            if kind == "elastic":
+                op.set_material(dev(hl), dev(hm))
+            op.set_option("deterministic", 1)
+            op.set_option("partial_assembly", pa)
+            out.append((f"hex-{kind}-pa{pa}", op, b))
+    op, b = make(F, "elastic", (14, 11, 9), 617)
+    op.set_option("partial_assembly", 1)
+    out.append(("box-pa", op, b))
+    op, b = make(F, "vector", (12, 10, 1), 618)
+    out.append(("box-degenerate", op, b))
+    return out
+
+
+def test_x_defer_unfused_iteration(F):
+    """The unfused iteration defers x the same way (p_{k+1} = r + beta p_k written into the next
+    ring buffer by the p-update kernel): bitwise equal to m = 1 (p updated in place)."""
+    for name, op, b in _unfused_ops(F):
+        for chunks in ([1], [5], [8], [11], [4, 5]):
+            xs = []
+            for m in (1, 2, 4, 8):
+                op.set_option("x_defer", m)
+                assert op.get_option("x_defer") == m, name
+                x, info = run(op, b, chunks)
+                assert info["iterations"] == sum(chunks) or info["converged"], name
+                xs.append(x)
+            for x in xs[1:]:
+                assert torch.equal(xs[0], x), (name, chunks, float((xs[0] - x).abs().max()))
