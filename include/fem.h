@@ -219,14 +219,15 @@ int fem_cg_end(fem_op_t op, fem_cg_info* info, void* stream);
  * varies from run to run); TMA path, cg_variant 0 only), "halo_overlap" (1, default: with an
  * exchange step -- nranks > 1 without peer_halo -- the halo runs on a library stream while the
  * interior node planes are applied, then the two boundary planes; 0: halo, then one apply),
- * "x_defer" (every CG iteration -- fused, single-reduction and unfused: 1, 2, 4 or 8, default 8 -- x is updated once per
- * group of m iterations, x = ((x + alpha_0 p_0) + ...) + alpha_{m-1} p_{m-1}, from the m p buffers
- * the fused apply writes in turn (the same FMAs in the same order as the per-iteration update,
- * so x is bitwise the same); the other updates of the group stream r and q only: 32 + 16 / m
- * instead of 48 B/DOF of update traffic per iteration (Table 4's axpy rows); m >= 4
- * allocates m - 2 more p vectors on the first solve (when they do not fit in device memory, m
- * drops to 4 or 2 for the operator's lifetime and reads back accordingly); cg_end adds the pending updates of an
- * unfinished group; with peer_halo at most 2 (Hestenes-Stiefel); reads back the m in use;
+ * "x_defer" (every CG iteration -- fused, single-reduction and unfused; 1, 2, 4 or 8, default
+ * 8: x is updated once per group of m iterations, x = ((x + alpha_0 p_0) + ...) + alpha_{m-1}
+ * p_{m-1}, from the m p buffers the iteration writes in turn -- the same FMAs in the same order as
+ * the per-iteration update, so x is bitwise the same; the other updates of the group leave x
+ * alone: 32 + 16 / m instead of 48 B/DOF of update traffic per iteration in the fused CG (Table
+ * 4's axpy rows); m >= 4 allocates up to m - 1 more p vectors on the first solve
+ * (when they do not fit in device memory, m drops to 4 or 2 for the operator's lifetime and
+ * reads back accordingly); cg_end adds the pending updates of an unfinished group; with
+ * peer_halo the fused Hestenes-Stiefel iteration uses m <= 2; reads back the m in use;
  * FEM_EINVAL for other values), "deterministic" (general hex meshes: 1 replaces
  * the FP64 atomic scatter by element outputs E[cell][8][C] and a per-node gather over the node's
  * (cell, corner) entries in ascending order -- bitwise reproducible results run after run, at
