@@ -88,10 +88,11 @@ def cg_vector_bytes(ndof, fused, x_defer=1, steps=None, cgcg=False):
         if steps:
             return (56 + -(-steps // x_defer) * per_group / steps) * ndof
         return (56 + per_group / x_defer) * ndof
-    if fused and x_defer > 1:
+    if x_defer > 1:  # fused: r, q -> r; unfused: the same + the p-update r, p -> p (24 B/DOF)
+        base = 24 if fused else 48
         if steps:
-            return (24 + -(-steps // x_defer) * (16 + 8 * x_defer) / steps) * ndof
-        return (32 + 16 / x_defer) * ndof
+            return (base + -(-steps // x_defer) * (16 + 8 * x_defer) / steps) * ndof
+        return (base + 8 + 16 / x_defer) * ndof
     return (48 if fused else 72) * ndof
 
 
