@@ -467,6 +467,7 @@ def run_native(args, cfg):
     cg_bytes = cg_apply_bytes(kind, nx, ny, nz, fused) + cg_vector_bytes(ndof_global, fused, x_defer, args.steps, cgcg)
     extra["cg_bytes_per_dof_alg"] = cg_bytes / ndof_global
     extra["cg_iteration_gbs"] = cg_bytes / (ms / args.steps / 1e3) / 1e9
+    extra["cg_iteration_frac"] = extra["cg_iteration_gbs"] / hbm_peak  # whole step (apply + updates)
     extra["fused_cg"] = fused
     extra["cg_variant"] = "chronopoulos-gear" if cgcg else "hestenes-stiefel"
     extra["dot_mode"] = "single reduction (CG-CG)" if cgcg else args.dot
