@@ -700,7 +700,7 @@ def relaunch_multi_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=24)  # a multiple of the x_defer group (8): steady-state x-update share
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3,
                     help="0-3: BASELINE.json configs[0..3]; 4/5: configs[4] weak scaling (scalar / elasticity)")
