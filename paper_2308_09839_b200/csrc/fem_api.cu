@@ -576,6 +576,7 @@ static int make_pl_maps(fem_op_s* op) {
 // Peer halo: tensor maps over the neighbours' ghost-plane sources (their last / first owned node
 // plane), same origin, box and pitches as the local maps; ghost planes outside the operator's
 // tensor range (the Dirichlet faces of the Laplace interior tensor) stay zero-filled locally.
+static void drop_graphs(fem_op_s* op);
 static int build_peer_maps(fem_op_s* op) {
   const Grid& g = op->mesh->g;
   const int C = op->comps;
@@ -599,6 +600,7 @@ static int build_peer_maps(fem_op_s* op) {
                          (uint64_t)(j1 - lo + 1), 1, op->pl_rp * 8, op->pl_pp * 8, bw, bh));
   }
   op->peer_on = true;
+  drop_graphs(op);  // captured iterations hold the halo path (and the x_defer group length) of their capture
   return FEM_OK;
 }
 
