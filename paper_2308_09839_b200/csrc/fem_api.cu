@@ -576,7 +576,9 @@ static int make_pl_maps(fem_op_s* op) {
 // Peer halo: tensor maps over the neighbours' ghost-plane sources (their last / first owned node
 // plane), same origin, box and pitches as the local maps; ghost planes outside the operator's
 // tensor range (the Dirichlet faces of the Laplace interior tensor) stay zero-filled locally.
-static void drop_graphs(fem_op_s* op);
+extern "C" {
+static void drop_graphs(fem_op_s* op);  // (defined inside the ABI block below)
+}
 static int build_peer_maps(fem_op_s* op) {
   const Grid& g = op->mesh->g;
   const int C = op->comps;
