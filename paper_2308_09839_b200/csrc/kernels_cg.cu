@@ -16,11 +16,22 @@
 namespace fem {
 
 constexpr int kVecThreads = 256;
+#ifndef FEM_UPD_MINB
+#define FEM_UPD_MINB 3  // resident blocks per SM the fused update kernel is compiled for (80 registers)
+#endif
 
-static inline unsigned vec_blocks(int64_t n, int sm_count) {
+// grid of a grid-stride vector kernel: at most one wave of resident blocks (per_sm per SM), so
+// every block streams an equal share and no partial last wave idles part of the GPU
+static inline unsigned vec_blocks(int64_t n, int sm_count, int per_sm = 8) {
   int64_t want = (n + kVecThreads * 4 - 1) / (kVecThreads * 4);
-  int64_t cap = (int64_t)sm_count * 8;
+  int64_t cap = (int64_t)sm_count * per_sm;
   return (unsigned)std::max<int64_t>(1, std::min(want, cap));
+}
+#ifndef FEM_UPD_WAVE
+#define FEM_UPD_WAVE 1  // update kernels (FEM_UPD_MINB resident blocks per SM): grid = one wave
+#endif
+static inline unsigned upd_blocks(int64_t n, int sm_count) {
+  return vec_blocks(n, sm_count, FEM_UPD_WAVE ? FEM_UPD_MINB : 8);
 }
 
 __global__ void __launch_bounds__(kVecThreads) cg_init_kernel(const double* __restrict__ b,
@@ -120,9 +131,6 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 //       then this one, in their sequential order -- bitwise the x of k + 1 per-iteration updates
 //       (k = 0: the plain x += alpha p, 48 B/DOF; k = 1: 56; k = 3: 72; k = 7: 104)
 // so a group of m iterations moves 32 m + 16 instead of 48 m B/DOF of update traffic.
-#ifndef FEM_UPD_MINB
-#define FEM_UPD_MINB 3  // resident blocks per SM the fused update kernel is compiled for (80 registers)
-#endif
 template <int NOLD>
 __global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
                                                                       double* __restrict__ r,
@@ -460,7 +468,7 @@ cudaError_t launch_cg_finish_init(CgScalars* sc, double tol, int maxit, cudaStre
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* q, int64_t n,
                              CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
                              const double* const* pold, int jpend) {
-  const unsigned nb = vec_blocks(n, sm_count);
+  const unsigned nb = upd_blocks(n, sm_count);
   OldP po{{p, p, p, p, p, p, p}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
@@ -477,7 +485,7 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
                                    CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
                                    const double* const* pold, int jpend) {
-  const unsigned nb = vec_blocks(n, sm_count);
+  const unsigned nb = upd_blocks(n, sm_count);
   OldP po{{p, p, p, p, p, p, p}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
@@ -518,7 +526,7 @@ cudaError_t launch_cg_xdefer_flush(double* x, const double* const* pend, int64_t
 cudaError_t launch_cg_cgcg_update(double* x, double* r, const double* pr, double* pw, double* s, const double* w,
                                   int64_t n, CgScalars* sc, Reduce red, cudaStream_t st, int sm_count, int nold,
                                   const double* const* pold, int jpend) {
-  const unsigned nb = vec_blocks(n, sm_count);
+  const unsigned nb = upd_blocks(n, sm_count);
   OldP po{{pr, pr, pr, pr, pr, pr, pr}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
