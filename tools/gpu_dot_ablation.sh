@@ -8,13 +8,13 @@ for spec in "1" "3" "1 --n 64" "3 --n 64"; do
   tag="c$c$(echo $@ | tr -d ' -')"
   for d in fused separate atomic cgcg; do
     if [ $d = cgcg ]; then flag="--cgcg"; else flag="--dot $d"; fi
-    timeout 300 python bench.py --config $c $@ $flag --steps 50 --warmup 5 --no-cpu --no-e2e --no-csr \
+    timeout 300 python bench.py --config $c $@ $flag --steps 48 --warmup 5 --no-cpu --no-e2e --no-csr \
       > $OUT/dot_${tag}_$d.json 2> $OUT/dot_${tag}_$d.err
     python - $OUT/dot_${tag}_$d.json <<'PY'
 import json,sys
 try:
     d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); e=d['extra']
-    print('%-28s CG %7.2f GDOF/s  iter %.4f ms  apply %.4f ms  plain-graph iter %.4f ms'%(d['config']['workload'], d['value'], d['ms_per_step'], e['apply_in_cg_ms'], e['cg_iteration_ms_plain_graph']))
+    print('%-28s CG %7.2f GDOF/s  iter %.4f ms  apply %.4f ms'%(d['config']['workload'], d['value'], d['ms_per_step'], e['apply_in_cg_ms']))
 except Exception as ex: print(sys.argv[1], 'parse failed', ex)
 PY
   done
