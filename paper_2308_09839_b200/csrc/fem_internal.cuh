@@ -140,14 +140,20 @@ constexpr bool kHexPrefetch = FEM_HEX_PREFETCH != 0;
 #ifndef FEM_LAP_S1
 #define FEM_LAP_S1 4  // ring stages of the scalar fused CG apply
 #endif
-constexpr int kLapTX = 32, kLapTY = FEM_LAP_TY, kLapR1 = FEM_LAP_R1, kLapR3 = 1;  // Laplace: C=1 / C=3 rows per thread
+#ifndef FEM_LAP_R3
+#define FEM_LAP_R3 2  // node rows per thread of the vector kernel (1: 2 CTAs / SM at 127 registers)
+#endif
+#ifndef FEM_LAP_MINB3
+#define FEM_LAP_MINB3 (FEM_LAP_R3 > 1 ? 1 : FEM_LAP_MINB)  // resident CTAs per SM of the vector kernel
+#endif
+constexpr int kLapTX = 32, kLapTY = FEM_LAP_TY, kLapR1 = FEM_LAP_R1, kLapR3 = FEM_LAP_R3;  // Laplace: C=1 / C=3 rows per thread
 #ifndef FEM_LAP_SELF1
 #define FEM_LAP_SELF1 1  // scalar TMA path without producer warp (consumer warp 0 issues the loads)
 #endif
 #ifndef FEM_LAP_TY1
 #define FEM_LAP_TY1 8  // consumer warps of the scalar TMA path
 #endif
-constexpr int kLapMinB = FEM_LAP_MINB, kLapS1 = FEM_LAP_S1, kLapTY1 = FEM_LAP_TY1;
+constexpr int kLapMinB = FEM_LAP_MINB, kLapMinB3 = FEM_LAP_MINB3, kLapS1 = FEM_LAP_S1, kLapTY1 = FEM_LAP_TY1;
 constexpr bool kLapSelf1 = FEM_LAP_SELF1 != 0;
 #ifndef FEM_LAP_SELF3
 #define FEM_LAP_SELF3 0  // vector TMA path without producer warp

@@ -32,7 +32,7 @@ namespace fem {
 // GLL: 2-point Gauss-Lobatto quadrature (BP5/BP6, reading R1): the 1-D mass is
 // lumped, M~ = [0, 3m, 0] instead of [1, 2m, 1]; K~ is exact under both rules.
 template <bool TM, int MODE, int C, int TX, int TY, int R, int S, bool GLL, bool PAIR = false>
-__global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSelf3)) ? 0 : 1)), kLapMinB)
+__global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSelf3)) ? 0 : 1)), (C == 1 ? kLapMinB : kLapMinB3))
     laplace_kernel(Grid g, PlaneSrc x, OutVec yo, const __grid_constant__ CUtensorMap umap,
                    TmaOrigin uorg, const __grid_constant__ CUtensorMap umap2, const double* pold,
                    double* pnew, int bc, int tmint, int64_t kchunk, int64_t kspan, CgScalars* sc, Reduce red,
@@ -314,7 +314,8 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   const int64_t yt = balanced_tiles(g.ny + 1, TY * R, &rya);
   const int64_t nplanes = g.k1 - g.k0;
   // z-chunks: about 4 resident waves of CTAs (2 per SM), chunks of >= 16 planes
-  int64_t zc = (4LL * kLapMinB * sm_count + xt * yt - 1) / (xt * yt);
+  constexpr int kRes = (C == 1) ? kLapMinB : kLapMinB3;  // resident CTAs per SM
+  int64_t zc = (4LL * kRes * sm_count + xt * yt - 1) / (xt * yt);
   // chunks of >= 16 planes amortise the pipeline fill; a mesh too small to fill the GPU that
   // way takes chunks down to 2 planes (latency: the z-march is the serial part of a CTA)
   const int64_t minchunk = (xt * yt * (nplanes / 16) < sm_count) ? 2 : FEM_LAP_MINCHUNK;
@@ -322,7 +323,7 @@ static cudaError_t launch_cfg(const Grid& g, PlaneSrc x, OutVec y, ApplyMaps map
   int64_t kchunk = (nplanes + zc - 1) / zc;
   zc = (nplanes + kchunk - 1) / kchunk;
   if (minchunk > 2) {  // wave-quantisation aware chunking (2 resident CTAs per SM)
-    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, (int64_t)kLapMinB * sm_count, minchunk, FEM_LAP_ROUNDS);
+    const WorkGrid w = make_workgrid((int)xt, (int)yt, nplanes, (int64_t)kRes * sm_count, minchunk, FEM_LAP_ROUNDS);
     zc = w.zc;
     kchunk = w.kchunk;
   }
