@@ -468,7 +468,7 @@ cudaError_t launch_cg_finish_init(CgScalars* sc, double tol, int maxit, cudaStre
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* q, int64_t n,
                              CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
                              const double* const* pold, int jpend) {
-  const unsigned nb = upd_blocks(n, sm_count);
+  const unsigned nb = nold > 0 ? vec_blocks(n, sm_count) : upd_blocks(n, sm_count);  // (group updates: 11 streams, more blocks in flight)
   OldP po{{p, p, p, p, p, p, p}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
@@ -485,7 +485,7 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
                                    CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
                                    const double* const* pold, int jpend) {
-  const unsigned nb = upd_blocks(n, sm_count);
+  const unsigned nb = nold > 0 ? vec_blocks(n, sm_count) : upd_blocks(n, sm_count);  // (group updates: 11 streams, more blocks in flight)
   OldP po{{p, p, p, p, p, p, p}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
@@ -526,7 +526,7 @@ cudaError_t launch_cg_xdefer_flush(double* x, const double* const* pend, int64_t
 cudaError_t launch_cg_cgcg_update(double* x, double* r, const double* pr, double* pw, double* s, const double* w,
                                   int64_t n, CgScalars* sc, Reduce red, cudaStream_t st, int sm_count, int nold,
                                   const double* const* pold, int jpend) {
-  const unsigned nb = upd_blocks(n, sm_count);
+  const unsigned nb = nold > 0 ? vec_blocks(n, sm_count) : upd_blocks(n, sm_count);  // (group updates: 11 streams, more blocks in flight)
   OldP po{{pr, pr, pr, pr, pr, pr, pr}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
