@@ -84,16 +84,9 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
   ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + 4 * TY));
   const uint32_t tfull_a = smem_u32(tfull), tempty_a = smem_u32(tempty);
 
-  // CG scalars, the four loads issued together up front (one L2 round trip instead of two) so
-  // their latency is covered by the barrier initialisation; the done test follows ring.init
-  int sc_done = 0, sc_first = 1;
-  double sc_rrn = 0.0, sc_rr = 1.0;
-  if (mode >= 1) sc_done = sc->done;
-  if (mode == 2) {
-    sc_first = sc->first;
-    sc_rrn = sc->rr_new;
-    sc_rr = sc->rr;
-  }
+  if (mode >= 1 && sc->done) return;
+  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
+  const double beta = (mode == 2) ? (sc->first ? 0.0 : sc->rr_new / sc->rr) : 0.0;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
@@ -111,9 +104,6 @@ __global__ void __launch_bounds__(32 * (TY + 1), (TY <= 7) ? 2 : 1)
     mbar_init(&tempty[tid], 1);
   }
   ring.init(tid, NT, TY);  // (fences + __syncthreads cover the hand-off barriers too)
-  if (mode >= 1 && sc_done) return;  // (uniform: every thread returns, after the init's barrier)
-  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
-  const double beta = (mode == 2) ? (sc_first ? 0.0 : sc_rrn / sc_rr) : 0.0;
   if (TM) ring.set_tshift(i0 - 1, uorg);
 
   double pq = 0.0, rr2 = 0.0;  // (rr2: mode 3, sum of the input's squares)
@@ -466,16 +456,9 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
   ring.carve(smem_raw, reinterpret_cast<unsigned char*>(tempty + HD * TY));
   const uint32_t tfull_a = smem_u32(tfull), tempty_a = smem_u32(tempty);
 
-  // CG scalars, the four loads issued together up front (one L2 round trip instead of two) so
-  // their latency is covered by the barrier initialisation; the done test follows ring.init
-  int sc_done = 0, sc_first = 1;
-  double sc_rrn = 0.0, sc_rr = 1.0;
-  if (mode >= 1) sc_done = sc->done;
-  if (mode == 2) {
-    sc_first = sc->first;
-    sc_rrn = sc->rr_new;
-    sc_rr = sc->rr;
-  }
+  if (mode >= 1 && sc->done) return;
+  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
+  const double beta = (mode == 2) ? (sc->first ? 0.0 : sc->rr_new / sc->rr) : 0.0;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
@@ -492,9 +475,6 @@ __global__ void __launch_bounds__(32 * (TY + ((TM && kEl2Self) ? 0 : 1)), 1)
     mbar_init(&tempty[tid], 1);
   }
   ring.init(tid, NT, TY);
-  if (mode >= 1 && sc_done) return;  // (uniform: every thread returns, after the init's barrier)
-  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
-  const double beta = (mode == 2) ? (sc_first ? 0.0 : sc_rrn / sc_rr) : 0.0;
   if (PAIR) ring.set_pair_tile(i0 - 1, j0 - 1, pg);
   const int tux = TM ? ring.set_tshift(i0 - 1, uorg) : 0, tuy = (int)(j0 - 1 - uorg.t_j0);
   const int tmx = (int)(2 * (i0 - 1)), tmy = (int)(j0 - 1);

@@ -55,16 +55,9 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
   Ring ring;
   ring.carve(smem_raw, smem_raw + Ring::BYTES);
 
-  // CG scalars, the four loads issued together up front (one L2 round trip instead of two) so
-  // their latency is covered by the barrier initialisation; the done test follows ring.init
-  int sc_done = 0, sc_first = 1;
-  double sc_rrn = 0.0, sc_rr = 1.0;
-  if (mode >= 1) sc_done = sc->done;
-  if (mode == 2) {
-    sc_first = sc->first;
-    sc_rrn = sc->rr_new;
-    sc_rr = sc->rr;
-  }
+  if (mode >= 1 && sc->done) return;
+  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
+  const double beta = (mode == 2) ? (sc->first ? 0.0 : sc->rr_new / sc->rr) : 0.0;
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + TX * ty;
@@ -76,9 +69,6 @@ __global__ void __launch_bounds__(TX*(TY + ((TM && (C == 1 ? kLapSelf1 : kLapSel
   const int64_t ke = min(g.k1, kb + kspan);
   const int64_t pfirst = kb - 1;
   ring.init(tid, NT, TY);
-  if (mode >= 1 && sc_done) return;  // (uniform: every thread returns, after the init's barrier)
-  // fused CG (mode 2): operator input p = r + beta p_old, beta = rr_new / rr (0 on the first step)
-  const double beta = (mode == 2) ? (sc_first ? 0.0 : sc_rrn / sc_rr) : 0.0;
   if (PAIR) ring.set_pair_tile(i0 - 1, j0 - 1, pg);
   const int tux = TM ? ring.set_tshift(i0 - 1, uorg) : 0, tuy = (int)(j0 - 1 - uorg.t_j0);
   const int nplane = (int)(ke - pfirst + 1);

@@ -19,6 +19,9 @@ constexpr int kVecThreads = 256;
 #ifndef FEM_UPD_MINB
 #define FEM_UPD_MINB 3  // resident blocks per SM the fused update kernel is compiled for (80 registers)
 #endif
+#ifndef FEM_UPD_MINB_PEND
+#define FEM_UPD_MINB_PEND 4  // ... its variants without the x group (64 registers: the 8-per-SM grid in two full waves)
+#endif
 
 // grid of a grid-stride vector kernel: at most one wave of resident blocks (per_sm per SM), so
 // every block streams an equal share and no partial last wave idles part of the GPU
@@ -26,12 +29,6 @@ static inline unsigned vec_blocks(int64_t n, int sm_count, int per_sm = 8) {
   int64_t want = (n + kVecThreads * 4 - 1) / (kVecThreads * 4);
   int64_t cap = (int64_t)sm_count * per_sm;
   return (unsigned)std::max<int64_t>(1, std::min(want, cap));
-}
-#ifndef FEM_UPD_WAVE
-#define FEM_UPD_WAVE 1  // update kernels (FEM_UPD_MINB resident blocks per SM): grid = one wave
-#endif
-static inline unsigned upd_blocks(int64_t n, int sm_count) {
-  return vec_blocks(n, sm_count, FEM_UPD_WAVE ? FEM_UPD_MINB : 8);
 }
 
 __global__ void __launch_bounds__(kVecThreads) cg_init_kernel(const double* __restrict__ b,
@@ -132,7 +129,7 @@ __global__ void __launch_bounds__(kVecThreads) cg_update_kernel(double* __restri
 //       (k = 0: the plain x += alpha p, 48 B/DOF; k = 1: 56; k = 3: 72; k = 7: 104)
 // so a group of m iterations moves 32 m + 16 instead of 48 m B/DOF of update traffic.
 template <int NOLD>
-__global__ void __launch_bounds__(kVecThreads, FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
+__global__ void __launch_bounds__(kVecThreads, NOLD <= 0 ? FEM_UPD_MINB_PEND : FEM_UPD_MINB) cg_update_fused_kernel(double* __restrict__ x,
                                                                       double* __restrict__ r,
                                                                       const double* __restrict__ p,
                                                                       const double* __restrict__ q,
@@ -468,7 +465,7 @@ cudaError_t launch_cg_finish_init(CgScalars* sc, double tol, int maxit, cudaStre
 cudaError_t launch_cg_update(double* x, double* r, const double* p, const double* q, int64_t n,
                              CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
                              const double* const* pold, int jpend) {
-  const unsigned nb = nold > 0 ? vec_blocks(n, sm_count) : upd_blocks(n, sm_count);  // (group updates: 11 streams, more blocks in flight)
+  const unsigned nb = vec_blocks(n, sm_count);  // (the same grid for every nold: the r.r grouping, hence x, is independent of x_defer)
   OldP po{{p, p, p, p, p, p, p}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
@@ -485,7 +482,7 @@ cudaError_t launch_cg_update(double* x, double* r, const double* p, const double
 cudaError_t launch_cg_update_fused(double* x, double* r, const double* p, const double* q, int64_t n,
                                    CgScalars* sc, Reduce red, cudaStream_t s, int sm_count, int nold,
                                    const double* const* pold, int jpend) {
-  const unsigned nb = nold > 0 ? vec_blocks(n, sm_count) : upd_blocks(n, sm_count);  // (group updates: 11 streams, more blocks in flight)
+  const unsigned nb = vec_blocks(n, sm_count);  // (the same grid for every nold: the r.r grouping, hence x, is independent of x_defer)
   OldP po{{p, p, p, p, p, p, p}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
@@ -526,7 +523,7 @@ cudaError_t launch_cg_xdefer_flush(double* x, const double* const* pend, int64_t
 cudaError_t launch_cg_cgcg_update(double* x, double* r, const double* pr, double* pw, double* s, const double* w,
                                   int64_t n, CgScalars* sc, Reduce red, cudaStream_t st, int sm_count, int nold,
                                   const double* const* pold, int jpend) {
-  const unsigned nb = nold > 0 ? vec_blocks(n, sm_count) : upd_blocks(n, sm_count);  // (group updates: 11 streams, more blocks in flight)
+  const unsigned nb = vec_blocks(n, sm_count);  // (the same grid for every nold: the r.r grouping, hence x, is independent of x_defer)
   OldP po{{pr, pr, pr, pr, pr, pr, pr}};
   for (int k = 0; k < nold && k < 7; ++k) po.p[k] = pold[k];
   switch (nold) {
